@@ -1,0 +1,220 @@
+"""ctypes wrapper of the plain-C FP64 oracle (oracle/akmc_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  The product package
+(paper_2604_24091_b200) never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "akmc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+ORC_OK, ORC_INVALID, ORC_TERMINAL = 0, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle: plain C11, -O2, no SIMD intrinsics, no FP contraction."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("cells", C.c_int32 * 3), ("n_voxels", C.c_int32), ("T", C.c_double),
+                ("nu0", C.c_double), ("kB", C.c_double), ("model", C.c_int32),
+                ("domain", C.c_int32 * 3), ("window_s", C.c_double), ("seed", C.c_uint64),
+                ("strict", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.POINTER
+        _lib.orc_philox.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+        _lib.orc_det_exp.argtypes = [C.c_double]; _lib.orc_det_exp.restype = C.c_double
+        _lib.orc_det_log.argtypes = [C.c_double]; _lib.orc_det_log.restype = C.c_double
+        _lib.orc_window_offsets.argtypes = [P(C.c_int32)]
+        _lib.orc_system_energy.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.orc_system_energy.restype = C.c_double
+        _lib.orc_delta_energy.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+        _lib.orc_delta_energy.restype = C.c_double
+        _lib.orc_window.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.orc_mlp_fp64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_barriers.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_run.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.orc_rates.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_cluster_stats.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                           C.c_void_p, C.c_void_p, C.c_int64]
+        _lib.orc_sector_perm.argtypes = [C.c_uint64, C.c_int64, P(C.c_int)]
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class Config:
+    cells: tuple = (16, 16, 16)
+    n_voxels: int = 1
+    T: float = 563.0
+    nu0: float = 6.0e12
+    kB: float = 8.617333262e-5
+    model: int = 0           # 0 pair KRA, 1 MLP
+    domain: tuple = (0, 0, 0)
+    window_s: float = 0.0
+    seed: int = 1
+    strict: int = 0
+
+    def c(self) -> _Cfg:
+        s = _Cfg()
+        s.cells[:] = [int(v) for v in self.cells]
+        s.n_voxels = int(self.n_voxels)
+        s.T, s.nu0, s.kB = float(self.T), float(self.nu0), float(self.kB)
+        s.model = int(self.model)
+        s.domain[:] = [int(v) for v in self.domain]
+        s.window_s = float(self.window_s)
+        s.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        s.strict = int(self.strict)
+        return s
+
+    @property
+    def sites_per_voxel(self) -> int:
+        return 2 * self.cells[0] * self.cells[1] * self.cells[2]
+
+
+def philox(ctr, key):
+    c = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (C.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (C.c_uint32 * 4)()
+    lib().orc_philox(c, k, o)
+    return list(o)
+
+
+def det_exp(x: float) -> float:
+    return lib().orc_det_exp(float(x))
+
+
+def det_log(u: float) -> float:
+    return lib().orc_det_log(float(u))
+
+
+def window_offsets() -> np.ndarray:
+    out = np.zeros((64, 4), dtype=np.int32)
+    n = lib().orc_window_offsets(out.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert n == 64, n
+    return out
+
+
+def sector_perm(seed: int, sweep: int):
+    p = (C.c_int * 8)()
+    lib().orc_sector_perm(int(seed) & 0xFFFFFFFFFFFFFFFF, int(sweep), p)
+    return list(p)
+
+
+def system_energy(cfg: Config, species: np.ndarray, vox: int, eps: np.ndarray) -> float:
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    e = np.ascontiguousarray(eps, dtype=np.float64)
+    return lib().orc_system_energy(C.byref(cfg.c()), _ptr(sp), int(vox), _ptr(e))
+
+
+def delta_energy(cfg: Config, species, vsite: int, k: int, eps) -> float:
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    e = np.ascontiguousarray(eps, dtype=np.float64)
+    return lib().orc_delta_energy(C.byref(cfg.c()), _ptr(sp), int(vsite), int(k), _ptr(e))
+
+
+def window(cfg: Config, species, vsite: int) -> np.ndarray:
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    out = np.zeros(64, dtype=np.uint8)
+    lib().orc_window(C.byref(cfg.c()), _ptr(sp), int(vsite), _ptr(out))
+    return out
+
+
+def mlp_fp64(sigma: np.ndarray, mlp: np.ndarray) -> np.ndarray:
+    s = np.ascontiguousarray(sigma, dtype=np.uint8)
+    m = np.ascontiguousarray(mlp, dtype=np.float64)
+    E = np.zeros(8)
+    lib().orc_mlp_fp64(_ptr(s), _ptr(m), _ptr(E))
+    return E
+
+
+def barriers(cfg: Config, species, vsite: int, eps=None, E0=None, mlp=None):
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
+    e0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
+    m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
+    E = np.zeros(8); G = np.zeros(8)
+    clamps = lib().orc_barriers(C.byref(cfg.c()), _ptr(sp), int(vsite), _ptr(e), _ptr(e0), _ptr(m),
+                                _ptr(E), _ptr(G))
+    return E, G, clamps
+
+
+@dataclass
+class State:
+    species: np.ndarray      # uint8, n_voxels * sites
+    vac: np.ndarray          # int64 global site ids, slot order
+    clock: np.ndarray        # float64 per voxel
+    nev: np.ndarray          # int64 per voxel (serial event counter)
+    sweep: np.ndarray        # int64[1]
+    counters: np.ndarray     # int64[4] events, hop_evals, terminal_voxels, clamps
+
+    @staticmethod
+    def from_species(cfg: Config, species: np.ndarray) -> "State":
+        sp = np.ascontiguousarray(species, dtype=np.uint8).copy()
+        vac = np.flatnonzero(sp == 6).astype(np.int64)       # slot = rank of initial site
+        return State(sp, vac, np.zeros(cfg.n_voxels), np.zeros(cfg.n_voxels, dtype=np.int64),
+                     np.zeros(1, dtype=np.int64), np.zeros(4, dtype=np.int64))
+
+    def copy(self) -> "State":
+        return State(self.species.copy(), self.vac.copy(), self.clock.copy(), self.nev.copy(),
+                     self.sweep.copy(), self.counters.copy())
+
+
+def run(cfg: Config, st: State, n: int, eps=None, E0=None, mlp=None) -> int:
+    e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
+    e0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
+    m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
+    return lib().orc_run(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
+                         _ptr(st.nev), _ptr(st.sweep), _ptr(e), _ptr(e0), _ptr(m), int(n), _ptr(st.counters))
+
+
+def rates(cfg: Config, species, vac, eps=None, E0=None, mlp=None):
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    v = np.ascontiguousarray(vac, dtype=np.int64)
+    e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
+    e0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
+    m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
+    R = np.zeros((v.size, 8)); E = np.zeros((v.size, 8))
+    lib().orc_rates(C.byref(cfg.c()), _ptr(sp), _ptr(v), int(v.size), _ptr(e), _ptr(e0), _ptr(m), _ptr(R), _ptr(E))
+    return R, E
+
+
+def cluster_stats(cfg: Config, species, vox: int = 0, cu: int = 1, nstar: int = 4, hist_len: int = 64):
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    out = np.zeros(8); hist = np.zeros(hist_len, dtype=np.int64)
+    lib().orc_cluster_stats(C.byref(cfg.c()), _ptr(sp), int(vox), int(cu), int(nstar), _ptr(out), _ptr(hist),
+                            int(hist_len))
+    keys = ["n_cu", "n_clusters", "n_clusters2", "largest", "monomers", "precipitates", "mean_size2",
+            "cucu_bonds"]
+    d = {k: float(v) for k, v in zip(keys, out)}
+    d["hist"] = hist
+    return d

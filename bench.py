@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 AKMC hot path (BASELINE.json metric: vacancy-hop evaluations/sec and
+simulated seconds per wall-second at 1/2/4/8 B200).
+
+Default workload = C5: 1024^3 bcc cells per GPU (2.1e9 sites), c_v = 1e-4 (214,748 vacancies),
+RPV composition, windowed synchronous sublattice (domains 8^3, lambda = 1/4), barrier network
+448-256-256-8 (physics-embedded weights + seeded residual) in the tensor-core FP32-equivalent mode.
+A step = one sublattice sweep (8 phases) over the GPU's block.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5|c4|c3|c2|c1]
+
+N > 1 is launched by torchrun (one rank per GPU).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "vacancy-hop evaluations/sec"
+UNIT = "hop-evals/s"
+FLOPS_PER_VAC = 2 * (256 * 256 + 256 * 8) + 64 * 256      # layers 2-3 FLOPs + layer-1 adds
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(name: str):
+    pr = synth.preset(name.upper())
+    cells = pr.cells
+    nvox = pr.n_voxels
+    if name == "c4":
+        nvox = 512                      # per GPU (4096 over 8 GPUs)
+    return pr, cells, nvox
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_inputs(name: str, rank: int, device):
+    """Synthetic inputs (seeded; recipe in DESIGN.md sec. 4).  Returns host species (pinned numpy)."""
+    import torch
+    pr, cells, nvox = workload(name)
+    seed = pr.seed + 1000 * rank
+    if name in ("c5", "c3"):
+        t = synth.make_lattice_iid(cells, pr.fractions, pr.n_vac_per_voxel, seed=seed, device=device)
+        host = torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True)
+        host.copy_(t)
+        del t
+        return host.numpy(), host
+    sp = synth.make_lattice(cells, nvox, pr.fractions, pr.n_vac_per_voxel, seed=seed)
+    host = torch.from_numpy(sp).pin_memory()
+    return host.numpy(), host
+
+
+def sim_config(name: str, precision: int, model: int, lam: float, E0):
+    import paper_2604_24091_b200 as akmc
+    pr, cells, nvox = workload(name)
+    win = synth.window_seconds(lam, E0[0]) if pr.domain[0] else 0.0
+    return akmc.Config(cells=cells, n_voxels=nvox, barrier_model=model, precision=precision,
+                       domain_cells=pr.domain, window_s=win, seed=pr.seed), pr
+
+
+def cpu_baseline(name: str, steps: int, lam: float, seconds_target: float = 15.0):
+    """The oracle as it stands (single thread, FP64 MLP) on a bounded sample of the workload."""
+    import oracle
+    oracle.build()
+    eps, E0 = synth.illustrative_pair_params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=1)
+    pr, cells, nvox = workload(name)
+    if pr.domain[0]:
+        # sample: a 256^3-cell block of the same recipe (same c_v, domains, lambda), whole sweeps
+        sc = (256, 256, 256)
+        nvac = max(1, int(round(pr.n_vac_per_voxel * (256 ** 3) / (cells[0] * cells[1] * cells[2]))))
+        import torch
+        sp = synth.make_lattice_iid(sc, pr.fractions, nvac, seed=pr.seed, device="cpu").numpy()
+        cfg = oracle.Config(cells=sc, model=1, domain=pr.domain, window_s=synth.window_seconds(lam, E0[0]),
+                            seed=pr.seed)
+        sample = f"{sc[0]}^3-cell block of the {name.upper()} recipe ({nvac} V), whole sublattice sweeps, FP64 MLP"
+    else:
+        sc = cells
+        sp = synth.make_lattice(sc, 1, pr.fractions, pr.n_vac_per_voxel, seed=pr.seed)
+        cfg = oracle.Config(cells=sc, model=1, seed=pr.seed)
+        sample = f"one {sc[0]}^3 voxel of {name.upper()} ({pr.n_vac_per_voxel} V), serial BKL events, FP64 MLP"
+    st = oracle.State.from_species(cfg, sp)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        oracle.run(cfg, st, 1, None, None, mlp)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds_target or done >= max(steps, 1) * 1000:
+            break
+    hop = int(st.counters[1])
+    return {"value": hop / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{sample}; {done} step(s), {hop} hop evals in {el:.1f} s"}, st, el
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    t_all = time.perf_counter()
+    cb, st, el = cpu_baseline(args.workload, args.steps, args.lam, seconds_target=max(10.0, 4.0 * args.steps))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload.upper(), "impl": "CPU FP64 oracle (oracle/akmc_oracle.c)"},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_24091_b200 as akmc
+    from paper_2604_24091_b200 import build as akbuild
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        akbuild.build()
+    if world > 1:
+        dist.barrier()
+    prec = akmc.PREC_FP32 if args.precision == "fp32" else akmc.PREC_FP64
+    model = akmc.MODEL_MLP if args.model == "mlp" else akmc.MODEL_PAIR
+    eps, E0 = synth.illustrative_pair_params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=1)
+    cfg, pr = sim_config(args.workload, prec, model, args.lam, E0)
+    sp_host, sp_keep = make_inputs(args.workload, rank, dev)
+    sites = sp_host.size
+
+    stream = torch.cuda.Stream(device=dev)
+    # ---------------- device-resident timing ("value")
+    sim = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    sim.set_stream(stream.cuda_stream)
+    sim.set_profiling(True)
+    for _ in range(args.warmup):
+        sim.step(1)
+    torch.cuda.synchronize()
+    _, _, clock0, tot0 = sim.state(species=False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as cs:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sim.step(1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    _, _, clock1, tot1 = sim.state(species=False)
+    hop = tot1["hop_evals"] - tot0["hop_evals"]
+    events = tot1["events"] - tot0["events"]
+    launches = tot1["kernel_launches"] - tot0["kernel_launches"]
+    mlp_ms = tot1["mlp_ms"] - tot0["mlp_ms"]
+    mlp_launch = tot1["mlp_launches"] - tot0["mlp_launches"]
+    mlp_rows = tot1["mlp_rows"] - tot0["mlp_rows"]
+    sim_s = float(np.mean(clock1 - clock0))
+    sim.close()
+
+    # ---------------- end to end through the C-ABI with host buffers (init H2D + steps + state D2H)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    sim2 = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    out = torch.empty(sites, dtype=torch.uint8, pin_memory=True).numpy()
+    hop_e2e = 0
+    for _ in range(args.steps):
+        c = sim2.step(1)
+        hop_e2e += c["hop_evals"]
+        sim2.state(species=False)
+    import ctypes
+    vac = np.empty(max(sim2.n_vac, 1), dtype=np.int64)
+    n = ctypes.c_int64(vac.size)
+    sim2.lib.akmc_state(sim2.h, ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(vac.ctypes.data), ctypes.byref(n),
+                        None, None)
+    t_e2e = time.perf_counter() - t0
+    sim2.close()
+
+    vals = torch.tensor([ms, float(hop), float(events), sim_s, t_e2e, float(hop_e2e), float(launches), mlp_ms,
+                         float(mlp_rows), float(mlp_launch)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vals.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    else:
+        mx = sm = vals
+    ms_max = float(mx[0])
+    hop_all = float(sm[1])
+    value = hop_all / (ms_max / 1e3)
+    e2e_value = float(sm[5]) / float(mx[4])
+
+    line = None
+    if rank == 0:
+        peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+        tc_peak = peaks.get("bf16_tflops_sustained", 1400.0) * 0.5
+        mlp_s = mlp_ms / 1e3 if mlp_ms > 0 else float("nan")
+        achieved = (mlp_rows * FLOPS_PER_VAC) / mlp_s / 1e12 if mlp_ms > 0 else None
+        roof = {"bound": "tensor", "kernel": "mlp_tc_kernel (gather+encode+layer1+tcgen05 layer2+layer3+rates)",
+                "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": (achieved / tc_peak) if achieved else None, "traffic": None,
+                "peak_note": "FP32-class tensor peak = measured bf16 sustained x 1/2 (TF32:BF16 nominal ratio)",
+                "algorithmic_flops_per_vac": FLOPS_PER_VAC, "launches": int(mlp_launch), "rows": int(mlp_rows),
+                "kernel_ms": mlp_ms, "share_of_step": (mlp_ms / ms) if ms > 0 else None}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / max(args.steps, 1), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "fp32-equivalent (3x fp16 tcgen05, fp32 accumulate) + fp64 selection"
+                if prec == akmc.PREC_FP32 else "f64",
+                "data": "synthetic",
+                "config": {"workload": args.workload.upper(), "cells_per_gpu": list(cfg.cells),
+                           "voxels_per_gpu": cfg.n_voxels, "sites_per_gpu": sites,
+                           "vacancies_per_gpu": pr.n_vac_per_voxel * cfg.n_voxels,
+                           "domain_cells": list(cfg.domain_cells), "lambda": args.lam, "window_s": cfg.window_s,
+                           "model": "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA",
+                           "parallelism": f"independent per-GPU blocks x{world}" if world > 1 else "1 GPU",
+                           "l2": "inputs > L2 (lattice %.2f GB per GPU)" % (sites / 1e9)},
+                "sim_seconds_per_wall_second": (sim_s * world / world) / (ms_max / 1e3),
+                "events_per_s": float(sm[2]) / (ms_max / 1e3),
+                "gpu_launches": int(float(sm[6])),
+                "roofline": roof,
+                "e2e": {"value": e2e_value, "unit": UNIT,
+                        "h2d_bytes_per_step": int(sites / max(args.steps, 1)),
+                        "d2h_bytes_per_step": int(sites / max(args.steps, 1)) + 256,
+                        "note": "akmc_init from pinned host lattice + K x (akmc_step + akmc_state counters) + "
+                                "final akmc_state lattice readback, host wall clock"},
+                "clocks": cs.summary()}
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, _, _ = cpu_baseline(args.workload, 1, args.lam)
+        line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--model", default="mlp", choices=["mlp", "pair"])
+    ap.add_argument("--lam", type=float, default=0.25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * akmc.h -- C-ABI of the B200-native AKMC vacancy-hop step (AtomWorld, arXiv 2604.24091).
+ *
+ * The library (paper_2604_24091_b200/lib/libakmc.so) runs the data-parallel hot path of the
+ * paper's atomistic world model on one B200 per process: for every vacancy it gathers the
+ * 64-site neighbourhood (sec. V.A.1, sec. VI.C), evaluates the barrier network
+ * (sec. V.B.1) or the pair KRA model, turns barriers
+ * into Arrhenius rates (Eq. 8), and selects/applies one hop per competing set with a
+ * residence-time draw (Eq. 2 read as BKL) from Philox4x32-10.
+ * Citations: P:NNN = PAPER.md line, S:NNN = SPEC.md line, A<n> = reading n in DESIGN.md sec. 3.
+ *
+ * Conventions common to every call
+ *  - All pointers passed IN are caller-owned HOST memory, copied before the call returns.
+ *    *_out buffers are caller-allocated host memory.  The handle owns all device memory.
+ *  - One handle per process and GPU (the device current at akmc_init).  Calls on one handle are
+ *    not reentrant.  Every call is synchronous: it returns after its device work completes.
+ *  - Return value: AKMC_OK or an AKMC_* status.  On a non-OK status, akmc_last_error() gives a
+ *    one-line message; the state is unchanged for AKMC_ERR_INVALID and AKMC_TERMINAL.
+ *  - Site index (canonical, per voxel): i = 2*(x + Lx*(y + Ly*z)) + b, basis b in {0,1};
+ *    a multi-voxel lattice is n_voxels such blocks back to back (global site = voxel*sites + i).
+ *  - Species codes (A6): Fe 0, Cu 1, Ni 2, Mn 3, Si 4, P 5, vacancy 6; n_species must be 7.
+ *  - Vacancy slot ids: the vacancies present at akmc_init, ordered by global site index; a
+ *    slot keeps its identity as the vacancy moves.
+ *  - Determinism: within one precision mode, equal (config, inputs, seed) give equal output
+ *    bits for any launch configuration.  In AKMC_PREC_FP64 mode the trajectory is bit-equal to
+ *    the FP64 CPU oracle (oracle/akmc_oracle.c) -- DESIGN.md sec. 5 fixes every FP operation.
+ */
+#ifndef AKMC_H
+#define AKMC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (categories follow SPEC cli exit codes S:724-725, terminal signal S:199) */
+enum {
+    AKMC_OK = 0,
+    AKMC_ERR_RUNTIME = 1,   /* internal error (bad handle, exceeded capacity)            */
+    AKMC_ERR_INVALID = 2,   /* invalid configuration or inputs (list at akmc_init)       */
+    AKMC_TERMINAL = 3,      /* no feasible event in a competing set       */
+    AKMC_ERR_CUDA = 4,      /* CUDA runtime error / no device / missing sm_100a          */
+    AKMC_ERR_NCCL = 5       /* NCCL error (multi-GPU)                                    */
+};
+
+enum { AKMC_MODEL_PAIR = 0, AKMC_MODEL_MLP = 1 };
+/* precision of the barrier evaluation (the selection is always FP64, A17):
+ *  FP64 : sequential fma in the oracle's order + det_exp -> bit-exact trajectories
+ *  FP32 : "matrix multiplication ... executed in FP32": layer 1 FP64-accumulated sparse
+ *         embedding bag rounded to FP32; layer 2 on tcgen05 tensor cores as an FP32-equivalent
+ *         3-pass fp16 split (hi*hi + hi*lo + lo*hi, FP32 accumulate in TMEM); layer 3 FP32.
+ *         Per-hop rates within 1e-5 relative of FP64 (north star).  Pair model: same as FP64. */
+enum { AKMC_PREC_FP64 = 0, AKMC_PREC_FP32 = 1 };
+
+typedef struct akmc_config {
+    int32_t  cells[3];        /* Lx,Ly,Lz bcc cells per voxel; each even and >= 4            */
+    int32_t  n_voxels;        /* >= 1 independent periodic voxels                          */
+    int32_t  n_species;       /* must be 7 (A6); vacancy code 6                                    */
+    int32_t  barrier_model;   /* AKMC_MODEL_PAIR or AKMC_MODEL_MLP        */
+    int32_t  precision;       /* AKMC_PREC_FP64 or AKMC_PREC_FP32                                  */
+    int32_t  domain_cells[3]; /* sublattice domain edge (reading A19/A21): {0,0,0} => serial BKL,  */
+                              /* one competing set per voxel (A15); else each even, >= 6, divides */
+                              /* cells (sector = domain/2 >= 3 cells, A20)                          */
+    double   temperature_K;   /* > 0                                                       */
+    double   nu0;             /* attempt frequency, > 0                                    */
+    double   kB;              /* Boltzmann constant eV/K; passed so both sides share bits  */
+    double   window_s;        /* Delta_win per phase (A22); > 0 in sublattice mode                 */
+    uint64_t seed;            /* Philox key (A16)                                                  */
+    int32_t  gpu_grid[3];     /* spatial decomposition over ranks; {1,1,1} (single rank) for now   */
+    int32_t  rank, world;     /* this process's rank / world size; world must equal prod(gpu_grid) */
+} akmc_config;
+
+typedef struct akmc_counters {
+    int64_t events;           /* hops applied                                                      */
+    int64_t hop_evals;        /* 8 x vacancy evaluations (masked hops included), S:587 accounting  */
+    int64_t iterations;       /* inner iterations (serial: events per voxel; sublattice: a8 loops) */
+    int64_t clamps;           /* pair-model barriers clamped at 0 (A12)                            */
+    int64_t terminal_voxels;  /* competing sets that hit Gamma_tot == 0 (serial mode)              */
+    int64_t sweeps;           /* sublattice sweeps completed since init                            */
+    int64_t kernel_launches;  /* kernels launched by the library                                   */
+    int64_t mlp_launches;     /* launches of the dominant (barrier) kernel                         */
+    int64_t mlp_rows;         /* vacancy rows evaluated by it                                      */
+    double  mlp_ms;           /* its summed CUDA-event time (only when profiling is enabled)       */
+    double  wall_ms;          /* host wall time inside akmc_step                                    */
+} akmc_counters;
+
+typedef struct akmc_handle akmc_handle;
+
+/* Create a simulation on the current CUDA device.
+ *  species : n_voxels * 2*Lx*Ly*Lz bytes, canonical order (see above).
+ *  eps     : [2][7][7] pair energies eV, eps[s][a][b] (s = 1NN, 2NN), symmetric;
+ *            required for AKMC_MODEL_PAIR, ignored (may be NULL) for the MLP.
+ *  E0      : [7] base barriers eV; required for the pair model.
+ *  mlp     : FP64 weights W1[448*256] (row f = 7*slot + species), b1[256], W2[256*256]
+ *            (row = input), b2[256], W3[256*8], b3[8]; required for AKMC_MODEL_MLP.
+ * AKMC_ERR_INVALID when: a cell count is odd or < 4; n_voxels < 1; n_species != 7; a species code
+ * > 6; vacancies exceed 1% of sites; T, nu0 or kB <= 0; domains do not divide the lattice
+ * or a sector is < 3 cells; window_s <= 0 in sublattice mode; world != prod(gpu_grid) or world != 1;
+ * eps not symmetric; a NaN/Inf in eps, E0 or mlp; an unknown model or precision.
+ * AKMC_ERR_CUDA when no CUDA device is present or the device is not sm_100.                       */
+int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps, const double* E0,
+              const double* mlp, akmc_handle** out);
+
+/* Advance: serial mode -> n events per voxel; sublattice mode -> n sweeps of 8
+ * phases (reading A19).  ctr (optional) receives the counters accumulated over this
+ * call.  Returns AKMC_TERMINAL when some competing set had no feasible event (its state is left
+ * unchanged from that point); other voxels still advance. */
+int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr);
+
+/* Read back the state.  species_out: n_voxels*sites bytes (may be NULL); vac_sites_out: global
+ * site index of each vacancy slot (may be NULL) with *n_vac_inout = capacity in / count out
+ * (a short buffer returns AKMC_ERR_INVALID without writing); clock_s_out: [n_voxels] simulated
+ * seconds (may be NULL); ctr_out: counters accumulated since init (may be NULL).              */
+int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int64_t* n_vac_inout,
+               double* clock_s_out, akmc_counters* ctr_out);
+
+/* Per-hop rates of the current state in the handle's precision, [n_vac][8] slot order, masked
+ * hops exactly 0; barriers_out (may be NULL) gets the barriers E [n_vac][8] eV.    */
+int akmc_rates(akmc_handle* h, double* rates_out, double* barriers_out);
+
+/* Diagnostics: evaluate the barrier model on n caller-given windows (host [n][64] species bytes in
+ * window-slot order) at the given precision; E_out [n][8] barriers in eV
+ * (mask not applied).  Uses the handle's weights/parameters; state untouched.                   */
+int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t precision, double* E_out);
+
+/* Launch the library's kernels on this CUDA stream (cudaStream_t as void*; NULL = the handle's
+ * own stream).  profile != 0 records CUDA events around every barrier-kernel launch (mlp_ms).  */
+int akmc_set_stream(akmc_handle* h, void* stream);
+int akmc_set_profiling(akmc_handle* h, int32_t profile);
+
+void akmc_free(akmc_handle* h);
+
+/* Message of the last non-OK status on this handle (or of the last failed akmc_init when h is
+ * NULL).  Never NULL; "" when there was no error.                                              */
+const char* akmc_last_error(const akmc_handle* h);
+
+/* Library version string, e.g. "akmc-b200 0.1 sm_100a". */
+const char* akmc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AKMC_H */

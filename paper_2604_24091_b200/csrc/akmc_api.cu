@@ -1,0 +1,681 @@
+// akmc_api.cu -- C-ABI (include/akmc.h) of the B200 AKMC hot path: handle, validation, host
+// loops of the serial (a10) and windowed-sublattice (a1-a9, reading A19) modes.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/akmc.h"
+#include "akmc_kernels.cuh"
+#include "akmc_mlp_tc.cuh"
+
+using namespace akmc;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+// ------------------------------------------------------------------ host geometry (independent of the oracle)
+// window: bcc vectors within 6.0 A at a0 = 2.866 A, sorted by (|h|^2, hx, hy, hz)  (A3, A4)
+bool build_geometry(GeomTables& G)
+{
+    struct O { int h2, x, y, z; };
+    std::vector<O> v;
+    const double half_a0 = 2.866 / 2.0, rc = 6.0;
+    for (int x = -5; x <= 5; ++x)
+        for (int y = -5; y <= 5; ++y)
+            for (int z = -5; z <= 5; ++z) {
+                if (((x & 1) != (y & 1)) || ((y & 1) != (z & 1))) continue;
+                if (x == 0 && y == 0 && z == 0) continue;
+                const int h2 = x * x + y * y + z * z;
+                if ((double)h2 * half_a0 * half_a0 <= rc * rc) v.push_back({h2, x, y, z});
+            }
+    std::sort(v.begin(), v.end(), [](const O& a, const O& b) {
+        if (a.h2 != b.h2) return a.h2 < b.h2;
+        if (a.x != b.x) return a.x < b.x;
+        if (a.y != b.y) return a.y < b.y;
+        return a.z < b.z;
+    });
+    if ((int)v.size() != kWin) return false;
+    for (int j = 0; j < kWin; ++j) {
+        G.off[j][0] = (int8_t)v[j].x; G.off[j][1] = (int8_t)v[j].y;
+        G.off[j][2] = (int8_t)v[j].z; G.off[j][3] = (int8_t)v[j].h2;
+    }
+    auto slot_of = [&](int x, int y, int z) -> int {
+        for (int j = 0; j < kWin; ++j)
+            if (G.off[j][0] == x && G.off[j][1] == y && G.off[j][2] == z) return j;
+        return -1;
+    };
+    // pair-KRA count lists per hop k: vacancy-side shells 1,2 without n_k (+1),
+    // target-side shells 1,2 without the vacancy (-1); all inside the window (A.1)
+    const int nn1[8][3] = {{-1,-1,-1},{-1,-1,1},{-1,1,-1},{-1,1,1},{1,-1,-1},{1,-1,1},{1,1,-1},{1,1,1}};
+    const int nn2[6][3] = {{-2,0,0},{2,0,0},{0,-2,0},{0,2,0},{0,0,-2},{0,0,2}};
+    for (int k = 0; k < kHops; ++k) {
+        const int ex = G.off[k][0], ey = G.off[k][1], ez = G.off[k][2];
+        int t = 0;
+        for (int sh = 0; sh < 2; ++sh) {
+            const int cnt = sh == 0 ? 8 : 6;
+            for (int i = 0; i < cnt; ++i) {
+                const int* d = sh == 0 ? nn1[i] : nn2[i];
+                if (!(d[0] == ex && d[1] == ey && d[2] == ez)) {          // vacancy side, skip n_k
+                    const int s = slot_of(d[0], d[1], d[2]);
+                    if (s < 0) return false;
+                    G.pair_slot[k][t] = (int8_t)s; G.pair_shell[k][t] = (int8_t)sh; G.pair_sign[k][t] = 1; ++t;
+                }
+                const int x = ex + d[0], y = ey + d[1], z = ez + d[2];
+                if (!(x == 0 && y == 0 && z == 0)) {                        // target side, skip vacancy
+                    const int s = slot_of(x, y, z);
+                    if (s < 0) return false;
+                    G.pair_slot[k][t] = (int8_t)s; G.pair_shell[k][t] = (int8_t)sh; G.pair_sign[k][t] = -1; ++t;
+                }
+            }
+        }
+        if (t != kPairTerms) return false;
+    }
+    return true;
+}
+
+// host Philox4x32-10 for the per-sweep sector permutation (A16/A19)
+void philox_host(uint32_t c[4], uint32_t k0, uint32_t k1)
+{
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[0] = n0; c[1] = (uint32_t)p1; c[2] = n2; c[3] = (uint32_t)p0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+}
+
+void sector_permutation(uint64_t seed, int64_t sweep, int perm[8])
+{
+    uint32_t y[8];
+    for (int j = 0; j < 2; ++j) {
+        uint32_t c[4] = {(uint32_t)j, 0xFFFFFFFFu, (uint32_t)sweep, (uint32_t)((uint64_t)sweep >> 32)};
+        philox_host(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+        for (int i = 0; i < 4; ++i) y[4 * j + i] = c[i];
+    }
+    for (int i = 0; i < 8; ++i) perm[i] = i;
+    for (int i = 7; i >= 1; --i) {
+        const int j = (int)(y[i] % (uint32_t)(i + 1));
+        std::swap(perm[i], perm[j]);
+    }
+}
+
+} // namespace
+
+struct akmc_handle {
+    akmc_config cfg{};
+    int dev = 0;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    bool sub = false;
+    Frame F{};
+    GeomTables G{};
+    PhysParams P{};
+    SubParams S{};
+    int nvox = 0;
+    int64_t nvac = 0, sites = 0;
+    long long ndom_total = 0;
+    uint8_t* d_species = nullptr;
+    int4* d_vac = nullptr;
+    double *d_rates = nullptr, *d_R = nullptr, *d_E = nullptr, *d_scratch = nullptr;
+    int* d_iscratch = nullptr;
+    int* d_vstart = nullptr;
+    double* d_clock = nullptr;
+    long long* d_nev = nullptr;
+    int* d_term = nullptr;
+    int *d_dmin = nullptr, *d_head = nullptr, *d_next = nullptr, *d_members = nullptr, *d_rows = nullptr;
+    Segment* d_segs = nullptr;
+    uint8_t* d_mactive = nullptr;
+    DevCounters* d_ctr = nullptr;
+    DevCounters* h_ctr = nullptr;     // pinned
+    double* d_mlp = nullptr;
+    float* d_W1p = nullptr;
+    double* d_b1p = nullptr;
+    __half* d_Bimg = nullptr;
+    float *d_b2 = nullptr, *d_W3 = nullptr, *d_b3 = nullptr;
+    float w2_unscale = 1.0f;
+    unsigned long long* d_overflow = nullptr;
+    int profile = 0;
+    std::vector<cudaEvent_t> ev;      // pairs
+    size_t ev_used = 0;
+    akmc_counters total{};
+    int64_t sweep = 0;
+    std::string err;
+};
+
+namespace {
+
+int fail(akmc_handle* h, int code, const std::string& msg)
+{
+    if (h) h->err = msg; else g_init_error = msg;
+    return code;
+}
+
+#define CK(h, x)                                                                                            \
+    do {                                                                                                    \
+        cudaError_t e_ = (x);                                                                               \
+        if (e_ != cudaSuccess) return fail(h, AKMC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+inline unsigned blocks_for(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+void free_all(akmc_handle* h)
+{
+    void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
+                    h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_rows,
+                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_W1p, h->d_b1p, h->d_Bimg, h->d_b2,
+                    h->d_W3, h->d_b3, h->d_overflow};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->h_ctr) cudaFreeHost(h->h_ctr);
+    for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+}
+
+int validate(const akmc_config* c, const double* eps, const double* E0, const double* mlp, std::string& why)
+{
+    for (int a = 0; a < 3; ++a)
+        if (c->cells[a] < 4 || (c->cells[a] & 1)) { why = "cells must be even and >= 4 (S:30)"; return AKMC_ERR_INVALID; }
+    if (c->n_voxels < 1) { why = "n_voxels must be >= 1"; return AKMC_ERR_INVALID; }
+    if (c->n_species != kSpecies) { why = "n_species must be 7 (Fe Cu Ni Mn Si P V)"; return AKMC_ERR_INVALID; }
+    if (!(c->temperature_K > 0.0) || !std::isfinite(c->temperature_K)) { why = "temperature must be > 0 (S:154)"; return AKMC_ERR_INVALID; }
+    if (!(c->nu0 > 0.0) || !std::isfinite(c->nu0) || !(c->kB > 0.0) || !std::isfinite(c->kB)) { why = "nu0 and kB must be > 0"; return AKMC_ERR_INVALID; }
+    if (c->barrier_model != AKMC_MODEL_PAIR && c->barrier_model != AKMC_MODEL_MLP) { why = "unknown barrier_model"; return AKMC_ERR_INVALID; }
+    if (c->precision != AKMC_PREC_FP64 && c->precision != AKMC_PREC_FP32) { why = "unknown precision"; return AKMC_ERR_INVALID; }
+    const bool sub = c->domain_cells[0] || c->domain_cells[1] || c->domain_cells[2];
+    if (sub) {
+        for (int a = 0; a < 3; ++a) {
+            const int D = c->domain_cells[a];
+            if (D < 6 || (D & 1) || c->cells[a] % D) { why = "domain_cells must be even, >= 6 and divide cells (sector >= 3 cells, A20)"; return AKMC_ERR_INVALID; }
+        }
+        if (!(c->window_s > 0.0) || !std::isfinite(c->window_s)) { why = "window_s must be > 0 in sublattice mode"; return AKMC_ERR_INVALID; }
+    }
+    const int grid = c->gpu_grid[0] * c->gpu_grid[1] * c->gpu_grid[2];
+    if (c->gpu_grid[0] < 1 || c->gpu_grid[1] < 1 || c->gpu_grid[2] < 1 || c->world != grid) { why = "world must equal prod(gpu_grid)"; return AKMC_ERR_INVALID; }
+    if (c->world != 1 || c->rank != 0) { why = "this build runs one rank per problem (world == 1); shard voxels over ranks instead"; return AKMC_ERR_INVALID; }
+    if (c->barrier_model == AKMC_MODEL_PAIR) {
+        if (!eps || !E0) { why = "pair model needs eps and E0"; return AKMC_ERR_INVALID; }
+        for (int s = 0; s < 2; ++s)
+            for (int a = 0; a < kSpecies; ++a)
+                for (int b = 0; b < kSpecies; ++b) {
+                    const double x = eps[(s * kSpecies + a) * kSpecies + b];
+                    if (!std::isfinite(x)) { why = "non-finite eps"; return AKMC_ERR_INVALID; }
+                    if (x != eps[(s * kSpecies + b) * kSpecies + a]) { why = "eps not symmetric (S:115)"; return AKMC_ERR_INVALID; }
+                }
+        for (int a = 0; a < kSpecies; ++a)
+            if (!std::isfinite(E0[a])) { why = "non-finite E0"; return AKMC_ERR_INVALID; }
+    } else {
+        if (!mlp) { why = "MLP model needs weights"; return AKMC_ERR_INVALID; }
+        const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
+        for (size_t i = 0; i < n; ++i)
+            if (!std::isfinite(mlp[i])) { why = "non-finite MLP weight"; return AKMC_ERR_INVALID; }
+    }
+    return AKMC_OK;
+}
+
+// fast-mode weight preparation
+int prepare_fast_weights(akmc_handle* h, const double* mlp)
+{
+    const double* W1 = mlp;
+    const double* b1 = W1 + 448 * kHid;
+    const double* W2 = b1 + kHid;
+    const double* b2 = W2 + kHid * kHid;
+    const double* W3 = b2 + kHid;
+    const double* b3 = W3 + kHid * 8;
+    std::vector<float> W1p((size_t)448 * kHid);
+    std::vector<double> b1p(kHid);
+    for (int j = 0; j < kHid; ++j) {
+        double acc = b1[j];
+        for (int s = 0; s < kWin; ++s) acc += W1[(size_t)(kSpecies * s + kFe) * kHid + j];
+        b1p[j] = acc;
+    }
+    for (int f = 0; f < 448; ++f) {
+        const int s = f / kSpecies;
+        for (int j = 0; j < kHid; ++j)
+            W1p[(size_t)f * kHid + j] = (float)(W1[(size_t)f * kHid + j] - W1[(size_t)(kSpecies * s + kFe) * kHid + j]);
+    }
+    double mx = 0.0;
+    for (int i = 0; i < kHid * kHid; ++i) mx = std::max(mx, std::fabs(W2[i]));
+    int sb = 0;
+    if (mx > 0.0) sb = 13 - (int)std::ceil(std::log2(mx));
+    const double scale = std::ldexp(1.0, sb);
+    h->w2_unscale = (float)std::ldexp(1.0, -sb);
+    std::vector<__half> img((size_t)kNChunks * kStageBytes / 2);
+    uint8_t* base = reinterpret_cast<uint8_t*>(img.data());
+    for (int c = 0; c < kNChunks; ++c)
+        for (int kl = 0; kl < kKChunk; ++kl)
+            for (int n = 0; n < kHid; ++n) {
+                const int k = c * kKChunk + kl;
+                const double w = W2[(size_t)k * kHid + n] * scale;    // B[n][k] = W2[k][n]
+                const __half hi = __float2half_rn((float)w);
+                const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
+                const size_t off = ((size_t)(kl / 8) * (kHid / 8) + n / 8) * 128 + (n % 8) * 16 + (kl % 8) * 2;
+                *reinterpret_cast<__half*>(base + (size_t)c * kStageBytes + off) = hi;
+                *reinterpret_cast<__half*>(base + (size_t)c * kStageBytes + kSplitBytes + off) = lo;
+            }
+    std::vector<float> b2f(kHid), W3f(kHid * 8), b3f(8);
+    for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
+    for (int i = 0; i < kHid * 8; ++i) W3f[i] = (float)W3[i];
+    for (int i = 0; i < 8; ++i) b3f[i] = (float)b3[i];
+    CK(h, cudaMalloc(&h->d_W1p, W1p.size() * 4));
+    CK(h, cudaMalloc(&h->d_b1p, kHid * 8));
+    CK(h, cudaMalloc(&h->d_Bimg, img.size() * 2));
+    CK(h, cudaMalloc(&h->d_b2, kHid * 4));
+    CK(h, cudaMalloc(&h->d_W3, kHid * 8 * 4));
+    CK(h, cudaMalloc(&h->d_b3, 8 * 4));
+    CK(h, cudaMemcpy(h->d_W1p, W1p.data(), W1p.size() * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b1p, b1p.data(), kHid * 8, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_W3, W3f.data(), kHid * 8 * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b3, b3f.data(), 8 * 4, cudaMemcpyHostToDevice));
+    CK(h, mlp_tc_setup());
+    return AKMC_OK;
+}
+
+// evaluate rows -> rates/R/E with the handle's model at `prec`
+int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_host, int max_rows,
+              const uint8_t* windows, int prec, double* rates, double* R, double* E)
+{
+    if (max_rows <= 0) return AKMC_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+        if (h->ev_used + 2 > h->ev.size()) {
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                CK(h, cudaEventCreate(&e));
+                h->ev.push_back(e);
+            }
+        }
+        e0 = h->ev[h->ev_used++];
+        e1 = h->ev[h->ev_used++];
+        CK(h, cudaEventRecord(e0, h->stream));
+    }
+    if (h->cfg.barrier_model == AKMC_MODEL_PAIR) {
+        eval_pair_kernel<<<blocks_for(max_rows, 128), 128, 0, h->stream>>>(
+            h->d_species, h->d_vac, windows, h->F, h->G, h->P, rows, nrows_dev, nrows_host, rates, R, E, h->d_ctr);
+        CK(h, cudaGetLastError());
+    } else if (prec == AKMC_PREC_FP64) {
+        eval_mlp_fp64_kernel<<<max_rows, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
+                                                               h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
+        CK(h, cudaGetLastError());
+    } else {
+        MlpTcParams p{};
+        p.species = h->d_species; p.vac = h->d_vac; p.windows = windows; p.F = h->F; p.G = h->G;
+        p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
+        p.W1p = h->d_W1p; p.b1p = h->d_b1p; p.Bimg = h->d_Bimg; p.b2 = h->d_b2; p.W3 = h->d_W3; p.b3 = h->d_b3;
+        p.w2_unscale = h->w2_unscale; p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
+        CK(h, launch_mlp_tc(p, max_rows, h->stream));
+    }
+    h->total.kernel_launches += 1;
+    h->total.mlp_launches += 1;
+    if (h->profile) CK(h, cudaEventRecord(e1, h->stream));
+    return AKMC_OK;
+}
+
+int harvest_events(akmc_handle* h)
+{
+    if (!h->profile) return AKMC_OK;
+    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+        float ms = 0.f;
+        CK(h, cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+        h->total.mlp_ms += ms;
+    }
+    h->ev_used = 0;
+    return AKMC_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* akmc_version(void) { return "akmc-b200 0.1 sm_100a"; }
+
+const char* akmc_last_error(const akmc_handle* h) { return h ? h->err.c_str() : g_init_error.c_str(); }
+
+int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps, const double* E0, const double* mlp,
+              akmc_handle** out)
+{
+    g_init_error.clear();
+    if (!cfg || !species || !out) return fail(nullptr, AKMC_ERR_INVALID, "null argument");
+    std::string why;
+    int rc = validate(cfg, eps, E0, mlp, why);
+    if (rc != AKMC_OK) return fail(nullptr, rc, why);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, AKMC_ERR_CUDA, "no CUDA device available (the AKMC path has no CPU fallback)");
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, AKMC_ERR_CUDA, "device is not sm_100 (B200); this library is built for sm_100a only");
+
+    akmc_handle* h = new akmc_handle();
+    h->cfg = *cfg;
+    h->dev = dev;
+    h->sub = cfg->domain_cells[0] != 0;
+    h->nvox = cfg->n_voxels;
+    for (int a = 0; a < 3; ++a) h->F.L[a] = cfg->cells[a];
+    h->F.sites = 2LL * cfg->cells[0] * cfg->cells[1] * cfg->cells[2];
+    h->sites = h->F.sites * cfg->n_voxels;
+    if (!build_geometry(h->G)) { delete h; return fail(nullptr, AKMC_ERR_RUNTIME, "geometry table construction failed"); }
+    // physical parameters
+    if (eps) {
+        for (int s = 0; s < 2; ++s)
+            for (int X = 0; X < kSpecies; ++X)
+                for (int y = 0; y < kSpecies; ++y) {
+                    const double* e = eps + s * kSpecies * kSpecies;
+                    const double d = e[X * kSpecies + y] - e[kVac * kSpecies + y];
+                    const double dfe = e[X * kSpecies + kFe] - e[kVac * kSpecies + kFe];
+                    h->P.Dp[s][X][y] = d - dfe;
+                }
+    }
+    for (int a = 0; a < kSpecies; ++a) h->P.E0[a] = E0 ? E0[a] : 0.0;
+    h->P.kT = cfg->kB * cfg->temperature_K;
+    h->P.nu0 = cfg->nu0;
+
+    // vacancy registry: slots = vacancies in ascending global site order
+    std::vector<int4> vac;
+    std::vector<int> vstart(h->nvox + 1, 0);
+    for (int64_t i = 0; i < h->sites; ++i) {
+        const uint8_t s = species[i];
+        if (s == kVac) {
+            const int v = (int)(i / h->F.sites);
+            const int64_t li = i - (int64_t)v * h->F.sites;
+            const int b = (int)(li & 1);
+            const int64_t cell = li >> 1;
+            const int x = (int)(cell % cfg->cells[0]);
+            const int y = (int)((cell / cfg->cells[0]) % cfg->cells[1]);
+            const int z = (int)(cell / ((int64_t)cfg->cells[0] * cfg->cells[1]));
+            vac.push_back(make_int4(v, 2 * x + b, 2 * y + b, 2 * z + b));
+            vstart[v + 1] += 1;
+        } else if (s > kVac) {
+            delete h;
+            return fail(nullptr, AKMC_ERR_INVALID, "species code > 6 at site " + std::to_string(i));
+        }
+    }
+    for (int v = 0; v < h->nvox; ++v) vstart[v + 1] += vstart[v];
+    h->nvac = (int64_t)vac.size();
+    if ((double)h->nvac > 0.01 * (double)h->sites) { delete h; return fail(nullptr, AKMC_ERR_INVALID, "vacancies exceed 1% of sites (S:48)"); }
+    if (h->nvac > INT32_MAX / 8) { delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies"); }
+
+#define CKI(x)                                                                                                \
+    do {                                                                                                      \
+        cudaError_t e_ = (x);                                                                                 \
+        if (e_ != cudaSuccess) {                                                                              \
+            std::string m_ = std::string(#x) + ": " + cudaGetErrorString(e_);                               \
+            free_all(h); delete h;                                                                            \
+            return fail(nullptr, AKMC_ERR_CUDA, m_);                                                          \
+        }                                                                                                     \
+    } while (0)
+
+    CKI(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    const size_t nv = (size_t)std::max<int64_t>(h->nvac, 1);
+    CKI(cudaMalloc(&h->d_species, (size_t)h->sites));
+    CKI(cudaMemcpy(h->d_species, species, (size_t)h->sites, cudaMemcpyHostToDevice));
+    CKI(cudaMalloc(&h->d_vac, nv * sizeof(int4)));
+    if (h->nvac) CKI(cudaMemcpy(h->d_vac, vac.data(), vac.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CKI(cudaMalloc(&h->d_rates, nv * 8 * sizeof(double)));
+    CKI(cudaMalloc(&h->d_E, nv * 8 * sizeof(double)));
+    CKI(cudaMalloc(&h->d_R, nv * sizeof(double)));
+    CKI(cudaMalloc(&h->d_scratch, (4 * nv + 64) * sizeof(double)));
+    CKI(cudaMalloc(&h->d_iscratch, (nv + 16) * sizeof(int)));
+    CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
+    CKI(cudaMemcpy(h->d_vstart, vstart.data(), (h->nvox + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CKI(cudaMalloc(&h->d_clock, h->nvox * sizeof(double)));
+    CKI(cudaMemset(h->d_clock, 0, h->nvox * sizeof(double)));
+    CKI(cudaMalloc(&h->d_nev, h->nvox * sizeof(long long)));
+    CKI(cudaMemset(h->d_nev, 0, h->nvox * sizeof(long long)));
+    CKI(cudaMalloc(&h->d_term, h->nvox * sizeof(int)));
+    CKI(cudaMemset(h->d_term, 0, h->nvox * sizeof(int)));
+    CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
+    CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
+    CKI(cudaMallocHost(&h->h_ctr, sizeof(DevCounters)));
+    CKI(cudaMalloc(&h->d_overflow, sizeof(unsigned long long)));
+    CKI(cudaMemset(h->d_overflow, 0, sizeof(unsigned long long)));
+    if (h->sub) {
+        for (int a = 0; a < 3; ++a) {
+            h->S.D[a] = cfg->domain_cells[a];
+            h->S.ND[a] = cfg->cells[a] / cfg->domain_cells[a];
+        }
+        h->S.ndom_vox = (long long)h->S.ND[0] * h->S.ND[1] * h->S.ND[2];
+        h->S.window = cfg->window_s;
+        h->S.seed = cfg->seed;
+        h->ndom_total = h->S.ndom_vox * h->nvox;
+        if (h->ndom_total >= 0xFFFFFFFFll) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many domains for 32-bit domain ids (A16)"); }
+        CKI(cudaMalloc(&h->d_dmin, h->ndom_total * sizeof(int)));
+        CKI(cudaMalloc(&h->d_head, h->ndom_total * sizeof(int)));
+        fill_int_kernel<<<blocks_for(h->ndom_total, 256), 256, 0, h->stream>>>(h->d_dmin, h->ndom_total, INT_MAX);
+        fill_int_kernel<<<blocks_for(h->ndom_total, 256), 256, 0, h->stream>>>(h->d_head, h->ndom_total, -1);
+        CKI(cudaGetLastError());
+        CKI(cudaMalloc(&h->d_next, nv * sizeof(int)));
+        CKI(cudaMalloc(&h->d_members, nv * sizeof(int)));
+        CKI(cudaMalloc(&h->d_rows, nv * sizeof(int)));
+        CKI(cudaMalloc(&h->d_segs, nv * sizeof(Segment)));
+        CKI(cudaMalloc(&h->d_mactive, nv));
+    }
+    if (cfg->barrier_model == AKMC_MODEL_MLP) {
+        const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
+        CKI(cudaMalloc(&h->d_mlp, n * sizeof(double)));
+        CKI(cudaMemcpy(h->d_mlp, mlp, n * sizeof(double), cudaMemcpyHostToDevice));
+        rc = prepare_fast_weights(h, mlp);
+        if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
+    }
+    CKI(cudaStreamSynchronize(h->stream));
+#undef CKI
+    *out = h;
+    return AKMC_OK;
+}
+
+int akmc_set_stream(akmc_handle* h, void* stream)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+    return AKMC_OK;
+}
+
+int akmc_set_profiling(akmc_handle* h, int32_t profile)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    h->profile = profile ? 1 : 0;
+    return AKMC_OK;
+}
+
+static int step_serial(akmc_handle* h, int64_t n)
+{
+    const int nv = (int)h->nvac;
+    for (int64_t it = 0; it < n; ++it) {
+        int rc = eval_rows(h, nullptr, nullptr, nv, nv, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
+        if (rc != AKMC_OK) return rc;
+        select_serial_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(
+            h->d_species, h->d_vac, h->F, h->G, h->nvox, h->d_vstart, h->d_rates, h->d_R, h->d_scratch, h->d_clock,
+            h->d_nev, h->d_term, h->cfg.seed, h->d_ctr);
+        CK(h, cudaGetLastError());
+        h->total.kernel_launches += 1;
+        h->total.iterations += 1;
+    }
+    return AKMC_OK;
+}
+
+static int step_sublattice(akmc_handle* h, int64_t n)
+{
+    const int nv = (int)h->nvac;
+    const size_t off_nseg = offsetof(DevCounters, nseg);
+    for (int64_t sw = 0; sw < n; ++sw) {
+        int perm[8];
+        sector_permutation(h->cfg.seed, h->sweep, perm);
+        for (int q = 0; q < 8; ++q) {
+            h->S.sector = perm[q];
+            h->S.phase = 8 * h->sweep + q;
+            // reset nseg and total
+            CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + off_nseg, 0, 2 * sizeof(unsigned long long), h->stream));
+            activate_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, h->d_dmin, h->d_head, h->d_next);
+            segments_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, h->d_dmin, h->d_head,
+                                                                         h->d_next, h->d_segs, h->d_members,
+                                                                         h->d_mactive, h->d_ctr);
+            CK(h, cudaGetLastError());
+            h->total.kernel_launches += 2;
+            CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
+            CK(h, cudaStreamSynchronize(h->stream));
+            const int nseg = (int)h->h_ctr->nseg;
+            const int ntot = (int)h->h_ctr->total;
+            if (nseg == 0) continue;
+            for (;;) {
+                CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrun), 0,
+                                      sizeof(unsigned long long), h->stream));
+                CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows), 0,
+                                      sizeof(unsigned long long), h->stream));
+                rows_kernel<<<blocks_for(nseg, 128), 128, 0, h->stream>>>(h->d_segs, h->d_members, h->d_mactive,
+                                                                          h->d_rows, h->d_ctr, nseg);
+                CK(h, cudaGetLastError());
+                h->total.kernel_launches += 1;
+                const int* nrows_dev = reinterpret_cast<const int*>(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows));
+                int rc = eval_rows(h, h->d_rows, nrows_dev, 0, ntot, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
+                if (rc != AKMC_OK) return rc;
+                select_sub_kernel<<<blocks_for(nseg, 128), 128, 0, h->stream>>>(
+                    h->d_species, h->d_vac, h->F, h->G, h->S, h->d_segs, h->d_members, h->d_mactive, h->d_rates,
+                    h->d_R, h->d_scratch, h->d_iscratch, h->d_ctr, nseg);
+                CK(h, cudaGetLastError());
+                h->total.kernel_launches += 1;
+                h->total.iterations += 1;
+                CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
+                CK(h, cudaStreamSynchronize(h->stream));
+                if (h->h_ctr->nrun == 0) break;
+            }
+        }
+        add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(h->d_clock, h->nvox, h->cfg.window_s);
+        CK(h, cudaGetLastError());
+        h->total.kernel_launches += 1;
+        h->sweep += 1;
+        h->total.sweeps += 1;
+    }
+    return AKMC_OK;
+}
+
+int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (n < 0) return fail(h, AKMC_ERR_INVALID, "n must be >= 0");
+    const akmc_counters before = h->total;
+    CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    const DevCounters c0 = *h->h_ctr;
+    const auto t0 = std::chrono::steady_clock::now();
+    int rc = h->sub ? step_sublattice(h, n) : step_serial(h, n);
+    if (rc != AKMC_OK) return rc;
+    CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    rc = harvest_events(h);
+    if (rc != AKMC_OK) return rc;
+    const DevCounters c1 = *h->h_ctr;
+    const auto t1 = std::chrono::steady_clock::now();
+    h->total.events += (int64_t)(c1.events - c0.events);
+    h->total.hop_evals += (int64_t)(c1.hop_evals - c0.hop_evals);
+    h->total.mlp_rows += (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
+    h->total.clamps += (int64_t)(c1.clamps - c0.clamps);
+    h->total.terminal_voxels += (int64_t)(c1.terminal - c0.terminal);
+    h->total.wall_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (ctr) {
+        akmc_counters d{};
+        d.events = h->total.events - before.events;
+        d.hop_evals = h->total.hop_evals - before.hop_evals;
+        d.iterations = h->total.iterations - before.iterations;
+        d.clamps = h->total.clamps - before.clamps;
+        d.terminal_voxels = h->total.terminal_voxels - before.terminal_voxels;
+        d.sweeps = h->total.sweeps - before.sweeps;
+        d.kernel_launches = h->total.kernel_launches - before.kernel_launches;
+        d.mlp_launches = h->total.mlp_launches - before.mlp_launches;
+        d.mlp_rows = d.hop_evals / 8;
+        d.mlp_ms = h->total.mlp_ms - before.mlp_ms;
+        d.wall_ms = h->total.wall_ms - before.wall_ms;
+        *ctr = d;
+    }
+    if (c1.terminal != c0.terminal) return fail(h, AKMC_TERMINAL, "a competing set has no feasible event (S:199)");
+    return AKMC_OK;
+}
+
+int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int64_t* n_vac_inout, double* clock_s_out,
+               akmc_counters* ctr_out)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (vac_sites_out) {
+        if (!n_vac_inout || *n_vac_inout < h->nvac) return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
+    }
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (species_out) CK(h, cudaMemcpy(species_out, h->d_species, (size_t)h->sites, cudaMemcpyDeviceToHost));
+    if (vac_sites_out && h->nvac) {
+        std::vector<int4> v((size_t)h->nvac);
+        CK(h, cudaMemcpy(v.data(), h->d_vac, v.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < h->nvac; ++i) {
+            const int4 p = v[(size_t)i];
+            const int64_t cell = (int64_t)(p.y >> 1) + (int64_t)h->F.L[0] * ((int64_t)(p.z >> 1) + (int64_t)h->F.L[1] * (int64_t)(p.w >> 1));
+            vac_sites_out[i] = (int64_t)p.x * h->F.sites + 2 * cell + (p.y & 1);
+        }
+    }
+    if (n_vac_inout) *n_vac_inout = h->nvac;
+    if (clock_s_out) CK(h, cudaMemcpy(clock_s_out, h->d_clock, h->nvox * sizeof(double), cudaMemcpyDeviceToHost));
+    if (ctr_out) *ctr_out = h->total;
+    return AKMC_OK;
+}
+
+int akmc_rates(akmc_handle* h, double* rates_out, double* barriers_out)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    const int nv = (int)h->nvac;
+    if (nv == 0) return AKMC_OK;
+    int rc = eval_rows(h, nullptr, nullptr, nv, nv, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
+    if (rc != AKMC_OK) return rc;
+    CK(h, cudaStreamSynchronize(h->stream));
+    rc = harvest_events(h);
+    if (rc != AKMC_OK) return rc;
+    if (rates_out) CK(h, cudaMemcpy(rates_out, h->d_rates, (size_t)nv * 8 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (barriers_out) CK(h, cudaMemcpy(barriers_out, h->d_E, (size_t)nv * 8 * sizeof(double), cudaMemcpyDeviceToHost));
+    return AKMC_OK;
+}
+
+int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t precision, double* E_out)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (n < 0 || n > (1 << 26) || !windows || !E_out) return fail(h, AKMC_ERR_INVALID, "bad window batch");
+    if (precision != AKMC_PREC_FP64 && precision != AKMC_PREC_FP32) return fail(h, AKMC_ERR_INVALID, "unknown precision");
+    for (int64_t i = 0; i < n * kWin; ++i)
+        if (windows[i] > kVac) return fail(h, AKMC_ERR_INVALID, "species code > 6 in window");
+    if (n == 0) return AKMC_OK;
+    uint8_t* d_w = nullptr;
+    double* d_e = nullptr;
+    CK(h, cudaMalloc(&d_w, (size_t)n * kWin));
+    CK(h, cudaMalloc(&d_e, (size_t)n * 8 * sizeof(double)));
+    CK(h, cudaMemcpy(d_w, windows, (size_t)n * kWin, cudaMemcpyHostToDevice));
+    int rc = eval_rows(h, nullptr, nullptr, (int)n, (int)n, d_w, precision, nullptr, nullptr, d_e);
+    if (rc == AKMC_OK) {
+        cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e == cudaSuccess) e = cudaMemcpy(E_out, d_e, (size_t)n * 8 * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = fail(h, AKMC_ERR_CUDA, std::string("eval_windows: ") + cudaGetErrorString(e));
+        else rc = harvest_events(h);
+    }
+    cudaFree(d_w);
+    cudaFree(d_e);
+    return rc;
+}
+
+void akmc_free(akmc_handle* h)
+{
+    if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+}
+
+} // extern "C"

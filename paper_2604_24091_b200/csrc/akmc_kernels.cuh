@@ -1,0 +1,378 @@
+// akmc_kernels.cuh -- FP64 evaluation, BKL selection/apply and sublattice bookkeeping kernels.
+//
+// Steps of SURVEY sec. 8(a): a1 activation/compaction, a2+a3 gather/encode (FP64 paths),
+// a4' pair KRA / a4 FP64 MLP (verify precision), a5 rates, a6 per-domain pairwise tree + Philox
+// draw, a7 apply, a10 serial/voxel-batch variant.  Operation order = DESIGN.md sec. 5.
+#pragma once
+#include <climits>
+#include "akmc_device.cuh"
+
+namespace akmc {
+
+struct DevCounters {                 // device-side counters (unsigned long long for atomics)
+    unsigned long long events, hop_evals, clamps, terminal, nrun, nseg, total, nrows;
+};
+
+// ------------------------------------------------------------------ window gather
+__device__ __forceinline__ void gather_window(const uint8_t* __restrict__ species, const Frame& F, const GeomTables& G,
+                                              const int4& v, uint8_t (&w)[kWin])
+{
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
+}
+
+// ------------------------------------------------------------------ pair KRA, FP64 (thread per row)
+__global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4* __restrict__ vac,
+                                 const uint8_t* __restrict__ windows, Frame F, GeomTables G, PhysParams P,
+                                 const int* __restrict__ rows, const int* __restrict__ nrows_dev, int nrows_host,
+                                 double* __restrict__ rates, double* __restrict__ Rsum, double* __restrict__ Eout,
+                                 DevCounters* ctr)
+{
+    const int nrows = nrows_dev ? *nrows_dev : nrows_host;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nrows) return;
+    uint8_t w[kWin];
+    int slot;
+    if (windows) {
+        slot = g;
+#pragma unroll
+        for (int j = 0; j < kWin; ++j) w[j] = windows[(size_t)g * kWin + j];
+    } else {
+        slot = rows ? rows[g] : g;
+        gather_window(species, F, G, vac[slot], w);
+    }
+    double R = 0.0;
+    int clamps = 0;
+#pragma unroll
+    for (int k = 0; k < kHops; ++k) {
+        double E = 0.0, Gk = 0.0;
+        if (w[k] != kVac) {
+            clamps += pair_barrier(w, k, G, P, E);
+            Gk = arrhenius(E, P);
+        }
+        R = __dadd_rn(R, Gk);
+        if (rates) rates[(size_t)slot * 8 + k] = Gk;
+        if (Eout) Eout[(size_t)slot * 8 + k] = E;
+    }
+    if (Rsum) Rsum[slot] = R;
+    if (clamps && ctr) atomicAdd(&ctr->clamps, (unsigned long long)clamps);
+}
+
+// ------------------------------------------------------------------ MLP, FP64 (block of 256 per row)
+// layer 1 as the embedding bag over the 64 one-hot rows in slot order (== dense fma loop, A8)
+__global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
+    const uint8_t* __restrict__ species, const int4* __restrict__ vac, const uint8_t* __restrict__ windows, Frame F,
+    GeomTables G, PhysParams P, const double* __restrict__ mlp, const int* __restrict__ rows,
+    const int* __restrict__ nrows_dev, int nrows_host, double* __restrict__ rates, double* __restrict__ Rsum,
+    double* __restrict__ Eout)
+{
+    const int nrows = nrows_dev ? *nrows_dev : nrows_host;
+    const int g = blockIdx.x;
+    if (g >= nrows) return;
+    __shared__ uint8_t w[kWin];
+    __shared__ double h1[kHid];
+    __shared__ double h2[kHid];
+    __shared__ double Ek[8];
+    __shared__ int slot_s;
+    const int j = threadIdx.x;
+    if (j == 0) slot_s = windows ? g : (rows ? rows[g] : g);
+    __syncthreads();
+    const int slot = slot_s;
+    if (j < kWin) {
+        if (windows) {
+            w[j] = windows[(size_t)g * kWin + j];
+        } else {
+            const int4 v = vac[slot];
+            w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
+        }
+    }
+    __syncthreads();
+    const double* W1 = mlp;
+    const double* b1 = W1 + 448 * kHid;
+    const double* W2 = b1 + kHid;
+    const double* b2 = W2 + kHid * kHid;
+    const double* W3 = b2 + kHid;
+    const double* b3 = W3 + kHid * 8;
+    double acc = b1[j];
+    for (int s = 0; s < kWin; ++s) acc = __dadd_rn(acc, W1[(size_t)(kSpecies * s + w[s]) * kHid + j]);
+    h1[j] = acc > 0.0 ? acc : 0.0;
+    __syncthreads();
+    acc = b2[j];
+    for (int i = 0; i < kHid; ++i) acc = __fma_rn(h1[i], W2[(size_t)i * kHid + j], acc);
+    h2[j] = acc > 0.0 ? acc : 0.0;
+    __syncthreads();
+    if (j < 8) {
+        acc = b3[j];
+        for (int i = 0; i < kHid; ++i) acc = __fma_rn(h2[i], W3[i * 8 + j], acc);
+        Ek[j] = acc > 0.0 ? acc : 0.0;
+    }
+    __syncthreads();
+    if (j == 0) {
+        double R = 0.0;
+        for (int k = 0; k < kHops; ++k) {
+            const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], P) : 0.0;
+            R = __dadd_rn(R, Gk);
+            if (rates) rates[(size_t)slot * 8 + k] = Gk;
+            if (Eout) Eout[(size_t)slot * 8 + k] = Ek[k];
+        }
+        if (Rsum) Rsum[slot] = R;
+    }
+}
+
+// ------------------------------------------------------------------ canonical pairwise tree (A17)
+// leaves buf[0..n) (already written); pads to P = 2^ceil(log2 n) with 0; node = left + right.
+__device__ __forceinline__ double tree_build(double* buf, int n, int& P, int& nlev)
+{
+    P = 1; nlev = 0;
+    while (P < n) { P <<= 1; ++nlev; }
+    for (int i = n; i < P; ++i) buf[i] = 0.0;
+    int off = 0, width = P;
+    while (width > 1) {
+        for (int i = 0; i < width / 2; ++i) buf[off + width + i] = __dadd_rn(buf[off + 2 * i], buf[off + 2 * i + 1]);
+        off += width;
+        width >>= 1;
+    }
+    return buf[off];
+}
+
+// descend: go left if r < L else r -= L; guard: a zero leaf -> last positive leaf
+__device__ __forceinline__ int tree_descend(const double* buf, int n, int P, int nlev, double& r)
+{
+    int idx = 0;
+    for (int l = nlev; l >= 1; --l) {
+        // offset of level (l-1): sum_{j < l-1} P >> j
+        int off = 0;
+        for (int jj = 0; jj < l - 1; ++jj) off += P >> jj;
+        const double left = buf[off + 2 * idx];
+        if (r < left) {
+            idx = 2 * idx;
+        } else {
+            r = __dsub_rn(r, left);
+            idx = 2 * idx + 1;
+        }
+    }
+    if (idx >= n || !(buf[idx] > 0.0)) {
+        int last = -1;
+        for (int i = 0; i < n; ++i)
+            if (buf[i] > 0.0) last = i;
+        idx = last;
+    }
+    return idx;
+}
+
+// first k with r < cumsum_k (sequential), guard: last k with Gamma > 0
+__device__ __forceinline__ int pick_hop(const double* G8, double r)
+{
+    double cs = 0.0;
+    for (int k = 0; k < kHops; ++k) {
+        cs = __dadd_rn(cs, G8[k]);
+        if (r < cs) return k;
+    }
+    int last = -1;
+    for (int k = 0; k < kHops; ++k)
+        if (G8[k] > 0.0) last = k;
+    return last;
+}
+
+// swap vacancy <-> atom at hop k; returns the new position
+__device__ __forceinline__ int4 apply_hop(uint8_t* species, int4* vac, int slot, int k, const Frame& F, const GeomTables& G)
+{
+    const int4 v = vac[slot];
+    int4 n = v;
+    n.y = wrap2(v.y + G.off[k][0], 2 * F.L[0]);
+    n.z = wrap2(v.z + G.off[k][1], 2 * F.L[1]);
+    n.w = wrap2(v.w + G.off[k][2], 2 * F.L[2]);
+    const int64_t sv = site_of(F, v.x, v.y, v.z, v.w);
+    const int64_t sn = site_of(F, n.x, n.y, n.z, n.w);
+    const uint8_t t = species[sv];
+    species[sv] = species[sn];
+    species[sn] = t;
+    vac[slot] = n;
+    return n;
+}
+
+// ------------------------------------------------------------------ serial BKL (a10): thread per voxel
+__global__ void select_serial_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, int nvox,
+                                     const int* __restrict__ vstart, const double* __restrict__ rates,
+                                     const double* __restrict__ Rsum, double* scratch, double* clock,
+                                     long long* nev, int* term, uint64_t seed, DevCounters* ctr)
+{
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nvox || term[v]) return;
+    const int a0 = vstart[v];
+    const int m = vstart[v + 1] - a0;
+    atomicAdd(&ctr->hop_evals, 8ull * (unsigned long long)m);
+    double* buf = scratch + 4 * (size_t)a0;     // [4*a0, 4*a0 + 4m) holds the 2P-1 tree nodes
+    for (int a = 0; a < m; ++a) buf[a] = Rsum[a0 + a];
+    int P = 1, nlev = 0;
+    const double tot = (m > 0) ? tree_build(buf, m, P, nlev) : 0.0;
+    if (!(tot > 0.0)) {
+        term[v] = 1;
+        atomicAdd(&ctr->terminal, 1ull);
+        return;
+    }
+    const unsigned long long n = (unsigned long long)nev[v];
+    double u_sel, u_t;
+    philox_uniforms(seed, make_uint4((uint32_t)n, (uint32_t)(n >> 32), (uint32_t)v, 0u), u_sel, u_t);
+    double r = __dmul_rn(u_sel, tot);
+    const int a = tree_descend(buf, m, P, nlev, r);
+    const int k = pick_hop(rates + (size_t)(a0 + a) * 8, r);
+    apply_hop(species, vac, a0 + a, k, F, G);
+    const double dt = __ddiv_rn(-det_log(u_t), tot);
+    clock[v] = __dadd_rn(clock[v], dt);
+    nev[v] = (long long)(n + 1);
+    atomicAdd(&ctr->events, 1ull);
+}
+
+// ------------------------------------------------------------------ sublattice (a1, a6-a8)
+struct SubParams {
+    int D[3];              // domain edge (cells)
+    int ND[3];             // domains per axis per voxel
+    long long ndom_vox;    // domains per voxel
+    int sector;            // active octant c
+    long long phase;       // global phase p = 8*sweep + q
+    double window;         // Delta_win
+    uint64_t seed;
+};
+
+struct Segment {
+    long long dom;
+    int off, cnt;
+    double t;
+    unsigned int it;
+    int running;
+};
+
+__device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, long long& dom, int& sec)
+{
+    const int cx = v.y >> 1, cy = v.z >> 1, cz = v.w >> 1;
+    const int dx = cx / S.D[0], dy = cy / S.D[1], dz = cz / S.D[2];
+    const int ox = (cx - dx * S.D[0]) >= (S.D[0] >> 1);
+    const int oy = (cy - dy * S.D[1]) >= (S.D[1] >> 1);
+    const int oz = (cz - dz * S.D[2]) >= (S.D[2] >> 1);
+    dom = (long long)v.x * S.ndom_vox + dx + (long long)S.ND[0] * (dy + (long long)S.ND[1] * dz);
+    sec = ox | (oy << 1) | (oz << 2);
+}
+
+__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, SubParams S, int* dmin, int* head, int* next)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nvac) return;
+    long long d; int sec;
+    dom_sector(vac[i], S, d, sec);
+    if (sec != S.sector) return;
+    atomicMin(&dmin[d], i);
+    next[i] = atomicExch(&head[d], i);
+}
+
+__global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S, int* dmin, int* head,
+                                const int* __restrict__ next, Segment* segs, int* members, uint8_t* mactive,
+                                DevCounters* ctr)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nvac) return;
+    long long d; int sec;
+    dom_sector(vac[i], S, d, sec);
+    if (sec != S.sector || dmin[d] != i) return;      // the minimum slot owns the domain
+    int cnt = 0;
+    for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
+    const int off = (int)atomicAdd(&ctr->total, (unsigned long long)cnt);
+    const int seg = (int)atomicAdd(&ctr->nseg, 1ull);
+    int c = 0;
+    for (int j = head[d]; j >= 0; j = next[j]) members[off + (c++)] = j;
+    for (int a = 1; a < cnt; ++a) {                     // insertion sort by slot id
+        const int key = members[off + a];
+        int b = a - 1;
+        while (b >= 0 && members[off + b] > key) { members[off + b + 1] = members[off + b]; --b; }
+        members[off + b + 1] = key;
+    }
+    for (int a = 0; a < cnt; ++a) mactive[off + a] = 1;
+    Segment sg;
+    sg.dom = d; sg.off = off; sg.cnt = cnt; sg.t = 0.0; sg.it = 0u; sg.running = 1;
+    segs[seg] = sg;
+    head[d] = -1;
+    dmin[d] = INT_MAX;
+}
+
+__global__ void rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
+                            const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr, int cap)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= (int)ctr->nseg || s >= cap) return;
+    const Segment sg = segs[s];
+    if (!sg.running) return;
+    for (int a = 0; a < sg.cnt; ++a)
+        if (mactive[sg.off + a]) {
+            const int r = (int)atomicAdd(&ctr->nrows, 1ull);
+            rows[r] = members[sg.off + a];
+        }
+}
+
+__global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, SubParams S, Segment* segs,
+                                  const int* __restrict__ members, uint8_t* mactive, const double* __restrict__ rates,
+                                  const double* __restrict__ Rsum, double* scratch, int* iscratch, DevCounters* ctr,
+                                  int cap)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= (int)ctr->nseg || s >= cap) return;
+    Segment sg = segs[s];
+    if (!sg.running) return;
+    double* buf = scratch + 4 * (size_t)sg.off;  // disjoint per segment: 2P-1 <= 4*cnt
+    int* idx = iscratch + sg.off;
+    int m = 0;
+    for (int a = 0; a < sg.cnt; ++a)
+        if (mactive[sg.off + a]) {
+            buf[m] = Rsum[members[sg.off + a]];
+            idx[m] = a;
+            ++m;
+        }
+    bool stop = false;
+    if (m == 0) {
+        stop = true;
+    } else {
+        atomicAdd(&ctr->hop_evals, 8ull * (unsigned long long)m);
+        int P = 1, nlev = 0;
+        const double Rd = tree_build(buf, m, P, nlev);
+        if (!(Rd > 0.0)) {
+            stop = true;
+        } else {
+            double u_sel, u_t;
+            const unsigned long long p = (unsigned long long)S.phase;
+            philox_uniforms(S.seed, make_uint4(sg.it, (uint32_t)sg.dom, (uint32_t)p, (uint32_t)(p >> 32)), u_sel, u_t);
+            const double dt = __ddiv_rn(-det_log(u_t), Rd);
+            if (__dadd_rn(sg.t, dt) > S.window) {
+                stop = true;                              // overshooting draw discarded
+            } else {
+                double r = __dmul_rn(u_sel, Rd);
+                const int leaf = tree_descend(buf, m, P, nlev, r);
+                const int a = idx[leaf];
+                const int slot = members[sg.off + a];
+                const int k = pick_hop(rates + (size_t)slot * 8, r);
+                const int4 nv = apply_hop(species, vac, slot, k, F, G);
+                long long d2; int sec2;
+                dom_sector(nv, S, d2, sec2);
+                if (d2 != sg.dom || sec2 != S.sector) mactive[sg.off + a] = 0;
+                sg.t = __dadd_rn(sg.t, dt);
+                sg.it += 1u;
+                atomicAdd(&ctr->events, 1ull);
+                atomicAdd(&ctr->nrun, 1ull);
+            }
+        }
+    }
+    if (stop) sg.running = 0;
+    segs[s] = sg;
+}
+
+__global__ void add_window_kernel(double* clock, int nvox, double w)
+{
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < nvox) clock[v] = __dadd_rn(clock[v], w);
+}
+
+__global__ void fill_int_kernel(int* p, long long n, int val)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = val;
+}
+
+} // namespace akmc

@@ -1,0 +1,192 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the FP64 CPU oracle.
+
+Bars (north star): integer lattice trajectories bit-exact in FP64 mode with the same Philox
+stream; per-hop rates of the tensor-core FP32-equivalent mode within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL_FAST = 1e-5        # north star: reduced-precision per-hop rates within 1e-5 relative
+
+
+@pytest.fixture(scope="module")
+def akmc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_24091_b200 as A
+    from paper_2604_24091_b200 import build
+    build.build()
+    return A
+
+
+def _params():
+    eps, E0 = synth.illustrative_pair_params()
+    return eps, E0
+
+
+def _ocfg(orc, acfg):
+    return orc.Config(cells=acfg.cells, n_voxels=acfg.n_voxels, T=acfg.temperature_K, nu0=acfg.nu0, kB=acfg.kB,
+                      model=acfg.barrier_model, domain=acfg.domain_cells, window_s=acfg.window_s, seed=acfg.seed)
+
+
+# ----------------------------------------------------------------------------- network evaluation
+@pytest.mark.parametrize("weights", ["random", "physics_residual"])
+def test_eval_windows_fp64_bitexact(akmc, orc, weights):
+    eps, E0 = _params()
+    mlp = synth.random_mlp(seed=3) if weights == "random" else synth.physics_mlp(eps, E0, residual=0.02, seed=4)
+    wins = synth.random_windows(1000, seed=5)
+    cfg = akmc.Config(cells=(8, 8, 8), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP64)
+    with akmc.Simulation(cfg, np.zeros(1024, np.uint8), mlp=mlp) as sim:
+        E = sim.eval_windows(wins, akmc.PREC_FP64)
+    ref = np.stack([orc.mlp_fp64(w, mlp) for w in wins])
+    assert np.array_equal(E, ref)
+
+
+@pytest.mark.parametrize("weights", ["random", "physics", "physics_residual"])
+@pytest.mark.parametrize("n", [1, 127, 128, 4096 + 77])
+def test_eval_windows_fp32_tensor_core(akmc, orc, weights, n):
+    """tcgen05 FP32-equivalent barrier network: rates within 1e-5 relative of FP64 (every hop),
+    tiles of 128 plus a ragged tail."""
+    eps, E0 = _params()
+    mlp = {"random": lambda: synth.random_mlp(seed=7),
+           "physics": lambda: synth.physics_mlp(eps, E0),
+           "physics_residual": lambda: synth.physics_mlp(eps, E0, residual=0.02, seed=8)}[weights]()
+    wins = synth.random_windows(n, seed=9 + n)
+    cfg = akmc.Config(cells=(8, 8, 8), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg, np.zeros(1024, np.uint8), mlp=mlp) as sim:
+        E32 = sim.eval_windows(wins, akmc.PREC_FP32)
+    ref = np.stack([orc.mlp_fp64(w, mlp) for w in wins])
+    kT = cfg.kB * cfg.temperature_K
+    rel = np.abs(np.expm1(-(E32 - ref) / kT))
+    assert rel.max() <= RTOL_FAST, (rel.max(), np.abs(E32 - ref).max())
+
+
+# ----------------------------------------------------------------------------- rates on lattices
+@pytest.mark.parametrize("model", ["pair", "mlp"])
+def test_rates_fp64_bitexact(akmc, orc, model):
+    eps, E0 = _params()
+    L = 16
+    sp = synth.make_lattice((L, L, L), 2, synth.a508_atomic_fractions(), 12, seed=11)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=1) if model == "mlp" else None
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=2, barrier_model=akmc.MODEL_PAIR if model == "pair" else akmc.MODEL_MLP,
+                      precision=akmc.PREC_FP64)
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        R, E = sim.rates()
+        _, vac, _, _ = sim.state(species=False)
+    oc = _ocfg(orc, cfg)
+    Ro, Eo = orc.rates(oc, sp, vac, eps, E0, mlp)
+    assert np.array_equal(R, Ro)
+    assert np.array_equal(E, Eo)
+
+
+def test_rates_fp32_lattice(akmc, orc):
+    eps, E0 = _params()
+    L = 24
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), 200, seed=12)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=2)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg, sp, mlp=mlp) as sim:
+        R, E = sim.rates()
+        _, vac, _, _ = sim.state(species=False)
+    Ro, Eo = orc.rates(_ocfg(orc, cfg), sp, vac, None, None, mlp)
+    assert np.array_equal(R == 0, Ro == 0)           # masks identical
+    m = Ro > 0
+    assert np.max(np.abs(R[m] / Ro[m] - 1)) <= RTOL_FAST
+
+
+# ----------------------------------------------------------------------------- trajectories
+def _run_both(akmc, orc, cfg, sp, n, eps=None, E0=None, mlp=None, chunks=1):
+    ost = orc.State.from_species(_ocfg(orc, cfg), sp)
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        for _ in range(chunks):
+            c = sim.step(n // chunks)
+            orc.run(_ocfg(orc, cfg), ost, n // chunks, eps, E0, mlp)
+        gsp, gvac, gclock, gctr = sim.state()
+    return ost, (gsp, gvac, gclock, gctr)
+
+
+def test_serial_C1_bitexact_1e4_steps(akmc, orc):
+    """C1: Fe-1at%Cu 16^3, 1 vacancy, 10^4 BKL steps at 563 K, pair model FP64: bit-exact."""
+    eps, E0 = _params()
+    pr = synth.preset("C1")
+    sp = synth.make_lattice(pr.cells, 1, pr.fractions, 1, seed=pr.seed)
+    cfg = akmc.Config(cells=pr.cells, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=2605)
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 10000, eps, E0, chunks=4)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0] == 10000
+    assert gctr["hop_evals"] == ost.counters[1]
+
+
+def test_serial_mlp_fp64_bitexact(akmc, orc):
+    eps, E0 = _params()
+    L = 16
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.03), 3, seed=21)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=3)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP64, seed=77)
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 600, mlp=mlp)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+
+
+def test_voxel_batch_bitexact(akmc, orc):
+    """C4-shaped (reduced): independent periodic voxels, one BKL competing set each."""
+    eps, E0 = _params()
+    L = 16
+    nvox = 12
+    sp = synth.make_lattice((L, L, L), nvox, synth.a508_atomic_fractions(), 10, seed=31)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=5)
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 300, eps, E0)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+
+
+@pytest.mark.parametrize("lam", [1.0, 0.25])
+def test_sublattice_bitexact(akmc, orc, lam):
+    """Windowed synchronous sublattice (reading A19), domains 8^3: bit-exact vs the oracle."""
+    eps, E0 = _params()
+    L = 32
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), 60, seed=41)
+    win = synth.window_seconds(lam, E0[0])
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=9,
+                      domain_cells=(8, 8, 8), window_s=win)
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 8, eps, E0, chunks=2)
+    assert ost.counters[0] > 20
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+    assert gctr["hop_evals"] == ost.counters[1]
+
+
+def test_sublattice_mlp_fp64_bitexact(akmc, orc):
+    eps, E0 = _params()
+    L = 24
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), 40, seed=42)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=6)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP64, seed=19,
+                      domain_cells=(6, 6, 6), window_s=synth.window_seconds(1.0, E0[0]))
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 3, mlp=mlp)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+
+
+def test_terminal_and_conservation(akmc):
+    L = 8
+    sp = np.zeros(2 * L ** 3, np.uint8)
+    eps, E0 = _params()
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        c = sim.step(5)
+        assert c["status"] == akmc.AKMC_TERMINAL
+        gsp, vac, clock, _ = sim.state()
+        assert np.array_equal(gsp, sp) and clock[0] == 0.0

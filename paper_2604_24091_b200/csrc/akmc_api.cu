@@ -137,7 +137,7 @@ struct akmc_handle {
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;     // pinned
     double* d_mlp = nullptr;
-    float* d_W1p = nullptr;
+    double* d_W1p = nullptr;
     double* d_b1p = nullptr;
     __half* d_Bimg = nullptr;
     float *d_b2 = nullptr, *d_W3 = nullptr, *d_b3 = nullptr;
@@ -149,6 +149,13 @@ struct akmc_handle {
     akmc_counters total{};
     int64_t sweep = 0;
     std::string err;
+    int num_sms = 148;
+    // per-sweep graph (sublattice mode): 8 phases, each with a conditional WHILE inner loop
+    PhaseInfo* d_phase = nullptr;
+    PhaseInfo* h_phase = nullptr;     // pinned
+    cudaGraphExec_t sweep_exec = nullptr;
+    cudaStream_t graph_stream = nullptr;   // stream the graph was instantiated for
+    int graph_launches_per_sweep = 0;
 };
 
 namespace {
@@ -175,6 +182,9 @@ void free_all(akmc_handle* h)
                     h->d_W3, h->d_b3, h->d_overflow};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (h->d_phase) cudaFree(h->d_phase);
+    if (h->h_phase) cudaFreeHost(h->h_phase);
+    if (h->sweep_exec) cudaGraphExecDestroy(h->sweep_exec);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -230,7 +240,7 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     const double* b2 = W2 + kHid * kHid;
     const double* W3 = b2 + kHid;
     const double* b3 = W3 + kHid * 8;
-    std::vector<float> W1p((size_t)448 * kHid);
+    std::vector<double> W1p((size_t)448 * kHid);
     std::vector<double> b1p(kHid);
     for (int j = 0; j < kHid; ++j) {
         double acc = b1[j];
@@ -240,7 +250,7 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     for (int f = 0; f < 448; ++f) {
         const int s = f / kSpecies;
         for (int j = 0; j < kHid; ++j)
-            W1p[(size_t)f * kHid + j] = (float)(W1[(size_t)f * kHid + j] - W1[(size_t)(kSpecies * s + kFe) * kHid + j]);
+            W1p[(size_t)f * kHid + j] = (W1[(size_t)f * kHid + j] - W1[(size_t)(kSpecies * s + kFe) * kHid + j]);
     }
     double mx = 0.0;
     for (int i = 0; i < kHid * kHid; ++i) mx = std::max(mx, std::fabs(W2[i]));
@@ -265,13 +275,13 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
     for (int i = 0; i < kHid * 8; ++i) W3f[i] = (float)W3[i];
     for (int i = 0; i < 8; ++i) b3f[i] = (float)b3[i];
-    CK(h, cudaMalloc(&h->d_W1p, W1p.size() * 4));
+    CK(h, cudaMalloc(&h->d_W1p, W1p.size() * 8));
     CK(h, cudaMalloc(&h->d_b1p, kHid * 8));
     CK(h, cudaMalloc(&h->d_Bimg, img.size() * 2));
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
     CK(h, cudaMalloc(&h->d_W3, kHid * 8 * 4));
     CK(h, cudaMalloc(&h->d_b3, 8 * 4));
-    CK(h, cudaMemcpy(h->d_W1p, W1p.data(), W1p.size() * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_W1p, W1p.data(), W1p.size() * 8, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b1p, b1p.data(), kHid * 8, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
@@ -300,12 +310,14 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         CK(h, cudaEventRecord(e0, h->stream));
     }
     if (h->cfg.barrier_model == AKMC_MODEL_PAIR) {
-        eval_pair_kernel<<<blocks_for(max_rows, 128), 128, 0, h->stream>>>(
+        const unsigned grid = std::min<unsigned>(blocks_for(max_rows, 128), (unsigned)h->num_sms * 16u);
+        eval_pair_kernel<<<grid, 128, 0, h->stream>>>(
             h->d_species, h->d_vac, windows, h->F, h->G, h->P, rows, nrows_dev, nrows_host, rates, R, E, h->d_ctr);
         CK(h, cudaGetLastError());
     } else if (prec == AKMC_PREC_FP64) {
-        eval_mlp_fp64_kernel<<<max_rows, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
-                                                               h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
+        const unsigned grid = std::min<unsigned>((unsigned)max_rows, (unsigned)h->num_sms * 8u);
+        eval_mlp_fp64_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
+                                                           h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
         CK(h, cudaGetLastError());
     } else {
         MlpTcParams p{};
@@ -313,7 +325,7 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
         p.W1p = h->d_W1p; p.b1p = h->d_b1p; p.Bimg = h->d_Bimg; p.b2 = h->d_b2; p.W3 = h->d_W3; p.b3 = h->d_b3;
         p.w2_unscale = h->w2_unscale; p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
-        CK(h, launch_mlp_tc(p, max_rows, h->stream));
+        CK(h, launch_mlp_tc(p, max_rows, h->num_sms, h->stream));
     }
     h->total.kernel_launches += 1;
     h->total.mlp_launches += 1;
@@ -384,31 +396,6 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     h->P.kT = cfg->kB * cfg->temperature_K;
     h->P.nu0 = cfg->nu0;
 
-    // vacancy registry: slots = vacancies in ascending global site order
-    std::vector<int4> vac;
-    std::vector<int> vstart(h->nvox + 1, 0);
-    for (int64_t i = 0; i < h->sites; ++i) {
-        const uint8_t s = species[i];
-        if (s == kVac) {
-            const int v = (int)(i / h->F.sites);
-            const int64_t li = i - (int64_t)v * h->F.sites;
-            const int b = (int)(li & 1);
-            const int64_t cell = li >> 1;
-            const int x = (int)(cell % cfg->cells[0]);
-            const int y = (int)((cell / cfg->cells[0]) % cfg->cells[1]);
-            const int z = (int)(cell / ((int64_t)cfg->cells[0] * cfg->cells[1]));
-            vac.push_back(make_int4(v, 2 * x + b, 2 * y + b, 2 * z + b));
-            vstart[v + 1] += 1;
-        } else if (s > kVac) {
-            delete h;
-            return fail(nullptr, AKMC_ERR_INVALID, "species code > 6 at site " + std::to_string(i));
-        }
-    }
-    for (int v = 0; v < h->nvox; ++v) vstart[v + 1] += vstart[v];
-    h->nvac = (int64_t)vac.size();
-    if ((double)h->nvac > 0.01 * (double)h->sites) { delete h; return fail(nullptr, AKMC_ERR_INVALID, "vacancies exceed 1% of sites (S:48)"); }
-    if (h->nvac > INT32_MAX / 8) { delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies"); }
-
 #define CKI(x)                                                                                                \
     do {                                                                                                      \
         cudaError_t e_ = (x);                                                                                 \
@@ -419,29 +406,64 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         }                                                                                                     \
     } while (0)
 
+    h->num_sms = prop.multiProcessorCount;
     CKI(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
-    const size_t nv = (size_t)std::max<int64_t>(h->nvac, 1);
     CKI(cudaMalloc(&h->d_species, (size_t)h->sites));
     CKI(cudaMemcpy(h->d_species, species, (size_t)h->sites, cudaMemcpyHostToDevice));
-    CKI(cudaMalloc(&h->d_vac, nv * sizeof(int4)));
-    if (h->nvac) CKI(cudaMemcpy(h->d_vac, vac.data(), vac.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
+    CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
+    CKI(cudaMallocHost(&h->h_ctr, sizeof(DevCounters)));
+
+    // a0: vacancy registry by a device scan; slots = vacancies in ascending global site order
+    {
+        const long long nwords = h->sites / 16;                 // sites is a multiple of 128
+        const unsigned nblk = blocks_for(nwords, kScanThreads);
+        int* d_bc = nullptr;
+        unsigned int* d_max = nullptr;
+        long long* d_tot = nullptr;
+        CKI(cudaMalloc(&d_bc, (size_t)nblk * sizeof(int)));
+        h->d_iscratch = d_bc;                                    // freed with the handle on error
+        CKI(cudaMalloc(&d_max, sizeof(unsigned int) + sizeof(long long) * 2));
+        h->d_overflow = reinterpret_cast<unsigned long long*>(d_max);
+        d_tot = reinterpret_cast<long long*>(reinterpret_cast<char*>(d_max) + 8);
+        CKI(cudaMemset(d_max, 0, sizeof(unsigned int) + sizeof(long long) * 2));
+        const uint4* sp4 = reinterpret_cast<const uint4*>(h->d_species);
+        scan_count_kernel<<<nblk, kScanThreads, 0, h->stream>>>(sp4, nwords, d_bc, d_max);
+        scan_blocks_kernel<<<1, 1024, 0, h->stream>>>(d_bc, (int)nblk, d_tot);
+        CKI(cudaGetLastError());
+        unsigned int maxcode = 0;
+        long long total = 0;
+        CKI(cudaMemcpyAsync(&maxcode, d_max, sizeof(unsigned int), cudaMemcpyDeviceToHost, h->stream));
+        CKI(cudaMemcpyAsync(&total, d_tot, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+        CKI(cudaStreamSynchronize(h->stream));
+        if (maxcode > (unsigned)kVac) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "species code > 6 in the lattice"); }
+        h->nvac = total;
+        if ((double)h->nvac > 0.01 * (double)h->sites) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "vacancies exceed 1% of sites (S:48)"); }
+        if (h->nvac > INT32_MAX / 8) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies"); }
+        CKI(cudaMalloc(&h->d_vac, (size_t)std::max<int64_t>(h->nvac, 1) * sizeof(int4)));
+        scan_write_kernel<<<nblk, kScanThreads, 0, h->stream>>>(sp4, nwords, d_bc, h->F, h->d_vac);
+        CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
+        vstart_kernel<<<blocks_for(h->nvox + 1, 128), 128, 0, h->stream>>>(h->d_vac, (int)h->nvac, h->nvox, h->d_vstart);
+        CKI(cudaGetLastError());
+        CKI(cudaStreamSynchronize(h->stream));
+        cudaFree(d_bc);
+        cudaFree(d_max);
+        h->d_iscratch = nullptr;
+        h->d_overflow = nullptr;
+    }
+    const size_t nv = (size_t)std::max<int64_t>(h->nvac, 1);
     CKI(cudaMalloc(&h->d_rates, nv * 8 * sizeof(double)));
     CKI(cudaMalloc(&h->d_E, nv * 8 * sizeof(double)));
     CKI(cudaMalloc(&h->d_R, nv * sizeof(double)));
     CKI(cudaMalloc(&h->d_scratch, (4 * nv + 64) * sizeof(double)));
     CKI(cudaMalloc(&h->d_iscratch, (nv + 16) * sizeof(int)));
-    CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
-    CKI(cudaMemcpy(h->d_vstart, vstart.data(), (h->nvox + 1) * sizeof(int), cudaMemcpyHostToDevice));
     CKI(cudaMalloc(&h->d_clock, h->nvox * sizeof(double)));
     CKI(cudaMemset(h->d_clock, 0, h->nvox * sizeof(double)));
     CKI(cudaMalloc(&h->d_nev, h->nvox * sizeof(long long)));
     CKI(cudaMemset(h->d_nev, 0, h->nvox * sizeof(long long)));
     CKI(cudaMalloc(&h->d_term, h->nvox * sizeof(int)));
     CKI(cudaMemset(h->d_term, 0, h->nvox * sizeof(int)));
-    CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
-    CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
-    CKI(cudaMallocHost(&h->h_ctr, sizeof(DevCounters)));
     CKI(cudaMalloc(&h->d_overflow, sizeof(unsigned long long)));
     CKI(cudaMemset(h->d_overflow, 0, sizeof(unsigned long long)));
     if (h->sub) {
@@ -464,6 +486,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaMalloc(&h->d_rows, nv * sizeof(int)));
         CKI(cudaMalloc(&h->d_segs, nv * sizeof(Segment)));
         CKI(cudaMalloc(&h->d_mactive, nv));
+        CKI(cudaMalloc(&h->d_phase, 8 * sizeof(PhaseInfo)));
+        CKI(cudaMallocHost(&h->h_phase, 8 * sizeof(PhaseInfo)));
     }
     if (cfg->barrier_model == AKMC_MODEL_MLP) {
         const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
@@ -509,55 +533,167 @@ static int step_serial(akmc_handle* h, int64_t n)
     return AKMC_OK;
 }
 
-static int step_sublattice(akmc_handle* h, int64_t n)
+static void phase_table(const akmc_handle* h, int64_t sweep, PhaseInfo ph[8])
+{
+    int perm[8];
+    sector_permutation(h->cfg.seed, sweep, perm);
+    for (int q = 0; q < 8; ++q) {
+        ph[q].sector = perm[q];
+        ph[q].pad = 0;
+        ph[q].phase = 8 * sweep + q;
+    }
+}
+
+struct PhaseTable8 { PhaseInfo p[8]; };
+
+__global__ void set_phase_kernel(PhaseInfo* dst, PhaseTable8 t)
+{
+    if (threadIdx.x < 8) dst[threadIdx.x] = t.p[threadIdx.x];
+}
+
+// one inner iteration (a1 rows, a2-a5 eval, a6-a7 select) on stream s; cond != 0 adds the a8 condition kernel
+static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s, bool graph,
+                             cudaGraphConditionalHandle cond)
 {
     const int nv = (int)h->nvac;
-    const size_t off_nseg = offsetof(DevCounters, nseg);
+    const unsigned gs = std::min<unsigned>(blocks_for(nv, 128), (unsigned)h->num_sms * 4u);
+    rows_kernel<<<gs, 128, 0, s>>>(h->d_segs, h->d_members, h->d_mactive, h->d_rows, h->d_ctr);
+    CK(h, cudaGetLastError());
+    const int* nrows_dev = reinterpret_cast<const int*>(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows));
+    cudaStream_t keep = h->stream;
+    h->stream = s;
+    int rc = eval_rows(h, h->d_rows, nrows_dev, 0, nv, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
+    h->stream = keep;
+    if (rc != AKMC_OK) return rc;
+    select_sub_kernel<<<gs, 128, 0, s>>>(h->d_species, h->d_vac, h->F, h->G, h->S, ph, h->d_segs, h->d_members,
+                                         h->d_mactive, h->d_rates, h->d_R, h->d_scratch, h->d_iscratch, h->d_ctr);
+    CK(h, cudaGetLastError());
+    if (graph) {
+        loop_cond_kernel<<<1, 1, 0, s>>>(h->d_ctr, cond);
+        CK(h, cudaGetLastError());
+    }
+    return AKMC_OK;
+}
+
+// Per-sweep CUDA graph: for each of the 8 phases, activate + segments, then a conditional WHILE node
+// whose body is one inner iteration (rows, eval, select, condition) -- the a8 loop runs on the device
+// with no host synchronisation; the phase table (sector permutation) is a device array updated per sweep.
+static int build_sweep_graph(akmc_handle* h)
+{
+    const int nv = (int)h->nvac;
+    cudaStream_t cs = nullptr, bs = nullptr;
+    CK(h, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(h, cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+    const int ev_profile = h->profile;
+    h->profile = 0;                                  // no event nodes inside the graph
+    int rc = AKMC_OK;
+    int launches = 0;
+    cudaGraph_t g = nullptr;
+    auto done = [&](int code) {
+        h->profile = ev_profile;
+        cudaStreamDestroy(cs);
+        cudaStreamDestroy(bs);
+        return code;
+    };
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return done(fail(h, AKMC_ERR_CUDA, "graph capture begin failed"));
+    for (int q = 0; q < 8 && rc == AKMC_OK; ++q) {
+        const PhaseInfo* ph = h->d_phase + q;
+        activate_kernel<<<blocks_for(nv, 256), 256, 0, cs>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head, h->d_next,
+                                                             h->d_ctr);
+        segments_kernel<<<blocks_for(nv, 256), 256, 0, cs>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head, h->d_next,
+                                                             h->d_segs, h->d_members, h->d_mactive, h->d_ctr);
+        launches += 2;
+        cudaStreamCaptureStatus st;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, &deps, &nd) != cudaSuccess) { rc = fail(h, AKMC_ERR_CUDA, "capture info"); break; }
+        cudaGraphConditionalHandle hc;
+        if (cudaGraphConditionalHandleCreate(&hc, cg, 1, cudaGraphCondAssignDefault) != cudaSuccess) { rc = fail(h, AKMC_ERR_CUDA, "conditional handle"); break; }
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = hc;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t cn;
+        if (cudaGraphAddNode(&cn, cg, deps, nd, &np) != cudaSuccess) { rc = fail(h, AKMC_ERR_CUDA, "conditional node"); break; }
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        if (cudaStreamUpdateCaptureDependencies(cs, &cn, 1, cudaStreamSetCaptureDependencies) != cudaSuccess) { rc = fail(h, AKMC_ERR_CUDA, "capture deps"); break; }
+        if (cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { rc = fail(h, AKMC_ERR_CUDA, "body capture"); break; }
+        rc = enqueue_iteration(h, ph, bs, true, hc);
+        cudaGraph_t bout = nullptr;
+        cudaStreamEndCapture(bs, &bout);
+        launches += 4;
+    }
+    add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, cs>>>(h->d_clock, h->nvox, h->cfg.window_s);
+    launches += 1;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+    if (rc != AKMC_OK) { if (g) cudaGraphDestroy(g); return done(rc); }
+    if (ec != cudaSuccess) return done(fail(h, AKMC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec)));
+    const cudaError_t ei = cudaGraphInstantiate(&h->sweep_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return done(fail(h, AKMC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)));
+    h->graph_launches_per_sweep = launches;
+    return done(AKMC_OK);
+}
+
+// host-stepped sublattice loop (used when profiling: CUDA events around every barrier-kernel launch)
+static int step_sublattice_host(akmc_handle* h, int64_t n)
+{
+    const int nv = (int)h->nvac;
     for (int64_t sw = 0; sw < n; ++sw) {
-        int perm[8];
-        sector_permutation(h->cfg.seed, h->sweep, perm);
+        PhaseTable8 t;
+        phase_table(h, h->sweep, t.p);
+        set_phase_kernel<<<1, 32, 0, h->stream>>>(h->d_phase, t);
+        h->total.kernel_launches += 1;
         for (int q = 0; q < 8; ++q) {
-            h->S.sector = perm[q];
-            h->S.phase = 8 * h->sweep + q;
-            // reset nseg and total
-            CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + off_nseg, 0, 2 * sizeof(unsigned long long), h->stream));
-            activate_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, h->d_dmin, h->d_head, h->d_next);
-            segments_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, h->d_dmin, h->d_head,
+            const PhaseInfo* ph = h->d_phase + q;
+            activate_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head,
+                                                                         h->d_next, h->d_ctr);
+            segments_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head,
                                                                          h->d_next, h->d_segs, h->d_members,
                                                                          h->d_mactive, h->d_ctr);
             CK(h, cudaGetLastError());
             h->total.kernel_launches += 2;
-            CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
-            CK(h, cudaStreamSynchronize(h->stream));
-            const int nseg = (int)h->h_ctr->nseg;
-            const int ntot = (int)h->h_ctr->total;
-            if (nseg == 0) continue;
             for (;;) {
+                int rc = enqueue_iteration(h, ph, h->stream, false, 0);
+                if (rc != AKMC_OK) return rc;
+                h->total.kernel_launches += 2;
+                h->total.iterations += 1;
+                CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
+                CK(h, cudaStreamSynchronize(h->stream));
+                const bool more = h->h_ctr->nrun > 0;
                 CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrun), 0,
                                       sizeof(unsigned long long), h->stream));
                 CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows), 0,
                                       sizeof(unsigned long long), h->stream));
-                rows_kernel<<<blocks_for(nseg, 128), 128, 0, h->stream>>>(h->d_segs, h->d_members, h->d_mactive,
-                                                                          h->d_rows, h->d_ctr, nseg);
-                CK(h, cudaGetLastError());
-                h->total.kernel_launches += 1;
-                const int* nrows_dev = reinterpret_cast<const int*>(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows));
-                int rc = eval_rows(h, h->d_rows, nrows_dev, 0, ntot, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
-                if (rc != AKMC_OK) return rc;
-                select_sub_kernel<<<blocks_for(nseg, 128), 128, 0, h->stream>>>(
-                    h->d_species, h->d_vac, h->F, h->G, h->S, h->d_segs, h->d_members, h->d_mactive, h->d_rates,
-                    h->d_R, h->d_scratch, h->d_iscratch, h->d_ctr, nseg);
-                CK(h, cudaGetLastError());
-                h->total.kernel_launches += 1;
-                h->total.iterations += 1;
-                CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
-                CK(h, cudaStreamSynchronize(h->stream));
-                if (h->h_ctr->nrun == 0) break;
+                if (!more) break;
             }
         }
         add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(h->d_clock, h->nvox, h->cfg.window_s);
         CK(h, cudaGetLastError());
         h->total.kernel_launches += 1;
+        h->sweep += 1;
+        h->total.sweeps += 1;
+    }
+    return AKMC_OK;
+}
+
+static int step_sublattice(akmc_handle* h, int64_t n)
+{
+    if (h->profile) return step_sublattice_host(h, n);
+    if (!h->sweep_exec) {
+        const int rc = build_sweep_graph(h);
+        if (rc != AKMC_OK) return rc;
+    }
+    for (int64_t sw = 0; sw < n; ++sw) {
+        PhaseTable8 t;
+        phase_table(h, h->sweep, t.p);
+        set_phase_kernel<<<1, 32, 0, h->stream>>>(h->d_phase, t);
+        CK(h, cudaGetLastError());
+        CK(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+        h->total.kernel_launches += 1 + h->graph_launches_per_sweep;   // body kernels counted once per phase
         h->sweep += 1;
         h->total.sweeps += 1;
     }

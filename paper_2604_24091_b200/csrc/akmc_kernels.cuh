@@ -1,8 +1,12 @@
-// akmc_kernels.cuh -- FP64 evaluation, BKL selection/apply and sublattice bookkeeping kernels.
+// akmc_kernels.cuh -- FP64 evaluation, BKL selection/apply, sublattice bookkeeping and lattice-scan
+// kernels of the B200 AKMC path.
 //
-// Steps of SURVEY sec. 8(a): a1 activation/compaction, a2+a3 gather/encode (FP64 paths),
-// a4' pair KRA / a4 FP64 MLP (verify precision), a5 rates, a6 per-domain pairwise tree + Philox
-// draw, a7 apply, a10 serial/voxel-batch variant.  Operation order = DESIGN.md sec. 5.
+// Steps of SURVEY sec. 8(a): a0 vacancy registry (device scan), a1 activation/compaction, a2+a3
+// gather/encode (FP64 paths), a4' pair KRA / a4 FP64 MLP (verify precision), a5 rates, a6 per-domain
+// pairwise tree + Philox draw, a7 apply, a8 inner loop condition, a10 serial/voxel-batch variant.
+// Operation order = DESIGN.md sec. 5.  Kernels that run inside the per-sweep CUDA graph read their
+// per-phase parameters from device memory (PhaseInfo) and their sizes from device counters, and use
+// grid-stride loops, so one graph serves every sweep.
 #pragma once
 #include <climits>
 #include "akmc_device.cuh"
@@ -21,6 +25,11 @@ __device__ __forceinline__ void gather_window(const uint8_t* __restrict__ specie
     for (int j = 0; j < kWin; ++j) w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
 }
 
+__device__ __forceinline__ int row_count(const int* nrows_dev, int nrows_host)
+{
+    return nrows_dev ? *nrows_dev : nrows_host;
+}
+
 // ------------------------------------------------------------------ pair KRA, FP64 (thread per row)
 __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4* __restrict__ vac,
                                  const uint8_t* __restrict__ windows, Frame F, GeomTables G, PhysParams P,
@@ -28,33 +37,33 @@ __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4
                                  double* __restrict__ rates, double* __restrict__ Rsum, double* __restrict__ Eout,
                                  DevCounters* ctr)
 {
-    const int nrows = nrows_dev ? *nrows_dev : nrows_host;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= nrows) return;
-    uint8_t w[kWin];
-    int slot;
-    if (windows) {
-        slot = g;
-#pragma unroll
-        for (int j = 0; j < kWin; ++j) w[j] = windows[(size_t)g * kWin + j];
-    } else {
-        slot = rows ? rows[g] : g;
-        gather_window(species, F, G, vac[slot], w);
-    }
-    double R = 0.0;
+    const int nrows = row_count(nrows_dev, nrows_host);
     int clamps = 0;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nrows; g += gridDim.x * blockDim.x) {
+        uint8_t w[kWin];
+        int slot;
+        if (windows) {
+            slot = g;
 #pragma unroll
-    for (int k = 0; k < kHops; ++k) {
-        double E = 0.0, Gk = 0.0;
-        if (w[k] != kVac) {
-            clamps += pair_barrier(w, k, G, P, E);
-            Gk = arrhenius(E, P);
+            for (int j = 0; j < kWin; ++j) w[j] = windows[(size_t)g * kWin + j];
+        } else {
+            slot = rows ? rows[g] : g;
+            gather_window(species, F, G, vac[slot], w);
         }
-        R = __dadd_rn(R, Gk);
-        if (rates) rates[(size_t)slot * 8 + k] = Gk;
-        if (Eout) Eout[(size_t)slot * 8 + k] = E;
+        double R = 0.0;
+#pragma unroll
+        for (int k = 0; k < kHops; ++k) {
+            double E = 0.0, Gk = 0.0;
+            if (w[k] != kVac) {
+                clamps += pair_barrier(w, k, G, P, E);
+                Gk = arrhenius(E, P);
+            }
+            R = __dadd_rn(R, Gk);
+            if (rates) rates[(size_t)slot * 8 + k] = Gk;
+            if (Eout) Eout[(size_t)slot * 8 + k] = E;
+        }
+        if (Rsum) Rsum[slot] = R;
     }
-    if (Rsum) Rsum[slot] = R;
     if (clamps && ctr) atomicAdd(&ctr->clamps, (unsigned long long)clamps);
 }
 
@@ -66,56 +75,57 @@ __global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
     const int* __restrict__ nrows_dev, int nrows_host, double* __restrict__ rates, double* __restrict__ Rsum,
     double* __restrict__ Eout)
 {
-    const int nrows = nrows_dev ? *nrows_dev : nrows_host;
-    const int g = blockIdx.x;
-    if (g >= nrows) return;
+    const int nrows = row_count(nrows_dev, nrows_host);
     __shared__ uint8_t w[kWin];
     __shared__ double h1[kHid];
     __shared__ double h2[kHid];
     __shared__ double Ek[8];
     __shared__ int slot_s;
-    const int j = threadIdx.x;
-    if (j == 0) slot_s = windows ? g : (rows ? rows[g] : g);
-    __syncthreads();
-    const int slot = slot_s;
-    if (j < kWin) {
-        if (windows) {
-            w[j] = windows[(size_t)g * kWin + j];
-        } else {
-            const int4 v = vac[slot];
-            w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
-        }
-    }
-    __syncthreads();
     const double* W1 = mlp;
     const double* b1 = W1 + 448 * kHid;
     const double* W2 = b1 + kHid;
     const double* b2 = W2 + kHid * kHid;
     const double* W3 = b2 + kHid;
     const double* b3 = W3 + kHid * 8;
-    double acc = b1[j];
-    for (int s = 0; s < kWin; ++s) acc = __dadd_rn(acc, W1[(size_t)(kSpecies * s + w[s]) * kHid + j]);
-    h1[j] = acc > 0.0 ? acc : 0.0;
-    __syncthreads();
-    acc = b2[j];
-    for (int i = 0; i < kHid; ++i) acc = __fma_rn(h1[i], W2[(size_t)i * kHid + j], acc);
-    h2[j] = acc > 0.0 ? acc : 0.0;
-    __syncthreads();
-    if (j < 8) {
-        acc = b3[j];
-        for (int i = 0; i < kHid; ++i) acc = __fma_rn(h2[i], W3[i * 8 + j], acc);
-        Ek[j] = acc > 0.0 ? acc : 0.0;
-    }
-    __syncthreads();
-    if (j == 0) {
-        double R = 0.0;
-        for (int k = 0; k < kHops; ++k) {
-            const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], P) : 0.0;
-            R = __dadd_rn(R, Gk);
-            if (rates) rates[(size_t)slot * 8 + k] = Gk;
-            if (Eout) Eout[(size_t)slot * 8 + k] = Ek[k];
+    const int j = threadIdx.x;
+    for (int g = blockIdx.x; g < nrows; g += gridDim.x) {
+        if (j == 0) slot_s = windows ? g : (rows ? rows[g] : g);
+        __syncthreads();
+        const int slot = slot_s;
+        if (j < kWin) {
+            if (windows) {
+                w[j] = windows[(size_t)g * kWin + j];
+            } else {
+                const int4 v = vac[slot];
+                w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
+            }
         }
-        if (Rsum) Rsum[slot] = R;
+        __syncthreads();
+        double acc = b1[j];
+        for (int s = 0; s < kWin; ++s) acc = __dadd_rn(acc, W1[(size_t)(kSpecies * s + w[s]) * kHid + j]);
+        h1[j] = acc > 0.0 ? acc : 0.0;
+        __syncthreads();
+        acc = b2[j];
+        for (int i = 0; i < kHid; ++i) acc = __fma_rn(h1[i], W2[(size_t)i * kHid + j], acc);
+        h2[j] = acc > 0.0 ? acc : 0.0;
+        __syncthreads();
+        if (j < 8) {
+            acc = b3[j];
+            for (int i = 0; i < kHid; ++i) acc = __fma_rn(h2[i], W3[i * 8 + j], acc);
+            Ek[j] = acc > 0.0 ? acc : 0.0;
+        }
+        __syncthreads();
+        if (j == 0) {
+            double R = 0.0;
+            for (int k = 0; k < kHops; ++k) {
+                const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], P) : 0.0;
+                R = __dadd_rn(R, Gk);
+                if (rates) rates[(size_t)slot * 8 + k] = Gk;
+                if (Eout) Eout[(size_t)slot * 8 + k] = Ek[k];
+            }
+            if (Rsum) Rsum[slot] = R;
+        }
+        __syncthreads();
     }
 }
 
@@ -140,8 +150,7 @@ __device__ __forceinline__ int tree_descend(const double* buf, int n, int P, int
 {
     int idx = 0;
     for (int l = nlev; l >= 1; --l) {
-        // offset of level (l-1): sum_{j < l-1} P >> j
-        int off = 0;
+        int off = 0;                                   // offset of level l-1: sum_{j < l-1} P >> j
         for (int jj = 0; jj < l - 1; ++jj) off += P >> jj;
         const double left = buf[off + 2 * idx];
         if (r < left) {
@@ -229,10 +238,14 @@ struct SubParams {
     int D[3];              // domain edge (cells)
     int ND[3];             // domains per axis per voxel
     long long ndom_vox;    // domains per voxel
-    int sector;            // active octant c
-    long long phase;       // global phase p = 8*sweep + q
     double window;         // Delta_win
     uint64_t seed;
+};
+
+struct PhaseInfo {         // per phase, written to device memory before each sweep's graph launch
+    int sector;            // active octant c = perm_sweep[q]
+    int pad;
+    long long phase;       // global phase p = 8*sweep + q
 };
 
 struct Segment {
@@ -254,26 +267,28 @@ __device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, lo
     sec = ox | (oy << 1) | (oz << 2);
 }
 
-__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, SubParams S, int* dmin, int* head, int* next)
+__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, SubParams S, const PhaseInfo* __restrict__ ph,
+                                int* dmin, int* head, int* next, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; }
     if (i >= nvac) return;
     long long d; int sec;
     dom_sector(vac[i], S, d, sec);
-    if (sec != S.sector) return;
+    if (sec != ph->sector) return;
     atomicMin(&dmin[d], i);
     next[i] = atomicExch(&head[d], i);
 }
 
-__global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S, int* dmin, int* head,
-                                const int* __restrict__ next, Segment* segs, int* members, uint8_t* mactive,
-                                DevCounters* ctr)
+__global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S, const PhaseInfo* __restrict__ ph,
+                                int* dmin, int* head, const int* __restrict__ next, Segment* segs, int* members,
+                                uint8_t* mactive, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nvac) return;
     long long d; int sec;
     dom_sector(vac[i], S, d, sec);
-    if (sec != S.sector || dmin[d] != i) return;      // the minimum slot owns the domain
+    if (sec != ph->sector || dmin[d] != i) return;    // the minimum slot owns the domain
     int cnt = 0;
     for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
     const int off = (int)atomicAdd(&ctr->total, (unsigned long long)cnt);
@@ -294,73 +309,91 @@ __global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParam
     dmin[d] = INT_MAX;
 }
 
+// rows of this inner iteration = active members of running segments; also resets nrun
 __global__ void rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
-                            const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr, int cap)
+                            const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr)
 {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= (int)ctr->nseg || s >= cap) return;
-    const Segment sg = segs[s];
-    if (!sg.running) return;
-    for (int a = 0; a < sg.cnt; ++a)
-        if (mactive[sg.off + a]) {
-            const int r = (int)atomicAdd(&ctr->nrows, 1ull);
-            rows[r] = members[sg.off + a];
-        }
+    const int nseg = (int)ctr->nseg;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+        const Segment sg = segs[s];
+        if (!sg.running) continue;
+        for (int a = 0; a < sg.cnt; ++a)
+            if (mactive[sg.off + a]) {
+                const int r = (int)atomicAdd(&ctr->nrows, 1ull);
+                rows[r] = members[sg.off + a];
+            }
+    }
 }
 
-__global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, SubParams S, Segment* segs,
-                                  const int* __restrict__ members, uint8_t* mactive, const double* __restrict__ rates,
-                                  const double* __restrict__ Rsum, double* scratch, int* iscratch, DevCounters* ctr,
-                                  int cap)
+__global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, SubParams S,
+                                  const PhaseInfo* __restrict__ ph, Segment* segs, const int* __restrict__ members,
+                                  uint8_t* mactive, const double* __restrict__ rates, const double* __restrict__ Rsum,
+                                  double* scratch, int* iscratch, DevCounters* ctr)
 {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= (int)ctr->nseg || s >= cap) return;
-    Segment sg = segs[s];
-    if (!sg.running) return;
-    double* buf = scratch + 4 * (size_t)sg.off;  // disjoint per segment: 2P-1 <= 4*cnt
-    int* idx = iscratch + sg.off;
-    int m = 0;
-    for (int a = 0; a < sg.cnt; ++a)
-        if (mactive[sg.off + a]) {
-            buf[m] = Rsum[members[sg.off + a]];
-            idx[m] = a;
-            ++m;
-        }
-    bool stop = false;
-    if (m == 0) {
-        stop = true;
-    } else {
-        atomicAdd(&ctr->hop_evals, 8ull * (unsigned long long)m);
-        int P = 1, nlev = 0;
-        const double Rd = tree_build(buf, m, P, nlev);
-        if (!(Rd > 0.0)) {
+    const int nseg = (int)ctr->nseg;
+    const int sector = ph->sector;
+    const unsigned long long p = (unsigned long long)ph->phase;
+    unsigned long long evals = 0, events = 0;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+        Segment sg = segs[s];
+        if (!sg.running) continue;
+        double* buf = scratch + 4 * (size_t)sg.off;   // disjoint per segment: 2P-1 <= 4*cnt
+        int* idx = iscratch + sg.off;
+        int m = 0;
+        for (int a = 0; a < sg.cnt; ++a)
+            if (mactive[sg.off + a]) {
+                buf[m] = Rsum[members[sg.off + a]];
+                idx[m] = a;
+                ++m;
+            }
+        bool stop = false;
+        if (m == 0) {
             stop = true;
         } else {
-            double u_sel, u_t;
-            const unsigned long long p = (unsigned long long)S.phase;
-            philox_uniforms(S.seed, make_uint4(sg.it, (uint32_t)sg.dom, (uint32_t)p, (uint32_t)(p >> 32)), u_sel, u_t);
-            const double dt = __ddiv_rn(-det_log(u_t), Rd);
-            if (__dadd_rn(sg.t, dt) > S.window) {
-                stop = true;                              // overshooting draw discarded
+            evals += 8ull * (unsigned long long)m;
+            int P = 1, nlev = 0;
+            const double Rd = tree_build(buf, m, P, nlev);
+            if (!(Rd > 0.0)) {
+                stop = true;
             } else {
-                double r = __dmul_rn(u_sel, Rd);
-                const int leaf = tree_descend(buf, m, P, nlev, r);
-                const int a = idx[leaf];
-                const int slot = members[sg.off + a];
-                const int k = pick_hop(rates + (size_t)slot * 8, r);
-                const int4 nv = apply_hop(species, vac, slot, k, F, G);
-                long long d2; int sec2;
-                dom_sector(nv, S, d2, sec2);
-                if (d2 != sg.dom || sec2 != S.sector) mactive[sg.off + a] = 0;
-                sg.t = __dadd_rn(sg.t, dt);
-                sg.it += 1u;
-                atomicAdd(&ctr->events, 1ull);
-                atomicAdd(&ctr->nrun, 1ull);
+                double u_sel, u_t;
+                philox_uniforms(S.seed, make_uint4(sg.it, (uint32_t)sg.dom, (uint32_t)p, (uint32_t)(p >> 32)), u_sel, u_t);
+                const double dt = __ddiv_rn(-det_log(u_t), Rd);
+                if (__dadd_rn(sg.t, dt) > S.window) {
+                    stop = true;                          // overshooting draw discarded
+                } else {
+                    double r = __dmul_rn(u_sel, Rd);
+                    const int leaf = tree_descend(buf, m, P, nlev, r);
+                    const int a = idx[leaf];
+                    const int slot = members[sg.off + a];
+                    const int k = pick_hop(rates + (size_t)slot * 8, r);
+                    const int4 nv = apply_hop(species, vac, slot, k, F, G);
+                    long long d2; int sec2;
+                    dom_sector(nv, S, d2, sec2);
+                    if (d2 != sg.dom || sec2 != sector) mactive[sg.off + a] = 0;
+                    sg.t = __dadd_rn(sg.t, dt);
+                    sg.it += 1u;
+                    events += 1;
+                }
             }
         }
+        if (stop) sg.running = 0;
+        segs[s] = sg;
     }
-    if (stop) sg.running = 0;
-    segs[s] = sg;
+    if (evals) atomicAdd(&ctr->hop_evals, evals);
+    if (events) {
+        atomicAdd(&ctr->events, events);
+        atomicAdd(&ctr->nrun, events);
+    }
+}
+
+// a8: continue the inner loop while some domain applied an event; resets nrun/nrows for the next trip
+__global__ void loop_cond_kernel(DevCounters* ctr, cudaGraphConditionalHandle handle)
+{
+    const unsigned long long run = ctr->nrun;
+    ctr->nrun = 0;
+    ctr->nrows = 0;
+    cudaGraphSetConditional(handle, run > 0 ? 1u : 0u);
 }
 
 __global__ void add_window_kernel(double* clock, int nvox, double w)
@@ -373,6 +406,125 @@ __global__ void fill_int_kernel(int* p, long long n, int val)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = val;
+}
+
+// ------------------------------------------------------------------ a0: vacancy registry by device scan
+// 16 sites per thread (one uint4), 4096 per block.  Pass 1 counts vacancies and the max species code
+// per block; pass 2 (one block) scans the block counts; pass 3 writes positions in site order.
+constexpr int kScanThreads = 256;
+constexpr int kScanSites = kScanThreads * 16;
+
+__device__ __forceinline__ int vac_in_word(uint32_t w)
+{
+    int c = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) c += ((w >> (8 * b)) & 0xFF) == kVac;
+    return c;
+}
+
+__global__ void scan_count_kernel(const uint4* __restrict__ sp, long long nwords, int* bcount, unsigned int* maxcode)
+{
+    const long long wi = (long long)blockIdx.x * kScanThreads + threadIdx.x;
+    int c = 0;
+    unsigned int mx = 0;
+    if (wi < nwords) {
+        const uint4 v = sp[wi];
+        c = vac_in_word(v.x) + vac_in_word(v.y) + vac_in_word(v.z) + vac_in_word(v.w);
+        const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) mx = max(mx, (ws[q] >> (8 * b)) & 0xFFu);
+    }
+    __shared__ int sc[kScanThreads / 32];
+    __shared__ unsigned int sm[kScanThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) { sc[threadIdx.x >> 5] = c; sm[threadIdx.x >> 5] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0; unsigned int m = 0;
+        for (int i = 0; i < kScanThreads / 32; ++i) { t += sc[i]; m = max(m, sm[i]); }
+        bcount[blockIdx.x] = t;
+        if (m > kVac) atomicMax(maxcode, m);
+    }
+}
+
+// exclusive scan of n ints in place (single block of 1024 threads); total -> *total
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(int* a, int n, long long* total)
+{
+    __shared__ long long part[1024];
+    const int per = (n + 1023) / 1024;
+    const int b0 = threadIdx.x * per;
+    long long s = 0;
+    for (int i = b0; i < min(n, b0 + per); ++i) s += a[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long acc = 0;
+        for (int i = 0; i < 1024; ++i) { const long long t = part[i]; part[i] = acc; acc += t; }
+        *total = acc;
+    }
+    __syncthreads();
+    long long acc = part[threadIdx.x];
+    for (int i = b0; i < min(n, b0 + per); ++i) { const int t = a[i]; a[i] = (int)acc; acc += t; }
+}
+
+__global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords, const int* __restrict__ boff,
+                                  Frame F, int4* vac)
+{
+    const long long wi = (long long)blockIdx.x * kScanThreads + threadIdx.x;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    int c = 0;
+    if (wi < nwords) {
+        v = sp[wi];
+        c = vac_in_word(v.x) + vac_in_word(v.y) + vac_in_word(v.z) + vac_in_word(v.w);
+    }
+    // block-exclusive prefix of per-thread counts (thread order == site order)
+    __shared__ int wsum[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int i = 0; i < wid; ++i) wbase += wsum[i];
+    if (c == 0) return;
+    int pos = boff[blockIdx.x] + wbase + incl - c;
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+    for (int q = 0; q < 4; ++q)
+        for (int b = 0; b < 4; ++b)
+            if (((ws[q] >> (8 * b)) & 0xFF) == kVac) {
+                const long long site = wi * 16 + q * 4 + b;
+                const int vox = (int)(site / F.sites);
+                const long long li = site - (long long)vox * F.sites;
+                const int bb = (int)(li & 1);
+                const long long cell = li >> 1;
+                const int x = (int)(cell % F.L[0]);
+                const int y = (int)((cell / F.L[0]) % F.L[1]);
+                const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
+                vac[pos++] = make_int4(vox, 2 * x + bb, 2 * y + bb, 2 * z + bb);
+            }
+}
+
+// vstart[v] = first slot whose voxel >= v (slots are in site order, hence voxel-major)
+__global__ void vstart_kernel(const int4* __restrict__ vac, int nvac, int nvox, int* vstart)
+{
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > nvox) return;
+    int lo = 0, hi = nvac;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (vac[mid].x < v) lo = mid + 1; else hi = mid;
+    }
+    vstart[v] = lo;
 }
 
 } // namespace akmc

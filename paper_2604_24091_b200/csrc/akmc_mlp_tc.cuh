@@ -7,11 +7,11 @@
 namespace akmc {
 
 constexpr int kTileM = 128;          // rows (vacancies) per CTA tile = TMEM lanes
-constexpr int kKChunk = 32;          // K per pipeline stage
+constexpr int kKChunk = 16;          // K per pipeline stage (one UMMA K-step)
 constexpr int kNChunks = kHid / kKChunk;
-constexpr int kStages = 2;
-constexpr int kSplitBytes = kHid * kKChunk * 2;        // one fp16 split of a B chunk: 16 KiB
-constexpr int kStageBytes = 2 * kSplitBytes;           // hi + lo: 32 KiB
+constexpr int kStages = 4;
+constexpr int kSplitBytes = kHid * kKChunk * 2;        // one fp16 split of a B chunk: 8 KiB
+constexpr int kStageBytes = 2 * kSplitBytes;           // hi + lo: 16 KiB
 constexpr int kABytes = kTileM * kHid * 2;             // one fp16 split of the A tile: 64 KiB
 constexpr float kLoScale = 2048.0f;                    // lo parts are stored * 2^11
 
@@ -26,7 +26,7 @@ struct MlpTcParams {
     const int* nrows_dev;            // device row count (nullptr => nrows_host)
     int nrows_host;
     // weights (prepared at init)
-    const float* W1p;                // [448][256] Fe-referenced layer-1 rows (fp32)
+    const double* W1p;               // [448][256] Fe-referenced layer-1 rows (fp64)
     const double* b1p;               // [256] layer-1 bias + sum of Fe rows (fp64)
     const __half* Bimg;              // [kNChunks][2][kSplitBytes/2] W2^T splits in UMMA smem image
     const float* b2;                 // [256]
@@ -43,8 +43,8 @@ struct MlpTcParams {
 
 // smem bytes needed by the kernel
 size_t mlp_tc_smem_bytes();
-// launch over ceil(max_rows / 128) CTAs; CTAs beyond the device row count exit early
-cudaError_t launch_mlp_tc(const MlpTcParams& p, int max_rows, cudaStream_t s);
+// persistent launch: min(num_sms, ceil(max_rows/128)) CTAs loop over the tiles of the device row count
+cudaError_t launch_mlp_tc(const MlpTcParams& p, int max_rows, int num_sms, cudaStream_t s);
 // one-time attribute setup (max dynamic smem)
 cudaError_t mlp_tc_setup();
 

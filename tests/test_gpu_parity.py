@@ -150,16 +150,23 @@ def test_voxel_batch_bitexact(akmc, orc):
     assert gctr["events"] == ost.counters[0]
 
 
-@pytest.mark.parametrize("lam", [1.0, 0.25])
-def test_sublattice_bitexact(akmc, orc, lam):
-    """Windowed synchronous sublattice (reading A19), domains 8^3: bit-exact vs the oracle."""
+@pytest.mark.parametrize("lam,driver", [(1.0, "graph"), (0.25, "graph"), (1.0, "host")])
+def test_sublattice_bitexact(akmc, orc, lam, driver):
+    """Windowed synchronous sublattice (reading A19), domains 8^3: bit-exact vs the oracle, with the
+    per-sweep CUDA graph (device-side inner loop) and with the host-stepped (profiling) driver."""
     eps, E0 = _params()
     L = 32
     sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), 60, seed=41)
     win = synth.window_seconds(lam, E0[0])
     cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=9,
                       domain_cells=(8, 8, 8), window_s=win)
-    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 8, eps, E0, chunks=2)
+    ost = orc.State.from_species(_ocfg(orc, cfg), sp)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        sim.set_profiling(driver == "host")
+        for _ in range(2):
+            sim.step(4)
+            orc.run(_ocfg(orc, cfg), ost, 4, eps, E0)
+        gsp, gvac, gclock, gctr = sim.state()
     assert ost.counters[0] > 20
     assert np.array_equal(gsp, ost.species)
     assert np.array_equal(gvac, ost.vac)

@@ -121,7 +121,8 @@ struct akmc_handle {
     PhysParams P{};
     SubParams S{};
     int nvox = 0;
-    int64_t nvac = 0, sites = 0;
+    int64_t nvac = 0, sites = 0;      // sites = canonical sites (all voxels)
+    int64_t csites = 0, ssites = 0;   // canonical sites per voxel, storage sites (all voxels, with halos)
     long long ndom_total = 0;
     uint8_t* d_species = nullptr;
     int4* d_vac = nullptr;
@@ -137,11 +138,12 @@ struct akmc_handle {
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;     // pinned
     double* d_mlp = nullptr;
-    double* d_W1p = nullptr;
-    double* d_b1p = nullptr;
-    __half* d_Bimg = nullptr;
-    float *d_b2 = nullptr, *d_W3 = nullptr, *d_b3 = nullptr;
-    float w2_unscale = 1.0f;
+    uint8_t* d_Bimg = nullptr;        // ring image: W1'^T (24 chunks) + W2^T (16 chunks), fp16 hi/lo
+    uint8_t* d_W3img = nullptr;       // W3^T hi/lo, N padded to 16
+    float *d_b1h = nullptr, *d_b1l = nullptr, *d_b2 = nullptr;
+    double* d_b3 = nullptr;
+    float s1u = 1.0f, s2u = 1.0f;
+    double s3u = 1.0;
     unsigned long long* d_overflow = nullptr;
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
@@ -156,6 +158,7 @@ struct akmc_handle {
     cudaGraphExec_t sweep_exec = nullptr;
     cudaStream_t graph_stream = nullptr;   // stream the graph was instantiated for
     int graph_launches_per_sweep = 0;
+    unsigned long long* d_phase_cycles = nullptr;   // AKMC_PHASE_TIMING diagnostics
 };
 
 namespace {
@@ -178,8 +181,8 @@ void free_all(akmc_handle* h)
 {
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_rows,
-                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_W1p, h->d_b1p, h->d_Bimg, h->d_b2,
-                    h->d_W3, h->d_b3, h->d_overflow};
+                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img, h->d_b1h, h->d_b1l,
+                    h->d_b2, h->d_b3, h->d_overflow};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -240,54 +243,81 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     const double* b2 = W2 + kHid * kHid;
     const double* W3 = b2 + kHid;
     const double* b3 = W3 + kHid * 8;
-    std::vector<double> W1p((size_t)448 * kHid);
-    std::vector<double> b1p(kHid);
+    // power-of-two scale so that max|w| * 2^s <= 2^13 (fp16 hi/lo splits stay in range)
+    auto scale_exp = [](const double* w, size_t n) {
+        double mx = 0.0;
+        for (size_t i = 0; i < n; ++i) mx = std::max(mx, std::fabs(w[i]));
+        return mx > 0.0 ? 13 - (int)std::ceil(std::log2(mx)) : 0;
+    };
+    // UMMA K-major no-swizzle image of B[n][k] (N rows, K cols): core matrices of 8 rows x 16 B
+    auto put = [](uint8_t* img, int N, int n, int k, double w) {
+        const __half hi = __float2half_rn((float)w);
+        const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
+        const size_t off = ((size_t)(k / 8) * (N / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+        const size_t split = (size_t)N * 16 * 2;    // per K-step of 16, hi then lo
+        reinterpret_cast<__half*>(img + (size_t)(k / 16) * 2 * split + (off % split))[0] = hi;
+        reinterpret_cast<__half*>(img + (size_t)(k / 16) * 2 * split + split + (off % split))[0] = lo;
+    };
+    // layer 1: Fe-referenced rows W1'[6*slot + s-1] = W1[7*slot+s] - W1[7*slot+Fe] (s = 1..6), bias
+    // b1' = b1 + sum_slot W1[7*slot+Fe] (exact algebra: one species per slot)
+    std::vector<double> W1p((size_t)kK1 * kHid), b1p(kHid);
     for (int j = 0; j < kHid; ++j) {
         double acc = b1[j];
         for (int s = 0; s < kWin; ++s) acc += W1[(size_t)(kSpecies * s + kFe) * kHid + j];
         b1p[j] = acc;
     }
-    for (int f = 0; f < 448; ++f) {
-        const int s = f / kSpecies;
-        for (int j = 0; j < kHid; ++j)
-            W1p[(size_t)f * kHid + j] = (W1[(size_t)f * kHid + j] - W1[(size_t)(kSpecies * s + kFe) * kHid + j]);
+    for (int slot = 0; slot < kWin; ++slot)
+        for (int s = 1; s < kSpecies; ++s)
+            for (int j = 0; j < kHid; ++j)
+                W1p[(size_t)((kSpecies - 1) * slot + s - 1) * kHid + j] =
+                    W1[(size_t)(kSpecies * slot + s) * kHid + j] - W1[(size_t)(kSpecies * slot + kFe) * kHid + j];
+    const int s1 = scale_exp(W1p.data(), W1p.size());
+    const int s2 = scale_exp(W2, (size_t)kHid * kHid);
+    const int s3 = scale_exp(W3, (size_t)kHid * 8);
+    h->s1u = (float)std::ldexp(1.0, -s1);
+    h->s2u = (float)std::ldexp(1.0, -s2);
+    h->s3u = std::ldexp(1.0, -s3);
+    std::vector<uint8_t> img((size_t)kChunksTile * kStageBytes, 0);
+    for (int k = 0; k < kK1; ++k)                                // chunks 0..23: W1'^T
+        for (int n = 0; n < kHid; ++n) put(img.data(), kHid, n, k, std::ldexp(W1p[(size_t)k * kHid + n], s1));
+    for (int k = 0; k < kHid; ++k)                               // chunks 24..39: W2^T
+        for (int n = 0; n < kHid; ++n)
+            put(img.data() + (size_t)kChunksL1 * kStageBytes, kHid, n, k, std::ldexp(W2[(size_t)k * kHid + n], s2));
+    // W3^T padded to N = 16: per K-step of 16 the layout above interleaves hi/lo, so build the two
+    // K=256 splits separately (no-swizzle, LBO = 256 B)
+    std::vector<uint8_t> w3img((size_t)2 * kW3SplitBytes, 0);
+    for (int k = 0; k < kHid; ++k)
+        for (int n = 0; n < 8; ++n) {
+            const double w = std::ldexp(W3[(size_t)k * 8 + n], s3);
+            const __half hi = __float2half_rn((float)w);
+            const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
+            const size_t off = ((size_t)(k / 8) * (kN3 / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+            reinterpret_cast<__half*>(w3img.data() + off)[0] = hi;
+            reinterpret_cast<__half*>(w3img.data() + kW3SplitBytes + off)[0] = lo;
+        }
+    std::vector<float> b1h(kHid), b1l(kHid), b2f(kHid);
+    for (int i = 0; i < kHid; ++i) {
+        b1h[i] = (float)b1p[i];
+        b1l[i] = (float)(b1p[i] - (double)b1h[i]);
+        b2f[i] = (float)b2[i];
     }
-    double mx = 0.0;
-    for (int i = 0; i < kHid * kHid; ++i) mx = std::max(mx, std::fabs(W2[i]));
-    int sb = 0;
-    if (mx > 0.0) sb = 13 - (int)std::ceil(std::log2(mx));
-    const double scale = std::ldexp(1.0, sb);
-    h->w2_unscale = (float)std::ldexp(1.0, -sb);
-    std::vector<__half> img((size_t)kNChunks * kStageBytes / 2);
-    uint8_t* base = reinterpret_cast<uint8_t*>(img.data());
-    for (int c = 0; c < kNChunks; ++c)
-        for (int kl = 0; kl < kKChunk; ++kl)
-            for (int n = 0; n < kHid; ++n) {
-                const int k = c * kKChunk + kl;
-                const double w = W2[(size_t)k * kHid + n] * scale;    // B[n][k] = W2[k][n]
-                const __half hi = __float2half_rn((float)w);
-                const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
-                const size_t off = ((size_t)(kl / 8) * (kHid / 8) + n / 8) * 128 + (n % 8) * 16 + (kl % 8) * 2;
-                *reinterpret_cast<__half*>(base + (size_t)c * kStageBytes + off) = hi;
-                *reinterpret_cast<__half*>(base + (size_t)c * kStageBytes + kSplitBytes + off) = lo;
-            }
-    std::vector<float> b2f(kHid), W3f(kHid * 8), b3f(8);
-    for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
-    for (int i = 0; i < kHid * 8; ++i) W3f[i] = (float)W3[i];
-    for (int i = 0; i < 8; ++i) b3f[i] = (float)b3[i];
-    CK(h, cudaMalloc(&h->d_W1p, W1p.size() * 8));
-    CK(h, cudaMalloc(&h->d_b1p, kHid * 8));
-    CK(h, cudaMalloc(&h->d_Bimg, img.size() * 2));
+    CK(h, cudaMalloc(&h->d_Bimg, img.size()));
+    CK(h, cudaMalloc(&h->d_W3img, w3img.size()));
+    CK(h, cudaMalloc(&h->d_b1h, kHid * 4));
+    CK(h, cudaMalloc(&h->d_b1l, kHid * 4));
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
-    CK(h, cudaMalloc(&h->d_W3, kHid * 8 * 4));
-    CK(h, cudaMalloc(&h->d_b3, 8 * 4));
-    CK(h, cudaMemcpy(h->d_W1p, W1p.data(), W1p.size() * 8, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_b1p, b1p.data(), kHid * 8, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
+    CK(h, cudaMalloc(&h->d_b3, 8 * 8));
+    CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size(), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_W3img, w3img.data(), w3img.size(), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b1h, b1h.data(), kHid * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b1l, b1l.data(), kHid * 4, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_W3, W3f.data(), kHid * 8 * 4, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_b3, b3f.data(), 8 * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     CK(h, mlp_tc_setup());
+    if (std::getenv("AKMC_PHASE_TIMING")) {
+        CK(h, cudaMalloc(&h->d_phase_cycles, 10 * sizeof(unsigned long long)));
+        CK(h, cudaMemset(h->d_phase_cycles, 0, 10 * sizeof(unsigned long long)));
+    }
     return AKMC_OK;
 }
 
@@ -323,8 +353,12 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         MlpTcParams p{};
         p.species = h->d_species; p.vac = h->d_vac; p.windows = windows; p.F = h->F; p.G = h->G;
         p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
-        p.W1p = h->d_W1p; p.b1p = h->d_b1p; p.Bimg = h->d_Bimg; p.b2 = h->d_b2; p.W3 = h->d_W3; p.b3 = h->d_b3;
-        p.w2_unscale = h->w2_unscale; p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
+        p.Bimg = reinterpret_cast<const __half*>(h->d_Bimg);
+        p.W3img = reinterpret_cast<const __half*>(h->d_W3img);
+        p.b1hi = h->d_b1h; p.b1lo = h->d_b1l; p.b2 = h->d_b2; p.b3 = h->d_b3;
+        p.s1_unscale = h->s1u; p.s2_unscale = h->s2u; p.s3_unscale = h->s3u;
+        p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
+        p.phase_cycles = h->d_phase_cycles;
         CK(h, launch_mlp_tc(p, max_rows, h->num_sms, h->stream));
     }
     h->total.kernel_launches += 1;
@@ -377,9 +411,15 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     h->dev = dev;
     h->sub = cfg->domain_cells[0] != 0;
     h->nvox = cfg->n_voxels;
-    for (int a = 0; a < 3; ++a) h->F.L[a] = cfg->cells[a];
-    h->F.sites = 2LL * cfg->cells[0] * cfg->cells[1] * cfg->cells[2];
-    h->sites = h->F.sites * cfg->n_voxels;
+    for (int a = 0; a < 3; ++a) {
+        h->F.L[a] = cfg->cells[a];
+        h->F.Ls[a] = (cfg->cells[a] + 2 * kHalo + 3) & ~3;               // bricks of 4 cells
+        h->F.NB[a] = h->F.Ls[a] / 4;
+    }
+    h->F.sites = 128LL * h->F.NB[0] * h->F.NB[1] * h->F.NB[2];          // storage bytes per voxel
+    h->csites = 2LL * cfg->cells[0] * cfg->cells[1] * cfg->cells[2];    // canonical sites per voxel
+    h->sites = h->csites * cfg->n_voxels;
+    h->ssites = h->F.sites * cfg->n_voxels;
     if (!build_geometry(h->G)) { delete h; return fail(nullptr, AKMC_ERR_RUNTIME, "geometry table construction failed"); }
     // physical parameters
     if (eps) {
@@ -409,7 +449,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     h->num_sms = prop.multiProcessorCount;
     CKI(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
-    CKI(cudaMalloc(&h->d_species, (size_t)h->sites));
+    CKI(cudaMalloc(&h->d_species, (size_t)h->sites));        // canonical upload buffer (temporary)
     CKI(cudaMemcpy(h->d_species, species, (size_t)h->sites, cudaMemcpyHostToDevice));
     CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
     CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
@@ -449,6 +489,14 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaStreamSynchronize(h->stream));
         cudaFree(d_bc);
         cudaFree(d_max);
+        // storage layout with halo ghosts (periodic images)
+        uint8_t* st = nullptr;
+        CKI(cudaMalloc(&st, (size_t)h->ssites));
+        scatter_storage_kernel<<<blocks_for(h->sites, 256), 256, 0, h->stream>>>(h->d_species, st, h->F, h->sites);
+        const cudaError_t es = cudaStreamSynchronize(h->stream);
+        cudaFree(h->d_species);
+        h->d_species = st;
+        CKI(es);
         h->d_iscratch = nullptr;
         h->d_overflow = nullptr;
     }
@@ -557,7 +605,8 @@ static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s
 {
     const int nv = (int)h->nvac;
     const unsigned gs = std::min<unsigned>(blocks_for(nv, 128), (unsigned)h->num_sms * 4u);
-    rows_kernel<<<gs, 128, 0, s>>>(h->d_segs, h->d_members, h->d_mactive, h->d_rows, h->d_ctr);
+    const unsigned gr = std::min<unsigned>(blocks_for(nv, 256), (unsigned)h->num_sms * 2u);
+    rows_kernel<<<gr, 256, 0, s>>>(h->d_segs, h->d_members, h->d_mactive, h->d_rows, h->d_ctr);
     CK(h, cudaGetLastError());
     const int* nrows_dev = reinterpret_cast<const int*>(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, nrows));
     cudaStream_t keep = h->stream;
@@ -750,14 +799,22 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
         if (!n_vac_inout || *n_vac_inout < h->nvac) return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
     }
     CK(h, cudaStreamSynchronize(h->stream));
-    if (species_out) CK(h, cudaMemcpy(species_out, h->d_species, (size_t)h->sites, cudaMemcpyDeviceToHost));
+    if (species_out) {
+        uint8_t* canon = nullptr;
+        CK(h, cudaMalloc(&canon, (size_t)h->sites));
+        gather_canonical_kernel<<<blocks_for(h->sites, 256), 256, 0, h->stream>>>(h->d_species, canon, h->F, h->sites);
+        cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e == cudaSuccess) e = cudaMemcpy(species_out, canon, (size_t)h->sites, cudaMemcpyDeviceToHost);
+        cudaFree(canon);
+        CK(h, e);
+    }
     if (vac_sites_out && h->nvac) {
         std::vector<int4> v((size_t)h->nvac);
         CK(h, cudaMemcpy(v.data(), h->d_vac, v.size() * sizeof(int4), cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < h->nvac; ++i) {
             const int4 p = v[(size_t)i];
             const int64_t cell = (int64_t)(p.y >> 1) + (int64_t)h->F.L[0] * ((int64_t)(p.z >> 1) + (int64_t)h->F.L[1] * (int64_t)(p.w >> 1));
-            vac_sites_out[i] = (int64_t)p.x * h->F.sites + 2 * cell + (p.y & 1);
+            vac_sites_out[i] = (int64_t)p.x * h->csites + 2 * cell + (p.y & 1);
         }
     }
     if (n_vac_inout) *n_vac_inout = h->nvac;
@@ -810,6 +867,16 @@ void akmc_free(akmc_handle* h)
 {
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->d_phase_cycles) {
+        unsigned long long c[10] = {0};
+        cudaMemcpy(c, h->d_phase_cycles, sizeof(c), cudaMemcpyDeviceToHost);
+        const double t = c[7] ? (double)c[7] : 1.0;
+        std::fprintf(stderr, "[akmc phase timing] tiles=%llu cycles/tile: gather %.0f encode %.0f M1 %.0f E1 %.0f M2 %.0f"
+                     " E2 %.0f M3+E3 %.0f; CTA loop %.0f cycles x %llu CTAs\n", c[7], c[0] / t, c[1] / t, c[2] / t,
+                     c[3] / t, c[4] / t, c[5] / t, c[6] / t, c[9] ? (double)c[8] / (double)c[9] : 0.0, c[9]);
+        cudaFree(h->d_phase_cycles);
+        h->d_phase_cycles = nullptr;
+    }
     free_all(h);
     delete h;
 }

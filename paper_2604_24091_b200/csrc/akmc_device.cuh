@@ -35,10 +35,17 @@ struct PhysParams {
     double nu0;
 };
 
-// Lattice frame of one voxel (periodic).
+// Lattice frame of one voxel.  The voxel's L^3 owned cells are stored inside a halo of kHalo cells
+// per face (storage (L + 2 kHalo)^3 cells x 2 basis, x fastest): the halo holds the periodic images
+// (ghosts), so every 64-site window of an owned vacancy is a plain linear offset.
+constexpr int kHalo = 2;                 // window reach: |h| <= 4 half-cells -> 2 cells
+// Storage is bricked: 4x4x4 cells x 2 basis = 128 B = one L2 line per brick, bricks
+// x-fastest; inside a brick the byte is ((z*4 + y)*4 + x)*2 + b.  A 64-site window touches ~8-12 lines.
 struct Frame {
-    int L[3];                            // cells
-    int64_t sites;                       // 2*Lx*Ly*Lz
+    int L[3];                            // owned cells
+    int Ls[3];                           // storage cells = roundup4(L + 2*kHalo)
+    int NB[3];                           // bricks per axis = Ls / 4
+    int64_t sites;                       // storage sites (bytes) per voxel = 128 * NB0*NB1*NB2
 };
 
 // ------------------------------------------------------------------ Philox4x32-10
@@ -119,18 +126,37 @@ __device__ __forceinline__ double arrhenius(double E, const PhysParams& P)
 }
 
 // ------------------------------------------------------------------ lattice addressing
-// vacancy position: x = voxel, y/z/w = half-cell coordinates px, py, pz in [0, 2L)
+// vacancy position: x = voxel, y/z/w = OWNED half-cell coordinates px, py, pz in [0, 2L)
 __device__ __forceinline__ int wrap2(int p, int twoL) { return p < 0 ? p + twoL : (p >= twoL ? p - twoL : p); }
 
+// storage site of owned half-cell coordinates (p may reach kHalo cells outside [0, 2L))
 __device__ __forceinline__ int64_t site_of(const Frame& F, int vox, int px, int py, int pz)
 {
-    const int64_t cell = (int64_t)(px >> 1) + (int64_t)F.L[0] * ((int64_t)(py >> 1) + (int64_t)F.L[1] * (int64_t)(pz >> 1));
-    return (int64_t)vox * F.sites + 2 * cell + (px & 1);
+    const int cx = (px >> 1) + kHalo, cy = (py >> 1) + kHalo, cz = (pz >> 1) + kHalo;
+    const int64_t brick = (int64_t)(cx >> 2) + (int64_t)F.NB[0] * ((int64_t)(cy >> 2) + (int64_t)F.NB[1] * (int64_t)(cz >> 2));
+    const int inb = ((((cz & 3) << 2) | (cy & 3)) << 3) | ((cx & 3) << 1) | (px & 1);
+    return (int64_t)vox * F.sites + (brick << 7) + inb;
 }
 
+// window site of an owned vacancy: no wrap needed, the halo holds the periodic images
 __device__ __forceinline__ int64_t neighbour_site(const Frame& F, const int4& v, int dx, int dy, int dz)
 {
-    return site_of(F, v.x, wrap2(v.y + dx, 2 * F.L[0]), wrap2(v.z + dy, 2 * F.L[1]), wrap2(v.w + dz, 2 * F.L[2]));
+    return site_of(F, v.x, v.y + dx, v.z + dy, v.w + dz);
+}
+
+// write an owned site and all its ghost images in the halo (periodic voxel)
+__device__ __forceinline__ void write_site(uint8_t* species, const Frame& F, int vox, int px, int py, int pz, uint8_t val)
+{
+    int ix[2], iy[2], iz[2];
+    int nx = 1, ny = 1, nz = 1;
+    ix[0] = px; iy[0] = py; iz[0] = pz;
+    const int cx = px >> 1, cy = py >> 1, cz = pz >> 1;
+    if (cx < kHalo) ix[nx++] = px + 2 * F.L[0]; else if (cx >= F.L[0] - kHalo) ix[nx++] = px - 2 * F.L[0];
+    if (cy < kHalo) iy[ny++] = py + 2 * F.L[1]; else if (cy >= F.L[1] - kHalo) iy[ny++] = py - 2 * F.L[1];
+    if (cz < kHalo) iz[nz++] = pz + 2 * F.L[2]; else if (cz >= F.L[2] - kHalo) iz[nz++] = pz - 2 * F.L[2];
+    for (int a = 0; a < nx; ++a)
+        for (int b = 0; b < ny; ++b)
+            for (int c = 0; c < nz; ++c) species[site_of(F, vox, ix[a], iy[b], iz[c])] = val;
 }
 
 // ------------------------------------------------------------------ pair KRA barrier

@@ -191,11 +191,10 @@ __device__ __forceinline__ int4 apply_hop(uint8_t* species, int4* vac, int slot,
     n.y = wrap2(v.y + G.off[k][0], 2 * F.L[0]);
     n.z = wrap2(v.z + G.off[k][1], 2 * F.L[1]);
     n.w = wrap2(v.w + G.off[k][2], 2 * F.L[2]);
-    const int64_t sv = site_of(F, v.x, v.y, v.z, v.w);
-    const int64_t sn = site_of(F, n.x, n.y, n.z, n.w);
-    const uint8_t t = species[sv];
-    species[sv] = species[sn];
-    species[sn] = t;
+    const uint8_t tv = species[site_of(F, v.x, v.y, v.z, v.w)];
+    const uint8_t tn = species[site_of(F, n.x, n.y, n.z, n.w)];
+    write_site(species, F, v.x, v.y, v.z, v.w, tn);     // owned sites and their ghost images
+    write_site(species, F, n.x, n.y, n.z, n.w, tv);
     vac[slot] = n;
     return n;
 }
@@ -280,19 +279,53 @@ __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, SubParam
     next[i] = atomicExch(&head[d], i);
 }
 
-__global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S, const PhaseInfo* __restrict__ ph,
-                                int* dmin, int* head, const int* __restrict__ next, Segment* segs, int* members,
-                                uint8_t* mactive, DevCounters* ctr)
+// Block-aggregated allocation: one atomic per block, offsets in thread (= slot) order inside the
+// block, so consecutive segments/rows are spatially close (slots are numbered in site order) and a
+// 128-row tile of the barrier kernel touches few lattice pages.  Returns this thread's exclusive
+// offset; `total` receives the block sum.  blockDim.x must be 256.
+__device__ __forceinline__ int block_alloc(int v, unsigned long long* counter)
+{
+    __shared__ int wsum[8];
+    __shared__ int base_s;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < 8; ++w) { const int t = wsum[w]; wsum[w] = tot; tot += t; }
+        base_s = tot ? (int)atomicAdd(counter, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    const int r = base_s + wsum[wid] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S,
+                                                       const PhaseInfo* __restrict__ ph, int* dmin, int* head,
+                                                       const int* __restrict__ next, Segment* segs, int* members,
+                                                       uint8_t* mactive, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nvac) return;
-    long long d; int sec;
-    dom_sector(vac[i], S, d, sec);
-    if (sec != ph->sector || dmin[d] != i) return;    // the minimum slot owns the domain
+    long long d = 0;
+    int sec = -1;
+    bool owner = false;
     int cnt = 0;
-    for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
-    const int off = (int)atomicAdd(&ctr->total, (unsigned long long)cnt);
-    const int seg = (int)atomicAdd(&ctr->nseg, 1ull);
+    if (i < nvac) {
+        dom_sector(vac[i], S, d, sec);
+        owner = (sec == ph->sector && dmin[d] == i);  // the minimum slot owns the domain
+        if (owner)
+            for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
+    }
+    const int off = block_alloc(cnt, &ctr->total);
+    const int seg = block_alloc(owner ? 1 : 0, &ctr->nseg);
+    if (!owner) return;
     int c = 0;
     for (int j = head[d]; j >= 0; j = next[j]) members[off + (c++)] = j;
     for (int a = 1; a < cnt; ++a) {                     // insertion sort by slot id
@@ -310,18 +343,23 @@ __global__ void segments_kernel(const int4* __restrict__ vac, int nvac, SubParam
 }
 
 // rows of this inner iteration = active members of running segments; also resets nrun
-__global__ void rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
-                            const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr)
+__global__ void __launch_bounds__(256) rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
+                                                   const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr)
 {
     const int nseg = (int)ctr->nseg;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
-        const Segment sg = segs[s];
-        if (!sg.running) continue;
-        for (int a = 0; a < sg.cnt; ++a)
-            if (mactive[sg.off + a]) {
-                const int r = (int)atomicAdd(&ctr->nrows, 1ull);
-                rows[r] = members[sg.off + a];
-            }
+    for (int s0 = blockIdx.x * blockDim.x; s0 < nseg; s0 += gridDim.x * blockDim.x) {   // block-uniform loop
+        const int s = s0 + threadIdx.x;
+        Segment sg;
+        int m = 0;
+        if (s < nseg) {
+            sg = segs[s];
+            if (sg.running)
+                for (int a = 0; a < sg.cnt; ++a) m += mactive[sg.off + a] ? 1 : 0;
+        }
+        int r = block_alloc(m, &ctr->nrows);
+        if (m)
+            for (int a = 0; a < sg.cnt; ++a)
+                if (mactive[sg.off + a]) rows[r++] = members[sg.off + a];
     }
 }
 
@@ -337,8 +375,11 @@ __global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTabl
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
         Segment sg = segs[s];
         if (!sg.running) continue;
-        double* buf = scratch + 4 * (size_t)sg.off;   // disjoint per segment: 2P-1 <= 4*cnt
-        int* idx = iscratch + sg.off;
+        double lbuf[32];                               // small competing sets: tree in registers/L1
+        int lidx[16];
+        const bool small = sg.cnt <= 16;
+        double* buf = small ? lbuf : scratch + 4 * (size_t)sg.off;   // disjoint per segment: 2P-1 <= 4*cnt
+        int* idx = small ? lidx : iscratch + sg.off;
         int m = 0;
         for (int a = 0; a < sg.cnt; ++a)
             if (mactive[sg.off + a]) {
@@ -499,12 +540,13 @@ __global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords
     if (c == 0) return;
     int pos = boff[blockIdx.x] + wbase + incl - c;
     const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+    const long long csites = 2ll * F.L[0] * F.L[1] * F.L[2];      // canonical sites per voxel
     for (int q = 0; q < 4; ++q)
         for (int b = 0; b < 4; ++b)
             if (((ws[q] >> (8 * b)) & 0xFF) == kVac) {
                 const long long site = wi * 16 + q * 4 + b;
-                const int vox = (int)(site / F.sites);
-                const long long li = site - (long long)vox * F.sites;
+                const int vox = (int)(site / csites);
+                const long long li = site - (long long)vox * csites;
                 const int bb = (int)(li & 1);
                 const long long cell = li >> 1;
                 const int x = (int)(cell % F.L[0]);
@@ -512,6 +554,37 @@ __global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords
                 const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
                 vac[pos++] = make_int4(vox, 2 * x + bb, 2 * y + bb, 2 * z + bb);
             }
+}
+
+// canonical (x fastest, basis interleaved) <-> storage (halo + ghosts) layout conversions
+__global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_t* storage, Frame F, long long ncanon)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncanon) return;
+    const long long csites = 2ll * F.L[0] * F.L[1] * F.L[2];
+    const int vox = (int)(i / csites);
+    const long long li = i - (long long)vox * csites;
+    const int b = (int)(li & 1);
+    const long long cell = li >> 1;
+    const int x = (int)(cell % F.L[0]);
+    const int y = (int)((cell / F.L[0]) % F.L[1]);
+    const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
+    write_site(storage, F, vox, 2 * x + b, 2 * y + b, 2 * z + b, canon[i]);
+}
+
+__global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uint8_t* canon, Frame F, long long ncanon)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncanon) return;
+    const long long csites = 2ll * F.L[0] * F.L[1] * F.L[2];
+    const int vox = (int)(i / csites);
+    const long long li = i - (long long)vox * csites;
+    const int b = (int)(li & 1);
+    const long long cell = li >> 1;
+    const int x = (int)(cell % F.L[0]);
+    const int y = (int)((cell / F.L[0]) % F.L[1]);
+    const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
+    canon[i] = storage[site_of(F, vox, 2 * x + b, 2 * y + b, 2 * z + b)];
 }
 
 // vstart[v] = first slot whose voxel >= v (slots are in site order, hence voxel-major)

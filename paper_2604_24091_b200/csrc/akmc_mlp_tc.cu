@@ -1,19 +1,21 @@
-// akmc_mlp_tc.cu -- fused gather -> encode -> barrier MLP (tcgen05) -> Arrhenius rates, sm_100a.
+// akmc_mlp_tc.cu -- fused gather -> encode -> barrier MLP (3 x tcgen05) -> Arrhenius rates, sm_100a.
 //
-// Persistent kernel (<= one CTA per SM); each CTA loops over tiles of 128 vacancies (rows):
-//   1. gather the 64-site window of every row and encode it sparsely: the
-//      one-hot 448-vector is summarised by its non-Fe features f = 7*slot + species (A5);
-//   2. layer 1 as a Fe-referenced embedding bag accumulated in FP64 (exact algebra: the Fe rows
-//      are folded into the bias); one warp per row, lanes over columns, coalesced 2 KiB W1' rows;
-//      ReLU, rounded to FP32 and split into fp16 hi + lo*2^11, stored K-major SWIZZLE_128B;
-//   3. layer 2 (256x256, "swarm gathering" GEMM) on the 5th-gen tensor cores:
-//      D1 = Ahi*Bhi, D2 = Ahi*Blo + Alo*Bhi accumulated in TMEM (FP32); W2 streamed through a
-//      4-stage cp.async.bulk + mbarrier ring; one elected thread issues tcgen05.mma;
-//   4. epilogue from TMEM (tcgen05.ld): h2 = ReLU(D1 + 2^-11 D2 + b2), layer 3 (256x8) as FP32
-//      16-term partials folded into FP64, E = max(0, out), Gamma = nu0 * det_exp(-E/kT) with the
-//      feasibility mask (Eq. 1, Eq. 8).
-// The split is FP32-equivalent (22-bit products, FP32 accumulation), the paper's "matrix
-// multiplication ... executed in FP32"; DESIGN.md sec. 6 gives the error budget.
+// Persistent kernel (<= one CTA per SM, 256 threads); each CTA loops over tiles of 128 vacancies:
+//   G  gather the 64-site window of every row: 2 threads per row, linear-offset
+//      fast path for windows that do not wrap;
+//   X  encode: one-hot over the 6 non-Fe species, X[m][6*slot + s-1] = [sigma_slot == s] (exact in
+//      fp16; the Fe column is folded into the bias, A5), K1 = 384, K-major SWIZZLE_128B in smem;
+//   M1 layer 1 on tcgen05: D1 = X*W1'hi, D2 = X*W1'lo (W1' = W1 - W1[slot,Fe], scaled by 2^s1 and
+//      split hi + lo*2^-11; every product is exact, FP32 accumulation in TMEM);
+//   E1 h1 = ReLU(b1' + 2^-s1 (D1 + 2^-11 D2)) with an error-free FP32 TwoSum against b1' (hi+lo),
+//      rounded to FP32, split into fp16 hi + lo*2^11 -> A (smem, SW128);
+//   M2 layer 2 (256x256, "swarm gathering" GEMM): D1 = Ahi*W2hi, D2 = Ahi*W2lo + Alo*W2hi;
+//   E2 h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> split -> A;
+//   M3 layer 3 (256x8 padded to N = 16) with 4 K-groups of 64 in separate TMEM accumulators;
+//   E3 E = max(0, b3 + 2^-s3 sum_g (Da_g + 2^-11 Db_g)) in FP64; Gamma = nu0 det_exp(-E/kT), masked.
+// W1' and W2 are streamed through one continuous 4-stage cp.async.bulk + mbarrier ring (40 chunks of
+// 16 KiB per tile) by a single control thread that also issues every tcgen05.mma.  The 3-pass fp16
+// split is FP32-equivalent ("matrix multiplication ... executed in FP32"); DESIGN.md sec. 6.
 #include "akmc_mlp_tc.cuh"
 #include <cuda_fp16.h>
 
@@ -22,28 +24,31 @@ namespace akmc {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kNnzCap = kWin;                  // non-Fe features per row (<= 64)
-constexpr uint32_t kAtomBytes = kTileM * 128;  // one SW128 K-atom (64 fp16 of K) of the A tile: 16 KiB
-constexpr uint32_t kLboB = (kHid / 8) * 128;   // K-direction core-matrix stride of a B chunk split: 4096 B
-constexpr uint32_t kSboB = 128;                // B: 8-row group stride (no swizzle)
-constexpr uint32_t kSboA = 1024;               // A: 8-row group stride (SWIZZLE_128B atom)
+constexpr uint32_t kAtomBytes = kTileM * 128;  // one SW128 K-atom (64 fp16 of K) of a 128-row tile: 16 KiB
+constexpr uint32_t kLboB = (kHid / 8) * 128;   // ring chunk split (N = 256, K = 16): K-dir core-matrix stride
+constexpr uint32_t kLboW3 = (kN3 / 8) * 128;   // W3 image (N = 16): K-dir core-matrix stride = 256 B
+constexpr uint32_t kSboNoSw = 128;             // no-swizzle 8-row group stride
+constexpr uint32_t kSboA = 1024;               // SW128 8-row group stride
+constexpr int kWinStride = 68;                 // window bytes per row in smem (17 words: conflict-free)
 
 // smem carve-up (offsets from a 1024-aligned base)
-constexpr size_t kOffAhi = 0;
-constexpr size_t kOffAlo = kOffAhi + kABytes;
-constexpr size_t kOffB = kOffAlo + kABytes;
-constexpr size_t kOffNnz = kOffB + (size_t)kStages * kStageBytes;      // uint16 [128][64] (reused: double [128][8])
-constexpr size_t kOffW3 = kOffNnz + (size_t)kTileM * kNnzCap * 2;      // float [256][8]
-constexpr size_t kOffB2 = kOffW3 + (size_t)kHid * 8 * 4;               // float [256]
-constexpr size_t kOffB1 = kOffB2 + (size_t)kHid * 4;                   // double [256]
-constexpr size_t kOffSlot = kOffB1 + (size_t)kHid * 8;                 // int [128]
-constexpr size_t kOffCnt = kOffSlot + (size_t)kTileM * 4;              // uint8 [128]
-constexpr size_t kOffMask = kOffCnt + kTileM;                          // uint8 [128]
-constexpr size_t kOffBar = kOffMask + kTileM;                          // 8-B aligned
-constexpr size_t kOffTmem = kOffBar + 16 * 8;
+constexpr size_t kOffA = 0;                                   // A_hi [0,64K), A_lo [64K,128K); X overlays [0,96K)
+constexpr size_t kOffB = kOffA + 2 * (size_t)kABytes;         // ring 4 x 16 KiB
+constexpr size_t kOffW3 = kOffB + (size_t)kStages * kStageBytes;   // W3 image 16 KiB
+constexpr size_t kOffWin = kOffW3 + 2 * (size_t)kW3SplitBytes;     // uint8 [128][68]
+constexpr size_t kOffB1h = kOffWin + (size_t)kTileM * kWinStride;  // float [256]
+constexpr size_t kOffB1l = kOffB1h + kHid * 4;                     // float [256]
+constexpr size_t kOffB2 = kOffB1l + kHid * 4;                      // float [256]
+constexpr size_t kOffOffl = kOffB2 + kHid * 4;                     // int [2][64]
+constexpr size_t kOffSlot = kOffOffl + 2 * kWin * 4;               // int [128]
+constexpr size_t kOffMask = kOffSlot + kTileM * 4;                 // uint8 [128]
+constexpr size_t kOffBar = kOffMask + kTileM;                      // 8-B aligned barriers
+constexpr int kNumBars = 2 * kStages + 4;                          // full[4], empty[4], done1..3, w3
+constexpr size_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr size_t kSmemUsed = kOffTmem + 16;
-constexpr size_t kSmemTotal = kSmemUsed + 1024;                        // alignment slack
+constexpr size_t kSmemTotal = kSmemUsed + 1024;                    // alignment slack
 static_assert(kSmemTotal <= 232448, "shared memory budget");
+static_assert(kOffBar % 8 == 0, "barrier alignment");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
@@ -89,6 +94,11 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
+__device__ __forceinline__ uint64_t desc_a(uint32_t base, int kstep)   // SW128 A/X operand, K-step of 16
+{
+    return umma_desc(base + (uint32_t)(kstep >> 2) * kAtomBytes + (uint32_t)(kstep & 3) * 32u, 16, kSboA, 2);
+}
+
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
 {
     asm volatile(
@@ -105,6 +115,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar)
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
 {
@@ -116,6 +127,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_half2(__half a, __half b)
@@ -123,11 +141,30 @@ __device__ __forceinline__ uint32_t pack_half2(__half a, __half b)
     return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
 
-// byte offset of (row m, 8-column group kg) in a K-major SWIZZLE_128B A tile of 128 rows x 256 K
-__device__ __forceinline__ uint32_t a_sw128_off(int m, int kg)
+// byte offset of (row m, 8-column group kg) in a K-major SWIZZLE_128B tile of 128 rows
+__device__ __forceinline__ uint32_t sw128_off(int m, int kg)
 {
     return (uint32_t)(kg >> 3) * kAtomBytes + (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u +
            (uint32_t)(((kg & 7) ^ (m & 7)) << 4);
+}
+
+// split 8 FP32 values into fp16 hi and lo*2^11 and store them at (m, kg) of the A tile
+__device__ __forceinline__ void store_split8(uint8_t* A_hi, uint8_t* A_lo, int m, int kg, const float (&h)[8],
+                                             unsigned long long& ovf)
+{
+    __half hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float v = h[i];
+        if (v > 60000.0f) { v = 60000.0f; ++ovf; }
+        hi[i] = __float2half_rn(v);
+        lo[i] = __float2half_rn((v - __half2float(hi[i])) * kLoScale);
+    }
+    const uint32_t off = sw128_off(m, kg);
+    *reinterpret_cast<uint4*>(A_hi + off) =
+        make_uint4(pack_half2(hi[0], hi[1]), pack_half2(hi[2], hi[3]), pack_half2(hi[4], hi[5]), pack_half2(hi[6], hi[7]));
+    *reinterpret_cast<uint4*>(A_lo + off) =
+        make_uint4(pack_half2(lo[0], lo[1]), pack_half2(lo[2], lo[3]), pack_half2(lo[4], lo[5]), pack_half2(lo[6], lo[7]));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_constant__ MlpTcParams p)
@@ -136,35 +173,44 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
     const int nrows = p.nrows_dev ? *p.nrows_dev : p.nrows_host;
     const int ntiles = (nrows + kTileM - 1) / kTileM;
     if ((int)blockIdx.x >= ntiles) return;         // uniform early exit: no barrier/TMEM touched
+    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total_chunks = my_tiles * kChunksTile;
 
-    // 1024-B aligned base, keeping shared-space provenance (so accesses compile to LDS/STS)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* A_hi = smem + kOffAhi;
-    uint8_t* A_lo = smem + kOffAlo;
+    uint8_t* A_hi = smem + kOffA;
+    uint8_t* A_lo = smem + kOffA + kABytes;
+    uint8_t* Xs = smem + kOffA;                    // layer-1 operand overlays A
     uint8_t* Bst = smem + kOffB;
-    uint16_t* nnz = reinterpret_cast<uint16_t*>(smem + kOffNnz);
-    float* sW3 = reinterpret_cast<float*>(smem + kOffW3);
+    uint8_t* W3s = smem + kOffW3;
+    uint8_t* win = smem + kOffWin;
+    float* sb1h = reinterpret_cast<float*>(smem + kOffB1h);
+    float* sb1l = reinterpret_cast<float*>(smem + kOffB1l);
     float* sb2 = reinterpret_cast<float*>(smem + kOffB2);
-    double* sb1 = reinterpret_cast<double*>(smem + kOffB1);
+
     int* sslot = reinterpret_cast<int*>(smem + kOffSlot);
-    uint8_t* scnt = smem + kOffCnt;
     uint8_t* smask = smem + kOffMask;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);   // full[4], empty[4], done
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
-    double* spartd = reinterpret_cast<double*>(smem + kOffNnz);    // aliases nnz after layer 1
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t bar_full0 = smem_u32(&bars[0]);
     const uint32_t bar_empty0 = smem_u32(&bars[kStages]);
-    const uint32_t bar_done = smem_u32(&bars[2 * kStages]);
+    const uint32_t bar_done1 = smem_u32(&bars[2 * kStages + 0]);
+    const uint32_t bar_done2 = smem_u32(&bars[2 * kStages + 1]);
+    const uint32_t bar_done3 = smem_u32(&bars[2 * kStages + 2]);
+    const uint32_t bar_w3 = smem_u32(&bars[2 * kStages + 3]);
+    const bool ctrl = (warp == 1 && lane == 0);    // control thread: ring loads + every tcgen05.mma
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full0 + 8 * s, 1);
             mbar_init(bar_empty0 + 8 * s, 1);
         }
-        mbar_init(bar_done, 1);
+        mbar_init(bar_done1, 1);
+        mbar_init(bar_done2, 1);
+        mbar_init(bar_done3, 1);
+        mbar_init(bar_w3, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -172,229 +218,298 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                      ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < kHid * 8; i += kThreads) sW3[i] = p.W3[i];
-    for (int i = threadIdx.x; i < kHid; i += kThreads) { sb2[i] = p.b2[i]; sb1[i] = p.b1p[i]; }
+    for (int i = threadIdx.x; i < kHid; i += kThreads) { sb1h[i] = p.b1hi[i]; sb1l[i] = p.b1lo[i]; sb2[i] = p.b2[i]; }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t idesc = (1u << 4)                         // D = F32
-                         | ((uint32_t)(kHid >> 3) << 17)     // N = 256
-                         | ((uint32_t)(kTileM >> 4) << 24);  // M = 128; A, B = F16, K-major
+    const uint32_t idesc256 = (1u << 4) | ((uint32_t)(kHid >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+    const uint32_t idesc16 = (1u << 4) | ((uint32_t)(kN3 >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
 
-    // W2 chunk gc (global over this CTA's tiles) lives in stage gc % kStages; its u-th use is u = gc / kStages
-    auto load_chunk = [&](int gc) {
-        const int s = gc % kStages;
-        const int u = gc / kStages;
-        if (u > 0) mbar_wait(bar_empty0 + 8 * s, (u - 1) & 1);
+    // ring: chunk x (global over this CTA's tiles) = image chunk x % 40, in stage x % 4
+    auto load_chunk = [&](int x) {
+        const int s = x % kStages;
+        if (x >= kStages) mbar_wait(bar_empty0 + 8 * s, ((x - kStages) / kStages) & 1);
         mbar_expect_tx(bar_full0 + 8 * s, kStageBytes);
         bulk_g2s(smem_u32(Bst + (size_t)s * kStageBytes),
-                 reinterpret_cast<const uint8_t*>(p.Bimg) + (size_t)(gc % kNChunks) * kStageBytes, kStageBytes,
+                 reinterpret_cast<const uint8_t*>(p.Bimg) + (size_t)(x % kChunksTile) * kStageBytes, kStageBytes,
                  bar_full0 + 8 * s);
     };
+    // consume chunk x: wait for its bytes; after the MMAs are committed, refill the ring 3 ahead
+    auto chunk_ready = [&](int x) {
+        mbar_wait(bar_full0 + 8 * (x % kStages), (x / kStages) & 1);
+        tc_fence_after();
+        return smem_u32(Bst + (size_t)(x % kStages) * kStageBytes);
+    };
+    auto chunk_done = [&](int x) {
+        umma_commit(bar_empty0 + 8 * (x % kStages));
+        if (x + kStages - 1 < total_chunks) load_chunk(x + kStages - 1);
+    };
+    if (ctrl) {
+        mbar_expect_tx(bar_w3, 2 * kW3SplitBytes);
+        bulk_g2s(smem_u32(W3s), p.W3img, 2 * kW3SplitBytes, bar_w3);
+        for (int x = 0; x < kStages - 1 && x < total_chunks; ++x) load_chunk(x);
+    }
 
+    const long long tk0 = clock64();
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int tile0 = tile * kTileM;
-        const int gc0 = it * kNChunks;
-        // producer: the first stages of W2 stream in while the rows are gathered and encoded
-        if (threadIdx.x == 0)
-            for (int c = 0; c < kStages; ++c) load_chunk(gc0 + c);
+        const int cx0 = it * kChunksTile;
+        long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const bool timing = p.phase_cycles && threadIdx.x == 64;
+        if (timing) tp[0] = clock64();
 
-        // ---- gather + sparse encode (threads 0..127, one row each)
-        if (threadIdx.x < kTileM) {
-            const int r = threadIdx.x;
-            const int g = tile0 + r;
-            int cnt = 0, mask = 0, slot = -1;
-            if (g < nrows) {
-                uint8_t w[kWin];
-                if (p.windows) {
-                    slot = g;
-                    const uint4* src = reinterpret_cast<const uint4*>(p.windows + (size_t)g * kWin);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 v = __ldg(src + q);
-                        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                        for (int b = 0; b < 16; ++b) w[16 * q + b] = (uint8_t)(wd[b >> 2] >> (8 * (b & 3)));
-                    }
-                } else {
-                    slot = p.rows ? p.rows[g] : g;
-                    const int4 v = p.vac[slot];
-#pragma unroll
-                    for (int j = 0; j < kWin; ++j)
-                        w[j] = __ldg(p.species + neighbour_site(p.F, v, p.G.off[j][0], p.G.off[j][1], p.G.off[j][2]));
-                }
-#pragma unroll
-                for (int j = 0; j < kWin; ++j) {
-                    const int s = w[j];
-                    if (s != kFe) nnz[r * kNnzCap + (cnt++)] = (uint16_t)(kSpecies * j + s);
-                    if (j < kHops && s != kVac) mask |= 1 << j;
-                }
-            }
-            scnt[r] = (uint8_t)cnt;
-            smask[r] = (uint8_t)mask;
-            sslot[r] = slot;
-        }
-        __syncthreads();
-
-        // ---- layer 1: one warp per row (4 rows in flight), lane = 8-column group; FP64 accumulate
+        // ---- G: gather, one warp per row (lane = window slots j and j+32), 16 rows per warp in two
+        //      batches of 8 so that the dependent loads (row -> vacancy -> window) overlap across rows;
+        //      one LDG instruction then touches the ~10 bricks (L2 lines) of one window, not 32 windows
         {
-            double bias[8];
+            const int ox0 = p.G.off[lane][0], oy0 = p.G.off[lane][1], oz0 = p.G.off[lane][2];
+            const int ox1 = p.G.off[lane + 32][0], oy1 = p.G.off[lane + 32][1], oz1 = p.G.off[lane + 32][2];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) bias[i] = sb1[lane * 8 + i];
-            unsigned long long ovf = 0;
-            for (int grp = 0; grp < kTileM / 32; ++grp) {
-                int rr[4], cc[4];
-                int nmax = 0;
+            for (int half8 = 0; half8 < 2; ++half8) {
+                uint32_t b0[8], b1[8];
+                int sl[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    rr[j] = warp + 8 * (4 * grp + j);
-                    cc[j] = scnt[rr[j]];
-                    nmax = max(nmax, cc[j]);
-                }
-                double acc[4][8];
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[j][i] = bias[i];
-                for (int q = 0; q < nmax; ++q) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (q < cc[j]) {
-                            const int f = nnz[rr[j] * kNnzCap + q];
-                            const double2* wp = reinterpret_cast<const double2*>(p.W1p + (size_t)f * kHid + lane * 8);
-                            const double2 x0 = __ldg(wp), x1 = __ldg(wp + 1), x2 = __ldg(wp + 2), x3 = __ldg(wp + 3);
-                            acc[j][0] += x0.x; acc[j][1] += x0.y; acc[j][2] += x1.x; acc[j][3] += x1.y;
-                            acc[j][4] += x2.x; acc[j][5] += x2.y; acc[j][6] += x3.x; acc[j][7] += x3.y;
+                for (int i = 0; i < 8; ++i) {
+                    const int r = warp + 8 * (8 * half8 + i);
+                    const int g = tile0 + r;
+                    b0[i] = 0; b1[i] = 0; sl[i] = -1;
+                    if (g < nrows) {
+                        if (p.windows) {
+                            sl[i] = g;
+                            b0[i] = __ldg(p.windows + (size_t)g * kWin + lane);
+                            b1[i] = __ldg(p.windows + (size_t)g * kWin + lane + 32);
+                        } else {
+                            const int slot = p.rows ? __ldg(p.rows + g) : g;
+                            const int4 v = p.vac[slot];
+                            sl[i] = slot;
+                            b0[i] = __ldg(p.species + site_of(p.F, v.x, v.y + ox0, v.z + oy0, v.w + oz0));
+                            b1[i] = __ldg(p.species + site_of(p.F, v.x, v.y + ox1, v.z + oy1, v.w + oz1));
                         }
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    __half hi[8], lo[8];
+                for (int i = 0; i < 8; ++i) {
+                    const int r = warp + 8 * (8 * half8 + i);
+                    win[r * kWinStride + lane] = (uint8_t)b0[i];
+                    win[r * kWinStride + lane + 32] = (uint8_t)b1[i];
+                    const unsigned feas = __ballot_sync(0xffffffffu, lane < kHops && b0[i] != (uint32_t)kVac);
+                    if (lane == 0) {
+                        smask[r] = (uint8_t)(feas & 0xFFu);
+                        sslot[r] = sl[i];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (timing) tp[1] = clock64();
+
+        // ---- X: one-hot layer-1 operand (K = 384, SW128); thread = (row, half of the 48 chunks)
+        {
+            // thread (row m, half hx) owns feature chunks [24hx, 24hx+24) == window slots [32hx, 32hx+32):
+            // zero-fill them, then write fp16 1.0 at f = 6*slot + species - 1 for every non-Fe slot
+            const int m = 32 * (warp & 3) + lane;
+            const int hx = warp >> 2;
+            const uint32_t* wr = reinterpret_cast<const uint32_t*>(win + m * kWinStride) + 8 * hx;
+            uint32_t w32[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) w32[q] = wr[q];
+#pragma unroll
+            for (int kgi = 0; kgi < 24; ++kgi)
+                *reinterpret_cast<uint4*>(Xs + sw128_off(m, 24 * hx + kgi)) = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+                const int s = (int)((w32[jj >> 2] >> (8 * (jj & 3))) & 0xFFu);
+                if (s != kFe) {
+                    const int f = (kSpecies - 1) * (32 * hx + jj) + s - 1;
+                    *reinterpret_cast<__half*>(Xs + sw128_off(m, f >> 3) + 2 * (f & 7)) = __ushort_as_half(0x3C00);
+                }
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (timing) tp[2] = clock64();
+
+        // ---- M1: layer 1 on tcgen05 (24 K-steps; W1' hi/lo from the ring)
+        if (ctrl) {
+            tc_fence_after();
+            const uint32_t xb = smem_u32(Xs);
+            for (int c = 0; c < kChunksL1; ++c) {
+                const int x = cx0 + c;
+                const uint32_t bh = chunk_ready(x);
+                const uint64_t da = desc_a(xb, c);
+                umma_f16(tmem + 0, da, umma_desc(bh, kLboB, kSboNoSw, 0), idesc256, c > 0 ? 1u : 0u);
+                umma_f16(tmem + kHid, da, umma_desc(bh + kSplitBytes, kLboB, kSboNoSw, 0), idesc256, c > 0 ? 1u : 0u);
+                chunk_done(x);
+            }
+            umma_commit(bar_done1);
+        }
+        __syncwarp();
+        mbar_wait(bar_done1, it & 1);
+        tc_fence_after();
+        if (timing) tp[3] = clock64();
+
+        // ---- E1: h1 = ReLU(b1' + 2^-s1 (D1 + 2^-11 D2)) -> split -> A
+        const int q4 = warp & 3, half = warp >> 2;
+        const int row = 32 * q4 + lane;
+        const uint32_t tlane = tmem + ((uint32_t)(32 * q4) << 16);
+        unsigned long long ovf = 0;
+        {
+            const float s1 = p.s1_unscale, s1lo = p.s1_unscale * (1.0f / kLoScale);
+            for (int cb = 0; cb < 8; ++cb) {
+                const int col = half * 128 + cb * 16;
+                uint32_t d1[16], d2[16];
+                tmem_ld16(tlane + (uint32_t)col, d1);
+                tmem_ld16(tlane + (uint32_t)(kHid + col), d2);
+                tmem_wait_ld();
+#pragma unroll
+                for (int g8 = 0; g8 < 2; ++g8) {
+                    float h[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        float h = (float)(acc[j][i] > 0.0 ? acc[j][i] : 0.0);
-                        if (h > 60000.0f) { h = 60000.0f; ++ovf; }
-                        hi[i] = __float2half_rn(h);
-                        lo[i] = __float2half_rn((h - __half2float(hi[i])) * kLoScale);
+                        const int n = col + 8 * g8 + i;
+                        const float a = __uint_as_float(d1[8 * g8 + i]) * s1;        // exact (power of 2)
+                        const float b = sb1h[n];
+                        const float s = __fadd_rn(a, b);                            // TwoSum(a, b)
+                        const float bb = __fsub_rn(s, a);
+                        const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+                        const float small = __fmaf_rn(__uint_as_float(d2[8 * g8 + i]), s1lo, sb1l[n]);
+                        const float v = __fadd_rn(s, __fadd_rn(err, small));
+                        h[i] = v > 0.0f ? v : 0.0f;
                     }
-                    const uint32_t off = a_sw128_off(rr[j], lane);
-                    *reinterpret_cast<uint4*>(A_hi + off) = make_uint4(pack_half2(hi[0], hi[1]), pack_half2(hi[2], hi[3]),
-                                                                       pack_half2(hi[4], hi[5]), pack_half2(hi[6], hi[7]));
-                    *reinterpret_cast<uint4*>(A_lo + off) = make_uint4(pack_half2(lo[0], lo[1]), pack_half2(lo[2], lo[3]),
-                                                                       pack_half2(lo[4], lo[5]), pack_half2(lo[6], lo[7]));
+                    store_split8(A_hi, A_lo, row, (col >> 3) + g8, h, ovf);
                 }
             }
-            if (ovf && p.overflow) atomicAdd(p.overflow, ovf);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> async proxy
+        fence_async_smem();
+        tc_fence_before();
         __syncthreads();
+        if (timing) tp[4] = clock64();
 
-        // ---- roles: W2 producer (warp 0), MMA issuer (warp 1)
-        if (warp == 0) {
-            if (lane == 0)
-                for (int c = kStages; c < kNChunks; ++c) load_chunk(gc0 + c);
-            __syncwarp();
-        } else if (warp == 1) {
-            if (lane == 0) {
-                tc_fence_after();
-                const uint32_t a_hi = smem_u32(A_hi), a_lo = smem_u32(A_lo);
-                for (int c = 0; c < kNChunks; ++c) {        // one UMMA K-step (16) per chunk
-                    const int gc = gc0 + c;
-                    const int s = gc % kStages;
-                    mbar_wait(bar_full0 + 8 * s, (gc / kStages) & 1);
-                    tc_fence_after();
-                    const uint32_t aoff = (uint32_t)(c >> 2) * kAtomBytes + (uint32_t)(c & 3) * 32u;
-                    const uint64_t dah = umma_desc(a_hi + aoff, 16, kSboA, 2);
-                    const uint64_t dal = umma_desc(a_lo + aoff, 16, kSboA, 2);
-                    const uint32_t b_hi = smem_u32(Bst + (size_t)s * kStageBytes);
-                    const uint64_t dbh = umma_desc(b_hi, kLboB, kSboB, 0);
-                    const uint64_t dbl = umma_desc(b_hi + kSplitBytes, kLboB, kSboB, 0);
-                    umma_f16(tmem + 0, dah, dbh, idesc, c > 0 ? 1u : 0u);
-                    umma_f16(tmem + kHid, dah, dbl, idesc, c > 0 ? 1u : 0u);
-                    umma_f16(tmem + kHid, dal, dbh, idesc, 1u);
-                    umma_commit(bar_empty0 + 8 * s);       // stage free once these MMAs retire
-                }
-                umma_commit(bar_done);
+        // ---- M2: layer 2 on tcgen05 (16 K-steps; W2 hi/lo from the ring)
+        if (ctrl) {
+            tc_fence_after();
+            const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo);
+            for (int c = 0; c < kChunksL2; ++c) {
+                const int x = cx0 + kChunksL1 + c;
+                const uint32_t bh = chunk_ready(x);
+                const uint64_t dah = desc_a(ah, c), dal = desc_a(al, c);
+                const uint64_t dbh = umma_desc(bh, kLboB, kSboNoSw, 0);
+                const uint64_t dbl = umma_desc(bh + kSplitBytes, kLboB, kSboNoSw, 0);
+                umma_f16(tmem + 0, dah, dbh, idesc256, c > 0 ? 1u : 0u);
+                umma_f16(tmem + kHid, dah, dbl, idesc256, c > 0 ? 1u : 0u);
+                umma_f16(tmem + kHid, dal, dbh, idesc256, 1u);
+                chunk_done(x);
             }
-            __syncwarp();
+            umma_commit(bar_done2);
         }
-
-        // ---- epilogue: TMEM -> registers, ReLU, layer 3, rates
-        mbar_wait(bar_done, it & 1);
+        __syncwarp();
+        mbar_wait(bar_done2, it & 1);
         tc_fence_after();
+        if (timing) tp[5] = clock64();
+
+        // ---- E2: h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> split -> A
         {
-            const int q = warp & 3;
-            const int half = warp >> 2;
-            const int row = 32 * q + lane;
-            const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16);
-            // layer 3: FP32 products summed in chunks of 16 columns, chunk partials folded into FP64
-            // (a single long FP32 chain loses ~1e-6 eV when one large gate term dominates the sum)
-            double acc[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] = 0.0;
             const float inv_lo = 1.0f / kLoScale;
             for (int cb = 0; cb < 8; ++cb) {
                 const int col = half * 128 + cb * 16;
                 uint32_t d1[16], d2[16];
-                tmem_ld16(tbase + (uint32_t)col, d1);
-                tmem_ld16(tbase + (uint32_t)(kHid + col), d2);
+                tmem_ld16(tlane + (uint32_t)col, d1);
+                tmem_ld16(tlane + (uint32_t)(kHid + col), d2);
                 tmem_wait_ld();
-                float part[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) part[k] = 0.0f;
+                for (int g8 = 0; g8 < 2; ++g8) {
+                    float h[8];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int n = col + i;
-                    float z = fmaf(__uint_as_float(d2[i]), inv_lo, __uint_as_float(d1[i]));
-                    z = fmaf(z, p.w2_unscale, sb2[n]);
-                    const float h = fmaxf(z, 0.0f);
-                    const float4 w0 = *reinterpret_cast<const float4*>(sW3 + n * 8);
-                    const float4 w1 = *reinterpret_cast<const float4*>(sW3 + n * 8 + 4);
-                    part[0] = fmaf(h, w0.x, part[0]); part[1] = fmaf(h, w0.y, part[1]);
-                    part[2] = fmaf(h, w0.z, part[2]); part[3] = fmaf(h, w0.w, part[3]);
-                    part[4] = fmaf(h, w1.x, part[4]); part[5] = fmaf(h, w1.y, part[5]);
-                    part[6] = fmaf(h, w1.z, part[6]); part[7] = fmaf(h, w1.w, part[7]);
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) acc[k] += (double)part[k];
-            }
-            if (half == 1) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) spartd[row * 8 + k] = acc[k];
-            }
-            tc_fence_before();
-            __syncthreads();
-            if (half == 0) {
-                const int slot = sslot[row];
-                if (slot >= 0) {
-                    const int mask = smask[row];
-                    double Rs = 0.0;
-                    double Ek[8], Gk[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const double out = (acc[k] + spartd[row * 8 + k]) + (double)__ldg(p.b3 + k);
-                        Ek[k] = out > 0.0 ? out : 0.0;
-                        Gk[k] = ((mask >> k) & 1) ? arrhenius(Ek[k], p.P) : 0.0;
-                        Rs = __dadd_rn(Rs, Gk[k]);
+                    for (int i = 0; i < 8; ++i) {
+                        const int n = col + 8 * g8 + i;
+                        float z = __fmaf_rn(__uint_as_float(d2[8 * g8 + i]), inv_lo, __uint_as_float(d1[8 * g8 + i]));
+                        z = __fmaf_rn(z, p.s2_unscale, sb2[n]);
+                        h[i] = z > 0.0f ? z : 0.0f;
                     }
-                    if (p.E) {
-                        double2* e2 = reinterpret_cast<double2*>(p.E + (size_t)slot * 8);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) e2[k] = make_double2(Ek[2 * k], Ek[2 * k + 1]);
-                    }
-                    if (p.rates) {
-                        double2* g2 = reinterpret_cast<double2*>(p.rates + (size_t)slot * 8);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) g2[k] = make_double2(Gk[2 * k], Gk[2 * k + 1]);
-                    }
-                    if (p.Rsum) p.Rsum[slot] = Rs;
+                    store_split8(A_hi, A_lo, row, (col >> 3) + g8, h, ovf);
                 }
             }
         }
-        __syncthreads();          // spart/nnz and TMEM free for the next tile
+        if (ovf && p.overflow) atomicAdd(p.overflow, ovf);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (timing) tp[6] = clock64();
+
+        // ---- M3: layer 3 (N = 16), 4 K-groups x {hi*hi, hi*lo + lo*hi} accumulators in TMEM cols [0,128)
+        if (ctrl) {
+            if (it == 0) mbar_wait(bar_w3, 0);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo), w3 = smem_u32(W3s);
+            for (int c = 0; c < kHid / 16; ++c) {
+                const uint32_t g = (uint32_t)(c >> 2);
+                const uint32_t acc = (c & 3) ? 1u : 0u;
+                const uint64_t dah = desc_a(ah, c), dal = desc_a(al, c);
+                const uint64_t dbh = umma_desc(w3 + (uint32_t)c * 2 * kLboW3, kLboW3, kSboNoSw, 0);
+                const uint64_t dbl = umma_desc(w3 + kW3SplitBytes + (uint32_t)c * 2 * kLboW3, kLboW3, kSboNoSw, 0);
+                umma_f16(tmem + 32 * g, dah, dbh, idesc16, acc);
+                umma_f16(tmem + 32 * g + 16, dah, dbl, idesc16, acc);
+                umma_f16(tmem + 32 * g + 16, dal, dbh, idesc16, 1u);
+            }
+            umma_commit(bar_done3);
+        }
+        __syncwarp();
+        mbar_wait(bar_done3, it & 1);
+        tc_fence_after();
+
+        // ---- E3: barriers and rates (warps 0..3, one row per thread)
+        if (half == 0) {
+            double accE[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) accE[k] = 0.0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint32_t da[8], db[8];
+                tmem_ld8(tlane + (uint32_t)(32 * g), da);
+                tmem_ld8(tlane + (uint32_t)(32 * g + 16), db);
+                tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    accE[k] += (double)__uint_as_float(da[k]) + (double)__uint_as_float(db[k]) * (1.0 / 2048.0);
+            }
+            const int slot = sslot[row];
+            if (slot >= 0) {
+                const int mask = smask[row];
+                double Rs = 0.0;
+                double Ek[8], Gk[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double out = __ldg(p.b3 + k) + accE[k] * p.s3_unscale;
+                    Ek[k] = out > 0.0 ? out : 0.0;
+                    Gk[k] = ((mask >> k) & 1) ? arrhenius(Ek[k], p.P) : 0.0;
+                    Rs = __dadd_rn(Rs, Gk[k]);
+                }
+                if (p.E) {
+                    double2* e2 = reinterpret_cast<double2*>(p.E + (size_t)slot * 8);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) e2[k] = make_double2(Ek[2 * k], Ek[2 * k + 1]);
+                }
+                if (p.rates) {
+                    double2* g2 = reinterpret_cast<double2*>(p.rates + (size_t)slot * 8);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) g2[k] = make_double2(Gk[2 * k], Gk[2 * k + 1]);
+                }
+                if (p.Rsum) p.Rsum[slot] = Rs;
+            }
+        }
+        tc_fence_before();
+        __syncthreads();          // TMEM, A/X and window buffers free for the next tile
+        if (timing) {
+            tp[7] = clock64();
+            for (int ph = 0; ph < 7; ++ph) atomicAdd(p.phase_cycles + ph, (unsigned long long)(tp[ph + 1] - tp[ph]));
+            atomicAdd(p.phase_cycles + 7, 1ull);
+        }
+    }
+    if (p.phase_cycles && threadIdx.x == 64) {
+        atomicAdd(p.phase_cycles + 8, (unsigned long long)(clock64() - tk0));   // CTA loop time
+        atomicAdd(p.phase_cycles + 9, 1ull);                                    // CTAs with work
     }
     __syncthreads();
     if (warp == 2) {

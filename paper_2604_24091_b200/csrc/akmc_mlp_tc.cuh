@@ -6,13 +6,18 @@
 
 namespace akmc {
 
-constexpr int kTileM = 128;          // rows (vacancies) per CTA tile = TMEM lanes
-constexpr int kKChunk = 16;          // K per pipeline stage (one UMMA K-step)
-constexpr int kNChunks = kHid / kKChunk;
+constexpr int kTileM = 128;                    // rows (vacancies) per CTA tile = TMEM lanes
+constexpr int kK1 = kWin * (kSpecies - 1);     // layer-1 K: one-hot over the 6 non-Fe species = 384
+constexpr int kKChunk = 16;                    // K per ring stage (one UMMA K-step)
+constexpr int kChunksL1 = kK1 / kKChunk;       // 24
+constexpr int kChunksL2 = kHid / kKChunk;      // 16
+constexpr int kChunksTile = kChunksL1 + kChunksL2;   // 40 ring chunks per tile (W1' then W2)
 constexpr int kStages = 4;
-constexpr int kSplitBytes = kHid * kKChunk * 2;        // one fp16 split of a B chunk: 8 KiB
+constexpr int kSplitBytes = kHid * kKChunk * 2;        // one fp16 split of a B chunk (N = 256): 8 KiB
 constexpr int kStageBytes = 2 * kSplitBytes;           // hi + lo: 16 KiB
-constexpr int kABytes = kTileM * kHid * 2;             // one fp16 split of the A tile: 64 KiB
+constexpr int kABytes = kTileM * kHid * 2;             // one fp16 split of the A tile (K = 256): 64 KiB
+constexpr int kN3 = 16;                                // layer-3 N padded from 8 to the UMMA minimum
+constexpr int kW3SplitBytes = kN3 * kHid * 2;          // 8 KiB
 constexpr float kLoScale = 2048.0f;                    // lo parts are stored * 2^11
 
 struct MlpTcParams {
@@ -25,20 +30,23 @@ struct MlpTcParams {
     const int* rows;                 // slot ids to evaluate (nullptr => row i = slot i)
     const int* nrows_dev;            // device row count (nullptr => nrows_host)
     int nrows_host;
-    // weights (prepared at init, DESIGN.md sec. 6.2)
-    const double* W1p;               // [448][256] Fe-referenced layer-1 rows (fp64)
-    const double* b1p;               // [256] layer-1 bias + sum of Fe rows (fp64)
-    const __half* Bimg;              // [kNChunks][2][kSplitBytes/2] W2^T splits in UMMA smem image
+    // weights (prepared at init, DESIGN.md sec. 6)
+    const __half* Bimg;              // [40][2][N=256 x K=16] W1'^T (24 chunks) then W2^T (16 chunks), UMMA images
+    const __half* W3img;             // [2][N=16 x K=256] W3^T splits, UMMA image
+    const float* b1hi;               // [256] layer-1 bias b1' = b1 + sum_slot W1[slot,Fe] as a float pair
+    const float* b1lo;               // [256]
     const float* b2;                 // [256]
-    const float* W3;                 // [256][8]
-    const float* b3;                 // [8]
-    float w2_unscale;                // 2^-sb (W2 was scaled by 2^sb before splitting)
+    const double* b3;                // [8]
+    float s1_unscale;                // 2^-s1 (W1' scaled by 2^s1 before splitting)
+    float s2_unscale;                // 2^-s2
+    double s3_unscale;               // 2^-s3
     PhysParams P;
     // outputs indexed by slot (or by window index)
     double* rates;                   // [.][8] or nullptr
     double* Rsum;                    // [.]    or nullptr
     double* E;                       // [.][8] or nullptr
-    unsigned long long* overflow;    // count of |h1| beyond the fp16 range (diagnostic)
+    unsigned long long* overflow;    // count of |h| beyond the fp16 range (diagnostic)
+    unsigned long long* phase_cycles; // [8] optional: summed clock64 per tile phase (AKMC_PHASE_TIMING)
 };
 
 // smem bytes needed by the kernel

@@ -67,8 +67,13 @@ typedef struct akmc_config {
     double   kB;              /* Boltzmann constant eV/K; passed so both sides share bits  */
     double   window_s;        /* Delta_win per phase (A22); > 0 in sublattice mode                 */
     uint64_t seed;            /* Philox key (A16)                                                  */
-    int32_t  gpu_grid[3];     /* spatial decomposition over ranks; {1,1,1} (single rank) for now   */
-    int32_t  rank, world;     /* this process's rank / world size; world must equal prod(gpu_grid) */
+    int32_t  gpu_grid[3];     /* spatial decomposition over ranks (C5): the global lattice  */
+                              /* is gpu_grid x cells; rank r owns block (r%gx, r/gx%gy, r/(gx*gy)).      */
+                              /* {1,1,1} for a single rank.  world > 1 requires sublattice mode and      */
+                              /* n_voxels == 1; axes with gpu_grid == 1 stay periodic inside the block.  */
+    int32_t  rank, world;     /* this process's rank / world size; world must equal prod(gpu_grid)     */
+    uint8_t  nccl_id[128];    /* ncclUniqueId from akmc_nccl_unique_id() on rank 0, broadcast by the    */
+                              /* caller (e.g. torch.distributed); ignored when world == 1               */
 } akmc_config;
 
 typedef struct akmc_counters {
@@ -114,6 +119,14 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr);
  * seconds (may be NULL); ctr_out: counters accumulated since init (may be NULL).              */
 int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int64_t* n_vac_inout,
                double* clock_s_out, akmc_counters* ctr_out);
+
+/* Vacancies currently owned by this rank (multi-rank: vacancies migrate between blocks): global slot
+ * ids (gid_out, may be NULL) and global canonical site indices over the global lattice (site_out, may
+ * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
+int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
+
+/* Write a fresh ncclUniqueId (128 bytes) for akmc_config.nccl_id (call on rank 0 only). */
+int akmc_nccl_unique_id(uint8_t* out128);
 
 /* Per-hop rates of the current state in the handle's precision, [n_vac][8] slot order, masked
  * hops exactly 0; barriers_out (may be NULL) gets the barriers E [n_vac][8] eV.    */

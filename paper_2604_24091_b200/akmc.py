@@ -24,7 +24,8 @@ class CConfig(C.Structure):
     _fields_ = [("cells", C.c_int32 * 3), ("n_voxels", C.c_int32), ("n_species", C.c_int32),
                 ("barrier_model", C.c_int32), ("precision", C.c_int32), ("domain_cells", C.c_int32 * 3),
                 ("temperature_K", C.c_double), ("nu0", C.c_double), ("kB", C.c_double), ("window_s", C.c_double),
-                ("seed", C.c_uint64), ("gpu_grid", C.c_int32 * 3), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("seed", C.c_uint64), ("gpu_grid", C.c_int32 * 3), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_id", C.c_uint8 * 128)]
 
 
 class CCounters(C.Structure):
@@ -60,6 +61,8 @@ def load() -> C.CDLL:
     lib.akmc_state.argtypes = [P, P, P, C.POINTER(C.c_int64), P, C.POINTER(CCounters)]
     lib.akmc_rates.argtypes = [P, P, P]
     lib.akmc_eval_windows.argtypes = [P, P, C.c_int64, C.c_int32, P]
+    lib.akmc_vacancies.argtypes = [P, P, P, C.POINTER(C.c_int64)]
+    lib.akmc_nccl_unique_id.argtypes = [P]
     lib.akmc_set_stream.argtypes = [P, P]
     lib.akmc_set_profiling.argtypes = [P, C.c_int32]
     lib.akmc_free.argtypes = [P]
@@ -68,7 +71,7 @@ def load() -> C.CDLL:
     lib.akmc_last_error.restype = C.c_char_p
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
-              "akmc_set_profiling"):
+              "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -96,6 +99,7 @@ class Config:
     gpu_grid: tuple = (1, 1, 1)
     rank: int = 0
     world: int = 1
+    nccl_id: bytes = b""
 
     def c(self) -> CConfig:
         s = CConfig()
@@ -110,6 +114,8 @@ class Config:
         s.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
         s.gpu_grid[:] = [int(v) for v in self.gpu_grid]
         s.rank, s.world = int(self.rank), int(self.world)
+        if self.nccl_id:
+            s.nccl_id[:] = list(bytes(self.nccl_id)[:128].ljust(128, b"\0"))
         return s
 
     @property
@@ -155,17 +161,30 @@ class Simulation:
 
     def state(self, species=True):
         sp = np.empty(self.cfg.sites, dtype=np.uint8) if species else None
-        vac = np.empty(max(self.n_vac, 1), dtype=np.int64)
+        nv = C.c_int64(0)
+        self._check(self.lib.akmc_vacancies(self.h, None, None, C.byref(nv)))
+        vac = np.empty(max(int(nv.value), 1), dtype=np.int64)
         n = C.c_int64(vac.size)
         clock = np.empty(self.cfg.n_voxels, dtype=np.float64)
         ctr = CCounters()
         self._check(self.lib.akmc_state(self.h, _ptr(sp), _ptr(vac), C.byref(n), _ptr(clock), C.byref(ctr)))
         return sp, vac[: n.value], clock, ctr.as_dict()
 
+    def vacancies(self):
+        """(global slot ids, global canonical sites) of the vacancies this rank owns, sorted by id."""
+        n = C.c_int64(0)
+        self._check(self.lib.akmc_vacancies(self.h, None, None, C.byref(n)))
+        cap = max(int(n.value), 1)
+        gid = np.empty(cap, dtype=np.int64); site = np.empty(cap, dtype=np.int64)
+        n = C.c_int64(cap)
+        self._check(self.lib.akmc_vacancies(self.h, _ptr(gid), _ptr(site), C.byref(n)))
+        return gid[: n.value], site[: n.value]
+
     def rates(self):
-        R = np.empty((self.n_vac, 8)); E = np.empty((self.n_vac, 8))
+        gid, _ = self.vacancies()
+        R = np.empty((max(gid.size, 1), 8)); E = np.empty((max(gid.size, 1), 8))
         self._check(self.lib.akmc_rates(self.h, _ptr(R), _ptr(E)))
-        return R, E
+        return R[: gid.size], E[: gid.size]
 
     def eval_windows(self, windows, precision: int) -> np.ndarray:
         w = np.ascontiguousarray(windows, dtype=np.uint8).reshape(-1, 64)
@@ -195,3 +214,12 @@ class Simulation:
 
     def __exit__(self, *a):
         self.close()
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId for Config.nccl_id (call on rank 0, broadcast to the other ranks)."""
+    buf = (C.c_uint8 * 128)()
+    rc = load().akmc_nccl_unique_id(buf)
+    if rc != AKMC_OK:
+        raise AkmcError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)

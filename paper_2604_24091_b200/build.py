@@ -9,9 +9,22 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libakmc.so")
 SOURCES = ["akmc_api.cu", "akmc_mlp_tc.cu"]
-HEADERS = ["akmc_device.cuh", "akmc_kernels.cuh", "akmc_mlp_tc.cuh"]
+HEADERS = ["akmc_device.cuh", "akmc_kernels.cuh", "akmc_mlp_tc.cuh", "akmc_dist.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+
+
+def nccl_flags() -> list:
+    """NCCL from the wheel torch uses (same libnccl.so.2 in-process), else the system one."""
+    import glob
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        root = list(spec.submodule_search_locations)[0]
+        inc, lib = os.path.join(root, "include"), os.path.join(root, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and glob.glob(os.path.join(lib, "libnccl.so*")):
+            return ["-I" + inc, "-L" + lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib]
+    return ["-lnccl"]
 
 
 def _stale() -> bool:
@@ -29,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = LIB + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    cmd = [nvcc, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], *nccl_flags(), "-o", tmp]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -14,6 +14,7 @@
 #include "../../include/akmc.h"
 #include "akmc_kernels.cuh"
 #include "akmc_mlp_tc.cuh"
+#include <nccl.h>
 
 using namespace akmc;
 
@@ -159,6 +160,21 @@ struct akmc_handle {
     cudaStream_t graph_stream = nullptr;   // stream the graph was instantiated for
     int graph_launches_per_sweep = 0;
     unsigned long long* d_phase_cycles = nullptr;   // AKMC_PHASE_TIMING diagnostics
+    int vcap = 1;                     // vacancy slot capacity (multi-rank: arrivals append)
+    // multi-rank spatial decomposition (C5); see akmc_dist.cuh
+    bool multi = false;
+    ncclComm_t comm = nullptr;
+    int rc[3] = {0, 0, 0};            // this rank's block coordinates
+    DistParams DP{};
+    int peer_rank[kMaxPeers] = {};
+    int* d_gid = nullptr;             // global slot id per local slot
+    int* d_nvac = nullptr;            // live local slot count (device)
+    int4* d_log = nullptr;
+    unsigned long long* d_nlog = nullptr;
+    int4 *d_send = nullptr, *d_recv = nullptr;
+    int* d_dist_overflow = nullptr;
+    cudaGraphExec_t phase_exec[8] = {};
+    int64_t exchanges = 0, exchange_bytes = 0;
 };
 
 namespace {
@@ -173,6 +189,12 @@ int fail(akmc_handle* h, int code, const std::string& msg)
     do {                                                                                                    \
         cudaError_t e_ = (x);                                                                               \
         if (e_ != cudaSuccess) return fail(h, AKMC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NCK(h, x)                                                                                           \
+    do {                                                                                                    \
+        ncclResult_t r_ = (x);                                                                              \
+        if (r_ != ncclSuccess) return fail(h, AKMC_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
     } while (0)
 
 inline unsigned blocks_for(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -190,6 +212,12 @@ void free_all(akmc_handle* h)
     if (h->sweep_exec) cudaGraphExecDestroy(h->sweep_exec);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+    void* dptrs[] = {h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow};
+    for (void* p : dptrs)
+        if (p) cudaFree(p);
+    for (int q = 0; q < 8; ++q)
+        if (h->phase_exec[q]) cudaGraphExecDestroy(h->phase_exec[q]);
+    if (h->comm) ncclCommDestroy(h->comm);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
 }
 
@@ -213,7 +241,13 @@ int validate(const akmc_config* c, const double* eps, const double* E0, const do
     }
     const int grid = c->gpu_grid[0] * c->gpu_grid[1] * c->gpu_grid[2];
     if (c->gpu_grid[0] < 1 || c->gpu_grid[1] < 1 || c->gpu_grid[2] < 1 || c->world != grid) { why = "world must equal prod(gpu_grid)"; return AKMC_ERR_INVALID; }
-    if (c->world != 1 || c->rank != 0) { why = "this build runs one rank per problem (world == 1); shard voxels over ranks instead"; return AKMC_ERR_INVALID; }
+    if (c->rank < 0 || c->rank >= c->world) { why = "rank out of range"; return AKMC_ERR_INVALID; }
+    if (c->world > 1) {
+        if (!sub || c->n_voxels != 1) { why = "multi-rank decomposition needs sublattice mode and one voxel"; return AKMC_ERR_INVALID; }
+        if (c->world > 4096) { why = "world too large"; return AKMC_ERR_INVALID; }
+        for (int a = 0; a < 3; ++a)
+            if (c->gpu_grid[a] > 1 && c->cells[a] < 2 * (kHalo + 2)) { why = "blocks too thin for the halo"; return AKMC_ERR_INVALID; }
+    }
     if (c->barrier_model == AKMC_MODEL_PAIR) {
         if (!eps || !E0) { why = "pair model needs eps and E0"; return AKMC_ERR_INVALID; }
         for (int s = 0; s < 2; ++s)
@@ -379,6 +413,151 @@ int harvest_events(akmc_handle* h)
     return AKMC_OK;
 }
 
+// ------------------------------------------------------------------ multi-rank setup (C5)
+int rank_of(const akmc_config& c, int x, int y, int z)
+{
+    const int gx = c.gpu_grid[0], gy = c.gpu_grid[1], gz = c.gpu_grid[2];
+    x = ((x % gx) + gx) % gx; y = ((y % gy) + gy) % gy; z = ((z % gz) + gz) % gz;
+    return x + gx * (y + gy * z);
+}
+
+// initial halo fill by shift communication X -> Y -> Z: along axis a the face slab spans the
+// extended range of the axes already exchanged and the owned range of the later ones, so edges and
+// corners propagate in 3 stages of 2 messages instead of 26 direct ones.
+int halo_fill(akmc_handle* h)
+{
+    const akmc_config& c = h->cfg;
+    for (int a = 0; a < 3; ++a) {
+        if (h->F.wrap[a]) continue;
+        SlabRange face_lo{}, face_hi{}, halo_lo{}, halo_hi{};
+        long long cells = 1;
+        for (int b = 0; b < 3; ++b) {
+            int lo, hi;
+            if (b < a) { lo = -kHalo; hi = c.cells[b] + kHalo; }
+            else { lo = 0; hi = c.cells[b]; }
+            face_lo.lo[b] = face_hi.lo[b] = halo_lo.lo[b] = halo_hi.lo[b] = lo;
+            face_lo.hi[b] = face_hi.hi[b] = halo_lo.hi[b] = halo_hi.hi[b] = hi;
+            if (b != a) cells *= (hi - lo);
+        }
+        face_lo.lo[a] = 0;                  face_lo.hi[a] = kHalo;
+        face_hi.lo[a] = c.cells[a] - kHalo; face_hi.hi[a] = c.cells[a];
+        halo_hi.lo[a] = c.cells[a];         halo_hi.hi[a] = c.cells[a] + kHalo;
+        halo_lo.lo[a] = -kHalo;             halo_lo.hi[a] = 0;
+        const size_t bytes = (size_t)(2 * kHalo * cells * 2);
+        int e[3] = {0, 0, 0};
+        e[a] = 1;
+        const int minus = rank_of(c, h->rc[0] - e[0], h->rc[1] - e[1], h->rc[2] - e[2]);
+        const int plus = rank_of(c, h->rc[0] + e[0], h->rc[1] + e[1], h->rc[2] + e[2]);
+        uint8_t *sb = nullptr, *rb = nullptr;
+        CK(h, cudaMalloc(&sb, bytes));
+        CK(h, cudaMalloc(&rb, bytes));
+        const unsigned grid = (unsigned)h->num_sms * 4u;
+        // lower face -> minus neighbour's upper halo; upper face -> plus neighbour's lower halo
+        pack_slab_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->F, face_lo, sb);
+        NCK(h, ncclGroupStart());
+        NCK(h, ncclSend(sb, bytes, ncclChar, minus, h->comm, h->stream));
+        NCK(h, ncclRecv(rb, bytes, ncclChar, plus, h->comm, h->stream));
+        NCK(h, ncclGroupEnd());
+        unpack_slab_kernel<<<grid, 256, 0, h->stream>>>(rb, h->F, halo_hi, h->d_species);
+        pack_slab_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->F, face_hi, sb);
+        NCK(h, ncclGroupStart());
+        NCK(h, ncclSend(sb, bytes, ncclChar, plus, h->comm, h->stream));
+        NCK(h, ncclRecv(rb, bytes, ncclChar, minus, h->comm, h->stream));
+        NCK(h, ncclGroupEnd());
+        unpack_slab_kernel<<<grid, 256, 0, h->stream>>>(rb, h->F, halo_lo, h->d_species);
+        CK(h, cudaStreamSynchronize(h->stream));
+        cudaFree(sb);
+        cudaFree(rb);
+    }
+    return AKMC_OK;
+}
+
+int init_multi(akmc_handle* h)
+{
+    const akmc_config& c = h->cfg;
+    ncclUniqueId id;
+    static_assert(sizeof(ncclUniqueId) <= sizeof(c.nccl_id), "nccl id size");
+    std::memcpy(&id, c.nccl_id, sizeof(id));
+    NCK(h, ncclCommInitRank(&h->comm, c.world, id, c.rank));
+    // peers: distinct ranks at the 26 neighbour offsets along decomposed (non-wrap) axes
+    int np = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int d[3] = {dx, dy, dz};
+                bool skip = dx == 0 && dy == 0 && dz == 0;
+                for (int a = 0; a < 3; ++a)
+                    if (h->F.wrap[a] && d[a] != 0) skip = true;
+                if (skip) continue;
+                const int r = rank_of(c, h->rc[0] + dx, h->rc[1] + dy, h->rc[2] + dz);
+                if (r == c.rank) continue;
+                bool seen = false;
+                for (int i = 0; i < np; ++i) seen |= (h->peer_rank[i] == r);
+                if (seen) continue;
+                h->peer_rank[np] = r;
+                h->DP.peerO[np][0] = (r % c.gpu_grid[0]) * c.cells[0];
+                h->DP.peerO[np][1] = ((r / c.gpu_grid[0]) % c.gpu_grid[1]) * c.cells[1];
+                h->DP.peerO[np][2] = (r / (c.gpu_grid[0] * c.gpu_grid[1])) * c.cells[2];
+                ++np;
+            }
+    h->DP.npeer = np;
+    h->DP.cap = 8192;
+    h->S.logcap = 1 << 17;
+    const size_t per = (size_t)(h->DP.cap + 1);
+    CK(h, cudaMalloc(&h->d_log, (size_t)h->S.logcap * sizeof(int4)));
+    CK(h, cudaMalloc(&h->d_nlog, sizeof(unsigned long long)));
+    CK(h, cudaMalloc(&h->d_send, std::max<size_t>(1, np * per) * sizeof(int4)));
+    CK(h, cudaMalloc(&h->d_recv, std::max<size_t>(1, np * per) * sizeof(int4)));
+    CK(h, cudaMalloc(&h->d_dist_overflow, sizeof(int)));
+    CK(h, cudaMalloc(&h->d_gid, (size_t)h->vcap * sizeof(int)));
+    CK(h, cudaMalloc(&h->d_nvac, sizeof(int)));
+    CK(h, cudaMemset(h->d_nlog, 0, sizeof(unsigned long long)));
+    CK(h, cudaMemset(h->d_dist_overflow, 0, sizeof(int)));
+    CK(h, cudaMemset(h->d_send, 0, std::max<size_t>(1, np * per) * sizeof(int4)));
+    const int nloc = (int)h->nvac;
+    CK(h, cudaMemcpy(h->d_nvac, &nloc, sizeof(int), cudaMemcpyHostToDevice));
+    h->S.log = h->d_log;
+    h->S.nlog = h->d_nlog;
+    h->S.gid = h->d_gid;
+    // global slot ids: rank of the vacancy's global canonical site index among all ranks' vacancies
+    std::vector<int4> v((size_t)std::max<int64_t>(h->nvac, 1));
+    if (h->nvac) CK(h, cudaMemcpy(v.data(), h->d_vac, (size_t)h->nvac * sizeof(int4), cudaMemcpyDeviceToHost));
+    std::vector<long long> mine((size_t)h->nvac);
+    for (int64_t i = 0; i < h->nvac; ++i) {
+        const int4 p = v[(size_t)i];
+        const long long gx = (p.y >> 1) + h->S.O[0], gy = (p.z >> 1) + h->S.O[1], gz = (p.w >> 1) + h->S.O[2];
+        mine[(size_t)i] = 2 * (gx + (long long)h->S.Gc[0] * (gy + (long long)h->S.Gc[1] * gz)) + (p.y & 1);
+    }
+    long long *d_cnt = nullptr, *d_all = nullptr, *d_mine = nullptr, *d_gath = nullptr;
+    CK(h, cudaMalloc(&d_cnt, sizeof(long long)));
+    CK(h, cudaMalloc(&d_all, c.world * sizeof(long long)));
+    const long long cnt = h->nvac;
+    CK(h, cudaMemcpy(d_cnt, &cnt, sizeof(long long), cudaMemcpyHostToDevice));
+    NCK(h, ncclAllGather(d_cnt, d_all, 1, ncclInt64, h->comm, h->stream));
+    std::vector<long long> counts(c.world);
+    CK(h, cudaMemcpyAsync(counts.data(), d_all, c.world * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    long long mx = 1;
+    for (long long x : counts) mx = std::max(mx, x);
+    std::vector<long long> pad((size_t)mx, LLONG_MAX);
+    std::copy(mine.begin(), mine.end(), pad.begin());
+    CK(h, cudaMalloc(&d_mine, (size_t)mx * sizeof(long long)));
+    CK(h, cudaMalloc(&d_gath, (size_t)mx * c.world * sizeof(long long)));
+    CK(h, cudaMemcpy(d_mine, pad.data(), (size_t)mx * sizeof(long long), cudaMemcpyHostToDevice));
+    NCK(h, ncclAllGather(d_mine, d_gath, (size_t)mx, ncclInt64, h->comm, h->stream));
+    std::vector<long long> all((size_t)mx * c.world);
+    CK(h, cudaMemcpyAsync(all.data(), d_gath, all.size() * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    cudaFree(d_cnt); cudaFree(d_all); cudaFree(d_mine); cudaFree(d_gath);
+    all.erase(std::remove(all.begin(), all.end(), LLONG_MAX), all.end());
+    std::sort(all.begin(), all.end());
+    std::vector<int> gid((size_t)std::max<int64_t>(h->nvac, 1));
+    for (int64_t i = 0; i < h->nvac; ++i)
+        gid[(size_t)i] = (int)(std::lower_bound(all.begin(), all.end(), mine[(size_t)i]) - all.begin());
+    if (h->nvac) CK(h, cudaMemcpy(h->d_gid, gid.data(), (size_t)h->nvac * sizeof(int), cudaMemcpyHostToDevice));
+    return halo_fill(h);
+}
+
 } // namespace
 
 extern "C" {
@@ -411,10 +590,19 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     h->dev = dev;
     h->sub = cfg->domain_cells[0] != 0;
     h->nvox = cfg->n_voxels;
+    h->multi = cfg->world > 1;
+    h->rc[0] = cfg->rank % cfg->gpu_grid[0];
+    h->rc[1] = (cfg->rank / cfg->gpu_grid[0]) % cfg->gpu_grid[1];
+    h->rc[2] = cfg->rank / (cfg->gpu_grid[0] * cfg->gpu_grid[1]);
     for (int a = 0; a < 3; ++a) {
         h->F.L[a] = cfg->cells[a];
         h->F.Ls[a] = (cfg->cells[a] + 2 * kHalo + 3) & ~3;               // bricks of 4 cells
         h->F.NB[a] = h->F.Ls[a] / 4;
+        h->F.wrap[a] = cfg->gpu_grid[a] == 1 ? 1 : 0;                   // else the halo mirrors a neighbour rank
+        h->S.O[a] = h->rc[a] * cfg->cells[a];
+        h->S.Gc[a] = cfg->gpu_grid[a] * cfg->cells[a];
+        h->DP.O[a] = h->S.O[a];
+        h->DP.G[a] = h->S.Gc[a];
     }
     h->F.sites = 128LL * h->F.NB[0] * h->F.NB[1] * h->F.NB[2];          // storage bytes per voxel
     h->csites = 2LL * cfg->cells[0] * cfg->cells[1] * cfg->cells[2];    // canonical sites per voxel
@@ -481,7 +669,9 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->nvac = total;
         if ((double)h->nvac > 0.01 * (double)h->sites) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "vacancies exceed 1% of sites (S:48)"); }
         if (h->nvac > INT32_MAX / 8) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies"); }
-        CKI(cudaMalloc(&h->d_vac, (size_t)std::max<int64_t>(h->nvac, 1) * sizeof(int4)));
+        h->vcap = (int)std::max<int64_t>(h->nvac, 1);
+        if (cfg->world > 1) h->vcap = (int)std::min<int64_t>(INT32_MAX / 16, 2 * h->nvac + 65536);
+        CKI(cudaMalloc(&h->d_vac, (size_t)h->vcap * sizeof(int4)));
         scan_write_kernel<<<nblk, kScanThreads, 0, h->stream>>>(sp4, nwords, d_bc, h->F, h->d_vac);
         CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
         vstart_kernel<<<blocks_for(h->nvox + 1, 128), 128, 0, h->stream>>>(h->d_vac, (int)h->nvac, h->nvox, h->d_vstart);
@@ -500,7 +690,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->d_iscratch = nullptr;
         h->d_overflow = nullptr;
     }
-    const size_t nv = (size_t)std::max<int64_t>(h->nvac, 1);
+    const size_t nv = (size_t)h->vcap;
     CKI(cudaMalloc(&h->d_rates, nv * 8 * sizeof(double)));
     CKI(cudaMalloc(&h->d_E, nv * 8 * sizeof(double)));
     CKI(cudaMalloc(&h->d_R, nv * sizeof(double)));
@@ -517,7 +707,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     if (h->sub) {
         for (int a = 0; a < 3; ++a) {
             h->S.D[a] = cfg->domain_cells[a];
-            h->S.ND[a] = cfg->cells[a] / cfg->domain_cells[a];
+            h->S.ND[a] = h->S.Gc[a] / cfg->domain_cells[a];             // global domain grid (A16 ids)
         }
         h->S.ndom_vox = (long long)h->S.ND[0] * h->S.ND[1] * h->S.ND[2];
         h->S.window = cfg->window_s;
@@ -536,6 +726,10 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaMalloc(&h->d_mactive, nv));
         CKI(cudaMalloc(&h->d_phase, 8 * sizeof(PhaseInfo)));
         CKI(cudaMallocHost(&h->h_phase, 8 * sizeof(PhaseInfo)));
+    }
+    if (h->multi) {
+        rc = init_multi(h);
+        if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
     if (cfg->barrier_model == AKMC_MODEL_MLP) {
         const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
@@ -600,10 +794,21 @@ __global__ void set_phase_kernel(PhaseInfo* dst, PhaseTable8 t)
 }
 
 // one inner iteration (a1 rows, a2-a5 eval, a6-a7 select) on stream s; cond != 0 adds the a8 condition kernel
+static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s)
+{
+    const int nv = h->vcap;
+    const int* nd = h->multi ? h->d_nvac : nullptr;
+    activate_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
+                                                        h->d_ctr);
+    segments_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
+                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr);
+}
+
+// one inner iteration (a1 rows, a2-a5 eval, a6-a7 select) on stream s; graph adds the a8 condition kernel
 static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s, bool graph,
                              cudaGraphConditionalHandle cond)
 {
-    const int nv = (int)h->nvac;
+    const int nv = h->vcap;
     const unsigned gs = std::min<unsigned>(blocks_for(nv, 128), (unsigned)h->num_sms * 4u);
     const unsigned gr = std::min<unsigned>(blocks_for(nv, 256), (unsigned)h->num_sms * 2u);
     rows_kernel<<<gr, 256, 0, s>>>(h->d_segs, h->d_members, h->d_mactive, h->d_rows, h->d_ctr);
@@ -624,12 +829,11 @@ static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s
     return AKMC_OK;
 }
 
-// Per-sweep CUDA graph: for each of the 8 phases, activate + segments, then a conditional WHILE node
-// whose body is one inner iteration (rows, eval, select, condition) -- the a8 loop runs on the device
-// with no host synchronisation; the phase table (sector permutation) is a device array updated per sweep.
-static int build_sweep_graph(akmc_handle* h)
+// CUDA graph of phases [q0, q1): activate + segments, then a conditional WHILE node whose body is one
+// inner iteration (rows, eval, select, condition) -- the a8 loop runs on the device with no host
+// synchronisation; the phase table (sector permutation) is a device array updated per sweep.
+static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGraphExec_t* out, int* launches_out)
 {
-    const int nv = (int)h->nvac;
     cudaStream_t cs = nullptr, bs = nullptr;
     CK(h, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     CK(h, cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
@@ -646,12 +850,9 @@ static int build_sweep_graph(akmc_handle* h)
     };
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return done(fail(h, AKMC_ERR_CUDA, "graph capture begin failed"));
-    for (int q = 0; q < 8 && rc == AKMC_OK; ++q) {
+    for (int q = q0; q < q1 && rc == AKMC_OK; ++q) {
         const PhaseInfo* ph = h->d_phase + q;
-        activate_kernel<<<blocks_for(nv, 256), 256, 0, cs>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                             h->d_ctr);
-        segments_kernel<<<blocks_for(nv, 256), 256, 0, cs>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                             h->d_segs, h->d_members, h->d_mactive, h->d_ctr);
+        enqueue_phase_start(h, ph, cs);
         launches += 2;
         cudaStreamCaptureStatus st;
         cudaGraph_t cg = nullptr;
@@ -675,22 +876,47 @@ static int build_sweep_graph(akmc_handle* h)
         cudaStreamEndCapture(bs, &bout);
         launches += 4;
     }
-    add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, cs>>>(h->d_clock, h->nvox, h->cfg.window_s);
-    launches += 1;
+    if (with_window) {
+        add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, cs>>>(h->d_clock, h->nvox, h->cfg.window_s);
+        launches += 1;
+    }
     const cudaError_t ec = cudaStreamEndCapture(cs, &g);
     if (rc != AKMC_OK) { if (g) cudaGraphDestroy(g); return done(rc); }
     if (ec != cudaSuccess) return done(fail(h, AKMC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec)));
-    const cudaError_t ei = cudaGraphInstantiate(&h->sweep_exec, g, 0);
+    const cudaError_t ei = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (ei != cudaSuccess) return done(fail(h, AKMC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)));
-    h->graph_launches_per_sweep = launches;
+    *launches_out = launches;
     return done(AKMC_OK);
+}
+
+// multi-rank: after a phase, send logged boundary writes / departures to the peers and apply theirs
+static int exchange_deltas(akmc_handle* h)
+{
+    const int np = h->DP.npeer;
+    const size_t per = (size_t)(h->DP.cap + 1);
+    pack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_send,
+                                                          h->d_dist_overflow);
+    CK(h, cudaGetLastError());
+    NCK(h, ncclGroupStart());
+    for (int r = 0; r < np; ++r) {
+        NCK(h, ncclSend(h->d_send + r * per, per * sizeof(int4), ncclChar, h->peer_rank[r], h->comm, h->stream));
+        NCK(h, ncclRecv(h->d_recv + r * per, per * sizeof(int4), ncclChar, h->peer_rank[r], h->comm, h->stream));
+    }
+    NCK(h, ncclGroupEnd());
+    unpack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_recv, np, h->F, h->DP, h->d_species, h->d_vac, h->d_gid,
+                                                            h->d_nvac, h->vcap, h->d_dist_overflow);
+    clear_headers_kernel<<<1, 32, 0, h->stream>>>(h->d_send, np, h->DP.cap, h->d_nlog);
+    CK(h, cudaGetLastError());
+    h->total.kernel_launches += 3;
+    h->exchanges += 1;
+    h->exchange_bytes += (int64_t)(2 * np * per * sizeof(int4));
+    return AKMC_OK;
 }
 
 // host-stepped sublattice loop (used when profiling: CUDA events around every barrier-kernel launch)
 static int step_sublattice_host(akmc_handle* h, int64_t n)
 {
-    const int nv = (int)h->nvac;
     for (int64_t sw = 0; sw < n; ++sw) {
         PhaseTable8 t;
         phase_table(h, h->sweep, t.p);
@@ -698,11 +924,7 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
         h->total.kernel_launches += 1;
         for (int q = 0; q < 8; ++q) {
             const PhaseInfo* ph = h->d_phase + q;
-            activate_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head,
-                                                                         h->d_next, h->d_ctr);
-            segments_kernel<<<blocks_for(nv, 256), 256, 0, h->stream>>>(h->d_vac, nv, h->S, ph, h->d_dmin, h->d_head,
-                                                                         h->d_next, h->d_segs, h->d_members,
-                                                                         h->d_mactive, h->d_ctr);
+            enqueue_phase_start(h, ph, h->stream);
             CK(h, cudaGetLastError());
             h->total.kernel_launches += 2;
             for (;;) {
@@ -719,6 +941,10 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
                                       sizeof(unsigned long long), h->stream));
                 if (!more) break;
             }
+            if (h->multi) {
+                const int rc = exchange_deltas(h);
+                if (rc != AKMC_OK) return rc;
+            }
         }
         add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(h->d_clock, h->nvox, h->cfg.window_s);
         CK(h, cudaGetLastError());
@@ -732,16 +958,35 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
 static int step_sublattice(akmc_handle* h, int64_t n)
 {
     if (h->profile) return step_sublattice_host(h, n);
-    if (!h->sweep_exec) {
-        const int rc = build_sweep_graph(h);
+    int launches_phase = 0;
+    if (!h->multi && !h->sweep_exec) {
+        const int rc = build_graph(h, 0, 8, true, &h->sweep_exec, &h->graph_launches_per_sweep);
         if (rc != AKMC_OK) return rc;
+    }
+    if (h->multi && !h->phase_exec[0]) {
+        for (int q = 0; q < 8; ++q) {
+            const int rc = build_graph(h, q, q + 1, false, &h->phase_exec[q], &launches_phase);
+            if (rc != AKMC_OK) return rc;
+        }
+        h->graph_launches_per_sweep = 8 * launches_phase;
     }
     for (int64_t sw = 0; sw < n; ++sw) {
         PhaseTable8 t;
         phase_table(h, h->sweep, t.p);
         set_phase_kernel<<<1, 32, 0, h->stream>>>(h->d_phase, t);
         CK(h, cudaGetLastError());
-        CK(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+        if (!h->multi) {
+            CK(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+        } else {
+            for (int q = 0; q < 8; ++q) {
+                CK(h, cudaGraphLaunch(h->phase_exec[q], h->stream));
+                const int rc = exchange_deltas(h);
+                if (rc != AKMC_OK) return rc;
+            }
+            add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(h->d_clock, h->nvox, h->cfg.window_s);
+            CK(h, cudaGetLastError());
+            h->total.kernel_launches += 1;
+        }
         h->total.kernel_launches += 1 + h->graph_launches_per_sweep;   // body kernels counted once per phase
         h->sweep += 1;
         h->total.sweeps += 1;
@@ -787,7 +1032,38 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
         d.wall_ms = h->total.wall_ms - before.wall_ms;
         *ctr = d;
     }
+    if (h->multi) {
+        int ovf = 0;
+        CK(h, cudaMemcpy(&ovf, h->d_dist_overflow, sizeof(int), cudaMemcpyDeviceToHost));
+        if (ovf) return fail(h, AKMC_ERR_RUNTIME, "halo exchange buffer overflow (" + std::to_string(ovf) + " entries)");
+    }
     if (c1.terminal != c0.terminal) return fail(h, AKMC_TERMINAL, "a competing set has no feasible event (S:199)");
+    return AKMC_OK;
+}
+
+struct VacRec { int64_t gid, site; int slot; };
+
+// live vacancies of this handle: (global slot id, global canonical site, local slot), sorted by gid
+static int collect_vacancies(akmc_handle* h, std::vector<VacRec>& out)
+{
+    out.clear();
+    int n = (int)h->nvac;
+    if (h->multi) CK(h, cudaMemcpy(&n, h->d_nvac, sizeof(int), cudaMemcpyDeviceToHost));
+    n = std::min(n, h->vcap);
+    if (n <= 0) return AKMC_OK;
+    std::vector<int4> v((size_t)n);
+    std::vector<int> g((size_t)n);
+    CK(h, cudaMemcpy(v.data(), h->d_vac, (size_t)n * sizeof(int4), cudaMemcpyDeviceToHost));
+    if (h->multi) CK(h, cudaMemcpy(g.data(), h->d_gid, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+        const int4 p = v[(size_t)i];
+        if (p.x < 0) continue;
+        const int64_t gx = (p.y >> 1) + h->S.O[0], gy = (p.z >> 1) + h->S.O[1], gz = (p.w >> 1) + h->S.O[2];
+        const int64_t Gx = h->multi ? h->S.Gc[0] : h->F.L[0], Gy = h->multi ? h->S.Gc[1] : h->F.L[1];
+        const int64_t site = (int64_t)p.x * h->csites + 2 * (gx + Gx * (gy + Gy * gz)) + (p.y & 1);
+        out.push_back({h->multi ? (int64_t)g[(size_t)i] : (int64_t)i, site, i});
+    }
+    std::sort(out.begin(), out.end(), [](const VacRec& a, const VacRec& b) { return a.gid < b.gid; });
     return AKMC_OK;
 }
 
@@ -795,10 +1071,12 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
                akmc_counters* ctr_out)
 {
     if (!h) return AKMC_ERR_RUNTIME;
-    if (vac_sites_out) {
-        if (!n_vac_inout || *n_vac_inout < h->nvac) return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
-    }
     CK(h, cudaStreamSynchronize(h->stream));
+    std::vector<VacRec> vr;
+    int rc = collect_vacancies(h, vr);
+    if (rc != AKMC_OK) return rc;
+    if (vac_sites_out && (!n_vac_inout || *n_vac_inout < (int64_t)vr.size()))
+        return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
     if (species_out) {
         uint8_t* canon = nullptr;
         CK(h, cudaMalloc(&canon, (size_t)h->sites));
@@ -808,33 +1086,63 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
         cudaFree(canon);
         CK(h, e);
     }
-    if (vac_sites_out && h->nvac) {
-        std::vector<int4> v((size_t)h->nvac);
-        CK(h, cudaMemcpy(v.data(), h->d_vac, v.size() * sizeof(int4), cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < h->nvac; ++i) {
-            const int4 p = v[(size_t)i];
-            const int64_t cell = (int64_t)(p.y >> 1) + (int64_t)h->F.L[0] * ((int64_t)(p.z >> 1) + (int64_t)h->F.L[1] * (int64_t)(p.w >> 1));
-            vac_sites_out[i] = (int64_t)p.x * h->csites + 2 * cell + (p.y & 1);
-        }
-    }
-    if (n_vac_inout) *n_vac_inout = h->nvac;
+    if (vac_sites_out)
+        for (size_t i = 0; i < vr.size(); ++i) vac_sites_out[i] = vr[i].site;
+    if (n_vac_inout) *n_vac_inout = (int64_t)vr.size();
     if (clock_s_out) CK(h, cudaMemcpy(clock_s_out, h->d_clock, h->nvox * sizeof(double), cudaMemcpyDeviceToHost));
     if (ctr_out) *ctr_out = h->total;
+    return AKMC_OK;
+}
+
+int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout)
+{
+    if (!h || !n_inout) return AKMC_ERR_RUNTIME;
+    CK(h, cudaStreamSynchronize(h->stream));
+    std::vector<VacRec> vr;
+    int rc = collect_vacancies(h, vr);
+    if (rc != AKMC_OK) return rc;
+    if ((gid_out || site_out) && *n_inout < (int64_t)vr.size()) return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
+    for (size_t i = 0; i < vr.size(); ++i) {
+        if (gid_out) gid_out[i] = vr[i].gid;
+        if (site_out) site_out[i] = vr[i].site;
+    }
+    *n_inout = (int64_t)vr.size();
+    return AKMC_OK;
+}
+
+int akmc_nccl_unique_id(uint8_t* out128)
+{
+    if (!out128) return AKMC_ERR_INVALID;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return AKMC_ERR_NCCL;
+    std::memset(out128, 0, 128);
+    std::memcpy(out128, &id, sizeof(id));
     return AKMC_OK;
 }
 
 int akmc_rates(akmc_handle* h, double* rates_out, double* barriers_out)
 {
     if (!h) return AKMC_ERR_RUNTIME;
-    const int nv = (int)h->nvac;
-    if (nv == 0) return AKMC_OK;
-    int rc = eval_rows(h, nullptr, nullptr, nv, nv, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
+    std::vector<VacRec> vr;
+    int rc = collect_vacancies(h, vr);
+    if (rc != AKMC_OK) return rc;
+    int nslots = (int)h->nvac;
+    if (h->multi) CK(h, cudaMemcpy(&nslots, h->d_nvac, sizeof(int), cudaMemcpyDeviceToHost));
+    nslots = std::min(nslots, h->vcap);
+    if (nslots <= 0 || vr.empty()) return AKMC_OK;
+    rc = eval_rows(h, nullptr, nullptr, nslots, nslots, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
     if (rc != AKMC_OK) return rc;
     CK(h, cudaStreamSynchronize(h->stream));
     rc = harvest_events(h);
     if (rc != AKMC_OK) return rc;
-    if (rates_out) CK(h, cudaMemcpy(rates_out, h->d_rates, (size_t)nv * 8 * sizeof(double), cudaMemcpyDeviceToHost));
-    if (barriers_out) CK(h, cudaMemcpy(barriers_out, h->d_E, (size_t)nv * 8 * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> R((size_t)nslots * 8), E((size_t)nslots * 8);
+    CK(h, cudaMemcpy(R.data(), h->d_rates, R.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(E.data(), h->d_E, E.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < vr.size(); ++i)
+        for (int k = 0; k < 8; ++k) {
+            if (rates_out) rates_out[i * 8 + k] = R[(size_t)vr[i].slot * 8 + k];
+            if (barriers_out) barriers_out[i * 8 + k] = E[(size_t)vr[i].slot * 8 + k];
+        }
     return AKMC_OK;
 }
 

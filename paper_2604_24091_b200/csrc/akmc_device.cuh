@@ -46,6 +46,8 @@ struct Frame {
     int Ls[3];                           // storage cells = roundup4(L + 2*kHalo)
     int NB[3];                           // bricks per axis = Ls / 4
     int64_t sites;                       // storage sites (bytes) per voxel = 128 * NB0*NB1*NB2
+    int wrap[3];                         // 1: axis periodic within this voxel (ghost images); 0: halo holds
+                                         //    a neighbour rank's cells (multi-GPU spatial decomposition)
 };
 
 // ------------------------------------------------------------------ Philox4x32-10
@@ -151,9 +153,9 @@ __device__ __forceinline__ void write_site(uint8_t* species, const Frame& F, int
     int nx = 1, ny = 1, nz = 1;
     ix[0] = px; iy[0] = py; iz[0] = pz;
     const int cx = px >> 1, cy = py >> 1, cz = pz >> 1;
-    if (cx < kHalo) ix[nx++] = px + 2 * F.L[0]; else if (cx >= F.L[0] - kHalo) ix[nx++] = px - 2 * F.L[0];
-    if (cy < kHalo) iy[ny++] = py + 2 * F.L[1]; else if (cy >= F.L[1] - kHalo) iy[ny++] = py - 2 * F.L[1];
-    if (cz < kHalo) iz[nz++] = pz + 2 * F.L[2]; else if (cz >= F.L[2] - kHalo) iz[nz++] = pz - 2 * F.L[2];
+    if (F.wrap[0]) { if (cx < kHalo) ix[nx++] = px + 2 * F.L[0]; else if (cx >= F.L[0] - kHalo) ix[nx++] = px - 2 * F.L[0]; }
+    if (F.wrap[1]) { if (cy < kHalo) iy[ny++] = py + 2 * F.L[1]; else if (cy >= F.L[1] - kHalo) iy[ny++] = py - 2 * F.L[1]; }
+    if (F.wrap[2]) { if (cz < kHalo) iz[nz++] = pz + 2 * F.L[2]; else if (cz >= F.L[2] - kHalo) iz[nz++] = pz - 2 * F.L[2]; }
     for (int a = 0; a < nx; ++a)
         for (int b = 0; b < ny; ++b)
             for (int c = 0; c < nz; ++c) species[site_of(F, vox, ix[a], iy[b], iz[c])] = val;

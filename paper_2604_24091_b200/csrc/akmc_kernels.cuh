@@ -10,6 +10,7 @@
 #pragma once
 #include <climits>
 #include "akmc_device.cuh"
+#include "akmc_dist.cuh"
 
 namespace akmc {
 
@@ -188,9 +189,9 @@ __device__ __forceinline__ int4 apply_hop(uint8_t* species, int4* vac, int slot,
 {
     const int4 v = vac[slot];
     int4 n = v;
-    n.y = wrap2(v.y + G.off[k][0], 2 * F.L[0]);
-    n.z = wrap2(v.z + G.off[k][1], 2 * F.L[1]);
-    n.w = wrap2(v.w + G.off[k][2], 2 * F.L[2]);
+    n.y = F.wrap[0] ? wrap2(v.y + G.off[k][0], 2 * F.L[0]) : v.y + G.off[k][0];   // non-wrap: may enter the halo
+    n.z = F.wrap[1] ? wrap2(v.z + G.off[k][1], 2 * F.L[1]) : v.z + G.off[k][1];
+    n.w = F.wrap[2] ? wrap2(v.w + G.off[k][2], 2 * F.L[2]) : v.w + G.off[k][2];
     const uint8_t tv = species[site_of(F, v.x, v.y, v.z, v.w)];
     const uint8_t tn = species[site_of(F, n.x, n.y, n.z, n.w)];
     write_site(species, F, v.x, v.y, v.z, v.w, tn);     // owned sites and their ghost images
@@ -235,11 +236,20 @@ __global__ void select_serial_kernel(uint8_t* species, int4* vac, Frame F, GeomT
 // ------------------------------------------------------------------ sublattice (a1, a6-a8)
 struct SubParams {
     int D[3];              // domain edge (cells)
-    int ND[3];             // domains per axis per voxel
-    long long ndom_vox;    // domains per voxel
+    int ND[3];             // domains per axis per voxel (global: the whole decomposed lattice)
+    long long ndom_vox;    // domains per voxel (global)
     double window;         // Delta_win
     uint64_t seed;
+    int O[3];              // this rank's block origin (global cells); 0 for a single rank
+    int Gc[3];             // global cells per axis (= cells for a single rank)
+    const int* gid;        // global slot id per local slot (identity for a single rank)
+    // multi-rank: log of writes near non-wrap faces and vacancy departures (akmc_dist.cuh)
+    int4* log;
+    unsigned long long* nlog;
+    int logcap;
 };
+
+__device__ __forceinline__ int imodk(int a, int m) { const int r = a % m; return r < 0 ? r + m : r; }
 
 struct PhaseInfo {         // per phase, written to device memory before each sweep's graph launch
     int sector;            // active octant c = perm_sweep[q]
@@ -257,7 +267,10 @@ struct Segment {
 
 __device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, long long& dom, int& sec)
 {
-    const int cx = v.y >> 1, cy = v.z >> 1, cz = v.w >> 1;
+    // global cell (the block origin shifts local cells; halo positions wrap around the global torus)
+    const int cx = imodk((v.y >> 1) + S.O[0], S.Gc[0]);
+    const int cy = imodk((v.z >> 1) + S.O[1], S.Gc[1]);
+    const int cz = imodk((v.w >> 1) + S.O[2], S.Gc[2]);
     const int dx = cx / S.D[0], dy = cy / S.D[1], dz = cz / S.D[2];
     const int ox = (cx - dx * S.D[0]) >= (S.D[0] >> 1);
     const int oy = (cy - dy * S.D[1]) >= (S.D[1] >> 1);
@@ -266,16 +279,20 @@ __device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, lo
     sec = ox | (oy << 1) | (oz << 2);
 }
 
-__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, SubParams S, const PhaseInfo* __restrict__ ph,
-                                int* dmin, int* head, int* next, DevCounters* ctr)
+// nvac = slot capacity; nvac_dev (multi-rank) = live slot count (slots may be departed: vac.x < 0)
+__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, const int* __restrict__ nvac_dev, SubParams S,
+                                const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; }
-    if (i >= nvac) return;
+    const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
+    if (i >= n) return;
+    const int4 v = vac[i];
+    if (v.x < 0) return;
     long long d; int sec;
-    dom_sector(vac[i], S, d, sec);
+    dom_sector(v, S, d, sec);
     if (sec != ph->sector) return;
-    atomicMin(&dmin[d], i);
+    atomicMin(&dmin[d], S.gid ? S.gid[i] : i);       // owner = smallest global slot id
     next[i] = atomicExch(&head[d], i);
 }
 
@@ -307,31 +324,40 @@ __device__ __forceinline__ int block_alloc(int v, unsigned long long* counter)
     return r;
 }
 
-__global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac, SubParams S,
+__global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac,
+                                                       const int* __restrict__ nvac_dev, SubParams S,
                                                        const PhaseInfo* __restrict__ ph, int* dmin, int* head,
                                                        const int* __restrict__ next, Segment* segs, int* members,
                                                        uint8_t* mactive, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     long long d = 0;
     int sec = -1;
     bool owner = false;
     int cnt = 0;
-    if (i < nvac) {
-        dom_sector(vac[i], S, d, sec);
-        owner = (sec == ph->sector && dmin[d] == i);  // the minimum slot owns the domain
-        if (owner)
-            for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
+    if (i < n) {
+        const int4 v = vac[i];
+        if (v.x >= 0) {
+            dom_sector(v, S, d, sec);
+            owner = (sec == ph->sector && dmin[d] == (S.gid ? S.gid[i] : i));   // smallest global slot owns
+            if (owner)
+                for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
+        }
     }
     const int off = block_alloc(cnt, &ctr->total);
     const int seg = block_alloc(owner ? 1 : 0, &ctr->nseg);
     if (!owner) return;
     int c = 0;
     for (int j = head[d]; j >= 0; j = next[j]) members[off + (c++)] = j;
-    for (int a = 1; a < cnt; ++a) {                     // insertion sort by slot id
+    for (int a = 1; a < cnt; ++a) {                     // insertion sort by global slot id
         const int key = members[off + a];
+        const int kg = S.gid ? S.gid[key] : key;
         int b = a - 1;
-        while (b >= 0 && members[off + b] > key) { members[off + b + 1] = members[off + b]; --b; }
+        while (b >= 0 && (S.gid ? S.gid[members[off + b]] : members[off + b]) > kg) {
+            members[off + b + 1] = members[off + b];
+            --b;
+        }
         members[off + b + 1] = key;
     }
     for (int a = 0; a < cnt; ++a) mactive[off + a] = 1;
@@ -408,10 +434,27 @@ __global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTabl
                     const int a = idx[leaf];
                     const int slot = members[sg.off + a];
                     const int k = pick_hop(rates + (size_t)slot * 8, r);
+                    const int4 ov = vac[slot];
                     const int4 nv = apply_hop(species, vac, slot, k, F, G);
                     long long d2; int sec2;
                     dom_sector(nv, S, d2, sec2);
                     if (d2 != sg.dom || sec2 != sector) mactive[sg.off + a] = 0;
+                    if (S.log) {
+                        // multi-rank: log writes a neighbour rank must see, and departures from the block
+                        if (near_face(F, ov.y, ov.z, ov.w))
+                            log_entry(S.log, S.nlog, S.logcap, ov.y, ov.z, ov.w,
+                                      species[site_of(F, ov.x, ov.y, ov.z, ov.w)]);
+                        if (near_face(F, nv.y, nv.z, nv.w))
+                            log_entry(S.log, S.nlog, S.logcap, nv.y, nv.z, nv.w, kVac);
+                        bool out = false;
+                        const int np[3] = {nv.y, nv.z, nv.w};
+                        for (int ax = 0; ax < 3; ++ax)
+                            if (!F.wrap[ax] && (np[ax] < 0 || np[ax] >= 2 * F.L[ax])) out = true;
+                        if (out) {
+                            log_entry(S.log, S.nlog, S.logcap, nv.y, nv.z, nv.w, kMigrateBase + S.gid[slot]);
+                            vac[slot].x = -1;                   // departed: re-created by the owner rank
+                        }
+                    }
                     sg.t = __dadd_rn(sg.t, dt);
                     sg.it += 1u;
                     events += 1;

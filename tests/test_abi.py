@@ -21,7 +21,7 @@ def test_library_exports_header_symbols():
 
 def test_struct_layout_matches_header():
     # akmc_config: 3+1+1+1+1+3 int32 (40 B) + pad to 8 + 4 doubles + u64 + 3+2 int32
-    assert ctypes.sizeof(akmc.akmc.CConfig) == 40 + 32 + 8 + 20 + 4
+    assert ctypes.sizeof(akmc.akmc.CConfig) == 40 + 32 + 8 + 20 + 128 + 4
     assert ctypes.sizeof(akmc.akmc.CCounters) == 9 * 8 + 2 * 8
 
 

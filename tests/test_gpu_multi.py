@@ -1,0 +1,33 @@
+"""Multi-GPU parity (C5 spatial decomposition, NCCL halo deltas between phases): the same global problem
+on 2 ranks and on 1 rank gives bit-identical lattices, vacancy lists, clocks and event counts (GPU-count
+invariance, SURVEY 8(c) decomposition pin), and equals the FP64 oracle.  Needs >= 2 GPUs."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("grid,extra", [((2, 1, 1), ["--oracle"]), ((1, 2, 1), []),
+                                        ((2, 1, 1), ["--model", "mlp", "--precision", "fp32"])])
+def test_two_rank_invariance(tmp_path, grid, extra):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = tmp_path / "multi.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(29600 + grid[1]), os.path.join(ROOT, "tools", "multi_check.py"),
+           "--grid", *map(str, grid), "--out", str(out), *extra]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"], res
+    assert res["events"] > 20

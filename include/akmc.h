@@ -125,6 +125,10 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
  * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
 int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
 
+/* Diagnostics: the voxel-0 block INCLUDING its halo, cells [-2, L+2) per axis, canonical order
+ * (2*(x + (Lx+4)*(y + (Ly+4)*z)) + b over the extended box); out holds 2*(Lx+4)*(Ly+4)*(Lz+4) bytes.  */
+int akmc_debug_extended(akmc_handle* h, uint8_t* out);
+
 /* Write a fresh ncclUniqueId (128 bytes) for akmc_config.nccl_id (call on rank 0 only). */
 int akmc_nccl_unique_id(uint8_t* out128);
 

@@ -63,6 +63,7 @@ def load() -> C.CDLL:
     lib.akmc_eval_windows.argtypes = [P, P, C.c_int64, C.c_int32, P]
     lib.akmc_vacancies.argtypes = [P, P, P, C.POINTER(C.c_int64)]
     lib.akmc_nccl_unique_id.argtypes = [P]
+    lib.akmc_debug_extended.argtypes = [P, P]
     lib.akmc_set_stream.argtypes = [P, P]
     lib.akmc_set_profiling.argtypes = [P, C.c_int32]
     lib.akmc_free.argtypes = [P]
@@ -71,7 +72,7 @@ def load() -> C.CDLL:
     lib.akmc_last_error.restype = C.c_char_p
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
-              "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id"):
+              "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -179,6 +180,13 @@ class Simulation:
         n = C.c_int64(cap)
         self._check(self.lib.akmc_vacancies(self.h, _ptr(gid), _ptr(site), C.byref(n)))
         return gid[: n.value], site[: n.value]
+
+    def debug_extended(self) -> np.ndarray:
+        """Voxel-0 block including its 2-cell halo, canonical over the extended box (diagnostics)."""
+        Lx, Ly, Lz = (c + 4 for c in self.cfg.cells)
+        out = np.empty(2 * Lx * Ly * Lz, dtype=np.uint8)
+        self._check(self.lib.akmc_debug_extended(self.h, _ptr(out)))
+        return out
 
     def rates(self):
         gid, _ = self.vacancies()

@@ -622,6 +622,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     for (int a = 0; a < kSpecies; ++a) h->P.E0[a] = E0 ? E0[a] : 0.0;
     h->P.kT = cfg->kB * cfg->temperature_K;
+    h->P.inv_kT = 1.0 / h->P.kT;
     h->P.nu0 = cfg->nu0;
 
 #define CKI(x)                                                                                                \
@@ -895,7 +896,8 @@ static int exchange_deltas(akmc_handle* h)
 {
     const int np = h->DP.npeer;
     const size_t per = (size_t)(h->DP.cap + 1);
-    pack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_send,
+    pack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP,
+                                                          h->d_species, h->d_send,
                                                           h->d_dist_overflow);
     CK(h, cudaGetLastError());
     NCK(h, ncclGroupStart());
@@ -1107,6 +1109,23 @@ int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t*
         if (site_out) site_out[i] = vr[i].site;
     }
     *n_inout = (int64_t)vr.size();
+    return AKMC_OK;
+}
+
+int akmc_debug_extended(akmc_handle* h, uint8_t* out)
+{
+    if (!h || !out) return AKMC_ERR_INVALID;
+    CK(h, cudaStreamSynchronize(h->stream));
+    SlabRange R{};
+    for (int a = 0; a < 3; ++a) { R.lo[a] = -kHalo; R.hi[a] = h->F.L[a] + kHalo; }
+    const size_t bytes = 2ull * (h->F.L[0] + 2 * kHalo) * (h->F.L[1] + 2 * kHalo) * (h->F.L[2] + 2 * kHalo);
+    uint8_t* d = nullptr;
+    CK(h, cudaMalloc(&d, bytes));
+    pack_slab_kernel<<<h->num_sms * 4, 256, 0, h->stream>>>(h->d_species, h->F, R, d);
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CK(h, e);
     return AKMC_OK;
 }
 

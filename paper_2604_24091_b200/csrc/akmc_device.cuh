@@ -33,6 +33,7 @@ struct PhysParams {
     double E0[kSpecies];
     double kT;                           // kB * T (IEEE product, computed once on the host)
     double nu0;
+    double inv_kT;                       // 1 / kT (FP32-equivalent mode only; FP64 mode divides, A29)
 };
 
 // Lattice frame of one voxel.  The voxel's L^3 owned cells are stored inside a halo of kHalo cells

@@ -64,12 +64,17 @@ __device__ __forceinline__ void log_entry(int4* log, unsigned long long* nlog, i
 }
 
 // pack the phase's log into per-peer send buffers (header entry 0 = count); global half-cell coords
+// A site may be written several times in one phase (a vacancy enters and leaves it), so species entries
+// carry the site's FINAL value, read here after the phase: duplicates are identical and the receiver may
+// apply entries in any order.
 __global__ void pack_deltas_kernel(const int4* __restrict__ log, const unsigned long long* nlog_p, int logcap, Frame F,
-                                   DistParams D, int4* sendbuf, int* overflow)
+                                   DistParams D, const uint8_t* __restrict__ species, int4* sendbuf, int* overflow)
 {
     const int n = (int)min((unsigned long long)logcap, *nlog_p);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && *nlog_p > (unsigned long long)logcap) atomicAdd(overflow, 1);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 e = log[i];
+        int4 e = log[i];
+        if (e.w < kMigrateBase) e.w = species[site_of(F, 0, e.x, e.y, e.z)];
         const int p[3] = {e.x, e.y, e.z};
         int gc[3], gp[3];
         for (int a = 0; a < 3; ++a) {

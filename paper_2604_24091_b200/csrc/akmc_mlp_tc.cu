@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                 for (int k = 0; k < 8; ++k) {
                     const double out = __ldg(p.b3 + k) + accE[k] * p.s3_unscale;
                     Ek[k] = out > 0.0 ? out : 0.0;
-                    Gk[k] = ((mask >> k) & 1) ? arrhenius(Ek[k], p.P) : 0.0;
+                    Gk[k] = ((mask >> k) & 1) ? p.P.nu0 * det_exp(-(Ek[k] * p.P.inv_kT)) : 0.0;
                     Rs = __dadd_rn(Rs, Gk[k]);
                 }
                 if (p.E) {

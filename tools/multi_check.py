@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--model", default="pair", choices=["pair", "mlp"])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--debug", action="store_true")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -48,7 +49,35 @@ def main():
     cfg = akmc.Config(cells=block, barrier_model=model, precision=prec, domain_cells=(8, 8, 8), window_s=win, seed=5,
                       gpu_grid=grid, rank=rank, world=world, nccl_id=nid)
     sim = akmc.Simulation(cfg, D.block_of(glob, block, grid, rank), eps, E0, mlp)
-    c = sim.step(a.sweeps)
+    if a.debug:
+        # lockstep with a single-rank reference; after every sweep each rank's extended block (halo
+        # included) must equal the reference global lattice around its block (periodic images)
+        ref = akmc.Simulation(akmc.Config(cells=G, barrier_model=model, precision=prec, domain_cells=(8, 8, 8),
+                                          window_s=win, seed=5), glob, eps, E0, mlp)
+        cx, cy, cz = D.rank_coords(rank, grid)
+        O = (cx * block[0], cy * block[1], cz * block[2])
+        for sw in range(a.sweeps + 1):
+            rsp, _, _, _ = ref.state()
+            g4 = rsp.reshape(G[2], G[1], G[0], 2)
+            ext = sim.debug_extended().reshape(block[2] + 4, block[1] + 4, block[0] + 4, 2)
+            zz = (np.arange(-2, block[2] + 2) + O[2]) % G[2]
+            yy = (np.arange(-2, block[1] + 2) + O[1]) % G[1]
+            xx = (np.arange(-2, block[0] + 2) + O[0]) % G[0]
+            want = g4[zz][:, yy][:, :, xx]
+            bad = np.argwhere(ext != want)
+            print(f"[rank {rank}] sweep {sw}: {len(bad)} mismatching sites"
+                  + (f", first (z,y,x,b) local {tuple(int(t) - (2 if i < 3 else 0) for i, t in enumerate(bad[0]))}"
+                     f" got {ext[tuple(bad[0])]} want {want[tuple(bad[0])]}" if len(bad) else ""), flush=True)
+            flag = torch.tensor([len(bad)], device=torch.device("cuda", local))
+            tdist.all_reduce(flag)                      # collective decision: no rank may stop alone
+            if int(flag.item()) or sw == a.sweeps:
+                break
+            sim.step(1)
+            ref.step(1)
+        ref.close()
+        c = {"events": 0, "hop_evals": 0}
+    else:
+        c = sim.step(a.sweeps)
     sp, _, clock, _ = sim.state()
     gid, site = sim.vacancies()
     sim.close()

@@ -141,7 +141,7 @@ struct akmc_handle {
     double* d_mlp = nullptr;
     uint8_t* d_Bimg = nullptr;        // ring image: W1'^T (24 chunks) + W2^T (16 chunks), fp16 hi/lo
     uint8_t* d_W3img = nullptr;       // W3^T hi/lo, N padded to 16
-    float *d_b1h = nullptr, *d_b1l = nullptr, *d_b2 = nullptr;
+    float* d_b2 = nullptr;
     double* d_b3 = nullptr;
     float s1u = 1.0f, s2u = 1.0f;
     double s3u = 1.0;
@@ -203,7 +203,7 @@ void free_all(akmc_handle* h)
 {
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_rows,
-                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img, h->d_b1h, h->d_b1l,
+                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
                     h->d_b2, h->d_b3, h->d_overflow};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -294,7 +294,10 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     };
     // layer 1: Fe-referenced rows W1'[6*slot + s-1] = W1[7*slot+s] - W1[7*slot+Fe] (s = 1..6), bias
     // b1' = b1 + sum_slot W1[7*slot+Fe] (exact algebra: one species per slot)
-    std::vector<double> W1p((size_t)kK1 * kHid), b1p(kHid);
+    // layer-1 K: K-step 0 = bias columns, then species-major one-hot columns
+    // k = 16 + (s-1)*64 + slot (s = 1..6) so that a K-step is all-zero for a tile unless the tile holds
+    // species s in its 16-slot group (skipped exactly: a zero K-step adds exact zeros)
+    std::vector<double> W1p((size_t)kK1 * kHid, 0.0), b1p(kHid);
     for (int j = 0; j < kHid; ++j) {
         double acc = b1[j];
         for (int s = 0; s < kWin; ++s) acc += W1[(size_t)(kSpecies * s + kFe) * kHid + j];
@@ -303,18 +306,36 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     for (int slot = 0; slot < kWin; ++slot)
         for (int s = 1; s < kSpecies; ++s)
             for (int j = 0; j < kHid; ++j)
-                W1p[(size_t)((kSpecies - 1) * slot + s - 1) * kHid + j] =
+                W1p[(size_t)(16 + (s - 1) * kWin + slot) * kHid + j] =
                     W1[(size_t)(kSpecies * slot + s) * kHid + j] - W1[(size_t)(kSpecies * slot + kFe) * kHid + j];
-    const int s1 = scale_exp(W1p.data(), W1p.size());
+    double mx1 = 0.0;
+    for (int j = 0; j < kHid; ++j) mx1 = std::max(mx1, std::fabs(b1p[j]));
+    for (double w : W1p) mx1 = std::max(mx1, std::fabs(w));
+    const int s1 = mx1 > 0.0 ? 13 - (int)std::ceil(std::log2(mx1)) : 0;
     const int s2 = scale_exp(W2, (size_t)kHid * kHid);
     const int s3 = scale_exp(W3, (size_t)kHid * 8);
     h->s1u = (float)std::ldexp(1.0, -s1);
     h->s2u = (float)std::ldexp(1.0, -s2);
     h->s3u = std::ldexp(1.0, -s3);
     std::vector<uint8_t> img((size_t)kChunksTile * kStageBytes, 0);
-    for (int k = 0; k < kK1; ++k)                                // chunks 0..23: W1'^T
+    for (int k = 16; k < kK1; ++k)                               // chunks 1..24: W1'^T
         for (int n = 0; n < kHid; ++n) put(img.data(), kHid, n, k, std::ldexp(W1p[(size_t)k * kHid + n], s1));
-    for (int k = 0; k < kHid; ++k)                               // chunks 24..39: W2^T
+    // chunk 0: b1' (scaled) as three fp16 pieces: column 0 carries hi (D1) and mid (D2 = lo*2^11 frame),
+    // column 1 carries the third piece in the D2 frame, so D1 + 2^-11 D2 holds b1' to ~2^-33 relative
+    for (int n = 0; n < kHid; ++n) {
+        const double b = std::ldexp(b1p[n], s1);
+        const __half hi = __float2half_rn((float)b);
+        const double r1 = (b - (double)__half2float(hi)) * (double)kLoScale;
+        const __half mid = __float2half_rn((float)r1);
+        const __half lo2 = __float2half_rn((float)(r1 - (double)__half2float(mid)));
+        const size_t split = (size_t)kHid * 16 * 2;
+        for (int k = 0; k < 2; ++k) {
+            const size_t off = ((size_t)(k / 8) * (kHid / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+            reinterpret_cast<__half*>(img.data() + off)[0] = k == 0 ? hi : __float2half_rn(0.0f);
+            reinterpret_cast<__half*>(img.data() + split + off)[0] = k == 0 ? mid : lo2;
+        }
+    }
+    for (int k = 0; k < kHid; ++k)                               // chunks 25..40: W2^T
         for (int n = 0; n < kHid; ++n)
             put(img.data() + (size_t)kChunksL1 * kStageBytes, kHid, n, k, std::ldexp(W2[(size_t)k * kHid + n], s2));
     // W3^T padded to N = 16: per K-step of 16 the layout above interleaves hi/lo, so build the two
@@ -329,22 +350,14 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
             reinterpret_cast<__half*>(w3img.data() + off)[0] = hi;
             reinterpret_cast<__half*>(w3img.data() + kW3SplitBytes + off)[0] = lo;
         }
-    std::vector<float> b1h(kHid), b1l(kHid), b2f(kHid);
-    for (int i = 0; i < kHid; ++i) {
-        b1h[i] = (float)b1p[i];
-        b1l[i] = (float)(b1p[i] - (double)b1h[i]);
-        b2f[i] = (float)b2[i];
-    }
+    std::vector<float> b2f(kHid);
+    for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
     CK(h, cudaMalloc(&h->d_Bimg, img.size()));
     CK(h, cudaMalloc(&h->d_W3img, w3img.size()));
-    CK(h, cudaMalloc(&h->d_b1h, kHid * 4));
-    CK(h, cudaMalloc(&h->d_b1l, kHid * 4));
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
     CK(h, cudaMalloc(&h->d_b3, 8 * 8));
     CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size(), cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_W3img, w3img.data(), w3img.size(), cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_b1h, b1h.data(), kHid * 4, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_b1l, b1l.data(), kHid * 4, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     CK(h, mlp_tc_setup());
@@ -389,7 +402,7 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
         p.Bimg = reinterpret_cast<const __half*>(h->d_Bimg);
         p.W3img = reinterpret_cast<const __half*>(h->d_W3img);
-        p.b1hi = h->d_b1h; p.b1lo = h->d_b1l; p.b2 = h->d_b2; p.b3 = h->d_b3;
+        p.b2 = h->d_b2; p.b3 = h->d_b3;
         p.s1_unscale = h->s1u; p.s2_unscale = h->s2u; p.s3_unscale = h->s3u;
         p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
         p.phase_cycles = h->d_phase_cycles;

@@ -1,21 +1,26 @@
 // akmc_mlp_tc.cu -- fused gather -> encode -> barrier MLP (3 x tcgen05) -> Arrhenius rates, sm_100a.
 //
 // Persistent kernel (<= one CTA per SM, 256 threads); each CTA loops over tiles of 128 vacancies:
-//   G  gather the 64-site window of every row: 2 threads per row, linear-offset
-//      fast path for windows that do not wrap;
-//   X  encode: one-hot over the 6 non-Fe species, X[m][6*slot + s-1] = [sigma_slot == s] (exact in
-//      fp16; the Fe column is folded into the bias, A5), K1 = 384, K-major SWIZZLE_128B in smem;
-//   M1 layer 1 on tcgen05: D1 = X*W1'hi, D2 = X*W1'lo (W1' = W1 - W1[slot,Fe], scaled by 2^s1 and
-//      split hi + lo*2^-11; every product is exact, FP32 accumulation in TMEM);
-//   E1 h1 = ReLU(b1' + 2^-s1 (D1 + 2^-11 D2)) with an error-free FP32 TwoSum against b1' (hi+lo),
-//      rounded to FP32, split into fp16 hi + lo*2^11 -> A (smem, SW128);
+//   G  gather the 64-site window of every row: one warp per row (lanes = slots j and
+//      j+32) from the bricked halo storage, and the OR of the layer-1 K-steps the tile needs;
+//   X  encode: K1 = 400, K-major SWIZZLE_128B in smem.  Columns 0,1 = 1 (the bias K-step), then a
+//      species-major one-hot X[m][16 + 64(s-1) + slot] = [sigma_slot == s] over the 6 non-Fe species
+//      (exact in fp16; the Fe column is folded into the bias, A5).  A K-step of 16 columns is all zero
+//      for the tile unless some row holds species s in that 16-slot group: such K-steps are skipped
+//      (they add exact zeros), so a dilute alloy streams ~6-8 of the 24 one-hot chunks;
+//   M1 layer 1 on tcgen05: D1 = X*W1'hi, D2 = X*W1'lo, b1' inside the GEMM as three fp16 pieces
+//      (W1' = W1 - W1[slot,Fe], scaled by 2^s1 and split hi + lo*2^-11; every product is exact, FP32
+//      accumulation in TMEM);
+//   E1 h1 = ReLU(2^-s1 (D1 + 2^-11 D2)), rounded to FP32, split into fp16 hi + lo*2^11 -> A (SW128);
 //   M2 layer 2 (256x256, "swarm gathering" GEMM): D1 = Ahi*W2hi, D2 = Ahi*W2lo + Alo*W2hi;
 //   E2 h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> split -> A;
 //   M3 layer 3 (256x8 padded to N = 16) with 4 K-groups of 64 in separate TMEM accumulators;
-//   E3 E = max(0, b3 + 2^-s3 sum_g (Da_g + 2^-11 Db_g)) in FP64; Gamma = nu0 det_exp(-E/kT), masked.
-// W1' and W2 are streamed through one continuous 4-stage cp.async.bulk + mbarrier ring (40 chunks of
-// 16 KiB per tile) by a single control thread that also issues every tcgen05.mma.  The 3-pass fp16
-// split is FP32-equivalent ("matrix multiplication ... executed in FP32"); DESIGN.md sec. 6.
+//   E3 E = max(0, b3 + 2^-s3 sum_g (Da_g + 2^-11 Db_g)) in FP64; Gamma = nu0 det_exp(-E/kT), masked;
+//      the two warp halves take hops 0-3 and 4-7 of a row.
+// The needed W1' chunks and the 16 W2 chunks stream through one 4-stage cp.async.bulk + mbarrier ring
+// (16 KiB per chunk, in ascending K order) driven by a single control thread that also issues every
+// tcgen05.mma.  The 3-pass fp16 split is FP32-equivalent ("matrix multiplication ... executed in
+// FP32"); DESIGN.md sec. 6.
 #include "akmc_mlp_tc.cuh"
 #include <cuda_fp16.h>
 
@@ -32,17 +37,17 @@ constexpr uint32_t kSboA = 1024;               // SW128 8-row group stride
 constexpr int kWinStride = 68;                 // window bytes per row in smem (17 words: conflict-free)
 
 // smem carve-up (offsets from a 1024-aligned base)
-constexpr size_t kOffA = 0;                                   // A_hi [0,64K), A_lo [64K,128K); X overlays [0,96K)
+constexpr size_t kOffA = 0;                                   // A_hi [0,64K), A_lo [64K,128K); X overlays [0,112K)
 constexpr size_t kOffB = kOffA + 2 * (size_t)kABytes;         // ring 4 x 16 KiB
 constexpr size_t kOffW3 = kOffB + (size_t)kStages * kStageBytes;   // W3 image 16 KiB
 constexpr size_t kOffWin = kOffW3 + 2 * (size_t)kW3SplitBytes;     // uint8 [128][68]
-constexpr size_t kOffB1h = kOffWin + (size_t)kTileM * kWinStride;  // float [256]
-constexpr size_t kOffB1l = kOffB1h + kHid * 4;                     // float [256]
-constexpr size_t kOffB2 = kOffB1l + kHid * 4;                      // float [256]
-constexpr size_t kOffOffl = kOffB2 + kHid * 4;                     // int [2][64]
-constexpr size_t kOffSlot = kOffOffl + 2 * kWin * 4;               // int [128]
+constexpr size_t kOffB2 = kOffWin + (size_t)kTileM * kWinStride;   // float [256]
+constexpr size_t kOffG = kOffB2 + kHid * 4;                        // double [128][4]
+constexpr size_t kOffSlot = kOffG + (size_t)kTileM * 4 * 8;        // int [128]
 constexpr size_t kOffMask = kOffSlot + kTileM * 4;                 // uint8 [128]
-constexpr size_t kOffBar = kOffMask + kTileM;                      // 8-B aligned barriers
+constexpr size_t kOffKmask = kOffMask + kTileM;                    // uint32 (+pad)
+constexpr size_t kOffList = kOffKmask + 8;                         // uint8 [32]: the tile's W1' chunk ids
+constexpr size_t kOffBar = kOffList + 32;                          // 8-B aligned barriers
 constexpr int kNumBars = 2 * kStages + 4;                          // full[4], empty[4], done1..3, w3
 constexpr size_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr size_t kSmemUsed = kOffTmem + 16;
@@ -173,8 +178,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
     const int nrows = p.nrows_dev ? *p.nrows_dev : p.nrows_host;
     const int ntiles = (nrows + kTileM - 1) / kTileM;
     if ((int)blockIdx.x >= ntiles) return;         // uniform early exit: no barrier/TMEM touched
-    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int total_chunks = my_tiles * kChunksTile;
 
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* A_hi = smem + kOffA;
@@ -183,12 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
     uint8_t* Bst = smem + kOffB;
     uint8_t* W3s = smem + kOffW3;
     uint8_t* win = smem + kOffWin;
-    float* sb1h = reinterpret_cast<float*>(smem + kOffB1h);
-    float* sb1l = reinterpret_cast<float*>(smem + kOffB1l);
     float* sb2 = reinterpret_cast<float*>(smem + kOffB2);
-
+    double* sG = reinterpret_cast<double*>(smem + kOffG);        // [128][4] rates of hops 4..7
     int* sslot = reinterpret_cast<int*>(smem + kOffSlot);
     uint8_t* smask = smem + kOffMask;
+    uint32_t* skmask = reinterpret_cast<uint32_t*>(smem + kOffKmask);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
 
@@ -212,13 +214,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
         mbar_init(bar_done3, 1);
         mbar_init(bar_w3, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        *skmask = 1u;                              // K-step 0 (bias) is always needed
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < kHid; i += kThreads) { sb1h[i] = p.b1hi[i]; sb1l[i] = p.b1lo[i]; sb2[i] = p.b2[i]; }
+    for (int i = threadIdx.x; i < kHid; i += kThreads) sb2[i] = p.b2[i];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -226,46 +229,53 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
     const uint32_t idesc256 = (1u << 4) | ((uint32_t)(kHid >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
     const uint32_t idesc16 = (1u << 4) | ((uint32_t)(kN3 >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
 
-    // ring: chunk x (global over this CTA's tiles) = image chunk x % 40, in stage x % 4
-    auto load_chunk = [&](int x) {
-        const int s = x % kStages;
-        if (x >= kStages) mbar_wait(bar_empty0 + 8 * s, ((x - kStages) / kStages) & 1);
+    // ring (control thread only): position y in stage y % 4; chunks in ascending K order per tile
+    int issued = 0, consumed = 0;                  // ring positions over this CTA's whole life
+    int tile_base = 0, tile_n = 0, n1 = 0;         // current tile: first position, entries, W1' entries
+    uint8_t* list = smem + kOffList;               // W1' chunk ids needed by the current tile
+    auto chunk_id = [&](int e) { return e < n1 ? (int)list[e] : kChunksL1 + (e - n1); };
+    auto issue_next = [&]() {
+        if (issued >= tile_base + tile_n) return;
+        const int y = issued++;
+        const int s = y % kStages;
+        if (y >= kStages) mbar_wait(bar_empty0 + 8 * s, ((y - kStages) / kStages) & 1);
         mbar_expect_tx(bar_full0 + 8 * s, kStageBytes);
         bulk_g2s(smem_u32(Bst + (size_t)s * kStageBytes),
-                 reinterpret_cast<const uint8_t*>(p.Bimg) + (size_t)(x % kChunksTile) * kStageBytes, kStageBytes,
+                 reinterpret_cast<const uint8_t*>(p.Bimg) + (size_t)chunk_id(y - tile_base) * kStageBytes, kStageBytes,
                  bar_full0 + 8 * s);
     };
-    // consume chunk x: wait for its bytes; after the MMAs are committed, refill the ring 3 ahead
-    auto chunk_ready = [&](int x) {
-        mbar_wait(bar_full0 + 8 * (x % kStages), (x / kStages) & 1);
+    auto chunk_ready = [&]() {
+        const int y = consumed;
+        mbar_wait(bar_full0 + 8 * (y % kStages), (y / kStages) & 1);
         tc_fence_after();
-        return smem_u32(Bst + (size_t)(x % kStages) * kStageBytes);
+        return smem_u32(Bst + (size_t)(y % kStages) * kStageBytes);
     };
-    auto chunk_done = [&](int x) {
-        umma_commit(bar_empty0 + 8 * (x % kStages));
-        if (x + kStages - 1 < total_chunks) load_chunk(x + kStages - 1);
+    auto chunk_done = [&]() {
+        umma_commit(bar_empty0 + 8 * (consumed % kStages));
+        ++consumed;
+        issue_next();                              // keeps kStages-1 chunks in flight
     };
     if (ctrl) {
         mbar_expect_tx(bar_w3, 2 * kW3SplitBytes);
         bulk_g2s(smem_u32(W3s), p.W3img, 2 * kW3SplitBytes, bar_w3);
-        for (int x = 0; x < kStages - 1 && x < total_chunks; ++x) load_chunk(x);
     }
 
     const long long tk0 = clock64();
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int tile0 = tile * kTileM;
-        const int cx0 = it * kChunksTile;
         long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const bool timing = p.phase_cycles && threadIdx.x == 64;
         if (timing) tp[0] = clock64();
 
         // ---- G: gather, one warp per row (lane = window slots j and j+32), 16 rows per warp in two
         //      batches of 8 so that the dependent loads (row -> vacancy -> window) overlap across rows;
-        //      one LDG instruction then touches the ~10 bricks (L2 lines) of one window, not 32 windows
+        //      one LDG instruction then touches the ~10 bricks (L2 lines) of one window, not 32 windows.
+        //      Also collects which layer-1 K-steps the tile needs (species-major groups of 16 slots).
         {
             const int ox0 = p.G.off[lane][0], oy0 = p.G.off[lane][1], oz0 = p.G.off[lane][2];
             const int ox1 = p.G.off[lane + 32][0], oy1 = p.G.off[lane + 32][1], oz1 = p.G.off[lane + 32][2];
+            uint32_t kbits = 0;
 #pragma unroll
             for (int half8 = 0; half8 < 2; ++half8) {
                 uint32_t b0[8], b1[8];
@@ -294,6 +304,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                     const int r = warp + 8 * (8 * half8 + i);
                     win[r * kWinStride + lane] = (uint8_t)b0[i];
                     win[r * kWinStride + lane + 32] = (uint8_t)b1[i];
+                    if (b0[i] != kFe) kbits |= 1u << (1 + 4 * (b0[i] - 1) + (lane >> 4));
+                    if (b1[i] != kFe) kbits |= 1u << (1 + 4 * (b1[i] - 1) + 2 + (lane >> 4));
                     const unsigned feas = __ballot_sync(0xffffffffu, lane < kHops && b0[i] != (uint32_t)kVac);
                     if (lane == 0) {
                         smask[r] = (uint8_t)(feas & 0xFFu);
@@ -301,28 +313,48 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                     }
                 }
             }
+            kbits = __reduce_or_sync(0xffffffffu, kbits);
+            if (lane == 0 && kbits) atomicOr(skmask, kbits);
         }
         __syncthreads();
+        if (ctrl) {
+            // the tile's chunk list: needed W1' K-steps in ascending order, then the 16 W2 chunks
+            const uint32_t km = *skmask;
+            *skmask = 1u;                          // next OR comes after several __syncthreads
+            n1 = 0;
+            for (int c = 0; c < kChunksL1; ++c)
+                if ((km >> c) & 1u) list[n1++] = (uint8_t)c;
+            tile_base = issued;
+            tile_n = n1 + kChunksL2;
+            for (int q = 0; q < kStages - 1; ++q) issue_next();    // overlap with the encode
+        }
         if (timing) tp[1] = clock64();
 
-        // ---- X: one-hot layer-1 operand (K = 384, SW128); thread = (row, half of the 48 chunks)
+        // ---- X: one-hot layer-1 operand (K = 400, SW128): columns 0,1 = 1 (bias pieces), then
+        //      column 16 + (s-1)*64 + slot.  Thread (row m, half hx) owns the chunks of window slots
+        //      [32hx, 32hx+32) in every species block (plus the bias chunks for hx = 0): zero-fill them,
+        //      then write fp16 1.0 for its non-Fe slots -- no other thread writes those chunks.
         {
-            // thread (row m, half hx) owns feature chunks [24hx, 24hx+24) == window slots [32hx, 32hx+32):
-            // zero-fill them, then write fp16 1.0 at f = 6*slot + species - 1 for every non-Fe slot
             const int m = 32 * (warp & 3) + lane;
             const int hx = warp >> 2;
             const uint32_t* wr = reinterpret_cast<const uint32_t*>(win + m * kWinStride) + 8 * hx;
             uint32_t w32[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) w32[q] = wr[q];
+            if (hx == 0) {
+                *reinterpret_cast<uint4*>(Xs + sw128_off(m, 0)) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
+                *reinterpret_cast<uint4*>(Xs + sw128_off(m, 1)) = make_uint4(0u, 0u, 0u, 0u);
+            }
 #pragma unroll
-            for (int kgi = 0; kgi < 24; ++kgi)
-                *reinterpret_cast<uint4*>(Xs + sw128_off(m, 24 * hx + kgi)) = make_uint4(0u, 0u, 0u, 0u);
+            for (int s = 0; s < kSpecies - 1; ++s)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4*>(Xs + sw128_off(m, 2 + 8 * s + 4 * hx + q)) = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
                 const int s = (int)((w32[jj >> 2] >> (8 * (jj & 3))) & 0xFFu);
                 if (s != kFe) {
-                    const int f = (kSpecies - 1) * (32 * hx + jj) + s - 1;
+                    const int f = 16 + kWin * (s - 1) + 32 * hx + jj;
                     *reinterpret_cast<__half*>(Xs + sw128_off(m, f >> 3) + 2 * (f & 7)) = __ushort_as_half(0x3C00);
                 }
             }
@@ -331,17 +363,16 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
         __syncthreads();
         if (timing) tp[2] = clock64();
 
-        // ---- M1: layer 1 on tcgen05 (24 K-steps; W1' hi/lo from the ring)
+        // ---- M1: layer 1 on tcgen05 over the needed K-steps (skipped K-steps are all-zero: exact)
         if (ctrl) {
             tc_fence_after();
             const uint32_t xb = smem_u32(Xs);
-            for (int c = 0; c < kChunksL1; ++c) {
-                const int x = cx0 + c;
-                const uint32_t bh = chunk_ready(x);
-                const uint64_t da = desc_a(xb, c);
-                umma_f16(tmem + 0, da, umma_desc(bh, kLboB, kSboNoSw, 0), idesc256, c > 0 ? 1u : 0u);
-                umma_f16(tmem + kHid, da, umma_desc(bh + kSplitBytes, kLboB, kSboNoSw, 0), idesc256, c > 0 ? 1u : 0u);
-                chunk_done(x);
+            for (int e = 0; e < n1; ++e) {
+                const uint32_t bh = chunk_ready();
+                const uint64_t da = desc_a(xb, list[e]);
+                umma_f16(tmem + 0, da, umma_desc(bh, kLboB, kSboNoSw, 0), idesc256, e > 0 ? 1u : 0u);
+                umma_f16(tmem + kHid, da, umma_desc(bh + kSplitBytes, kLboB, kSboNoSw, 0), idesc256, e > 0 ? 1u : 0u);
+                chunk_done();
             }
             umma_commit(bar_done1);
         }
@@ -350,13 +381,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
         tc_fence_after();
         if (timing) tp[3] = clock64();
 
-        // ---- E1: h1 = ReLU(b1' + 2^-s1 (D1 + 2^-11 D2)) -> split -> A
+        // ---- E1: h1 = ReLU(2^-s1 (D1 + 2^-11 D2)) (b1' is inside the GEMM) -> split -> A
         const int q4 = warp & 3, half = warp >> 2;
         const int row = 32 * q4 + lane;
         const uint32_t tlane = tmem + ((uint32_t)(32 * q4) << 16);
         unsigned long long ovf = 0;
         {
-            const float s1 = p.s1_unscale, s1lo = p.s1_unscale * (1.0f / kLoScale);
+            const float s1 = p.s1_unscale, inv_lo = 1.0f / kLoScale;
             for (int cb = 0; cb < 8; ++cb) {
                 const int col = half * 128 + cb * 16;
                 uint32_t d1[16], d2[16];
@@ -368,14 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                     float h[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int n = col + 8 * g8 + i;
-                        const float a = __uint_as_float(d1[8 * g8 + i]) * s1;        // exact (power of 2)
-                        const float b = sb1h[n];
-                        const float s = __fadd_rn(a, b);                            // TwoSum(a, b)
-                        const float bb = __fsub_rn(s, a);
-                        const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
-                        const float small = __fmaf_rn(__uint_as_float(d2[8 * g8 + i]), s1lo, sb1l[n]);
-                        const float v = __fadd_rn(s, __fadd_rn(err, small));
+                        const float v = __fmaf_rn(__uint_as_float(d2[8 * g8 + i]), inv_lo, __uint_as_float(d1[8 * g8 + i])) * s1;
                         h[i] = v > 0.0f ? v : 0.0f;
                     }
                     store_split8(A_hi, A_lo, row, (col >> 3) + g8, h, ovf);
@@ -392,15 +416,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
             tc_fence_after();
             const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo);
             for (int c = 0; c < kChunksL2; ++c) {
-                const int x = cx0 + kChunksL1 + c;
-                const uint32_t bh = chunk_ready(x);
+                const uint32_t bh = chunk_ready();
                 const uint64_t dah = desc_a(ah, c), dal = desc_a(al, c);
                 const uint64_t dbh = umma_desc(bh, kLboB, kSboNoSw, 0);
                 const uint64_t dbl = umma_desc(bh + kSplitBytes, kLboB, kSboNoSw, 0);
                 umma_f16(tmem + 0, dah, dbh, idesc256, c > 0 ? 1u : 0u);
                 umma_f16(tmem + kHid, dah, dbl, idesc256, c > 0 ? 1u : 0u);
                 umma_f16(tmem + kHid, dal, dbh, idesc256, 1u);
-                chunk_done(x);
+                chunk_done();
             }
             umma_commit(bar_done2);
         }
@@ -459,11 +482,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
         mbar_wait(bar_done3, it & 1);
         tc_fence_after();
 
-        // ---- E3: barriers and rates (warps 0..3, one row per thread)
-        if (half == 0) {
-            double accE[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) accE[k] = 0.0;
+        // ---- E3: barriers and rates; warp half h handles hops [4h, 4h+4) of its row
+        {
+            double accE[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 uint32_t da[8], db[8];
@@ -471,36 +492,49 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
                 tmem_ld8(tlane + (uint32_t)(32 * g + 16), db);
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    accE[k] += (double)__uint_as_float(da[k]) + (double)__uint_as_float(db[k]) * (1.0 / 2048.0);
+                for (int k = 0; k < 4; ++k)
+                    accE[k] += (double)__uint_as_float(da[4 * half + k]) +
+                               (double)__uint_as_float(db[4 * half + k]) * (1.0 / 2048.0);
             }
             const int slot = sslot[row];
+            double Gk[4];
             if (slot >= 0) {
                 const int mask = smask[row];
-                double Rs = 0.0;
-                double Ek[8], Gk[8];
+                double Ek[4];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double out = __ldg(p.b3 + k) + accE[k] * p.s3_unscale;
+                for (int k = 0; k < 4; ++k) {
+                    const int kk = 4 * half + k;
+                    const double out = __ldg(p.b3 + kk) + accE[k] * p.s3_unscale;
                     Ek[k] = out > 0.0 ? out : 0.0;
-                    Gk[k] = ((mask >> k) & 1) ? p.P.nu0 * det_exp(-(Ek[k] * p.P.inv_kT)) : 0.0;
-                    Rs = __dadd_rn(Rs, Gk[k]);
+                    Gk[k] = ((mask >> kk) & 1) ? p.P.nu0 * det_exp(-(Ek[k] * p.P.inv_kT)) : 0.0;
                 }
                 if (p.E) {
-                    double2* e2 = reinterpret_cast<double2*>(p.E + (size_t)slot * 8);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) e2[k] = make_double2(Ek[2 * k], Ek[2 * k + 1]);
+                    double2* e2 = reinterpret_cast<double2*>(p.E + (size_t)slot * 8 + 4 * half);
+                    e2[0] = make_double2(Ek[0], Ek[1]);
+                    e2[1] = make_double2(Ek[2], Ek[3]);
                 }
                 if (p.rates) {
-                    double2* g2 = reinterpret_cast<double2*>(p.rates + (size_t)slot * 8);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) g2[k] = make_double2(Gk[2 * k], Gk[2 * k + 1]);
+                    double2* g2 = reinterpret_cast<double2*>(p.rates + (size_t)slot * 8 + 4 * half);
+                    g2[0] = make_double2(Gk[0], Gk[1]);
+                    g2[1] = make_double2(Gk[2], Gk[3]);
                 }
-                if (p.Rsum) p.Rsum[slot] = Rs;
+                if (half == 1) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) sG[row * 4 + k] = Gk[k];
+                }
+            }
+            tc_fence_before();
+            __syncthreads();
+            if (half == 0 && slot >= 0 && p.Rsum) {
+                double Rs = 0.0;                   // R = ((G0 + G1) + ...) + G7, fixed order
+#pragma unroll
+                for (int k = 0; k < 4; ++k) Rs = __dadd_rn(Rs, Gk[k]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) Rs = __dadd_rn(Rs, sG[row * 4 + k]);
+                p.Rsum[slot] = Rs;
             }
         }
-        tc_fence_before();
-        __syncthreads();          // TMEM, A/X and window buffers free for the next tile
+        __syncthreads();          // TMEM, A/X, window and sG buffers free for the next tile
         if (timing) {
             tp[7] = clock64();
             for (int ph = 0; ph < 7; ++ph) atomicAdd(p.phase_cycles + ph, (unsigned long long)(tp[ph + 1] - tp[ph]));

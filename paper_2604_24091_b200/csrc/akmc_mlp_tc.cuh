@@ -7,11 +7,11 @@
 namespace akmc {
 
 constexpr int kTileM = 128;                    // rows (vacancies) per CTA tile = TMEM lanes
-constexpr int kK1 = kWin * (kSpecies - 1);     // layer-1 K: one-hot over the 6 non-Fe species = 384
+constexpr int kK1 = 16 + kWin * (kSpecies - 1);   // layer-1 K: bias K-step + one-hot over 6 non-Fe species = 400
 constexpr int kKChunk = 16;                    // K per ring stage (one UMMA K-step)
-constexpr int kChunksL1 = kK1 / kKChunk;       // 24
+constexpr int kChunksL1 = kK1 / kKChunk;       // 25 (chunk 0 = bias, then species-major groups of 16 slots)
 constexpr int kChunksL2 = kHid / kKChunk;      // 16
-constexpr int kChunksTile = kChunksL1 + kChunksL2;   // 40 ring chunks per tile (W1' then W2)
+constexpr int kChunksTile = kChunksL1 + kChunksL2;   // 41 image chunks (W1' then W2)
 constexpr int kStages = 4;
 constexpr int kSplitBytes = kHid * kKChunk * 2;        // one fp16 split of a B chunk (N = 256): 8 KiB
 constexpr int kStageBytes = 2 * kSplitBytes;           // hi + lo: 16 KiB
@@ -31,10 +31,8 @@ struct MlpTcParams {
     const int* nrows_dev;            // device row count (nullptr => nrows_host)
     int nrows_host;
     // weights (prepared at init)
-    const __half* Bimg;              // [40][2][N=256 x K=16] W1'^T (24 chunks) then W2^T (16 chunks), UMMA images
+    const __half* Bimg;              // [41][2][N=256 x K=16] bias + W1'^T (25 chunks) then W2^T (16), UMMA images
     const __half* W3img;             // [2][N=16 x K=256] W3^T splits, UMMA image
-    const float* b1hi;               // [256] layer-1 bias b1' = b1 + sum_slot W1[slot,Fe] as a float pair
-    const float* b1lo;               // [256]
     const float* b2;                 // [256]
     const double* b3;                // [8]
     float s1_unscale;                // 2^-s1 (W1' scaled by 2^s1 before splitting)
@@ -46,7 +44,7 @@ struct MlpTcParams {
     double* Rsum;                    // [.]    or nullptr
     double* E;                       // [.][8] or nullptr
     unsigned long long* overflow;    // count of |h| beyond the fp16 range (diagnostic)
-    unsigned long long* phase_cycles; // [8] optional: summed clock64 per tile phase (AKMC_PHASE_TIMING)
+    unsigned long long* phase_cycles; // [10] optional: summed clock64 per tile phase (AKMC_PHASE_TIMING)
 };
 
 // smem bytes needed by the kernel

@@ -14,6 +14,7 @@
 #include "../../include/akmc.h"
 #include "akmc_kernels.cuh"
 #include "akmc_mlp_tc.cuh"
+#include "akmc_engine.cuh"
 #include <nccl.h>
 
 using namespace akmc;
@@ -146,6 +147,15 @@ struct akmc_handle {
     float s1u = 1.0f, s2u = 1.0f;
     double s3u = 1.0;
     unsigned long long* d_overflow = nullptr;
+    // phase engine (akmc_engine.cuh)
+    bool engine = true;               // false: legacy grid-synchronous inner loop (AKMC_LEGACY_LOOP=1)
+    bool tc = false;                  // MLP at FP32 precision: cluster tensor-core evaluator
+    int n_clusters = 0;
+    MemoEntry* d_memo = nullptr;      // [vcap][2]
+    float* d_W1f = nullptr;           // [385][256]
+    uint8_t* d_W2e = nullptr;         // [8][32 KiB]
+    uint8_t* d_W3e = nullptr;         // [8][2 KiB]
+    unsigned int* d_cursor = nullptr;
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
     size_t ev_used = 0;
@@ -204,7 +214,7 @@ void free_all(akmc_handle* h)
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
-                    h->d_b2, h->d_b3, h->d_overflow};
+                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -352,6 +362,42 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
         }
     std::vector<float> b2f(kHid);
     for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
+    // phase-engine evaluator images (akmc_engine.cu): FP32 layer-1 table (b1' then W1' rows), and per
+    // cluster CTA r the fp16 hi/lo UMMA images of W2^T columns [32r, 32r+32) and W3 rows [32r, 32r+32)
+    {
+        std::vector<float> w1f((size_t)kW1Rows * kHid);
+        for (int n = 0; n < kHid; ++n) w1f[n] = (float)b1p[n];
+        for (int s = 1; s < kSpecies; ++s)
+            for (int slot = 0; slot < kWin; ++slot)
+                for (int n = 0; n < kHid; ++n)
+                    w1f[(size_t)(1 + (s - 1) * kWin + slot) * kHid + n] = (float)W1p[(size_t)(16 + (s - 1) * kWin + slot) * kHid + n];
+        const size_t w2b = (size_t)(kHid / 16) * 2 * kSliceN * 16 * 2, w3b = (size_t)(kSliceN / 16) * 2 * 16 * 16 * 2;
+        std::vector<uint8_t> w2e((size_t)kClusterN * w2b, 0), w3e((size_t)kClusterN * w3b, 0);
+        auto put_split = [](uint8_t* stepbase, int N, int n, int kk, double w) {   // one K-step (16), hi then lo
+            const __half hi = __float2half_rn((float)w);
+            const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
+            const size_t off = ((size_t)(kk / 8) * (N / 8) + n / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2;
+            const size_t split = (size_t)N * 16 * 2;
+            reinterpret_cast<__half*>(stepbase + off)[0] = hi;
+            reinterpret_cast<__half*>(stepbase + split + off)[0] = lo;
+        };
+        for (int r = 0; r < kClusterN; ++r) {
+            for (int k = 0; k < kHid; ++k)
+                for (int c = 0; c < kSliceN; ++c)
+                    put_split(w2e.data() + r * w2b + (size_t)(k / 16) * 2 * kSliceN * 16 * 2, kSliceN, c, k % 16,
+                              std::ldexp(W2[(size_t)k * kHid + kSliceN * r + c], s2));
+            for (int kk = 0; kk < kSliceN; ++kk)
+                for (int n = 0; n < 8; ++n)
+                    put_split(w3e.data() + r * w3b + (size_t)(kk / 16) * 2 * 16 * 16 * 2, 16, n, kk % 16,
+                              std::ldexp(W3[(size_t)(kSliceN * r + kk) * 8 + n], s3));
+        }
+        CK(h, cudaMalloc(&h->d_W1f, w1f.size() * sizeof(float)));
+        CK(h, cudaMalloc(&h->d_W2e, w2e.size()));
+        CK(h, cudaMalloc(&h->d_W3e, w3e.size()));
+        CK(h, cudaMemcpy(h->d_W1f, w1f.data(), w1f.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(h->d_W2e, w2e.data(), w2e.size(), cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(h->d_W3e, w3e.data(), w3e.size(), cudaMemcpyHostToDevice));
+    }
     CK(h, cudaMalloc(&h->d_Bimg, img.size()));
     CK(h, cudaMalloc(&h->d_W3img, w3img.size()));
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
@@ -366,6 +412,20 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
         CK(h, cudaMemset(h->d_phase_cycles, 0, 10 * sizeof(unsigned long long)));
     }
     return AKMC_OK;
+}
+
+EngineParams engine_params(akmc_handle* h, int mode)
+{
+    EngineParams p{};
+    p.mode = mode;
+    p.model = h->cfg.barrier_model;
+    p.species = h->d_species; p.vac = h->d_vac; p.F = h->F; p.G = h->G; p.P = h->P; p.S = h->S;
+    p.segs = h->d_segs; p.members = h->d_members; p.ctr = h->d_ctr; p.memo = h->d_memo;
+    p.scratch = h->d_scratch; p.iscratch = h->d_iscratch; p.cursor = h->d_cursor;
+    p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
+    p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
+    p.overflow = h->d_overflow;
+    return p;
 }
 
 // evaluate rows -> rates/R/E with the handle's model at `prec`
@@ -396,6 +456,13 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         eval_mlp_fp64_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
                                                            h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
         CK(h, cudaGetLastError());
+    } else if (h->engine) {
+        EngineParams p = engine_params(h, kEngineEval);
+        p.windows = windows; p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
+        p.rates = rates; p.Rsum = R; p.E = E;
+        CK(h, cudaMemsetAsync(h->d_cursor, 0, sizeof(unsigned int), h->stream));
+        const int need = (max_rows + kRoundRows * kClusterN - 1) / (kRoundRows * kClusterN);
+        CK(h, launch_engine(p, true, std::max(1, std::min(h->n_clusters, need)), h->num_sms, h->stream));
     } else {
         MlpTcParams p{};
         p.species = h->d_species; p.vac = h->d_vac; p.windows = windows; p.F = h->F; p.G = h->G;
@@ -752,6 +819,18 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         rc = prepare_fast_weights(h, mlp);
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
+    h->tc = cfg->barrier_model == AKMC_MODEL_MLP && cfg->precision == AKMC_PREC_FP32;
+    h->engine = std::getenv("AKMC_LEGACY_LOOP") == nullptr;
+    CKI(engine_setup());
+    if (h->tc) {
+        h->n_clusters = engine_max_clusters();
+        if (h->n_clusters <= 0) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_CUDA, "no co-resident 8-CTA cluster for the evaluator"); }
+    }
+    CKI(cudaMalloc(&h->d_cursor, sizeof(unsigned int)));
+    if (h->sub) {
+        CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
+        CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
+    }
     CKI(cudaStreamSynchronize(h->stream));
 #undef CKI
     *out = h;
@@ -818,6 +897,18 @@ static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_
                                                         h->d_segs, h->d_members, h->d_mactive, h->d_ctr);
 }
 
+// the whole phase on the device: activate + segments, then the persistent phase engine runs every domain
+// of the phase to the end of its window (a2-a8 without any grid-wide synchronisation)
+static int enqueue_phase_engine(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s)
+{
+    enqueue_phase_start(h, ph, s);
+    CK(h, cudaGetLastError());
+    EngineParams p = engine_params(h, kEnginePhase);
+    p.ph = ph;
+    CK(h, launch_engine(p, h->tc, h->n_clusters, h->num_sms, s));
+    return AKMC_OK;
+}
+
 // one inner iteration (a1 rows, a2-a5 eval, a6-a7 select) on stream s; graph adds the a8 condition kernel
 static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s, bool graph,
                              cudaGraphConditionalHandle cond)
@@ -866,6 +957,11 @@ static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGra
         return done(fail(h, AKMC_ERR_CUDA, "graph capture begin failed"));
     for (int q = q0; q < q1 && rc == AKMC_OK; ++q) {
         const PhaseInfo* ph = h->d_phase + q;
+        if (h->engine) {
+            rc = enqueue_phase_engine(h, ph, cs);
+            launches += 3;
+            continue;
+        }
         enqueue_phase_start(h, ph, cs);
         launches += 2;
         cudaStreamCaptureStatus st;
@@ -939,6 +1035,29 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
         h->total.kernel_launches += 1;
         for (int q = 0; q < 8; ++q) {
             const PhaseInfo* ph = h->d_phase + q;
+            if (h->engine) {
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                if (h->ev_used + 2 > h->ev.size()) {
+                    for (int i = 0; i < 64; ++i) {
+                        cudaEvent_t e;
+                        CK(h, cudaEventCreate(&e));
+                        h->ev.push_back(e);
+                    }
+                }
+                e0 = h->ev[h->ev_used++];
+                e1 = h->ev[h->ev_used++];
+                CK(h, cudaEventRecord(e0, h->stream));
+                const int rc = enqueue_phase_engine(h, ph, h->stream);
+                if (rc != AKMC_OK) return rc;
+                CK(h, cudaEventRecord(e1, h->stream));
+                h->total.kernel_launches += 3;
+                h->total.mlp_launches += 1;
+                if (h->multi) {
+                    const int rc2 = exchange_deltas(h);
+                    if (rc2 != AKMC_OK) return rc2;
+                }
+                continue;
+            }
             enqueue_phase_start(h, ph, h->stream);
             CK(h, cudaGetLastError());
             h->total.kernel_launches += 2;
@@ -1028,7 +1147,7 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
     const auto t1 = std::chrono::steady_clock::now();
     h->total.events += (int64_t)(c1.events - c0.events);
     h->total.hop_evals += (int64_t)(c1.hop_evals - c0.hop_evals);
-    h->total.mlp_rows += (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
+    h->total.mlp_rows += (h->engine && h->sub) ? (int64_t)(c1.mrows - c0.mrows) : (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
     h->total.clamps += (int64_t)(c1.clamps - c0.clamps);
     h->total.terminal_voxels += (int64_t)(c1.terminal - c0.terminal);
     h->total.wall_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -1042,7 +1161,7 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
         d.sweeps = h->total.sweeps - before.sweeps;
         d.kernel_launches = h->total.kernel_launches - before.kernel_launches;
         d.mlp_launches = h->total.mlp_launches - before.mlp_launches;
-        d.mlp_rows = d.hop_evals / 8;
+        d.mlp_rows = h->total.mlp_rows - before.mlp_rows;
         d.mlp_ms = h->total.mlp_ms - before.mlp_ms;
         d.wall_ms = h->total.wall_ms - before.wall_ms;
         *ctr = d;

@@ -67,7 +67,7 @@ __device__ __forceinline__ void log_entry(int4* log, unsigned long long* nlog, i
 // A site may be written several times in one phase (a vacancy enters and leaves it), so species entries
 // carry the site's FINAL value, read here after the phase: duplicates are identical and the receiver may
 // apply entries in any order.
-__global__ void pack_deltas_kernel(const int4* __restrict__ log, const unsigned long long* nlog_p, int logcap, Frame F,
+static __global__ void pack_deltas_kernel(const int4* __restrict__ log, const unsigned long long* nlog_p, int logcap, Frame F,
                                    DistParams D, const uint8_t* __restrict__ species, int4* sendbuf, int* overflow)
 {
     const int n = (int)min((unsigned long long)logcap, *nlog_p);
@@ -92,7 +92,7 @@ __global__ void pack_deltas_kernel(const int4* __restrict__ log, const unsigned 
     }
 }
 
-__global__ void clear_headers_kernel(int4* sendbuf, int npeer, int cap, unsigned long long* nlog)
+static __global__ void clear_headers_kernel(int4* sendbuf, int npeer, int cap, unsigned long long* nlog)
 {
     const int r = threadIdx.x;
     if (r < npeer) sendbuf[(size_t)r * (cap + 1)] = make_int4(0, 0, 0, 0);
@@ -100,7 +100,7 @@ __global__ void clear_headers_kernel(int4* sendbuf, int npeer, int cap, unsigned
 }
 
 // apply received entries: species writes into block/halo (with wrap-axis ghosts); vacancy arrivals
-__global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, int npeer, Frame F, DistParams D, uint8_t* species,
+static __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, int npeer, Frame F, DistParams D, uint8_t* species,
                                      int4* vac, int* gid, int* nvac_local, int vcap, int* overflow)
 {
     for (int r = 0; r < npeer; ++r) {
@@ -138,7 +138,7 @@ __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, int npeer
 // cells (may extend into the halo); buffer order x fastest, basis interleaved.
 struct SlabRange { int lo[3], hi[3]; };
 
-__global__ void pack_slab_kernel(const uint8_t* __restrict__ species, Frame F, SlabRange R, uint8_t* buf)
+static __global__ void pack_slab_kernel(const uint8_t* __restrict__ species, Frame F, SlabRange R, uint8_t* buf)
 {
     const int nx = R.hi[0] - R.lo[0], ny = R.hi[1] - R.lo[1], nz = R.hi[2] - R.lo[2];
     const long long n = 2ll * nx * ny * nz;
@@ -150,7 +150,7 @@ __global__ void pack_slab_kernel(const uint8_t* __restrict__ species, Frame F, S
     }
 }
 
-__global__ void unpack_slab_kernel(const uint8_t* __restrict__ buf, Frame F, SlabRange R, uint8_t* species)
+static __global__ void unpack_slab_kernel(const uint8_t* __restrict__ buf, Frame F, SlabRange R, uint8_t* species)
 {
     const int nx = R.hi[0] - R.lo[0], ny = R.hi[1] - R.lo[1], nz = R.hi[2] - R.lo[2];
     const long long n = 2ll * nx * ny * nz;

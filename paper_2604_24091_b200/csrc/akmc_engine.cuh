@@ -1,0 +1,83 @@
+// akmc_engine.cuh -- the sublattice phase engine: a persistent, cluster-resident kernel that runs every
+// domain of a sublattice phase to the end of its time window with no grid-wide synchronisation.
+//
+// Why: in the windowed synchronous sublattice scheme (reading A19) the inner loop
+// of a phase runs until the LAST domain overshoots the window, and the per-domain event count has a
+// heavy tail (a vacancy next to a low-barrier solute flickers thousands of times per window).  A
+// grid-synchronous inner loop pays one full barrier-network latency per event of the slowest domain.
+// Here every CTA owns a handful of domains and iterates them independently; the 8 CTAs of a cluster
+// share one barrier-network evaluator whose weights stay resident in shared memory (each CTA holds a
+// 32-column slice of W2 and W3), and results are memoised per vacancy (exact: the rates are a pure
+// function of the 64-byte window).
+#pragma once
+#include "akmc_kernels.cuh"
+
+namespace akmc {
+
+constexpr int kClusterN = 8;                   // CTAs per cluster; CTA r owns hidden columns [32r, 32r+32)
+constexpr int kSliceN = kHid / kClusterN;      // 32
+constexpr int kRoundRows = 16;                 // rows a CTA contributes per evaluation round (tile M = 128)
+constexpr int kSegsPerCta = 16;                // domains (segments) a CTA holds at once
+constexpr int kRowCap = 128;                   // members (vacancies) a CTA holds at once
+constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
+
+// exact memo of the barrier network per vacancy slot (2 ways, most recent first)
+struct MemoEntry {
+    uint8_t key[kWin];      // window bytes (0xFF: empty -- species codes are < kSpecies)
+    double G[8];            // rates
+    double R;               // sum in hop order
+    int clamps;             // pair-model clamps of this evaluation (kept so counters match the oracle)
+    int pad;
+};
+static_assert(sizeof(MemoEntry) == 144, "memo entry layout");
+
+struct EngineWeights {
+    const float* W1f;       // [385][256] FP32: row 0 = b1' = b1 + sum_slot W1[slot,Fe]; row 1+(s-1)*64+slot = W1'
+    const uint8_t* W2img;   // [8 CTAs][16 K-steps][hi 1 KiB | lo 1 KiB] fp16 UMMA images of W2^T slices * 2^s2
+    const uint8_t* W3img;   // [8 CTAs][2 K-steps][hi 512 B | lo 512 B] of W3 rows [32r,32r+32) (N padded 16) * 2^s3
+    const float* b2;        // [256]
+    const double* b3;       // [8]
+    float s2u;              // 2^-s2
+    double s3u;             // 2^-s3
+    const double* mlp64;    // FP64 weights (verify precision)
+};
+
+enum EngineMode { kEnginePhase = 0, kEngineEval = 1 };
+
+struct EngineParams {
+    int mode;               // kEnginePhase: run the phase's domains; kEngineEval: evaluate a row list
+    int model;              // AKMC_MODEL_PAIR (0) / AKMC_MODEL_MLP (1)
+    uint8_t* species;
+    int4* vac;
+    Frame F;
+    GeomTables G;
+    PhysParams P;
+    SubParams S;
+    const PhaseInfo* ph;
+    const Segment* segs;
+    const int* members;
+    DevCounters* ctr;
+    MemoEntry* memo;        // [vcap][2] (phase mode) or nullptr
+    double* scratch;        // trees of segments with > 16 members (4 doubles per member, by member offset)
+    int* iscratch;
+    // eval mode
+    const uint8_t* windows; // [n][64] or nullptr (then rows -> vac slots, gathered)
+    const int* rows;        // slot list or nullptr (row i = slot i)
+    const int* nrows_dev;   // device row count or nullptr
+    int nrows_host;
+    unsigned int* cursor;   // work cursor (eval mode), zeroed before launch
+    double* rates;          // [.][8] outputs (eval mode)
+    double* Rsum;
+    double* E;
+    EngineWeights W;
+    unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
+};
+
+size_t engine_smem_bytes();
+cudaError_t engine_setup();
+// clusters of 8 that can be co-resident (persistent grid); 0 on failure
+int engine_max_clusters();
+// tc = 1: FP32-equivalent tensor-core evaluator (cluster launch); tc = 0: FP64 evaluator (plain launch)
+cudaError_t launch_engine(const EngineParams& p, bool tc, int nclusters, int num_sms, cudaStream_t s);
+
+} // namespace akmc

@@ -16,6 +16,8 @@ namespace akmc {
 
 struct DevCounters {                 // device-side counters (unsigned long long for atomics)
     unsigned long long events, hop_evals, clamps, terminal, nrun, nseg, total, nrows;
+    unsigned long long chunk;        // phase engine: next segment to hand out (reset per phase)
+    unsigned long long mrows;        // barrier-network rows actually evaluated (memo misses)
 };
 
 // ------------------------------------------------------------------ window gather
@@ -32,7 +34,7 @@ __device__ __forceinline__ int row_count(const int* nrows_dev, int nrows_host)
 }
 
 // ------------------------------------------------------------------ pair KRA, FP64 (thread per row)
-__global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4* __restrict__ vac,
+static __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4* __restrict__ vac,
                                  const uint8_t* __restrict__ windows, Frame F, GeomTables G, PhysParams P,
                                  const int* __restrict__ rows, const int* __restrict__ nrows_dev, int nrows_host,
                                  double* __restrict__ rates, double* __restrict__ Rsum, double* __restrict__ Eout,
@@ -70,7 +72,7 @@ __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, const int4
 
 // ------------------------------------------------------------------ MLP, FP64 (block of 256 per row)
 // layer 1 as the embedding bag over the 64 one-hot rows in slot order (== dense fma loop, A8)
-__global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
+static __global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
     const uint8_t* __restrict__ species, const int4* __restrict__ vac, const uint8_t* __restrict__ windows, Frame F,
     GeomTables G, PhysParams P, const double* __restrict__ mlp, const int* __restrict__ rows,
     const int* __restrict__ nrows_dev, int nrows_host, double* __restrict__ rates, double* __restrict__ Rsum,
@@ -201,7 +203,7 @@ __device__ __forceinline__ int4 apply_hop(uint8_t* species, int4* vac, int slot,
 }
 
 // ------------------------------------------------------------------ serial BKL (a10): thread per voxel
-__global__ void select_serial_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, int nvox,
+static __global__ void select_serial_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, int nvox,
                                      const int* __restrict__ vstart, const double* __restrict__ rates,
                                      const double* __restrict__ Rsum, double* scratch, double* clock,
                                      long long* nev, int* term, uint64_t seed, DevCounters* ctr)
@@ -280,11 +282,11 @@ __device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, lo
 }
 
 // nvac = slot capacity; nvac_dev (multi-rank) = live slot count (slots may be departed: vac.x < 0)
-__global__ void activate_kernel(const int4* __restrict__ vac, int nvac, const int* __restrict__ nvac_dev, SubParams S,
+static __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, const int* __restrict__ nvac_dev, SubParams S,
                                 const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; }
+    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; ctr->chunk = 0; }
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     if (i >= n) return;
     const int4 v = vac[i];
@@ -324,7 +326,7 @@ __device__ __forceinline__ int block_alloc(int v, unsigned long long* counter)
     return r;
 }
 
-__global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac,
+static __global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac,
                                                        const int* __restrict__ nvac_dev, SubParams S,
                                                        const PhaseInfo* __restrict__ ph, int* dmin, int* head,
                                                        const int* __restrict__ next, Segment* segs, int* members,
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ 
 }
 
 // rows of this inner iteration = active members of running segments; also resets nrun
-__global__ void __launch_bounds__(256) rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
+static __global__ void __launch_bounds__(256) rows_kernel(const Segment* __restrict__ segs, const int* __restrict__ members,
                                                    const uint8_t* __restrict__ mactive, int* rows, DevCounters* ctr)
 {
     const int nseg = (int)ctr->nseg;
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(256) rows_kernel(const Segment* __restrict__ s
     }
 }
 
-__global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, SubParams S,
+static __global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTables G, SubParams S,
                                   const PhaseInfo* __restrict__ ph, Segment* segs, const int* __restrict__ members,
                                   uint8_t* mactive, const double* __restrict__ rates, const double* __restrict__ Rsum,
                                   double* scratch, int* iscratch, DevCounters* ctr)
@@ -472,7 +474,7 @@ __global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, GeomTabl
 }
 
 // a8: continue the inner loop while some domain applied an event; resets nrun/nrows for the next trip
-__global__ void loop_cond_kernel(DevCounters* ctr, cudaGraphConditionalHandle handle)
+static __global__ void loop_cond_kernel(DevCounters* ctr, cudaGraphConditionalHandle handle)
 {
     const unsigned long long run = ctr->nrun;
     ctr->nrun = 0;
@@ -480,13 +482,13 @@ __global__ void loop_cond_kernel(DevCounters* ctr, cudaGraphConditionalHandle ha
     cudaGraphSetConditional(handle, run > 0 ? 1u : 0u);
 }
 
-__global__ void add_window_kernel(double* clock, int nvox, double w)
+static __global__ void add_window_kernel(double* clock, int nvox, double w)
 {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < nvox) clock[v] = __dadd_rn(clock[v], w);
 }
 
-__global__ void fill_int_kernel(int* p, long long n, int val)
+static __global__ void fill_int_kernel(int* p, long long n, int val)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = val;
@@ -506,7 +508,7 @@ __device__ __forceinline__ int vac_in_word(uint32_t w)
     return c;
 }
 
-__global__ void scan_count_kernel(const uint4* __restrict__ sp, long long nwords, int* bcount, unsigned int* maxcode)
+static __global__ void scan_count_kernel(const uint4* __restrict__ sp, long long nwords, int* bcount, unsigned int* maxcode)
 {
     const long long wi = (long long)blockIdx.x * kScanThreads + threadIdx.x;
     int c = 0;
@@ -538,7 +540,7 @@ __global__ void scan_count_kernel(const uint4* __restrict__ sp, long long nwords
 }
 
 // exclusive scan of n ints in place (single block of 1024 threads); total -> *total
-__global__ void __launch_bounds__(1024) scan_blocks_kernel(int* a, int n, long long* total)
+static __global__ void __launch_bounds__(1024) scan_blocks_kernel(int* a, int n, long long* total)
 {
     __shared__ long long part[1024];
     const int per = (n + 1023) / 1024;
@@ -557,7 +559,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(int* a, int n, long l
     for (int i = b0; i < min(n, b0 + per); ++i) { const int t = a[i]; a[i] = (int)acc; acc += t; }
 }
 
-__global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords, const int* __restrict__ boff,
+static __global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords, const int* __restrict__ boff,
                                   Frame F, int4* vac)
 {
     const long long wi = (long long)blockIdx.x * kScanThreads + threadIdx.x;
@@ -600,7 +602,7 @@ __global__ void scan_write_kernel(const uint4* __restrict__ sp, long long nwords
 }
 
 // canonical (x fastest, basis interleaved) <-> storage (halo + ghosts) layout conversions
-__global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_t* storage, Frame F, long long ncanon)
+static __global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_t* storage, Frame F, long long ncanon)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ncanon) return;
@@ -615,7 +617,7 @@ __global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_
     write_site(storage, F, vox, 2 * x + b, 2 * y + b, 2 * z + b, canon[i]);
 }
 
-__global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uint8_t* canon, Frame F, long long ncanon)
+static __global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uint8_t* canon, Frame F, long long ncanon)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ncanon) return;
@@ -631,7 +633,7 @@ __global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uin
 }
 
 // vstart[v] = first slot whose voxel >= v (slots are in site order, hence voxel-major)
-__global__ void vstart_kernel(const int4* __restrict__ vac, int nvac, int nvox, int* vstart)
+static __global__ void vstart_kernel(const int4* __restrict__ vac, int nvac, int nvox, int* vstart)
 {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v > nvox) return;

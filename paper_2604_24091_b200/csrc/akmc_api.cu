@@ -135,6 +135,7 @@ struct akmc_handle {
     long long* d_nev = nullptr;
     int* d_term = nullptr;
     int *d_dmin = nullptr, *d_head = nullptr, *d_next = nullptr, *d_members = nullptr, *d_rows = nullptr;
+    int4* d_mpos = nullptr;           // member positions (phase engine)
     Segment* d_segs = nullptr;
     uint8_t* d_mactive = nullptr;
     DevCounters* d_ctr = nullptr;
@@ -212,7 +213,7 @@ inline unsigned blocks_for(long long n, int bs) { return (unsigned)((n + bs - 1)
 void free_all(akmc_handle* h)
 {
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
-                    h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_rows,
+                    h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
                     h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor};
     for (void* p : ptrs)
@@ -408,8 +409,8 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     CK(h, mlp_tc_setup());
     if (std::getenv("AKMC_PHASE_TIMING")) {
-        CK(h, cudaMalloc(&h->d_phase_cycles, 10 * sizeof(unsigned long long)));
-        CK(h, cudaMemset(h->d_phase_cycles, 0, 10 * sizeof(unsigned long long)));
+        CK(h, cudaMalloc(&h->d_phase_cycles, 64 * sizeof(unsigned long long)));
+        CK(h, cudaMemset(h->d_phase_cycles, 0, 64 * sizeof(unsigned long long)));
     }
     return AKMC_OK;
 }
@@ -420,11 +421,12 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.mode = mode;
     p.model = h->cfg.barrier_model;
     p.species = h->d_species; p.vac = h->d_vac; p.F = h->F; p.G = h->G; p.P = h->P; p.S = h->S;
-    p.segs = h->d_segs; p.members = h->d_members; p.ctr = h->d_ctr; p.memo = h->d_memo;
+    p.segs = h->d_segs; p.members = h->d_members; p.mpos = h->d_mpos; p.ctr = h->d_ctr; p.memo = h->d_memo;
     p.scratch = h->d_scratch; p.iscratch = h->d_iscratch; p.cursor = h->d_cursor;
     p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
     p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
+    p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
     return p;
 }
 
@@ -802,6 +804,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaGetLastError());
         CKI(cudaMalloc(&h->d_next, nv * sizeof(int)));
         CKI(cudaMalloc(&h->d_members, nv * sizeof(int)));
+        CKI(cudaMalloc(&h->d_mpos, nv * sizeof(int4)));
         CKI(cudaMalloc(&h->d_rows, nv * sizeof(int)));
         CKI(cudaMalloc(&h->d_segs, nv * sizeof(Segment)));
         CKI(cudaMalloc(&h->d_mactive, nv));
@@ -894,7 +897,7 @@ static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_
     activate_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
                                                         h->d_ctr);
     segments_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr);
+                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr, h->d_mpos);
 }
 
 // the whole phase on the device: activate + segments, then the persistent phase engine runs every domain
@@ -1327,12 +1330,23 @@ void akmc_free(akmc_handle* h)
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->d_phase_cycles) {
-        unsigned long long c[10] = {0};
+        unsigned long long c[64] = {0};
         cudaMemcpy(c, h->d_phase_cycles, sizeof(c), cudaMemcpyDeviceToHost);
         const double t = c[7] ? (double)c[7] : 1.0;
-        std::fprintf(stderr, "[akmc phase timing] tiles=%llu cycles/tile: gather %.0f encode %.0f M1 %.0f E1 %.0f M2 %.0f"
-                     " E2 %.0f M3+E3 %.0f; CTA loop %.0f cycles x %llu CTAs\n", c[7], c[0] / t, c[1] / t, c[2] / t,
-                     c[3] / t, c[4] / t, c[5] / t, c[6] / t, c[9] ? (double)c[8] / (double)c[9] : 0.0, c[9]);
+        if (c[7])
+            std::fprintf(stderr, "[akmc phase timing] tiles=%llu cycles/tile: gather %.0f encode %.0f M1 %.0f E1 %.0f M2 %.0f"
+                         " E2 %.0f M3+E3 %.0f; CTA loop %.0f cycles x %llu CTAs\n", c[7], c[0] / t, c[1] / t, c[2] / t,
+                         c[3] / t, c[4] / t, c[5] / t, c[6] / t, c[9] ? (double)c[8] / (double)c[9] : 0.0, c[9]);
+        const unsigned long long* d = c + 32;
+        if (d[7]) {
+            const double n = (double)d[7];
+            std::fprintf(stderr, "[akmc engine] CTA-launches=%llu (phase %llu) iterations/CTA %.1f (max %llu) rounds/CTA %.1f"
+                         " eval-rounds/CTA %.1f refills/CTA %.1f; cycles/CTA: control %.0f rounds %.0f select %.0f total %.0f\n",
+                         d[7], d[10], d[0] / n, d[1], d[2] / n, d[3] / n, d[8] / n, d[4] / n, d[5] / n, d[6] / n, d[9] / n);
+            std::fprintf(stderr, "[akmc engine] cycles/CTA: refill %.0f rows %.0f gather+memo %.0f | L1 %.0f exchange %.0f"
+                         " L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n, d[14] / n, d[15] / n,
+                         d[16] / n, d[17] / n, d[18] / n);
+        }
         cudaFree(h->d_phase_cycles);
         h->d_phase_cycles = nullptr;
     }

@@ -1,26 +1,26 @@
 // akmc_engine.cu -- sublattice phase engine (see akmc_engine.cuh) and its barrier-network evaluator.
 //
-// Control (every CTA, independently): hold up to 16 domains (segments) of the current phase; per
-// iteration gather the 64-site window of every active vacancy, look the window up in the
-// per-vacancy memo, evaluate the misses, then run one BKL step per running domain (tree over the
-// domain's rates, Philox draw, window test, hop) exactly as the oracle's run_sublattice does; refill
-// from the phase's segment list when all held domains have stopped.
+// Control (every CTA, independently): hold up to 32 domains (segments) of the current phase in slots;
+// per iteration gather the 64-site window of every active vacancy, look the window up in
+// the per-vacancy memo, evaluate the misses, then run one BKL step per running domain (tree over the
+// domain's rates, Philox draw, window test, hop) exactly as the oracle's run_sublattice does.  Stopped
+// domains free their slots, which are refilled from the phase's segment list (domains of a phase are
+// independent, so the processing order does not change any trajectory).
 //
-// Evaluator, FP32-equivalent mode (cluster of 8 CTAs, rounds in lockstep): each CTA contributes up to
-// 16 miss rows per round (tile M = 128 rows = 8 x 16) and broadcasts their windows to the cluster;
-//   L1 (CUDA cores): CTA r computes h1[:, 32r:32r+32] = ReLU(b1' + sum over the row's non-Fe slots of
-//      W1'(s, slot)) -- the one-hot layer is a sparse gather-sum (~6 terms), not a dense contraction --
-//      in FP64, rounded once to FP32 and split into fp16 hi + lo*2^-11; the slice is bulk-copied into
-//      the A operand of the other 7 CTAs (DSMEM);
-//   L2 (tcgen05, M=128 N=32 K=256): D1 = Ahi*W2hi, D2 = Ahi*W2lo + Alo*W2hi with CTA r's resident
-//      W2 slice; h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> fp16 split (local);
+// Evaluator, FP32-equivalent mode (cluster of 8 CTAs, rounds in lockstep; tile M = 128 = 8 x 16 rows):
+//   L1 (CUDA cores, requesting CTA): h1 = ReLU(b1' + sum over the row's non-Fe slots of W1'(s, slot)) --
+//      the one-hot layer is a sparse gather-sum (~6 rows of W1'), not a dense contraction -- summed in
+//      FP64 in slot order, rounded once to FP32, split into fp16 hi + lo*2^-11 and written to rows
+//      [16r, 16r+16) of the A operand; the request bulk-copies those rows into the other 7 CTAs' A;
+//   L2 (tcgen05, M=128 N=32 K=256): CTA r computes columns [32r, 32r+32) with its resident W2 slice:
+//      D1 = Ahi*W2hi, D2 = Ahi*W2lo + Alo*W2hi; h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> fp16 split;
 //   L3 (tcgen05, M=128 N=16 K=32): CTA r's partial of the 8 outputs over its 32 h2 columns; the
 //      partials of row block [16s, 16s+16) are bulk-copied to CTA s, which sums them in fixed order
-//      (FP64), adds b3, clamps at 0 and forms Gamma = nu0 det_exp(-E/kT).
+//      (FP64), adds b3, clamps at 0 and forms Gamma = nu0 det_exp(-E/kT) (P:284-291).
 // The result of a row depends only on its window (rows of a tile do not interact, the order of every
 // sum is fixed), so memoisation and any tiling or decomposition give bit-identical trajectories.
-// FP64 verify mode: each CTA evaluates its own misses (pair KRA or FP64 MLP, same code as the FP64
-// kernels), no cluster.
+// FP64 verify mode: each CTA evaluates its own misses (pair KRA or FP64 MLP, same arithmetic as the
+// FP64 kernels), no cluster.
 #include "akmc_engine.cuh"
 #include "akmc_ptx.cuh"
 
@@ -30,68 +30,72 @@ namespace {
 using namespace ptx;
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kTileRows = kRoundRows * kClusterN;              // 128
-constexpr uint32_t kCoreCol = (kTileRows / 8) * 128;           // 2048 B between K-adjacent core matrices
+constexpr uint32_t kRowGroupA = (kHid / 8) * 128;              // 4096 B: one 8-row group of h1 (M-major layout)
 constexpr uint32_t kSplitA = kTileRows * kHid * 2;             // 64 KiB: one fp16 split of h1
+constexpr uint32_t kCoreColH2 = (kTileRows / 8) * 128;         // 2048 B: K-adjacent core matrices of H2
 constexpr uint32_t kSplitH2 = kTileRows * kSliceN * 2;         // 8 KiB: one fp16 split of the h2 slice
 constexpr uint32_t kW2Split = kSliceN * 16 * 2;                // 1 KiB: one split of a W2-slice K-step
 constexpr uint32_t kW2Bytes = (kHid / 16) * 2 * kW2Split;      // 32 KiB
 constexpr uint32_t kW3Split = 16 * 16 * 2;                     // 512 B
 constexpr uint32_t kW3Bytes = (kSliceN / 16) * 2 * kW3Split;   // 2 KiB
-constexpr uint32_t kReqBytes = 16 + kRoundRows * kWin;         // header + 16 windows
 constexpr float kLo = 2048.0f;
 
 struct ReqHdr { int n, more, alive, pad; };
 
 struct Ctl {
-    long long seg_dom[kSegsPerCta];
-    double seg_t[kSegsPerCta];
-    int seg_goff[kSegsPerCta];      // global member offset (scratch of big trees)
-    int seg_moff[kSegsPerCta];      // offset into the CTA's member arrays
-    int seg_cnt[kSegsPerCta];
-    unsigned seg_it[kSegsPerCta];
-    int seg_run[kSegsPerCta];
-    long long cand_dom[2 * kSegsPerCta];   // domains waiting to be loaded: [0, npend) carried over, then new
-    int cand_off[2 * kSegsPerCta];
-    int cand_cnt[2 * kSegsPerCta];
-    int npend, ncand, refill, drained, ntot, s0;
-    int nseg, nmem, nrows, nmiss, nrun, ebase;
-    int wsum[8];
+    long long seg_dom[kSlots];
+    double seg_t[kSlots];
+    int seg_goff[kSlots];           // global member offset (scratch of big trees)
+    int seg_cnt[kSlots];
+    int seg_span[kSlots];           // slots occupied by the domain (head slot only)
+    unsigned seg_it[kSlots];
+    uint8_t seg_used[kSlots];       // 0 free, 1 head of a held domain, 2 continuation slot
+    uint8_t seg_head[kSlots];       // head slot of a continuation slot
+    uint8_t seg_run[kSlots];
+    uint8_t seg_new[kSlots];
+    long long cand_dom[2 * kSlots]; // domains waiting for slots: [0, npend) carried over, then fetched
+    int cand_off[2 * kSlots];
+    int cand_cnt[2 * kSlots];
+    int npend, nnew, fetch, drained, ntot, s0;
+    unsigned freem;
+    int nrows, nmiss, nrun, ebase;
+    int wsum[kWarps];
     int4 mem_vac[kRowCap];          // positions of the held vacancies (this CTA is their only writer)
     int mem_slot[kRowCap];
     short mem_row[kRowCap];
     short row_mem[kRowCap];
     short miss[kRowCap];
     uint8_t mem_act[kRowCap];
-    uint8_t mem_seg[kRowCap];
+    uint8_t mem_seg[kRowCap];       // head slot of the member's domain
     uint8_t row_hit[kRowCap];
     unsigned long long events, evals, mrows, clamps;
 };
 
 // shared-memory carve-up (offsets from a 1024-aligned base)
 constexpr uint32_t kOffA = 0;                                        // h1 hi [0,64K) lo [64K,128K); FP64 scratch
-constexpr uint32_t kOffH2 = kOffA + 2 * kSplitA;                     // h2 hi/lo | layer-1 lists | partials out
+constexpr uint32_t kOffH2 = kOffA + 2 * kSplitA;                     // h2 hi/lo | partials out
 constexpr uint32_t kOffW2 = kOffH2 + 2 * kSplitH2;
 constexpr uint32_t kOffW3 = kOffW2 + kW2Bytes;
-constexpr uint32_t kOffReq = kOffW3 + kW3Bytes;                      // [8 sources][kReqBytes]
-constexpr uint32_t kOffPart = kOffReq + kClusterN * kReqBytes;       // [8 sources][16 rows][8] double
+constexpr uint32_t kOffHdr = kOffW3 + kW3Bytes;                      // [8 sources] ReqHdr
+constexpr uint32_t kOffPart = kOffHdr + kClusterN * 16;              // [8 sources][16 rows][8] double
 constexpr uint32_t kOffWin = kOffPart + kClusterN * kRoundRows * 8 * 8;   // own rows' windows [128][64]
 constexpr uint32_t kOffRowG = kOffWin + kRowCap * kWin;              // [128][8] double
 constexpr uint32_t kOffRowR = kOffRowG + kRowCap * 8 * 8;            // [128] double
 constexpr uint32_t kOffRowC = kOffRowR + kRowCap * 8;                // [128] int
 constexpr uint32_t kOffB2 = kOffRowC + kRowCap * 4;                  // float [32]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
-constexpr uint32_t kOffNl = kOffB3 + 8 * 8;                          // uint8 [128] layer-1 list lengths
-constexpr uint32_t kOffCtl = kOffNl + kTileRows;
+constexpr uint32_t kOffL1 = kOffB3 + 8 * 8;                          // uint16 [8 warps][64] layer-1 lists
+constexpr uint32_t kOffCtl = kOffL1 + kWarps * kWin * 2;
 constexpr uint32_t kOffBar = (kOffCtl + (uint32_t)sizeof(Ctl) + 7u) & ~7u;
-constexpr int kNumBars = 5;                                          // req, h1, part, mma, weights
+constexpr int kNumBars = 4;                                          // req, part, mma, weights
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemUsed = kOffTmem + 16;
 constexpr uint32_t kSmemTotal = kSmemUsed + 1024;
 static_assert(kSmemTotal <= 232448, "shared memory budget");
-static_assert(kOffReq % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
-static_assert(kReqBytes % 16 == 0, "bulk size");
-static_assert(kRoundRows * kWin * 2 * 8 <= 2 * kSplitH2, "layer-1 lists fit the h2 region");
+static_assert(kOffHdr % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
+static_assert(kRowCap <= 256, "row scan covers one element per thread");
 
 __device__ __forceinline__ uint32_t lanemask_lt()
 {
@@ -100,7 +104,7 @@ __device__ __forceinline__ uint32_t lanemask_lt()
     return m;
 }
 
-// exclusive block prefix of v over threads [0, 256); returns prefix, *total gets the sum (all threads)
+// exclusive block prefix of v over threads [0, 256); total gets the sum (all threads)
 __device__ __forceinline__ int block_excl(int v, int* wsum, int& total)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -116,7 +120,7 @@ __device__ __forceinline__ int block_excl(int v, int* wsum, int& total)
     int base = 0;
     total = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < kWarps; ++w) {
         const int t = wsum[w];
         if (w < wid) base += t;
         total += t;
@@ -132,16 +136,76 @@ __device__ __forceinline__ void split_h(float v, __half& hi, __half& lo, unsigne
     lo = __float2half_rn((v - __half2float(hi)) * kLo);
 }
 
-// no-swizzle K-major operand offset of element (m, k) in a 128-row tile
-__device__ __forceinline__ uint32_t kmaj_off(int m, int k)
+__device__ __forceinline__ uint4 pack8(const __half (&x)[8])
 {
-    return (uint32_t)(k >> 3) * kCoreCol + (uint32_t)(m >> 3) * 128u + (uint32_t)(m & 7) * 16u + (uint32_t)(k & 7) * 2u;
+    return make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]), pack_half2(x[6], x[7]));
 }
 
-// window byte loads of an owned vacancy: plain (coherent) loads -- the lattice is written by this kernel
+// H2 (K = 32): no-swizzle K-major, column-major core matrices (LBO 2048, SBO 128)
+__device__ __forceinline__ uint32_t h2_off(int m, int k)
+{
+    return (uint32_t)(k >> 3) * kCoreColH2 + (uint32_t)(m >> 3) * 128u + (uint32_t)(m & 7) * 16u + (uint32_t)(k & 7) * 2u;
+}
+
+// window byte of an owned vacancy: plain (coherent) load -- the lattice is written by this kernel
 __device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame& F, const int4& v, const int8_t* o)
 {
     return species[neighbour_site(F, v, o[0], o[1], o[2])];
+}
+
+// layer 1 of one row, all 256 columns (lane = columns 8*lane .. 8*lane+7): FP64 sum of b1' and the W1'
+// rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
+// row m of the A operand (M-major no-swizzle: 8-row group g at g*4096, core column c at c*128)
+__device__ __forceinline__ void layer1_row(const uint8_t* w, const float* __restrict__ W1f, uint16_t* lst, int m,
+                                           uint8_t* A_hi, uint8_t* A_lo, unsigned long long& ovf)
+{
+    const int lane = threadIdx.x & 31;
+    const uint32_t b0 = w[lane], b1 = w[lane + 32];
+    const unsigned m0 = __ballot_sync(0xffffffffu, b0 != (uint32_t)kFe);
+    const unsigned m1 = __ballot_sync(0xffffffffu, b1 != (uint32_t)kFe);
+    const uint32_t lt = lanemask_lt();
+    if (b0 != (uint32_t)kFe) lst[__popc(m0 & lt)] = (uint16_t)(1 + (b0 - 1) * kWin + lane);
+    if (b1 != (uint32_t)kFe) lst[__popc(m0) + __popc(m1 & lt)] = (uint16_t)(1 + (b1 - 1) * kWin + lane + 32);
+    __syncwarp();
+    const int n = __popc(m0) + __popc(m1);
+    const float4* base = reinterpret_cast<const float4*>(W1f) + 2 * lane;   // row stride 64 float4
+    double acc[8];
+    {
+        const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
+        acc[0] = x0.x; acc[1] = x0.y; acc[2] = x0.z; acc[3] = x0.w;
+        acc[4] = x1.x; acc[5] = x1.y; acc[6] = x1.z; acc[7] = x1.w;
+    }
+    for (int e = 0; e < n; e += 8) {
+        float4 xa[8], xb[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (e + t < n) {
+                const float4* rp = base + (size_t)lst[e + t] * (kHid / 4);
+                xa[t] = __ldg(rp);
+                xb[t] = __ldg(rp + 1);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (e + t < n) {
+                acc[0] = __dadd_rn(acc[0], (double)xa[t].x); acc[1] = __dadd_rn(acc[1], (double)xa[t].y);
+                acc[2] = __dadd_rn(acc[2], (double)xa[t].z); acc[3] = __dadd_rn(acc[3], (double)xa[t].w);
+                acc[4] = __dadd_rn(acc[4], (double)xb[t].x); acc[5] = __dadd_rn(acc[5], (double)xb[t].y);
+                acc[6] = __dadd_rn(acc[6], (double)xb[t].z); acc[7] = __dadd_rn(acc[7], (double)xb[t].w);
+            }
+        }
+    }
+    __half hi[8], lo[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        float h = (float)acc[c];
+        h = h > 0.0f ? h : 0.0f;
+        split_h(h, hi[c], lo[c], ovf);
+    }
+    const uint32_t off = (uint32_t)(m >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
+    *reinterpret_cast<uint4*>(A_hi + off) = pack8(hi);
+    *reinterpret_cast<uint4*>(A_lo + off) = pack8(lo);
+    __syncwarp();
 }
 
 template <bool kTC>
@@ -158,37 +222,38 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint8_t* A_lo = sm + kOffA + kSplitA;
     uint8_t* H2_hi = sm + kOffH2;
     uint8_t* H2_lo = sm + kOffH2 + kSplitH2;
-    uint16_t* lists = reinterpret_cast<uint16_t*>(sm + kOffH2);     // [128][64] (layer 1 only)
     double* part_out = reinterpret_cast<double*>(sm + kOffH2);      // [128][8]  (after layer 3)
     double* part_in = reinterpret_cast<double*>(sm + kOffPart);     // [8][16][8]
-    uint8_t* nl = sm + kOffNl;
+    ReqHdr* hdr = reinterpret_cast<ReqHdr*>(sm + kOffHdr);
     float* b2s = reinterpret_cast<float*>(sm + kOffB2);
     double* b3s = reinterpret_cast<double*>(sm + kOffB3);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffTmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint16_t* l1lst = reinterpret_cast<uint16_t*>(sm + kOffL1) + warp * kWin;
     const uint32_t rank = kTC ? cluster_rank() : 0u;
-    const uint32_t bar_req = smem_u32(&bars[0]), bar_h1 = smem_u32(&bars[1]), bar_part = smem_u32(&bars[2]);
-    const uint32_t bar_mma = smem_u32(&bars[3]), bar_w = smem_u32(&bars[4]);
+    const uint32_t bar_req = smem_u32(&bars[0]), bar_part = smem_u32(&bars[1]);
+    const uint32_t bar_mma = smem_u32(&bars[2]), bar_w = smem_u32(&bars[3]);
     const bool phase_mode = (p.mode == kEnginePhase);
     const bool mlp = (p.model == 1);
     unsigned long long ovf = 0;
 
     if (tid == 0) {
-        c.nseg = 0; c.npend = 0; c.drained = 0; c.nmem = 0; c.nrun = 0;
+        c.npend = 0; c.drained = 0; c.nrun = 0;
         c.ntot = phase_mode ? (int)p.ctr->nseg : 0;
         c.events = 0; c.evals = 0; c.mrows = 0; c.clamps = 0;
         if (kTC) {
             mbar_init(bar_req, kClusterN);
-            mbar_init(bar_h1, kClusterN - 1);
             mbar_init(bar_part, kClusterN);
             mbar_init(bar_mma, 1);
             mbar_init(bar_w, 1);
             mbar_fence_init();
         }
     }
+    if (tid < kSlots) { c.seg_used[tid] = 0; c.seg_run[tid] = 0; c.seg_new[tid] = 0; c.seg_head[tid] = 0; }
+    if (tid < kRowCap) c.mem_act[tid] = 0;
     uint32_t tmem = 0;
-    uint32_t ph_req = 0, ph_h1 = 0, ph_part = 0, ph_mma = 0;
+    uint32_t ph_req = 0, ph_part = 0, ph_mma = 0;
     if (kTC) {
         if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 128);
         if (tid < kSliceN) b2s[tid] = p.W.b2[rank * kSliceN + tid];
@@ -207,103 +272,158 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         __syncthreads();
     }
     const int nrows_eval = (!phase_mode) ? (p.nrows_dev ? *p.nrows_dev : p.nrows_host) : 0;
+    // diagnostics (thread 0): iterations, rounds, evaluation rounds, cycles in control / rounds / selection
+    unsigned long long d_it = 0, d_rounds = 0, d_erounds = 0, d_refill = 0;
+    long long d_cc = 0, d_cr = 0, d_cs = 0;
+    long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
+    const long long t_start = clock64();
+    long long t_mark = t_start;
+    auto lap = [&](long long& acc) { const long long t = clock64(); acc += t - t_mark; t_mark = t; };
 
     for (;;) {
-        // ================= control: refill, rows, gather + memo lookup =================
         int own_alive = 0;
         if (phase_mode) {
-            // ---- refill when every held domain has stopped: carried-over domains first, then the next
-            //      kSegsPerCta entries of the phase's segment list (domains are independent: any order)
+            // ================= slots: release stopped domains, refill from the segment list =================
+            __syncthreads();
+            if (warp == 0) {
+                // lane = slot; a slot is freed with its domain (head or continuation of a stopped head)
+                const int used = c.seg_used[lane];
+                const int head = used == 2 ? c.seg_head[lane] : lane;
+                const bool rel = used != 0 && !c.seg_run[head];
+                if (rel) {
+#pragma unroll
+                    for (int a = 0; a < kSlotCap; ++a) c.mem_act[kSlotCap * lane + a] = 0;
+                }
+                __syncwarp();
+                if (rel) c.seg_used[lane] = 0;
+                c.seg_new[lane] = 0;
+                const unsigned freem = __ballot_sync(0xffffffffu, used == 0 || rel);
+                const int nfree = __popc(freem);
+                const int nrun = __popc(__ballot_sync(0xffffffffu, used == 1 && c.seg_run[lane]));
+                if (lane == 0) {
+                    c.freem = freem;
+                    c.fetch = 0;
+                    c.nnew = 0;
+                    if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun == 0)) {
+                        const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)nfree);
+                        if (s0 >= c.ntot) {
+                            c.drained = 1;
+                        } else {
+                            c.fetch = 1; c.s0 = s0; c.nnew = min(nfree, c.ntot - s0);
+                            ++d_refill;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (c.fetch && tid < c.nnew) {
+                const Segment sg = p.segs[c.s0 + tid];
+                const int q = c.npend + tid;
+                c.cand_dom[q] = sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
+            }
             __syncthreads();
             if (tid == 0) {
-                c.refill = (c.nrun == 0) ? 1 : 0;
-                c.ncand = c.npend;
-                if (c.refill && c.npend == 0 && !c.drained) {
-                    const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)kSegsPerCta);
-                    if (s0 >= c.ntot) c.drained = 1;
-                    else { c.s0 = s0; c.ncand = min(kSegsPerCta, c.ntot - s0); }
-                }
-            }
-            __syncthreads();
-            if (c.refill && c.npend == 0 && tid < c.ncand) {
-                const Segment sg = p.segs[c.s0 + tid];
-                c.cand_dom[tid] = sg.dom; c.cand_off[tid] = sg.off; c.cand_cnt[tid] = sg.cnt;
-            }
-            __syncthreads();
-            if (tid == 0 && c.refill) {
-                int nseg = 0, nmem = 0, np = 0;
-                for (int q = 0; q < c.ncand; ++q) {
+                // first fit into runs of free slots (a domain of cnt vacancies needs ceil(cnt/4) consecutive
+                // slots); those that do not fit wait for the next refill
+                const int ncand = c.npend + c.nnew;
+                unsigned freem = c.freem;
+                int np = 0;
+                for (int q = 0; q < ncand; ++q) {
                     const int cnt = c.cand_cnt[q];
-                    if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); continue; }   // can never be held
-                    if (nseg < kSegsPerCta && nmem + cnt <= kRowCap) {
-                        c.seg_dom[nseg] = c.cand_dom[q]; c.seg_goff[nseg] = c.cand_off[q]; c.seg_cnt[nseg] = cnt;
-                        c.seg_moff[nseg] = nmem; c.seg_t[nseg] = 0.0; c.seg_it[nseg] = 0u; c.seg_run[nseg] = 1;
-                        nmem += cnt;
-                        ++nseg;
-                    } else {                                   // carried over (np <= q: in-place is safe)
+                    if (cnt > kRowCap || cnt <= 0) { atomicAdd(p.overflow, 1ull); continue; }
+                    const int need = (cnt + kSlotCap - 1) / kSlotCap;
+                    unsigned runs = freem;                    // bit i set: slots i .. i+need-1 all free
+                    for (int t = 1; t < need; ++t) runs &= freem >> t;
+                    if (need > 1) runs &= (need >= 32) ? 1u : (0xffffffffu >> (need - 1));
+                    if (!runs) {
                         c.cand_dom[np] = c.cand_dom[q]; c.cand_off[np] = c.cand_off[q]; c.cand_cnt[np] = cnt;
                         ++np;
+                        continue;
                     }
+                    const int h = __ffs(runs) - 1;
+                    c.seg_used[h] = 1;
+                    for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
+                    freem &= ~(((need >= 32) ? 0xffffffffu : ((1u << need) - 1u)) << h);
+                    c.seg_dom[h] = c.cand_dom[q]; c.seg_goff[h] = c.cand_off[q]; c.seg_cnt[h] = cnt;
+                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_run[h] = 1; c.seg_new[h] = 1;
                 }
-                c.npend = np; c.nseg = nseg; c.nmem = nmem; c.nrun = nseg;
+                c.npend = np;
             }
             __syncthreads();
-            if (c.refill) {
-                for (int i = warp; i < c.nseg; i += kThreads / 32) {
-                    const int cnt = c.seg_cnt[i], moff = c.seg_moff[i], goff = c.seg_goff[i];
-                    for (int a = lane; a < cnt; a += 32) {
-                        const int slot = p.members[goff + a];
-                        c.mem_slot[moff + a] = slot;
-                        c.mem_vac[moff + a] = p.vac[slot];
-                        c.mem_act[moff + a] = 1;
-                        c.mem_seg[moff + a] = (uint8_t)i;
-                    }
+            if (warp == 0) {
+                const int nrun = __popc(__ballot_sync(0xffffffffu, c.seg_used[lane] == 1 && c.seg_run[lane]));
+                if (lane == 0) c.nrun = nrun;
+            }
+            // members of newly placed domains: slot ids and positions (parallel loads)
+            for (int i = warp; i < kSlots; i += kWarps) {
+                if (!c.seg_new[i]) continue;
+                const int cnt = c.seg_cnt[i], goff = c.seg_goff[i];
+                for (int a = lane; a < cnt; a += 32) {
+                    c.mem_slot[kSlotCap * i + a] = p.members[goff + a];
+                    c.mem_vac[kSlotCap * i + a] = p.mpos[goff + a];
+                    c.mem_act[kSlotCap * i + a] = 1;
+                    c.mem_seg[kSlotCap * i + a] = (uint8_t)i;
                 }
             }
             __syncthreads();
+            if (tid == 0) lap(d_x[0]);
             own_alive = c.nrun > 0 ? 1 : 0;
-            // rows = active members of running domains, in member order
+            // ================= rows = active members of running domains, in slot/member order =================
             int total = 0;
             {
-                const int pidx = tid;
-                const bool act = pidx < c.nmem && c.mem_act[pidx] && c.seg_run[c.mem_seg[pidx]];
+                const bool act = tid < kRowCap && c.mem_act[tid] && c.seg_run[c.mem_seg[tid]];
                 const int r = block_excl(act ? 1 : 0, c.wsum, total);
-                if (pidx < kRowCap) c.mem_row[pidx] = act ? (short)r : (short)-1;
-                if (act) c.row_mem[r] = (short)pidx;
+                if (tid < kRowCap) c.mem_row[tid] = act ? (short)r : (short)-1;
+                if (act) c.row_mem[r] = (short)tid;
             }
             if (tid == 0) c.nrows = total;
             __syncthreads();
-            // gather + memo: warp per row, lane = window slots j and j+32
+            if (tid == 0) lap(d_x[1]);
+            // ================= gather + memo lookup: warp per row, lanes = window slots j and j+32 =================
             const int nrows = c.nrows;
-            for (int r = warp; r < nrows; r += kThreads / 32) {
-                const int slot = c.mem_slot[c.row_mem[r]];
-                const int4 v = c.mem_vac[c.row_mem[r]];
-                const MemoEntry* me = p.memo + 2 * (size_t)slot;
-                const uint32_t kw = reinterpret_cast<const uint32_t*>(me[lane >> 4].key)[lane & 15];
-                double gv = 0.0;
-                int cv = 0;
-                {
-                    const int k = lane & 15;
-                    const MemoEntry& e = me[lane >> 4];
-                    if (k < 8) gv = e.G[k];
-                    else if (k == 8) gv = e.R;
-                    else if (k == 9) cv = e.clamps;
+            for (int r0 = warp; r0 < nrows; r0 += 4 * kWarps) {
+                // 4 rows per warp in flight: memo ways (lanes 0-15 way 0, 16-31 way 1) and window bytes
+                const int k = lane & 15, way = lane >> 4;
+                uint32_t kw[4];
+                double gv[4];
+                int cv[4];
+                uint8_t b0[4], b1[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q * kWarps;
+                    kw[q] = 0; gv[q] = 0.0; cv[q] = 0; b0[q] = 0; b1[q] = 0;
+                    if (r < nrows) {
+                        const int pm = c.row_mem[r];
+                        const MemoEntry& e = p.memo[2 * (size_t)c.mem_slot[pm] + way];
+                        const int4 v = c.mem_vac[pm];
+                        kw[q] = reinterpret_cast<const uint32_t*>(e.key)[k];
+                        if (k < 8) gv[q] = e.G[k];
+                        else if (k == 8) gv[q] = e.R;
+                        else if (k == 9) cv[q] = e.clamps;
+                        b0[q] = site_byte(p.species, p.F, v, p.G.off[lane]);
+                        b1[q] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
+                    }
                 }
-                const uint8_t b0 = site_byte(p.species, p.F, v, p.G.off[lane]);
-                const uint8_t b1 = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
-                win[r * kWin + lane] = b0;
-                win[r * kWin + lane + 32] = b1;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q * kWarps;
+                    if (r < nrows) { win[r * kWin + lane] = b0[q]; win[r * kWin + lane + 32] = b1[q]; }
+                }
                 __syncwarp();
-                const uint32_t ww = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane & 15];
-                const unsigned eq = __ballot_sync(0xffffffffu, ww == kw);
-                const int hit = (eq & 0xFFFFu) == 0xFFFFu ? 0 : ((eq >> 16) == 0xFFFFu ? 1 : -1);
-                if (hit >= 0 && (lane >> 4) == hit) {
-                    const int k = lane & 15;
-                    if (k < 8) rowG[r * 8 + k] = gv;
-                    else if (k == 8) rowR[r] = gv;
-                    else if (k == 9) rowC[r] = cv;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q * kWarps;
+                    if (r >= nrows) break;
+                    const uint32_t ww = reinterpret_cast<const uint32_t*>(win + r * kWin)[k];
+                    const unsigned eq = __ballot_sync(0xffffffffu, ww == kw[q]);
+                    const int hit = (eq & 0xFFFFu) == 0xFFFFu ? 0 : ((eq >> 16) == 0xFFFFu ? 1 : -1);
+                    if (hit >= 0 && way == hit) {
+                        if (k < 8) rowG[r * 8 + k] = gv[q];
+                        else if (k == 8) rowR[r] = gv[q];
+                        else if (k == 9) rowC[r] = cv[q];
+                    }
+                    if (lane == 0) c.row_hit[r] = hit >= 0 ? 1 : 0;
                 }
-                if (lane == 0) c.row_hit[r] = hit >= 0 ? 1 : 0;
             }
             __syncthreads();
             {
@@ -314,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (tid == 0) { c.nmiss = total; c.mrows += (unsigned long long)total; }
             __syncthreads();
         }
+        if (tid == 0) { lap(d_x[2]); ++d_it; }
 
         // ================= evaluation of the misses =================
         bool all_dead = false;
@@ -381,15 +502,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             // memo insert: way 1 <- way 0, way 0 <- (window, rates)
-            for (int q = warp; q < nmiss; q += kThreads / 32) {
+            for (int q = warp; q < nmiss; q += kWarps) {
                 const int r = c.miss[q];
                 MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
-                uint4* d1 = reinterpret_cast<uint4*>(&me[1]);
-                const uint4* s0 = reinterpret_cast<const uint4*>(&me[0]);
                 uint4 t = make_uint4(0, 0, 0, 0);
-                if (lane < 9) t = s0[lane];
+                if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
                 __syncwarp();
-                if (lane < 9) d1[lane] = t;
+                if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
                 __syncwarp();
                 if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
                 else if (lane < 24) me[0].G[lane - 16] = rowG[r * 8 + lane - 16];
@@ -400,151 +519,84 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             // ---- FP32-equivalent evaluator: rounds in lockstep over the cluster
             int k_round = 0;
             for (;;) {
-                uint8_t* req_own = sm + kOffReq + rank * kReqBytes;
-                ReqHdr* hdr_own = reinterpret_cast<ReqHdr*>(req_own);
-                uint8_t* wreq = req_own + 16;
                 int own_n = 0;
                 if (phase_mode) {
-                    const int nmiss = c.nmiss;
-                    own_n = min(kRoundRows, max(0, nmiss - kRoundRows * k_round));
-                    // own request: windows of misses [16k, 16k+16); memo way 1 <- way 0, way 0 key <- window
-                    {
-                        const int i = tid >> 4, wd = tid & 15;
-                        if (i < own_n) {
-                            const int r = c.miss[kRoundRows * k_round + i];
-                            reinterpret_cast<uint32_t*>(wreq + i * kWin)[wd] = reinterpret_cast<const uint32_t*>(win + r * kWin)[wd];
-                        }
-                    }
-                    for (int i = warp; i < own_n; i += kThreads / 32) {
+                    own_n = min(kRoundRows, max(0, c.nmiss - kRoundRows * k_round));
+                    // layer 1 of this round's own rows; memo way 1 <- way 0, way 0 key <- window
+                    for (int i = warp; i < own_n; i += kWarps) {
                         const int r = c.miss[kRoundRows * k_round + i];
                         MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                         uint4 t = make_uint4(0, 0, 0, 0);
                         if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
-                        __syncwarp();
+                        layer1_row(win + r * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, ovf);
                         if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
                         __syncwarp();
                         if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
                     }
                     if (tid == 0) {
-                        hdr_own->n = own_n;
-                        hdr_own->more = (c.nmiss > kRoundRows * (k_round + 1)) ? 1 : 0;
-                        hdr_own->alive = own_alive;
+                        hdr[rank].n = own_n;
+                        hdr[rank].more = (c.nmiss > kRoundRows * (k_round + 1)) ? 1 : 0;
+                        hdr[rank].alive = own_alive;
                     }
                 } else {
-                    // eval mode: the next 16 rows from the cursor
+                    // eval mode: the next 16 rows from the cursor; windows into win[0..16)
                     __syncthreads();
                     if (tid == 0) c.ebase = (int)atomicAdd(p.cursor, (unsigned)kRoundRows);
                     __syncthreads();
                     const int base = c.ebase;
                     own_n = min(kRoundRows, max(0, nrows_eval - base));
-                    for (int i = warp; i < own_n; i += kThreads / 32) {
+                    for (int i = warp; i < own_n; i += kWarps) {
                         const int g = base + i;
                         if (p.windows) {
-                            wreq[i * kWin + lane] = p.windows[(size_t)g * kWin + lane];
-                            wreq[i * kWin + lane + 32] = p.windows[(size_t)g * kWin + lane + 32];
+                            win[i * kWin + lane] = p.windows[(size_t)g * kWin + lane];
+                            win[i * kWin + lane + 32] = p.windows[(size_t)g * kWin + lane + 32];
                         } else {
                             const int slot = p.rows ? p.rows[g] : g;
                             const int4 v = p.vac[slot];
-                            wreq[i * kWin + lane] = site_byte(p.species, p.F, v, p.G.off[lane]);
-                            wreq[i * kWin + lane + 32] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
+                            win[i * kWin + lane] = site_byte(p.species, p.F, v, p.G.off[lane]);
+                            win[i * kWin + lane + 32] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
                         }
+                        __syncwarp();
+                        layer1_row(win + i * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, ovf);
                     }
-                    if (tid == 0) { hdr_own->n = own_n; hdr_own->more = 0; hdr_own->alive = own_n > 0 ? 1 : 0; }
+                    if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
                 }
-                // ---- exchange requests (every CTA sends exactly one per round)
+                // ---- exchange: header + this CTA's h1 rows (8-row groups 2r, 2r+1) to every peer
                 fence_async_smem();
                 __syncthreads();
+                if (tid == 0) lap(d_x[3]);
                 if (tid == 0) {
+                    const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
+                    const uint32_t bytes = 16u + 2u * rg * kRowGroupA;
+                    const uint32_t aoff = 2u * rank * kRowGroupA;
                     for (uint32_t d = 0; d < (uint32_t)kClusterN; ++d) {
                         if (d == rank) continue;
                         const uint32_t cb = map_to(bar_req, d);
-                        mbar_remote_expect_tx(cb, kReqBytes);
-                        bulk_s2peer(map_to(smem_u32(req_own), d), smem_u32(req_own), kReqBytes, cb);
+                        mbar_remote_expect_tx(cb, bytes);
+                        bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
+                        if (rg) {
+                            bulk_s2peer(map_to(smem_u32(A_hi + aoff), d), smem_u32(A_hi + aoff), rg * kRowGroupA, cb);
+                            bulk_s2peer(map_to(smem_u32(A_lo + aoff), d), smem_u32(A_lo + aoff), rg * kRowGroupA, cb);
+                        }
                     }
                     mbar_arrive(bar_req);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 mbar_wait_cluster(bar_req, ph_req);
                 ph_req ^= 1u;
+                if (tid == 0) lap(d_x[4]);
                 int n_s[kClusterN];
-                int any_more = 0, any_alive = 0, maxrow = 0, total = 0;
+                int any_more = 0, any_alive = 0, total = 0;
 #pragma unroll
                 for (int s = 0; s < kClusterN; ++s) {
-                    const ReqHdr* hs = reinterpret_cast<const ReqHdr*>(sm + kOffReq + s * kReqBytes);
-                    n_s[s] = hs->n;
-                    any_more |= hs->more;
-                    any_alive |= hs->alive;
-                    total += hs->n;
-                    if (hs->n > 0) maxrow = kRoundRows * s + hs->n;
+                    n_s[s] = hdr[s].n;
+                    any_more |= hdr[s].more;
+                    any_alive |= hdr[s].alive;
+                    total += hdr[s].n;
                 }
-                if (k_round == 0 && !any_alive) { all_dead = true; }
+                if (k_round == 0 && !any_alive) all_dead = true;
                 if (total > 0) {
-                    // ---- L1: layer-1 lists (non-Fe slots in slot order) of all tile rows, warp per row
-                    for (int m = warp; m < kTileRows; m += kThreads / 32) {
-                        const int s = m >> 4, i = m & 15;
-                        if (i >= n_s[s]) continue;
-                        const uint8_t* w = sm + kOffReq + s * kReqBytes + 16 + i * kWin;
-                        const uint32_t b0 = w[lane], b1 = w[lane + 32];
-                        const unsigned m0 = __ballot_sync(0xffffffffu, b0 != (uint32_t)kFe);
-                        const unsigned m1 = __ballot_sync(0xffffffffu, b1 != (uint32_t)kFe);
-                        const uint32_t lt = lanemask_lt();
-                        if (b0 != (uint32_t)kFe) lists[m * kWin + __popc(m0 & lt)] = (uint16_t)(1 + (b0 - 1) * kWin + lane);
-                        if (b1 != (uint32_t)kFe) lists[m * kWin + __popc(m0) + __popc(m1 & lt)] = (uint16_t)(1 + (b1 - 1) * kWin + lane + 32);
-                        if (lane == 0) nl[m] = (uint8_t)(__popc(m0) + __popc(m1));
-                    }
-                    __syncthreads();
-                    // ---- L1: h1[:, 32r + lane] for the valid rows; FP64 sum in slot order, one FP32 rounding
-                    {
-                        const int col = (int)rank * kSliceN + lane;
-                        const float bias = p.W.W1f[col];
-                        for (int m = warp; m < kTileRows; m += kThreads / 32) {
-                            const int s = m >> 4, i = m & 15;
-                            if (i >= n_s[s]) continue;
-                            const int n = nl[m];
-                            const uint16_t* L = lists + m * kWin;
-                            double acc = (double)bias;
-                            int e = 0;
-                            for (; e + 4 <= n; e += 4) {
-                                const float x0 = p.W.W1f[(size_t)L[e] * kHid + col];
-                                const float x1 = p.W.W1f[(size_t)L[e + 1] * kHid + col];
-                                const float x2 = p.W.W1f[(size_t)L[e + 2] * kHid + col];
-                                const float x3 = p.W.W1f[(size_t)L[e + 3] * kHid + col];
-                                acc = __dadd_rn(acc, (double)x0);
-                                acc = __dadd_rn(acc, (double)x1);
-                                acc = __dadd_rn(acc, (double)x2);
-                                acc = __dadd_rn(acc, (double)x3);
-                            }
-                            for (; e < n; ++e) acc = __dadd_rn(acc, (double)p.W.W1f[(size_t)L[e] * kHid + col]);
-                            float h = (float)acc;
-                            h = h > 0.0f ? h : 0.0f;
-                            __half hi, lo;
-                            split_h(h, hi, lo, ovf);
-                            const uint32_t off = kmaj_off(m, col);
-                            *reinterpret_cast<__half*>(A_hi + off) = hi;
-                            *reinterpret_cast<__half*>(A_lo + off) = lo;
-                        }
-                    }
-                    // ---- broadcast this CTA's h1 slice (core columns 4r..4r+3, rows [0, 8g)) to the cluster
-                    const int g8 = (maxrow + 7) >> 3;
-                    fence_async_smem();
-                    __syncthreads();
-                    if (tid == 0) {
-                        const uint32_t bytes = (uint32_t)g8 * 128u;
-                        for (uint32_t d = 0; d < (uint32_t)kClusterN; ++d) {
-                            if (d == rank) continue;
-                            const uint32_t cb = map_to(bar_h1, d);
-                            mbar_remote_expect_tx(cb, 8u * bytes);
-                            for (int sp = 0; sp < 2; ++sp)
-                                for (int cc = 0; cc < 4; ++cc) {
-                                    const uint32_t off = (uint32_t)sp * kSplitA + (uint32_t)(4 * rank + cc) * kCoreCol;
-                                    bulk_s2peer(map_to(smem_u32(A_hi + off), d), smem_u32(A_hi + off), bytes, cb);
-                                }
-                        }
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    }
-                    mbar_wait_cluster(bar_h1, ph_h1);
-                    ph_h1 ^= 1u;
-                    // ---- L2 on tcgen05: D1 (cols 0-31), D2 (cols 32-63)
+                    // ---- L2 on tcgen05: D1 (TMEM cols 0-31), D2 (cols 32-63)
                     tc_fence_before();
                     __syncthreads();
                     tc_fence_after();
@@ -552,8 +604,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const uint32_t idesc = idesc_f16(kTileRows, kSliceN);
                         const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo), wb = smem_u32(sm + kOffW2);
                         for (int ks = 0; ks < kHid / 16; ++ks) {
-                            const uint64_t dah = umma_desc(ah + (uint32_t)ks * 2u * kCoreCol, kCoreCol, 128);
-                            const uint64_t dal = umma_desc(al + (uint32_t)ks * 2u * kCoreCol, kCoreCol, 128);
+                            const uint64_t dah = umma_desc(ah + (uint32_t)ks * 256u, 128, kRowGroupA);
+                            const uint64_t dal = umma_desc(al + (uint32_t)ks * 256u, 128, kRowGroupA);
                             const uint64_t dbh = umma_desc(wb + (uint32_t)ks * 2u * kW2Split, (kSliceN / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(wb + (uint32_t)ks * 2u * kW2Split + kW2Split, (kSliceN / 8) * 128, 128);
                             umma_f16(tmem + 0, dah, dbh, idesc, ks > 0 ? 1u : 0u);
@@ -568,8 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     // ---- E2: h2 slice -> H2 (fp16 split, K = 32)
                     {
                         const int q4 = warp & 3, hc = warp >> 2;
-                        const bool any = (n_s[2 * q4] > 0) || (n_s[2 * q4 + 1] > 0);
-                        if (any) {
+                        if (n_s[2 * q4] > 0 || n_s[2 * q4 + 1] > 0) {
                             uint32_t d1[16], d2[16];
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
                             tmem_ld16(tl + (uint32_t)(16 * hc), d1);
@@ -588,9 +639,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                     z = z > 0.0f ? z : 0.0f;
                                     split_h(z, hi[t], lo[t], ovf);
                                 }
-                                const uint32_t off = kmaj_off(m, 16 * hc + 8 * g);
-                                *reinterpret_cast<uint4*>(H2_hi + off) = make_uint4(pack_half2(hi[0], hi[1]), pack_half2(hi[2], hi[3]), pack_half2(hi[4], hi[5]), pack_half2(hi[6], hi[7]));
-                                *reinterpret_cast<uint4*>(H2_lo + off) = make_uint4(pack_half2(lo[0], lo[1]), pack_half2(lo[2], lo[3]), pack_half2(lo[4], lo[5]), pack_half2(lo[6], lo[7]));
+                                const uint32_t off = h2_off(m, 16 * hc + 8 * g);
+                                *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
+                                *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
                             }
                         }
                     }
@@ -598,13 +649,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     tc_fence_before();
                     __syncthreads();
                     tc_fence_after();
+                    if (tid == 0) lap(d_x[5]);
                     // ---- L3 on tcgen05: partial outputs of this CTA's 32 h2 columns, Da (64-79), Db (80-95)
                     if (tid == 0) {
                         const uint32_t idesc = idesc_f16(kTileRows, 16);
                         const uint32_t hh = smem_u32(H2_hi), hl = smem_u32(H2_lo), w3 = smem_u32(sm + kOffW3);
                         for (int ks = 0; ks < kSliceN / 16; ++ks) {
-                            const uint64_t dah = umma_desc(hh + (uint32_t)ks * 2u * kCoreCol, kCoreCol, 128);
-                            const uint64_t dal = umma_desc(hl + (uint32_t)ks * 2u * kCoreCol, kCoreCol, 128);
+                            const uint64_t dah = umma_desc(hh + (uint32_t)ks * 2u * kCoreColH2, kCoreColH2, 128);
+                            const uint64_t dal = umma_desc(hl + (uint32_t)ks * 2u * kCoreColH2, kCoreColH2, 128);
                             const uint64_t dbh = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split, (16 / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split + kW3Split, (16 / 8) * 128, 128);
                             umma_f16(tmem + 64, dah, dbh, idesc, ks > 0 ? 1u : 0u);
@@ -618,8 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     tc_fence_after();
                     if (warp < 4) {
                         const int q4 = warp;
-                        const bool any = (n_s[2 * q4] > 0) || (n_s[2 * q4 + 1] > 0);
-                        if (any) {
+                        if (n_s[2 * q4] > 0 || n_s[2 * q4 + 1] > 0) {
                             uint32_t da[8], db[8];
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
                             tmem_ld8(tl + 64u, da);
@@ -637,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             dst[3] = make_double2(pv[6], pv[7]);
                         }
                     }
-                    // ---- partials of row block s -> CTA s
+                    // ---- partials of row block s -> CTA s (every CTA arrives on every CTA's barrier)
                     fence_async_smem();
                     tc_fence_before();
                     __syncthreads();
@@ -654,10 +705,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     }
                     mbar_wait_cluster(bar_part, ph_part);
                     ph_part ^= 1u;
+                    if (tid == 0) lap(d_x[6]);
                     // ---- E3 for this CTA's own rows: thread (row i, hop k)
                     if (tid < kRoundRows * 8) {
                         const int i = tid >> 3, k = tid & 7;
                         const bool valid = i < own_n;
+                        const int r = phase_mode ? (valid ? (int)c.miss[kRoundRows * k_round + i] : 0) : i;
                         double Gk = 0.0, Ek = 0.0;
                         if (valid) {
                             double acc = 0.0;
@@ -665,15 +718,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             for (int s = 0; s < kClusterN; ++s) acc = __dadd_rn(acc, part_in[(s * kRoundRows + i) * 8 + k]);
                             const double out = __dadd_rn(b3s[k], __dmul_rn(acc, p.W.s3u));
                             Ek = out > 0.0 ? out : 0.0;
-                            const uint8_t wk = wreq[i * kWin + k];
-                            Gk = (wk != (uint8_t)kVac) ? arrhenius(Ek, p.P) : 0.0;
+                            Gk = (win[r * kWin + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P) : 0.0;
                         }
                         double R = 0.0;
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) R = __dadd_rn(R, __shfl_sync(0xffffffffu, Gk, (lane & ~7) + kk));
                         if (valid) {
                             if (phase_mode) {
-                                const int r = c.miss[kRoundRows * k_round + i];
                                 rowG[r * 8 + k] = Gk;
                                 MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                                 me[0].G[k] = Gk;
@@ -688,7 +739,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         }
                     }
                 }
-                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (tid == 0) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    lap(d_x[7]);
+                    ++d_rounds;
+                    d_erounds += total > 0 ? 1 : 0;
+                }
                 __syncthreads();
                 ++k_round;
                 if (!any_more) break;
@@ -697,11 +753,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (!phase_mode) continue;
         }
 
-        // ================= BKL step per running domain (thread per domain) =================
+        // ================= BKL step per running domain (thread per head slot) =================
         __syncthreads();
-        if (tid < c.nseg && c.seg_run[tid]) {
+        if (tid == 0) lap(d_cr);
+        if (tid < kSlots && c.seg_used[tid] == 1 && c.seg_run[tid]) {
             const int i = tid;
-            const int cnt = c.seg_cnt[i], moff = c.seg_moff[i];
+            const int cnt = c.seg_cnt[i], moff = kSlotCap * i;
             double lbuf[32];
             int lidx[16];
             const bool small = cnt <= 16;
@@ -740,9 +797,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const int leaf = tree_descend(buf, m, P, nlev, rr);
                         const int a = idx[leaf];
                         const int slot = c.mem_slot[moff + a];
-                        const int k = pick_hop(rowG + (size_t)c.mem_row[moff + a] * 8, rr);
+                        const int r = c.mem_row[moff + a];
+                        const int k = pick_hop(rowG + (size_t)r * 8, rr);
+                        // hop: the target's species is window slot k (1NN slots are 0..7)
                         const int4 ov = c.mem_vac[moff + a];
-                        const int4 nv = apply_hop(p.species, p.vac, slot, k, p.F, p.G);
+                        int4 nv = ov;
+                        nv.y = p.F.wrap[0] ? wrap2(ov.y + p.G.off[k][0], 2 * p.F.L[0]) : ov.y + p.G.off[k][0];
+                        nv.z = p.F.wrap[1] ? wrap2(ov.z + p.G.off[k][1], 2 * p.F.L[1]) : ov.z + p.G.off[k][1];
+                        nv.w = p.F.wrap[2] ? wrap2(ov.w + p.G.off[k][2], 2 * p.F.L[2]) : ov.w + p.G.off[k][2];
+                        const uint8_t tn = win[r * kWin + k];
+                        write_site(p.species, p.F, ov.x, ov.y, ov.z, ov.w, tn);
+                        write_site(p.species, p.F, nv.x, nv.y, nv.z, nv.w, (uint8_t)kVac);
+                        p.vac[slot] = nv;
                         c.mem_vac[moff + a] = nv;
                         long long d2;
                         int sec2;
@@ -750,8 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         if (d2 != c.seg_dom[i] || sec2 != p.ph->sector) c.mem_act[moff + a] = 0;
                         if (p.S.log) {
                             if (near_face(p.F, ov.y, ov.z, ov.w))
-                                log_entry(p.S.log, p.S.nlog, p.S.logcap, ov.y, ov.z, ov.w,
-                                          p.species[site_of(p.F, ov.x, ov.y, ov.z, ov.w)]);
+                                log_entry(p.S.log, p.S.nlog, p.S.logcap, ov.y, ov.z, ov.w, tn);
                             if (near_face(p.F, nv.y, nv.z, nv.w))
                                 log_entry(p.S.log, p.S.nlog, p.S.logcap, nv.y, nv.z, nv.w, kVac);
                             bool out = false;
@@ -772,11 +837,23 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (stop) c.seg_run[i] = 0;
         }
         __syncthreads();
-        if (tid == 0) {
-            int nr = 0;
-            for (int i = 0; i < c.nseg; ++i) nr += c.seg_run[i];
-            c.nrun = nr;
-        }
+        if (tid == 0) lap(d_cs);
+    }
+    if (tid == 0 && p.diag) {
+        d_cc = d_x[0] + d_x[1] + d_x[2];
+        d_cr += d_x[3] + d_x[4] + d_x[5] + d_x[6] + d_x[7];
+        atomicAdd(p.diag + 0, d_it);
+        atomicMax(p.diag + 1, d_it);
+        atomicAdd(p.diag + 2, d_rounds);
+        atomicAdd(p.diag + 3, d_erounds);
+        atomicAdd(p.diag + 4, (unsigned long long)d_cc);
+        atomicAdd(p.diag + 5, (unsigned long long)d_cr);
+        atomicAdd(p.diag + 6, (unsigned long long)d_cs);
+        atomicAdd(p.diag + 7, 1ull);
+        atomicAdd(p.diag + 8, d_refill);
+        atomicAdd(p.diag + 9, (unsigned long long)(clock64() - t_start));
+        atomicAdd(p.diag + 10, 1ull * (phase_mode ? 1 : 0));
+        for (int q = 0; q < 8; ++q) atomicAdd(p.diag + 11 + q, (unsigned long long)d_x[q]);
     }
 
     // ---- teardown

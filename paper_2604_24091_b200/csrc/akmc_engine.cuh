@@ -17,8 +17,9 @@ namespace akmc {
 constexpr int kClusterN = 8;                   // CTAs per cluster; CTA r owns hidden columns [32r, 32r+32)
 constexpr int kSliceN = kHid / kClusterN;      // 32
 constexpr int kRoundRows = 16;                 // rows a CTA contributes per evaluation round (tile M = 128)
-constexpr int kSegsPerCta = 16;                // domains (segments) a CTA holds at once
-constexpr int kRowCap = 128;                   // members (vacancies) a CTA holds at once
+constexpr int kSlots = 32;                     // domain slots per CTA (a domain with > 4 vacancies spans several)
+constexpr int kSlotCap = 4;                    // vacancies per slot
+constexpr int kRowCap = kSlots * kSlotCap;     // vacancies a CTA holds at once (128)
 constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
 
 // exact memo of the barrier network per vacancy slot (2 ways, most recent first)
@@ -56,6 +57,7 @@ struct EngineParams {
     const PhaseInfo* ph;
     const Segment* segs;
     const int* members;
+    const int4* mpos;       // member positions at phase start (parallel to members)
     DevCounters* ctr;
     MemoEntry* memo;        // [vcap][2] (phase mode) or nullptr
     double* scratch;        // trees of segments with > 16 members (4 doubles per member, by member offset)
@@ -71,6 +73,7 @@ struct EngineParams {
     double* E;
     EngineWeights W;
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
+    unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
 };
 
 size_t engine_smem_bytes();

@@ -330,7 +330,7 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
                                                        const int* __restrict__ nvac_dev, SubParams S,
                                                        const PhaseInfo* __restrict__ ph, int* dmin, int* head,
                                                        const int* __restrict__ next, Segment* segs, int* members,
-                                                       uint8_t* mactive, DevCounters* ctr)
+                                                       uint8_t* mactive, DevCounters* ctr, int4* mpos)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
@@ -363,6 +363,8 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
         members[off + b + 1] = key;
     }
     for (int a = 0; a < cnt; ++a) mactive[off + a] = 1;
+    if (mpos)
+        for (int a = 0; a < cnt; ++a) mpos[off + a] = vac[members[off + a]];   // positions for the phase engine
     Segment sg;
     sg.dom = d; sg.off = off; sg.cnt = cnt; sg.t = 0.0; sg.it = 0u; sg.running = 1;
     segs[seg] = sg;

@@ -24,13 +24,18 @@ def main():
     ap.add_argument("--sweeps", type=int, default=3)
     ap.add_argument("--lam", type=float, default=0.25)
     ap.add_argument("--residual", type=float, default=0.02)
+    ap.add_argument("--no-rates", action="store_true", help="skip the rate-distribution summaries")
     a = ap.parse_args()
     pr = synth.preset("C5")
     cells = (a.cells,) * 3
     eps, E0 = synth.illustrative_pair_params()
     mlp = synth.physics_mlp(eps, E0, residual=a.residual, seed=1)
     nvac = max(1, round(pr.n_vac_per_voxel * (a.cells / pr.cells[0]) ** 3))
-    sp = synth.make_lattice(cells, 1, pr.fractions, nvac, seed=pr.seed)
+    if a.cells >= 512:                       # same generator as bench.py (on device, then host copy)
+        import torch
+        sp = synth.make_lattice_iid(cells, pr.fractions, nvac, seed=pr.seed, device="cuda").cpu().numpy()
+    else:
+        sp = synth.make_lattice(cells, 1, pr.fractions, nvac, seed=pr.seed)
     win = synth.window_seconds(a.lam, E0[0])
     cfg = akmc.Config(cells=cells, n_voxels=1, barrier_model=akmc.MODEL_MLP if a.model == "mlp" else akmc.MODEL_PAIR,
                       precision=akmc.PREC_FP32 if a.prec == "fp32" else akmc.PREC_FP64,
@@ -47,12 +52,14 @@ def main():
                 "n_R_win_gt_10": int((tot > 10).sum()), "n_R_win_gt_100": int((tot > 100).sum()),
                 "Emin_q": dict(zip(map(str, [0.0, 0.001, 0.01, 0.5]), np.quantile(emin, [0.0, 0.001, 0.01, 0.5]).round(4).tolist()))}
 
-    print(json.dumps({"cells": a.cells, "nvac": nvac, "window_s": win, "before": rate_stats()}), flush=True)
+    print(json.dumps({"cells": a.cells, "nvac": nvac, "window_s": win,
+                      "before": None if a.no_rates else rate_stats()}), flush=True)
     for s in range(a.sweeps):
         c = sim.step(1)
         print(json.dumps({"sweep": s, **{k: c[k] for k in ("iterations", "events", "hop_evals", "clamps", "mlp_rows")},
                           "mlp_ms": round(c["mlp_ms"], 2), "wall_ms": round(c["wall_ms"], 2)}), flush=True)
-    print(json.dumps({"after": rate_stats()}), flush=True)
+    if not a.no_rates:
+        print(json.dumps({"after": rate_stats()}), flush=True)
     sim.close()
 
 

@@ -34,6 +34,18 @@ METRIC = "vacancy-hop evaluations/sec"
 UNIT = "hop-evals/s"
 FLOPS_PER_VAC = 2 * (256 * 256 + 256 * 8) + 64 * 256      # layers 2-3 FLOPs + layer-1 adds
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# DRAM bytes (read + write) per engine launch from the committed ncu --set full capture (profiles/)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_engine_ncu.json")
+
+
+def _traffic():
+    try:
+        return json.load(open(TRAFFIC_FILE)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+TRAFFIC_PER_LAUNCH = _traffic()
 
 
 def env_rank():
@@ -249,6 +261,12 @@ def run_ours(args):
     mlp_ms = p1["mlp_ms"] - p0["mlp_ms"]
     mlp_launch = p1["mlp_launches"] - p0["mlp_launches"]
     mlp_rows = p1["mlp_rows"] - p0["mlp_rows"]
+    bulk = None
+    if model and prec == akmc.PREC_FP32:
+        _, _, _, q0 = sim.state(species=False)
+        sim.rates()
+        _, _, _, q1 = sim.state(species=False)
+        bulk = {"rows": int(sim.n_vac), "ms": q1["mlp_ms"] - q0["mlp_ms"]}
     sim.close()
 
     # ---------------- end to end through the C-ABI with host buffers (init H2D + steps + state D2H)
@@ -291,15 +309,27 @@ def run_ours(args):
         tc_peak = peaks.get("bf16_tflops_sustained", 1400.0) * 0.5
         mlp_s = mlp_ms / 1e3 if mlp_ms > 0 else float("nan")
         achieved = (mlp_rows * FLOPS_PER_VAC) / mlp_s / 1e12 if mlp_ms > 0 else None
-        roof = {"bound": "tensor", "kernel": "mlp_tc_kernel (gather+encode+layer1+tcgen05 layer2+layer3+rates)",
+        roof = {"bound": "tensor",
+                "kernel": "engine_kernel (phase engine: gather + memo + layer 1 on CUDA cores + tcgen05 layers 2-3 + "
+                          "rates + BKL select/apply, one persistent cluster launch per phase)",
                 "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
-                "frac": (achieved / tc_peak) if achieved else None, "traffic": None,
+                "frac": (achieved / tc_peak) if achieved else None, "traffic": TRAFFIC_PER_LAUNCH,
                 "peak_note": "FP32-class tensor peak = measured bf16 sustained x 1/2 (TF32:BF16 nominal ratio)",
-                "algorithmic_flops_per_vac": FLOPS_PER_VAC, "launches": int(mlp_launch), "rows": int(mlp_rows),
+                "algorithmic_flops_per_vac": FLOPS_PER_VAC,
+                "work": "network rows actually evaluated (memo misses) x algorithmic FLOPs per row",
+                "launches": int(mlp_launch), "rows": int(mlp_rows),
                 "kernel_ms": mlp_ms, "avg_launch_us": 1e3 * mlp_ms / max(mlp_launch, 1),
                 "share_of_step": (mlp_ms / ms) if ms > 0 else None,
-                "timing": "CUDA events around each launch in an instrumented pass of K further sweeps "
+                "latency_bound": "the phase engine runs each domain's event chain to the window end; its time is "
+                                 "set by dependent event latency, not by tensor throughput (DESIGN.md sec. 8)",
+                "timing": "CUDA events around each engine launch in an instrumented pass of K further sweeps "
                           f"(host-stepped, {prof_ms:.2f} ms); share = kernel ms / graph-mode step ms"}
+        if bulk is not None:
+            b_ach = bulk["rows"] * FLOPS_PER_VAC / (bulk["ms"] / 1e3) / 1e12
+            roof["evaluator_bulk"] = {"rows": bulk["rows"], "ms": bulk["ms"], "achieved": b_ach, "peak": tc_peak,
+                                      "frac": b_ach / tc_peak, "unit": "TFLOP/s",
+                                      "what": "the same cluster evaluator on every vacancy of the block at once "
+                                              "(akmc_rates), CUDA events around the launch"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / max(args.steps, 1), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,

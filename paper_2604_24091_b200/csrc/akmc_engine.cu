@@ -58,8 +58,14 @@ struct Ctl {
     long long cand_dom[2 * kSlots]; // domains waiting for slots: [0, npend) carried over, then fetched
     int cand_off[2 * kSlots];
     int cand_cnt[2 * kSlots];
+    long long pend_dom[2 * kSlots]; // domains that did not fit (next refill's carried-over list)
+    int pend_off[2 * kSlots];
+    int pend_cnt[2 * kSlots];
+    short cand_slot[2 * kSlots];    // placement: slot, or -1 (single-slot, parallel) / -2 (deferred)
+    int nmulti_def, nfree_single;
+    unsigned long long freem_single;
     int npend, nnew, fetch, drained, ntot, s0;
-    unsigned freem;
+    unsigned freew[2], runw[2];
     int nrows, nmiss, nrun, ebase;
     int wsum[kWarps];
     int4 mem_vac[kRowCap];          // positions of the held vacancies (this CTA is their only writer)
@@ -285,75 +291,111 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (phase_mode) {
             // ================= slots: release stopped domains, refill from the segment list =================
             __syncthreads();
-            if (warp == 0) {
-                // lane = slot; a slot is freed with its domain (head or continuation of a stopped head)
-                const int used = c.seg_used[lane];
-                const int head = used == 2 ? c.seg_head[lane] : lane;
+            if (tid < kSlots) {
+                // thread = slot; a slot is freed with its domain (head or continuation of a stopped head)
+                const int sl = tid;
+                const int used = c.seg_used[sl];
+                const int head = used == 2 ? c.seg_head[sl] : sl;
                 const bool rel = used != 0 && !c.seg_run[head];
                 if (rel) {
 #pragma unroll
-                    for (int a = 0; a < kSlotCap; ++a) c.mem_act[kSlotCap * lane + a] = 0;
+                    for (int a = 0; a < kSlotCap; ++a) c.mem_act[kSlotCap * sl + a] = 0;
                 }
+                const bool running = used == 1 && c.seg_run[sl];
                 __syncwarp();
-                if (rel) c.seg_used[lane] = 0;
-                c.seg_new[lane] = 0;
-                const unsigned freem = __ballot_sync(0xffffffffu, used == 0 || rel);
-                const int nfree = __popc(freem);
-                const int nrun = __popc(__ballot_sync(0xffffffffu, used == 1 && c.seg_run[lane]));
-                if (lane == 0) {
-                    c.freem = freem;
-                    c.fetch = 0;
-                    c.nnew = 0;
-                    if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun == 0)) {
-                        const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)nfree);
-                        if (s0 >= c.ntot) {
-                            c.drained = 1;
-                        } else {
-                            c.fetch = 1; c.s0 = s0; c.nnew = min(nfree, c.ntot - s0);
-                            ++d_refill;
-                        }
+                if (rel) c.seg_used[sl] = 0;
+                c.seg_new[sl] = 0;
+                const unsigned fm = __ballot_sync(0xffffffffu, used == 0 || rel);
+                const unsigned rm = __ballot_sync(0xffffffffu, running);
+                if (lane == 0) { c.freew[warp] = fm; c.runw[warp] = rm; }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned long long freem = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
+                const int nfree = __popcll(freem);
+                const int nrun0 = __popc(c.runw[0]) + __popc(c.runw[1]);
+                c.fetch = 0;
+                c.nnew = 0;
+                if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
+                    const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)nfree);
+                    if (s0 >= c.ntot) {
+                        c.drained = 1;
+                    } else {
+                        c.fetch = 1; c.s0 = s0; c.nnew = min(nfree, c.ntot - s0);
+                        ++d_refill;
                     }
                 }
             }
             __syncthreads();
+            if (tid < c.npend) {                           // carried-over candidates first
+                c.cand_dom[tid] = c.pend_dom[tid]; c.cand_off[tid] = c.pend_off[tid]; c.cand_cnt[tid] = c.pend_cnt[tid];
+            }
             if (c.fetch && tid < c.nnew) {
                 const Segment sg = p.segs[c.s0 + tid];
                 const int q = c.npend + tid;
                 c.cand_dom[q] = sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
             }
             __syncthreads();
+            const int ncand = c.npend + c.nnew;
             if (tid == 0) {
-                // first fit into runs of free slots (a domain of cnt vacancies needs ceil(cnt/4) consecutive
-                // slots); those that do not fit wait for the next refill
-                const int ncand = c.npend + c.nnew;
-                unsigned freem = c.freem;
-                int np = 0;
+                // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
+                // single-slot domains are placed in parallel below
+                unsigned long long freem = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
+                int nd = 0;
                 for (int q = 0; q < ncand; ++q) {
                     const int cnt = c.cand_cnt[q];
-                    if (cnt > kRowCap || cnt <= 0) { atomicAdd(p.overflow, 1ull); continue; }
+                    if (cnt <= kSlotCap) { c.cand_slot[q] = -1; continue; }
+                    if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
                     const int need = (cnt + kSlotCap - 1) / kSlotCap;
-                    unsigned runs = freem;                    // bit i set: slots i .. i+need-1 all free
+                    unsigned long long runs = freem;          // bit i set: slots i .. i+need-1 all free
                     for (int t = 1; t < need; ++t) runs &= freem >> t;
-                    if (need > 1) runs &= (need >= 32) ? 1u : (0xffffffffu >> (need - 1));
-                    if (!runs) {
-                        c.cand_dom[np] = c.cand_dom[q]; c.cand_off[np] = c.cand_off[q]; c.cand_cnt[np] = cnt;
-                        ++np;
-                        continue;
-                    }
-                    const int h = __ffs(runs) - 1;
-                    c.seg_used[h] = 1;
+                    if (!runs) { c.cand_slot[q] = -2; ++nd; continue; }
+                    const int h = __ffsll((long long)runs) - 1;
+                    freem &= ~(((need >= 64) ? ~0ull : ((1ull << need) - 1ull)) << h);
+                    c.cand_slot[q] = (short)h;
                     for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
-                    freem &= ~(((need >= 32) ? 0xffffffffu : ((1u << need) - 1u)) << h);
-                    c.seg_dom[h] = c.cand_dom[q]; c.seg_goff[h] = c.cand_off[q]; c.seg_cnt[h] = cnt;
-                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_run[h] = 1; c.seg_new[h] = 1;
                 }
-                c.npend = np;
+                c.nmulti_def = nd;
+                c.freem_single = freem;
+                c.nfree_single = __popcll(freem);
             }
             __syncthreads();
-            if (warp == 0) {
-                const int nrun = __popc(__ballot_sync(0xffffffffu, c.seg_used[lane] == 1 && c.seg_run[lane]));
-                if (lane == 0) c.nrun = nrun;
+            {
+                // the j-th single-slot candidate takes the j-th free slot; the rest are deferred
+                const bool single = tid < ncand && c.cand_slot[tid] == -1;
+                int nsingle = 0;
+                const int j = block_excl(single ? 1 : 0, c.wsum, nsingle);
+                const unsigned long long fm = c.freem_single;
+                const int nf = c.nfree_single;
+                if (single) {
+                    if (j < nf) {
+                        const unsigned lo = (unsigned)fm, hi = (unsigned)(fm >> 32);
+                        const int nlo = __popc(lo);
+                        c.cand_slot[tid] = (short)(j < nlo ? __fns(lo, 0, j + 1) : 32 + __fns(hi, 0, j - nlo + 1));
+                    } else {
+                        c.cand_slot[tid] = -2;
+                    }
+                }
+                __syncthreads();
+                const int q = tid;
+                const bool deferred = q < ncand && c.cand_slot[q] == -2;
+                int ndef = 0;
+                const int pi = block_excl(deferred ? 1 : 0, c.wsum, ndef);
+                if (deferred) { c.pend_dom[pi] = c.cand_dom[q]; c.pend_off[pi] = c.cand_off[q]; c.pend_cnt[pi] = c.cand_cnt[q]; }
+                if (q < ncand && c.cand_slot[q] >= 0) {
+                    const int h = c.cand_slot[q];
+                    c.seg_used[h] = 1;
+                    c.seg_dom[h] = c.cand_dom[q]; c.seg_goff[h] = c.cand_off[q]; c.seg_cnt[h] = c.cand_cnt[q];
+                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_run[h] = 1; c.seg_new[h] = 1;
+                }
+                int nplaced = 0;
+                block_excl((q < ncand && c.cand_slot[q] >= 0) ? 1 : 0, c.wsum, nplaced);
+                if (tid == 0) {
+                    c.npend = ndef;
+                    c.nrun = __popc(c.runw[0]) + __popc(c.runw[1]) + nplaced;
+                }
             }
+            __syncthreads();
             // members of newly placed domains: slot ids and positions (parallel loads)
             for (int i = warp; i < kSlots; i += kWarps) {
                 if (!c.seg_new[i]) continue;
@@ -381,15 +423,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (tid == 0) lap(d_x[1]);
             // ================= gather + memo lookup: warp per row, lanes = window slots j and j+32 =================
             const int nrows = c.nrows;
-            for (int r0 = warp; r0 < nrows; r0 += 4 * kWarps) {
-                // 4 rows per warp in flight: memo ways (lanes 0-15 way 0, 16-31 way 1) and window bytes
+            constexpr int kGR = 8;     // rows per warp in flight
+            for (int r0 = warp; r0 < nrows; r0 += kGR * kWarps) {
+                // kGR rows per warp in flight: memo ways (lanes 0-15 way 0, 16-31 way 1) and window bytes
                 const int k = lane & 15, way = lane >> 4;
-                uint32_t kw[4];
-                double gv[4];
-                int cv[4];
-                uint8_t b0[4], b1[4];
+                uint32_t kw[kGR];
+                double gv[kGR];
+                int cv[kGR];
+                uint8_t b0[kGR], b1[kGR];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kGR; ++q) {
                     const int r = r0 + q * kWarps;
                     kw[q] = 0; gv[q] = 0.0; cv[q] = 0; b0[q] = 0; b1[q] = 0;
                     if (r < nrows) {
@@ -405,13 +448,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kGR; ++q) {
                     const int r = r0 + q * kWarps;
                     if (r < nrows) { win[r * kWin + lane] = b0[q]; win[r * kWin + lane + 32] = b1[q]; }
                 }
                 __syncwarp();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kGR; ++q) {
                     const int r = r0 + q * kWarps;
                     if (r >= nrows) break;
                     const uint32_t ww = reinterpret_cast<const uint32_t*>(win + r * kWin)[k];
@@ -565,12 +608,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 fence_async_smem();
                 __syncthreads();
                 if (tid == 0) lap(d_x[3]);
-                if (tid == 0) {
-                    const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
-                    const uint32_t bytes = 16u + 2u * rg * kRowGroupA;
-                    const uint32_t aoff = 2u * rank * kRowGroupA;
-                    for (uint32_t d = 0; d < (uint32_t)kClusterN; ++d) {
-                        if (d == rank) continue;
+                if (warp == 0 && lane < kClusterN) {        // lane d sends to CTA d
+                    const uint32_t d = (uint32_t)lane;
+                    if (d == rank) {
+                        mbar_arrive(bar_req);
+                    } else {
+                        const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
+                        const uint32_t bytes = 16u + 2u * rg * kRowGroupA;
+                        const uint32_t aoff = 2u * rank * kRowGroupA;
                         const uint32_t cb = map_to(bar_req, d);
                         mbar_remote_expect_tx(cb, bytes);
                         bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
@@ -578,9 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             bulk_s2peer(map_to(smem_u32(A_hi + aoff), d), smem_u32(A_hi + aoff), rg * kRowGroupA, cb);
                             bulk_s2peer(map_to(smem_u32(A_lo + aoff), d), smem_u32(A_lo + aoff), rg * kRowGroupA, cb);
                         }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                    mbar_arrive(bar_req);
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 mbar_wait_cluster(bar_req, ph_req);
                 ph_req ^= 1u;
@@ -692,15 +736,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     fence_async_smem();
                     tc_fence_before();
                     __syncthreads();
-                    if (tid == 0) {
-                        for (uint32_t s = 0; s < (uint32_t)kClusterN; ++s) {
-                            const uint32_t bytes = (uint32_t)n_s[s] * 64u;
-                            const uint32_t cb = map_to(bar_part, s);
-                            mbar_remote_expect_tx(cb, bytes);
-                            if (bytes)
-                                bulk_s2peer(map_to(smem_u32(part_in + rank * kRoundRows * 8), s),
-                                            smem_u32(part_out + s * kRoundRows * 8), bytes, cb);
-                        }
+                    if (warp == 0 && lane < kClusterN) {    // lane s sends row block s to CTA s
+                        const uint32_t s = (uint32_t)lane;
+                        const uint32_t bytes = (uint32_t)n_s[s] * 64u;
+                        const uint32_t cb = map_to(bar_part, s);
+                        mbar_remote_expect_tx(cb, bytes);
+                        if (bytes)
+                            bulk_s2peer(map_to(smem_u32(part_in + rank * kRoundRows * 8), s),
+                                        smem_u32(part_out + s * kRoundRows * 8), bytes, cb);
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                     mbar_wait_cluster(bar_part, ph_part);
@@ -739,8 +782,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         }
                     }
                 }
+                if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 if (tid == 0) {
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     lap(d_x[7]);
                     ++d_rounds;
                     d_erounds += total > 0 ? 1 : 0;

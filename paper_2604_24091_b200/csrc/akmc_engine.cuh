@@ -17,8 +17,8 @@ namespace akmc {
 constexpr int kClusterN = 8;                   // CTAs per cluster; CTA r owns hidden columns [32r, 32r+32)
 constexpr int kSliceN = kHid / kClusterN;      // 32
 constexpr int kRoundRows = 16;                 // rows a CTA contributes per evaluation round (tile M = 128)
-constexpr int kSlots = 32;                     // domain slots per CTA (a domain with > 4 vacancies spans several)
-constexpr int kSlotCap = 4;                    // vacancies per slot
+constexpr int kSlots = 64;                     // domain slots per CTA (a domain with > 2 vacancies spans several)
+constexpr int kSlotCap = 2;                    // vacancies per slot
 constexpr int kRowCap = kSlots * kSlotCap;     // vacancies a CTA holds at once (128)
 constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
 

@@ -157,6 +157,7 @@ struct akmc_handle {
     uint8_t* d_W2e = nullptr;         // [8][32 KiB]
     uint8_t* d_W3e = nullptr;         // [8][2 KiB]
     unsigned int* d_cursor = nullptr;
+    uint8_t* d_stage = nullptr;       // [clusters][8][16 KiB] L2 staging of h1 rows (multicast)
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
     size_t ev_used = 0;
@@ -215,7 +216,8 @@ void free_all(akmc_handle* h)
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
-                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor};
+                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
+                    h->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -426,6 +428,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
     p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
+    p.stage = h->d_stage;
     p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
     return p;
 }
@@ -830,6 +833,10 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         if (h->n_clusters <= 0) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_CUDA, "no co-resident 8-CTA cluster for the evaluator"); }
     }
     CKI(cudaMalloc(&h->d_cursor, sizeof(unsigned int)));
+    {
+        const int ncl = std::max(h->n_clusters, 1) + 1;
+        CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 16384));
+    }
     if (h->sub) {
         CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
         CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
@@ -1344,8 +1351,8 @@ void akmc_free(akmc_handle* h)
                          " eval-rounds/CTA %.1f refills/CTA %.1f; cycles/CTA: control %.0f rounds %.0f select %.0f total %.0f\n",
                          d[7], d[10], d[0] / n, d[1], d[2] / n, d[3] / n, d[8] / n, d[4] / n, d[5] / n, d[6] / n, d[9] / n);
             std::fprintf(stderr, "[akmc engine] cycles/CTA: refill %.0f rows %.0f gather+memo %.0f | L1 %.0f exchange %.0f"
-                         " L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n, d[14] / n, d[15] / n,
-                         d[16] / n, d[17] / n, d[18] / n);
+                         " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
+                         d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);
         }
         cudaFree(h->d_phase_cycles);
         h->d_phase_cycles = nullptr;

@@ -163,7 +163,8 @@ __device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame
 // rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
 // row m of the A operand (M-major no-swizzle: 8-row group g at g*4096, core column c at c*128)
 __device__ __forceinline__ void layer1_row(const uint8_t* w, const float* __restrict__ W1f, uint16_t* lst, int m,
-                                           uint8_t* A_hi, uint8_t* A_lo, unsigned long long& ovf)
+                                           uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi, uint8_t* g_lo,
+                                           unsigned long long& ovf)
 {
     const int lane = threadIdx.x & 31;
     const uint32_t b0 = w[lane], b1 = w[lane + 32];
@@ -209,8 +210,13 @@ __device__ __forceinline__ void layer1_row(const uint8_t* w, const float* __rest
         split_h(h, hi[c], lo[c], ovf);
     }
     const uint32_t off = (uint32_t)(m >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
-    *reinterpret_cast<uint4*>(A_hi + off) = pack8(hi);
-    *reinterpret_cast<uint4*>(A_lo + off) = pack8(lo);
+    const uint4 vh = pack8(hi), vl = pack8(lo);
+    *reinterpret_cast<uint4*>(A_hi + off) = vh;
+    *reinterpret_cast<uint4*>(A_lo + off) = vl;
+    // the same 16 B into the L2 staging block of this CTA (row m & 15 of its block)
+    const uint32_t goff = (uint32_t)((m & 15) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
+    *reinterpret_cast<uint4*>(g_hi + goff) = vh;
+    *reinterpret_cast<uint4*>(g_lo + goff) = vl;
     __syncwarp();
 }
 
@@ -243,6 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     const bool phase_mode = (p.mode == kEnginePhase);
     const bool mlp = (p.model == 1);
     unsigned long long ovf = 0;
+    constexpr uint32_t kStageCta = 2u * 2u * kRowGroupA;            // hi + lo, 16 rows
+    uint8_t* g_hi = kTC ? p.stage + ((size_t)cluster_id() * kClusterN + rank) * kStageCta : nullptr;
+    uint8_t* g_lo = kTC ? g_hi + 2u * kRowGroupA : nullptr;
 
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
@@ -281,8 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     // diagnostics (thread 0): iterations, rounds, evaluation rounds, cycles in control / rounds / selection
     unsigned long long d_it = 0, d_rounds = 0, d_erounds = 0, d_refill = 0;
     long long d_cc = 0, d_cr = 0, d_cs = 0;
-    long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
+    long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)   // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
     const long long t_start = clock64();
+    unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
     long long t_mark = t_start;
     auto lap = [&](long long& acc) { const long long t = clock64(); acc += t - t_mark; t_mark = t; };
 
@@ -337,14 +348,21 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             const int ncand = c.npend + c.nnew;
+            const bool multi = tid < ncand && c.cand_cnt[tid] > kSlotCap;
+            if (tid < ncand) c.cand_slot[tid] = -1;
+            const int any_multi = __syncthreads_or(multi ? 1 : 0);
             if (tid == 0) {
+                c.freem_single = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
+                c.nfree_single = __popcll(c.freem_single);
+            }
+            if (tid == 0 && any_multi) {
                 // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
                 // single-slot domains are placed in parallel below
                 unsigned long long freem = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
                 int nd = 0;
                 for (int q = 0; q < ncand; ++q) {
                     const int cnt = c.cand_cnt[q];
-                    if (cnt <= kSlotCap) { c.cand_slot[q] = -1; continue; }
+                    if (cnt <= kSlotCap) continue;
                     if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
                     const int need = (cnt + kSlotCap - 1) / kSlotCap;
                     unsigned long long runs = freem;          // bit i set: slots i .. i+need-1 all free
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                         uint4 t = make_uint4(0, 0, 0, 0);
                         if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
-                        layer1_row(win + r * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, ovf);
+                        layer1_row(win + r * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, g_hi, g_lo, ovf);
                         if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
                         __syncwarp();
                         if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
@@ -600,35 +618,37 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             win[i * kWin + lane + 32] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
                         }
                         __syncwarp();
-                        layer1_row(win + i * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, ovf);
+                        layer1_row(win + i * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, g_hi, g_lo, ovf);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
                 }
-                // ---- exchange: header + this CTA's h1 rows (8-row groups 2r, 2r+1) to every peer
+                // ---- exchange: header (DSMEM) + this CTA's h1 rows (8-row groups 2r, 2r+1), multicast from the
+                //      L2 staging copy into every peer's A (one L2 read, no SM-to-SM bandwidth limit)
                 fence_async_smem();
+                fence_async_global();
                 __syncthreads();
                 if (tid == 0) lap(d_x[3]);
-                if (warp == 0 && lane < kClusterN) {        // lane d sends to CTA d
+                if (warp == 0 && lane < kClusterN) {        // lane d signals CTA d
                     const uint32_t d = (uint32_t)lane;
+                    const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
                     if (d == rank) {
                         mbar_arrive(bar_req);
-                    } else {
-                        const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
-                        const uint32_t bytes = 16u + 2u * rg * kRowGroupA;
-                        const uint32_t aoff = 2u * rank * kRowGroupA;
-                        const uint32_t cb = map_to(bar_req, d);
-                        mbar_remote_expect_tx(cb, bytes);
-                        bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
                         if (rg) {
-                            bulk_s2peer(map_to(smem_u32(A_hi + aoff), d), smem_u32(A_hi + aoff), rg * kRowGroupA, cb);
-                            bulk_s2peer(map_to(smem_u32(A_lo + aoff), d), smem_u32(A_lo + aoff), rg * kRowGroupA, cb);
+                            const uint32_t aoff = 2u * rank * kRowGroupA;
+                            const uint16_t mask = (uint16_t)(((1u << kClusterN) - 1u) & ~(1u << rank));
+                            bulk_g2s_multicast(smem_u32(A_hi + aoff), g_hi, rg * kRowGroupA, bar_req, mask);
+                            bulk_g2s_multicast(smem_u32(A_lo + aoff), g_lo, rg * kRowGroupA, bar_req, mask);
                         }
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    } else {
+                        const uint32_t cb = map_to(bar_req, d);
+                        mbar_remote_expect_tx(cb, 16u + 2u * rg * kRowGroupA);
+                        bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
                     }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 mbar_wait_cluster(bar_req, ph_req);
                 ph_req ^= 1u;
-                if (tid == 0) lap(d_x[4]);
+                if (tid == 0) { const long long before = d_x[4]; lap(d_x[4]); if (k_round > 0) d_xk += d_x[4] - before; }
                 int n_s[kClusterN];
                 int any_more = 0, any_alive = 0, total = 0;
 #pragma unroll
@@ -821,8 +841,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (m == 0) {
                 stop = true;
             } else {
-                atomicAdd(&c.evals, 8ull * (unsigned long long)m);
-                if (cl) atomicAdd(&c.clamps, cl);
+                my_evals += 8ull * (unsigned long long)m;
+                my_clamps += cl;
                 int P = 1, nlev = 0;
                 const double Rd = tree_build(buf, m, P, nlev);
                 if (!(Rd > 0.0)) {
@@ -873,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         }
                         c.seg_t[i] = __dadd_rn(c.seg_t[i], dt);
                         c.seg_it[i] += 1u;
-                        atomicAdd(&c.events, 1ull);
+                        my_events += 1ull;
                     }
                 }
             }
@@ -897,10 +917,20 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         atomicAdd(p.diag + 9, (unsigned long long)(clock64() - t_start));
         atomicAdd(p.diag + 10, 1ull * (phase_mode ? 1 : 0));
         for (int q = 0; q < 8; ++q) atomicAdd(p.diag + 11 + q, (unsigned long long)d_x[q]);
+        atomicAdd(p.diag + 19, (unsigned long long)d_xk);
     }
 
     // ---- teardown
     if (ovf && p.overflow) atomicAdd(p.overflow, ovf);
+    if (phase_mode && tid < kSlots) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            my_events += __shfl_xor_sync(0xffffffffu, my_events, o);
+            my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
+            my_clamps += __shfl_xor_sync(0xffffffffu, my_clamps, o);
+        }
+        if (lane == 0) { atomicAdd(&c.events, my_events); atomicAdd(&c.evals, my_evals); atomicAdd(&c.clamps, my_clamps); }
+    }
     __syncthreads();
     if (tid == 0 && phase_mode) {
         if (c.events) atomicAdd(&p.ctr->events, c.events);

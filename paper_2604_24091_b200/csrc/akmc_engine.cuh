@@ -72,6 +72,7 @@ struct EngineParams {
     double* Rsum;
     double* E;
     EngineWeights W;
+    uint8_t* stage;         // [clusters][8 CTAs][hi 8 KiB | lo 8 KiB] h1 rows staged in L2 for the multicast
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
 };

@@ -197,3 +197,75 @@ def test_terminal_and_conservation(akmc):
         assert c["status"] == akmc.AKMC_TERMINAL
         gsp, vac, clock, _ = sim.state()
         assert np.array_equal(gsp, sp) and clock[0] == 0.0
+
+
+# ----------------------------------------------------------------------------- phase engine specifics
+def _crowded_lattice(L, n_spread, cluster_center, n_cluster, seed):
+    """Fe-5%Cu lattice with n_spread random vacancies plus n_cluster vacancies packed around one site, so
+    that some domains hold > 2 vacancies (multi-slot placement) and one holds > 16 (tree in scratch)."""
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), n_spread, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    cx, cy, cz = cluster_center
+    placed = 0
+    while placed < n_cluster:
+        x, y, z = (int(v) for v in rng.integers(-2, 3, size=3))
+        b = int(rng.integers(0, 2))
+        i = 2 * (((cx + x) % L) + L * (((cy + y) % L) + L * ((cz + z) % L))) + b
+        if sp[i] != 6:
+            sp[i] = 6
+            placed += 1
+    return sp
+
+
+@pytest.mark.parametrize("lam", [1.0, 0.25])
+def test_engine_crowded_domains_bitexact(akmc, orc, lam):
+    """Domains with many vacancies: multi-slot placement, carried-over (pending) domains and > 16-member
+    competing sets (tree in global scratch) stay bit-exact vs the oracle."""
+    eps, E0 = _params()
+    L = 32
+    sp = _crowded_lattice(L, 120, (12, 12, 12), 40, seed=77)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=23,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(lam, E0[0]))
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 4, eps=eps, E0=E0)
+    assert ost.counters[0] > 50
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0] and gctr["hop_evals"] == ost.counters[1]
+
+
+def test_engine_evaluator_row_purity(akmc):
+    """The FP32-equivalent evaluator's result for a window does not depend on the tile it is evaluated in
+    (order, neighbours, batch size): the property that makes the per-vacancy memo and any decomposition
+    exact."""
+    eps, E0 = _params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=4)
+    rng = np.random.default_rng(5)
+    w = synth.random_windows(700, seed=5)
+    cfg = akmc.Config(cells=(8, 8, 8), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg, np.zeros(2 * 8 ** 3, np.uint8), eps, E0, mlp) as sim:
+        e_all = sim.eval_windows(w, akmc.PREC_FP32)
+        perm = rng.permutation(len(w))
+        e_perm = sim.eval_windows(w[perm], akmc.PREC_FP32)
+        e_one = np.stack([sim.eval_windows(w[i:i + 1], akmc.PREC_FP32)[0] for i in range(0, len(w), 97)])
+    assert np.array_equal(e_perm, e_all[perm])
+    assert np.array_equal(e_one, e_all[::97])
+
+
+def test_engine_matches_legacy_loop(akmc, orc, monkeypatch):
+    """The phase engine and the grid-synchronous legacy inner loop (AKMC_LEGACY_LOOP=1) run the same FP64
+    trajectory (both equal the oracle's)."""
+    eps, E0 = _params()
+    L = 32
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), 50, seed=91)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=3,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(0.5, E0[0]))
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        sim.step(6)
+        a = sim.state()
+    monkeypatch.setenv("AKMC_LEGACY_LOOP", "1")
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        sim.step(6)
+        b = sim.state()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    assert a[3]["events"] == b[3]["events"] and a[3]["hop_evals"] == b[3]["hop_evals"]

@@ -171,6 +171,12 @@ class Simulation:
         self._check(self.lib.akmc_state(self.h, _ptr(sp), _ptr(vac), C.byref(n), _ptr(clock), C.byref(ctr)))
         return sp, vac[: n.value], clock, ctr.as_dict()
 
+    def counters(self) -> dict:
+        """Cumulative counters only (one small device->host read, no lattice or vacancy transfer)."""
+        ctr = CCounters()
+        self._check(self.lib.akmc_state(self.h, None, None, None, None, C.byref(ctr)))
+        return ctr.as_dict()
+
     def vacancies(self):
         """(global slot ids, global canonical sites) of the vacancies this rank owns, sorted by id."""
         n = C.c_int64(0)

@@ -158,6 +158,7 @@ struct akmc_handle {
     uint8_t* d_W3e = nullptr;         // [8][2 KiB]
     unsigned int* d_cursor = nullptr;
     uint8_t* d_stage = nullptr;       // [clusters][8][16 KiB] L2 staging of h1 rows (multicast)
+    uint8_t* d_canon = nullptr;       // canonical-order lattice for akmc_state readbacks (lazy)
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
     size_t ev_used = 0;
@@ -217,7 +218,7 @@ void free_all(akmc_handle* h)
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
                     h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
-                    h->d_stage};
+                    h->d_stage, h->d_canon};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -411,8 +412,8 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     CK(h, mlp_tc_setup());
     if (std::getenv("AKMC_PHASE_TIMING")) {
-        CK(h, cudaMalloc(&h->d_phase_cycles, 64 * sizeof(unsigned long long)));
-        CK(h, cudaMemset(h->d_phase_cycles, 0, 64 * sizeof(unsigned long long)));
+        CK(h, cudaMalloc(&h->d_phase_cycles, 128 * sizeof(unsigned long long)));
+        CK(h, cudaMemset(h->d_phase_cycles, 0, 128 * sizeof(unsigned long long)));
     }
     return AKMC_OK;
 }
@@ -768,7 +769,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         // storage layout with halo ghosts (periodic images)
         uint8_t* st = nullptr;
         CKI(cudaMalloc(&st, (size_t)h->ssites));
-        scatter_storage_kernel<<<blocks_for(h->sites, 256), 256, 0, h->stream>>>(h->d_species, st, h->F, h->sites);
+        const long long nlines = 16ll * h->F.NB[0] * h->F.NB[1] * h->F.NB[2] * h->nvox;
+        scatter_storage_kernel<<<blocks_for(nlines, 256), 256, 0, h->stream>>>(h->d_species, st, h->F, h->nvox);
         const cudaError_t es = cudaStreamSynchronize(h->stream);
         cudaFree(h->d_species);
         h->d_species = st;
@@ -835,7 +837,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     CKI(cudaMalloc(&h->d_cursor, sizeof(unsigned int)));
     {
         const int ncl = std::max(h->n_clusters, 1) + 1;
-        CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 16384));
+        CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
     }
     if (h->sub) {
         CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
@@ -1217,17 +1219,19 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
     if (!h) return AKMC_ERR_RUNTIME;
     CK(h, cudaStreamSynchronize(h->stream));
     std::vector<VacRec> vr;
-    int rc = collect_vacancies(h, vr);
-    if (rc != AKMC_OK) return rc;
+    if (vac_sites_out || n_vac_inout) {
+        const int rc = collect_vacancies(h, vr);
+        if (rc != AKMC_OK) return rc;
+    }
     if (vac_sites_out && (!n_vac_inout || *n_vac_inout < (int64_t)vr.size()))
         return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
     if (species_out) {
-        uint8_t* canon = nullptr;
-        CK(h, cudaMalloc(&canon, (size_t)h->sites));
-        gather_canonical_kernel<<<blocks_for(h->sites, 256), 256, 0, h->stream>>>(h->d_species, canon, h->F, h->sites);
+        if (!h->d_canon) CK(h, cudaMalloc(&h->d_canon, (size_t)h->sites));   // kept for later readbacks
+        uint8_t* canon = h->d_canon;
+        const long long nchunks = (long long)((h->F.L[0] + 3) / 4) * h->F.L[1] * h->F.L[2] * h->nvox;
+        gather_canonical_kernel<<<blocks_for(nchunks, 256), 256, 0, h->stream>>>(h->d_species, canon, h->F, h->nvox);
         cudaError_t e = cudaStreamSynchronize(h->stream);
         if (e == cudaSuccess) e = cudaMemcpy(species_out, canon, (size_t)h->sites, cudaMemcpyDeviceToHost);
-        cudaFree(canon);
         CK(h, e);
     }
     if (vac_sites_out)
@@ -1337,7 +1341,7 @@ void akmc_free(akmc_handle* h)
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->d_phase_cycles) {
-        unsigned long long c[64] = {0};
+        unsigned long long c[128] = {0};
         cudaMemcpy(c, h->d_phase_cycles, sizeof(c), cudaMemcpyDeviceToHost);
         const double t = c[7] ? (double)c[7] : 1.0;
         if (c[7])
@@ -1350,6 +1354,11 @@ void akmc_free(akmc_handle* h)
             std::fprintf(stderr, "[akmc engine] CTA-launches=%llu (phase %llu) iterations/CTA %.1f (max %llu) rounds/CTA %.1f"
                          " eval-rounds/CTA %.1f refills/CTA %.1f; cycles/CTA: control %.0f rounds %.0f select %.0f total %.0f\n",
                          d[7], d[10], d[0] / n, d[1], d[2] / n, d[3] / n, d[8] / n, d[4] / n, d[5] / n, d[6] / n, d[9] / n);
+            if (d[40] || d[46])
+                std::fprintf(stderr, "[akmc engine-tc] per CTA: rounds %.1f (with rows %.1f) group-iterations %.1f refills %.1f;"
+                             " evaluator cycles: exchange %.0f L2+E2 %.0f L3+partials %.0f E3 %.0f | control cycles: wait %.0f"
+                             " select %.0f refill %.0f rows+gather %.0f L1 %.0f\n", d[40] / n, d[41] / n, d[51] / n, d[52] / n,
+                             d[42] / n, d[43] / n, d[44] / n, d[45] / n, d[46] / n, d[47] / n, d[48] / n, d[49] / n, d[50] / n);
             std::fprintf(stderr, "[akmc engine] cycles/CTA: refill %.0f rows %.0f gather+memo %.0f | L1 %.0f exchange %.0f"
                          " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
                          d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);

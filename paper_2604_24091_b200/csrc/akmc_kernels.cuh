@@ -603,35 +603,81 @@ static __global__ void scan_write_kernel(const uint4* __restrict__ sp, long long
             }
 }
 
-// canonical (x fastest, basis interleaved) <-> storage (halo + ghosts) layout conversions
-static __global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_t* storage, Frame F, long long ncanon)
+// canonical (x fastest, basis interleaved) <-> storage (halo + ghosts) layout conversions, one 8-byte
+// brick line (4 cells along x x 2 basis sites) per thread, 16 threads per 128-byte brick: every brick is
+// written (scatter) or read (gather) by one half-warp as a whole L2 line.
+__device__ __forceinline__ int wrap_axis(int c, int L, int wrap, bool& ok)
 {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ncanon) return;
-    const long long csites = 2ll * F.L[0] * F.L[1] * F.L[2];
-    const int vox = (int)(i / csites);
-    const long long li = i - (long long)vox * csites;
-    const int b = (int)(li & 1);
-    const long long cell = li >> 1;
-    const int x = (int)(cell % F.L[0]);
-    const int y = (int)((cell / F.L[0]) % F.L[1]);
-    const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
-    write_site(storage, F, vox, 2 * x + b, 2 * y + b, 2 * z + b, canon[i]);
+    if (c >= 0 && c < L) return c;
+    if (!wrap) { ok = false; return 0; }
+    return ((c % L) + L) % L;
 }
 
-static __global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uint8_t* canon, Frame F, long long ncanon)
+// storage brick lines (including the halo) <- canonical; halo cells on periodic axes get the images, on
+// decomposed axes zeros (filled later by the halo exchange)
+static __global__ void scatter_storage_kernel(const uint8_t* __restrict__ canon, uint8_t* storage, Frame F, int nvox)
 {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ncanon) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nbv = (long long)F.NB[0] * F.NB[1] * F.NB[2];
+    if (t >= 16 * nbv * nvox) return;
+    const long long brick = t >> 4;
+    const int l = (int)(t & 15), ly = l & 3, lz = l >> 2;
+    const int vox = (int)(brick / nbv);
+    const long long bi = brick - (long long)vox * nbv;
+    const int bx = (int)(bi % F.NB[0]), by = (int)((bi / F.NB[0]) % F.NB[1]), bz = (int)(bi / ((long long)F.NB[0] * F.NB[1]));
+    bool ok = true;
+    const int y = wrap_axis(4 * by + ly - kHalo, F.L[1], F.wrap[1], ok);
+    const int z = wrap_axis(4 * bz + lz - kHalo, F.L[2], F.wrap[2], ok);
     const long long csites = 2ll * F.L[0] * F.L[1] * F.L[2];
-    const int vox = (int)(i / csites);
-    const long long li = i - (long long)vox * csites;
-    const int b = (int)(li & 1);
-    const long long cell = li >> 1;
-    const int x = (int)(cell % F.L[0]);
-    const int y = (int)((cell / F.L[0]) % F.L[1]);
-    const int z = (int)(cell / ((long long)F.L[0] * F.L[1]));
-    canon[i] = storage[site_of(F, vox, 2 * x + b, 2 * y + b, 2 * z + b)];
+    const uint8_t* row = canon + (long long)vox * csites + 2ll * F.L[0] * (y + (long long)F.L[1] * z);
+    unsigned long long v = 0;
+    if (ok) {
+        const int x0 = 4 * bx - kHalo;
+        if (x0 >= 0 && x0 + 3 < F.L[0]) {
+            const uint32_t* r4 = reinterpret_cast<const uint32_t*>(row + 2 * x0);   // 2*x0 = 8bx - 4: 4-aligned
+            v = (unsigned long long)__ldg(r4) | ((unsigned long long)__ldg(r4 + 1) << 32);
+        } else {
+            for (int q = 0; q < 4; ++q) {
+                bool okx = true;
+                const int x = wrap_axis(x0 + q, F.L[0], F.wrap[0], okx);
+                if (okx) v |= ((unsigned long long)row[2 * x] | ((unsigned long long)row[2 * x + 1] << 8)) << (16 * q);
+            }
+        }
+    }
+    uint8_t* dst = storage + (long long)vox * F.sites + (brick - (long long)vox * nbv) * 128 + (((lz << 2) | ly) << 3);
+    *reinterpret_cast<unsigned long long*>(dst) = v;
+}
+
+// canonical <- storage (owned cells only): 8 canonical bytes per thread from two half brick lines
+static __global__ void gather_canonical_kernel(const uint8_t* __restrict__ storage, uint8_t* canon, Frame F, int nvox)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nx = (F.L[0] + 3) >> 2;
+    const long long per_vox = (long long)nx * F.L[1] * F.L[2];
+    if (t >= per_vox * nvox) return;
+    const int vox = (int)(t / per_vox);
+    const long long r = t - (long long)vox * per_vox;
+    const int k = (int)(r % nx);
+    const long long yz = r / nx;
+    const int y = (int)(yz % F.L[1]), z = (int)(yz / F.L[1]);
+    uint8_t* dst = canon + (long long)vox * 2ll * F.L[0] * F.L[1] * F.L[2] + 2ll * F.L[0] * (y + (long long)F.L[1] * z);
+    const int x0 = 4 * k;
+    if (x0 + 3 < F.L[0]) {
+        // storage cells x0+2 .. x0+5: the upper half of brick line k and the lower half of line k+1
+        const uint8_t* base = storage + site_of(F, vox, 2 * x0, 2 * y, 2 * z);           // (x0+2)&3 == 2: +4 bytes
+        const uint32_t lo = *reinterpret_cast<const uint32_t*>(base);
+        const uint32_t hi = *reinterpret_cast<const uint32_t*>(storage + site_of(F, vox, 2 * x0 + 4, 2 * y, 2 * z));
+        const unsigned long long v = (unsigned long long)lo | ((unsigned long long)hi << 32);
+        if ((reinterpret_cast<uintptr_t>(dst + 2 * x0) & 7) == 0) {
+            *reinterpret_cast<unsigned long long*>(dst + 2 * x0) = v;
+        } else {
+            *reinterpret_cast<uint32_t*>(dst + 2 * x0) = lo;
+            *reinterpret_cast<uint32_t*>(dst + 2 * x0 + 4) = hi;
+        }
+    } else {
+        for (int x = x0; x < F.L[0]; ++x)
+            for (int bb = 0; bb < 2; ++bb) dst[2 * x + bb] = storage[site_of(F, vox, 2 * x + bb, 2 * y + bb, 2 * z + bb)];
+    }
 }
 
 // vstart[v] = first slot whose voxel >= v (slots are in site order, hence voxel-major)

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <thread>
 
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -159,6 +160,8 @@ struct akmc_handle {
     unsigned int* d_cursor = nullptr;
     uint8_t* d_stage = nullptr;       // [clusters][8][16 KiB] L2 staging of h1 rows (multicast)
     uint8_t* d_canon = nullptr;       // canonical-order lattice for akmc_state readbacks (lazy)
+    int* h_watch = nullptr;           // AKMC_WATCHDOG: engine progress words (mapped host memory)
+    int* d_watch = nullptr;
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
     size_t ev_used = 0;
@@ -225,6 +228,7 @@ void free_all(akmc_handle* h)
     if (h->h_phase) cudaFreeHost(h->h_phase);
     if (h->sweep_exec) cudaGraphExecDestroy(h->sweep_exec);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
+    if (h->h_watch) cudaFreeHost(h->h_watch);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
     void* dptrs[] = {h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow};
     for (void* p : dptrs)
@@ -430,6 +434,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
     p.stage = h->d_stage;
+    p.watch = h->d_watch;
     p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
     return p;
 }
@@ -835,6 +840,11 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         if (h->n_clusters <= 0) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_CUDA, "no co-resident 8-CTA cluster for the evaluator"); }
     }
     CKI(cudaMalloc(&h->d_cursor, sizeof(unsigned int)));
+    if (std::getenv("AKMC_WATCHDOG")) {
+        CKI(cudaHostAlloc(&h->h_watch, 4096 * 8 * sizeof(int), cudaHostAllocMapped));
+        std::memset(h->h_watch, 0, 4096 * 8 * sizeof(int));
+        CKI(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_watch), h->h_watch, 0));
+    }
     {
         const int ncl = std::max(h->n_clusters, 1) + 1;
         CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
@@ -1038,6 +1048,26 @@ static int exchange_deltas(akmc_handle* h)
 }
 
 // host-stepped sublattice loop (used when profiling: CUDA events around every barrier-kernel launch)
+// AKMC_WATCHDOG: wait for the stream with a deadline; on expiry print every CTA's last progress word and abort
+static void watchdog_wait(akmc_handle* h, const char* where)
+{
+    if (!h->h_watch) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (cudaStreamQuery(h->stream) == cudaErrorNotReady) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+            std::fprintf(stderr, "[akmc watchdog] %s: engine did not finish in 20 s; CTA: it code a b nrun drained npend phase\n", where);
+            for (int b = 0; b < 4096; ++b) {
+                const volatile int* w = h->h_watch + b * 8;
+                if (w[1] == 0 && w[0] == 0) continue;
+                std::fprintf(stderr, "  cta %4d: %d %d %d %d %d %d %d %d\n", b, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+            }
+            std::fflush(stderr);
+            std::abort();
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+}
+
 static int step_sublattice_host(akmc_handle* h, int64_t n)
 {
     for (int64_t sw = 0; sw < n; ++sw) {
@@ -1061,6 +1091,7 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
                 CK(h, cudaEventRecord(e0, h->stream));
                 const int rc = enqueue_phase_engine(h, ph, h->stream);
                 if (rc != AKMC_OK) return rc;
+                watchdog_wait(h, "phase");
                 CK(h, cudaEventRecord(e1, h->stream));
                 h->total.kernel_launches += 3;
                 h->total.mlp_launches += 1;
@@ -1123,6 +1154,7 @@ static int step_sublattice(akmc_handle* h, int64_t n)
         CK(h, cudaGetLastError());
         if (!h->multi) {
             CK(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+            watchdog_wait(h, "sweep");
         } else {
             for (int q = 0; q < 8; ++q) {
                 CK(h, cudaGraphLaunch(h->phase_exec[q], h->stream));

@@ -7,15 +7,15 @@
 // domains free their slots, which are refilled from the phase's segment list (domains of a phase are
 // independent, so the processing order does not change any trajectory).
 //
-// Evaluator, FP32-equivalent mode (cluster of 8 CTAs, rounds in lockstep; tile M = 128 = 8 x 16 rows):
+// Evaluator, FP32-equivalent mode (cluster of 4 CTAs, rounds in lockstep; tile M = 128 = 4 x 32 rows):
 //   L1 (CUDA cores, requesting CTA): h1 = ReLU(b1' + sum over the row's non-Fe slots of W1'(s, slot)) --
 //      the one-hot layer is a sparse gather-sum (~6 rows of W1'), not a dense contraction -- summed in
 //      FP64 in slot order, rounded once to FP32, split into fp16 hi + lo*2^-11 and written to rows
-//      [16r, 16r+16) of the A operand; the request bulk-copies those rows into the other 7 CTAs' A;
-//   L2 (tcgen05, M=128 N=32 K=256): CTA r computes columns [32r, 32r+32) with its resident W2 slice:
+//      [32r, 32r+32) of the A operand; the request multicasts those rows into the other 3 CTAs' A;
+//   L2 (tcgen05, M=128 N=64 K=256): CTA r computes columns [64r, 64r+64) with its resident W2 slice:
 //      D1 = Ahi*W2hi, D2 = Ahi*W2lo + Alo*W2hi; h2 = ReLU(2^-s2 (D1 + 2^-11 D2) + b2) -> fp16 split;
-//   L3 (tcgen05, M=128 N=16 K=32): CTA r's partial of the 8 outputs over its 32 h2 columns; the
-//      partials of row block [16s, 16s+16) are bulk-copied to CTA s, which sums them in fixed order
+//   L3 (tcgen05, M=128 N=16 K=64): CTA r's partial of the 8 outputs over its 64 h2 columns; the
+//      partials of row block [32s, 32s+32) are bulk-copied to CTA s, which sums them in fixed order
 //      (FP64), adds b3, clamps at 0 and forms Gamma = nu0 det_exp(-E/kT).
 // The result of a row depends only on its window (rows of a tile do not interact, the order of every
 // sum is fixed), so memoisation and any tiling or decomposition give bit-identical trajectories.
@@ -45,22 +45,18 @@ constexpr float kLo = 2048.0f;
 struct ReqHdr { int n, more, alive, pad; };
 
 struct Ctl {
-    long long seg_dom[kSlots];
+    unsigned seg_dom[kSlots];       // domain ids are < 2^32 (checked at init)
     double seg_t[kSlots];
     int seg_goff[kSlots];           // global member offset (scratch of big trees)
     int seg_cnt[kSlots];
-    int seg_span[kSlots];           // slots occupied by the domain (head slot only)
     unsigned seg_it[kSlots];
     uint8_t seg_used[kSlots];       // 0 free, 1 head of a held domain, 2 continuation slot
     uint8_t seg_head[kSlots];       // head slot of a continuation slot
     uint8_t seg_run[kSlots];
     uint8_t seg_new[kSlots];
-    long long cand_dom[2 * kSlots]; // domains waiting for slots: [0, npend) carried over, then fetched
+    unsigned cand_dom[2 * kSlots];  // domains waiting for slots: [0, npend) carried over, then fetched
     int cand_off[2 * kSlots];
     int cand_cnt[2 * kSlots];
-    long long pend_dom[2 * kSlots]; // domains that did not fit (next refill's carried-over list)
-    int pend_off[2 * kSlots];
-    int pend_cnt[2 * kSlots];
     short cand_slot[2 * kSlots];    // placement: slot, or -1 (single-slot, parallel) / -2 (deferred)
     int nmulti_def, nfree_single;
     unsigned long long freem_single;
@@ -81,27 +77,28 @@ struct Ctl {
 
 // shared-memory carve-up (offsets from a 1024-aligned base)
 constexpr uint32_t kOffA = 0;                                        // h1 hi [0,64K) lo [64K,128K); FP64 scratch
-constexpr uint32_t kOffH2 = kOffA + 2 * kSplitA;                     // h2 hi/lo | partials out
-constexpr uint32_t kOffW2 = kOffH2 + 2 * kSplitH2;
+constexpr uint32_t kOffW2 = kOffA + 2 * kSplitA;
 constexpr uint32_t kOffW3 = kOffW2 + kW2Bytes;
 constexpr uint32_t kOffHdr = kOffW3 + kW3Bytes;                      // [8 sources] ReqHdr
 constexpr uint32_t kOffPart = kOffHdr + kClusterN * 16;              // [8 sources][16 rows][8] double
 constexpr uint32_t kOffWin = kOffPart + kClusterN * kRoundRows * 8 * 8;   // own rows' windows [128][64]
 constexpr uint32_t kOffRowG = kOffWin + kRowCap * kWin;              // [128][8] double
 constexpr uint32_t kOffRowR = kOffRowG + kRowCap * 8 * 8;            // [128] double
-constexpr uint32_t kOffRowC = kOffRowR + kRowCap * 8;                // [128] int
-constexpr uint32_t kOffB2 = kOffRowC + kRowCap * 4;                  // float [32]
+constexpr uint32_t kOffRowC = kOffA + 16384;                         // [kRowCap] int, FP64 mode only (A is scratch there)
+constexpr uint32_t kOffB2 = kOffRowR + kRowCap * 8;                  // float [kSliceN]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
-constexpr uint32_t kOffL1 = kOffB3 + 8 * 8;                          // uint16 [8 warps][64] layer-1 lists
-constexpr uint32_t kOffCtl = kOffL1 + kWarps * kWin * 2;
+constexpr uint32_t kOffCtl = kOffB3 + 8 * 8;
 constexpr uint32_t kOffBar = (kOffCtl + (uint32_t)sizeof(Ctl) + 7u) & ~7u;
 constexpr int kNumBars = 4;                                          // req, part, mma, weights
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemUsed = kOffTmem + 16;
-constexpr uint32_t kSmemTotal = kSmemUsed + 1024;
+constexpr uint32_t kSmemTotal = kSmemUsed + 128;                     // 128-B alignment slack (no-swizzle layouts)
 static_assert(kSmemTotal <= 232448, "shared memory budget");
+static_assert(kSplitH2 == (kRoundRows / 8) * kRowGroupA && kTileRows * 8 * 8 <= kSplitH2,
+              "h2 (one split per half) and the partials fit in the CTA's own row block of A");
 static_assert(kOffHdr % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
 static_assert(kRowCap <= 256, "row scan covers one element per thread");
+static_assert(kSlots <= 64, "slot threads are warps 0-1");
 
 __device__ __forceinline__ uint32_t lanemask_lt()
 {
@@ -147,7 +144,19 @@ __device__ __forceinline__ uint4 pack8(const __half (&x)[8])
     return make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]), pack_half2(x[6], x[7]));
 }
 
-// H2 (K = 32): no-swizzle K-major, column-major core matrices (LBO 2048, SBO 128)
+constexpr uint32_t kTmemDa = 2 * kSliceN;                          // layer-3 accumulators after D1, D2
+
+// does TMEM lane quadrant q (tile rows [32q, 32q+32)) hold any valid row of this round?
+__device__ __forceinline__ bool quad_has_rows(const int (&n_s)[kClusterN], int q)
+{
+    bool any = false;
+#pragma unroll
+    for (int s = 0; s < kClusterN; ++s)
+        if (n_s[s] > 0 && s * kRoundRows < 32 * q + 32 && s * kRoundRows + n_s[s] > 32 * q) any = true;
+    return any;
+}
+
+// H2 (K = kSliceN): no-swizzle K-major, column-major core matrices (LBO 2048, SBO 128)
 __device__ __forceinline__ uint32_t h2_off(int m, int k)
 {
     return (uint32_t)(k >> 3) * kCoreColH2 + (uint32_t)(m >> 3) * 128u + (uint32_t)(m & 7) * 16u + (uint32_t)(k & 7) * 2u;
@@ -159,49 +168,33 @@ __device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame
     return species[neighbour_site(F, v, o[0], o[1], o[2])];
 }
 
-// layer 1 of one row, all 256 columns (lane = columns 8*lane .. 8*lane+7): FP64 sum of b1' and the W1'
-// rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
-// row m of the A operand (M-major no-swizzle: 8-row group g at g*4096, core column c at c*128)
-__device__ __forceinline__ void layer1_row(const uint8_t* w, const float* __restrict__ W1f, uint16_t* lst, int m,
-                                           uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi, uint8_t* g_lo,
-                                           unsigned long long& ovf)
+// layer 1 of up to two rows, all 256 columns (lane = columns 8*lane .. 8*lane+7): FP64 sum of b1' and the
+// W1' rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
+// row m of the A operand (M-major no-swizzle: 8-row group g at g*4096, core column c at c*128) and into the
+// CTA's L2 staging block.  The two rows' loads are interleaved (independent latency chains).
+// non-Fe slots of a window as two ballot masks (slots 0-31, 32-63); entry e of the slot-ordered list is the
+// e-th set bit (no list is stored: the masks are warp-uniform registers)
+struct L1Masks { unsigned m0, m1; int c0, n; };
+__device__ __forceinline__ L1Masks l1_masks(const uint8_t* w)
 {
     const int lane = threadIdx.x & 31;
-    const uint32_t b0 = w[lane], b1 = w[lane + 32];
-    const unsigned m0 = __ballot_sync(0xffffffffu, b0 != (uint32_t)kFe);
-    const unsigned m1 = __ballot_sync(0xffffffffu, b1 != (uint32_t)kFe);
-    const uint32_t lt = lanemask_lt();
-    if (b0 != (uint32_t)kFe) lst[__popc(m0 & lt)] = (uint16_t)(1 + (b0 - 1) * kWin + lane);
-    if (b1 != (uint32_t)kFe) lst[__popc(m0) + __popc(m1 & lt)] = (uint16_t)(1 + (b1 - 1) * kWin + lane + 32);
-    __syncwarp();
-    const int n = __popc(m0) + __popc(m1);
-    const float4* base = reinterpret_cast<const float4*>(W1f) + 2 * lane;   // row stride 64 float4
-    double acc[8];
-    {
-        const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
-        acc[0] = x0.x; acc[1] = x0.y; acc[2] = x0.z; acc[3] = x0.w;
-        acc[4] = x1.x; acc[5] = x1.y; acc[6] = x1.z; acc[7] = x1.w;
-    }
-    for (int e = 0; e < n; e += 8) {
-        float4 xa[8], xb[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            if (e + t < n) {
-                const float4* rp = base + (size_t)lst[e + t] * (kHid / 4);
-                xa[t] = __ldg(rp);
-                xb[t] = __ldg(rp + 1);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            if (e + t < n) {
-                acc[0] = __dadd_rn(acc[0], (double)xa[t].x); acc[1] = __dadd_rn(acc[1], (double)xa[t].y);
-                acc[2] = __dadd_rn(acc[2], (double)xa[t].z); acc[3] = __dadd_rn(acc[3], (double)xa[t].w);
-                acc[4] = __dadd_rn(acc[4], (double)xb[t].x); acc[5] = __dadd_rn(acc[5], (double)xb[t].y);
-                acc[6] = __dadd_rn(acc[6], (double)xb[t].z); acc[7] = __dadd_rn(acc[7], (double)xb[t].w);
-            }
-        }
-    }
+    L1Masks r;
+    r.m0 = __ballot_sync(0xffffffffu, w[lane] != (uint8_t)kFe);
+    r.m1 = __ballot_sync(0xffffffffu, w[lane + 32] != (uint8_t)kFe);
+    r.c0 = __popc(r.m0);
+    r.n = r.c0 + __popc(r.m1);
+    return r;
+}
+__device__ __forceinline__ int l1_row_index(const uint8_t* w, const L1Masks& k, int e)
+{
+    const int slot = e < k.c0 ? (int)__fns(k.m0, 0, e + 1) : 32 + (int)__fns(k.m1, 0, e - k.c0 + 1);
+    return 1 + ((int)w[slot] - 1) * kWin + slot;
+}
+
+__device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi,
+                                         uint8_t* g_lo, unsigned long long& ovf)
+{
+    const int lane = threadIdx.x & 31;
     __half hi[8], lo[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -213,18 +206,68 @@ __device__ __forceinline__ void layer1_row(const uint8_t* w, const float* __rest
     const uint4 vh = pack8(hi), vl = pack8(lo);
     *reinterpret_cast<uint4*>(A_hi + off) = vh;
     *reinterpret_cast<uint4*>(A_lo + off) = vl;
-    // the same 16 B into the L2 staging block of this CTA (row m & 15 of its block)
-    const uint32_t goff = (uint32_t)((m & 15) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
+    // the same 16 B into the L2 staging block of this CTA (row m % kRoundRows of its block)
+    const uint32_t goff = (uint32_t)((m % kRoundRows) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
     *reinterpret_cast<uint4*>(g_hi + goff) = vh;
     *reinterpret_cast<uint4*>(g_lo + goff) = vl;
+}
+
+__device__ __forceinline__ void layer1_rows(const uint8_t* w0, const uint8_t* w1, const float* __restrict__ W1f,
+                                            int m0, int m1, uint8_t* A_hi, uint8_t* A_lo,
+                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf)
+{
+    const int lane = threadIdx.x & 31;
+    const L1Masks k0 = l1_masks(w0);
+    L1Masks k1{0u, 0u, 0, 0};
+    if (w1) k1 = l1_masks(w1);
+    const float4* base = reinterpret_cast<const float4*>(W1f) + 2 * lane;
+    double a0[8], a1[8];
+    {
+        const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
+        a0[0] = x0.x; a0[1] = x0.y; a0[2] = x0.z; a0[3] = x0.w; a0[4] = x1.x; a0[5] = x1.y; a0[6] = x1.z; a0[7] = x1.w;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a1[c] = a0[c];
+    }
+    const int nmax = k0.n > k1.n ? k0.n : k1.n;
+    for (int e = 0; e < nmax; e += 4) {
+        float4 xa[4], xb[4], ya[4], yb[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (e + t < k0.n) {
+                const float4* rp = base + (size_t)l1_row_index(w0, k0, e + t) * (kHid / 4);
+                xa[t] = __ldg(rp); xb[t] = __ldg(rp + 1);
+            }
+            if (e + t < k1.n) {
+                const float4* rp = base + (size_t)l1_row_index(w1, k1, e + t) * (kHid / 4);
+                ya[t] = __ldg(rp); yb[t] = __ldg(rp + 1);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (e + t < k0.n) {
+                a0[0] = __dadd_rn(a0[0], (double)xa[t].x); a0[1] = __dadd_rn(a0[1], (double)xa[t].y);
+                a0[2] = __dadd_rn(a0[2], (double)xa[t].z); a0[3] = __dadd_rn(a0[3], (double)xa[t].w);
+                a0[4] = __dadd_rn(a0[4], (double)xb[t].x); a0[5] = __dadd_rn(a0[5], (double)xb[t].y);
+                a0[6] = __dadd_rn(a0[6], (double)xb[t].z); a0[7] = __dadd_rn(a0[7], (double)xb[t].w);
+            }
+            if (e + t < k1.n) {
+                a1[0] = __dadd_rn(a1[0], (double)ya[t].x); a1[1] = __dadd_rn(a1[1], (double)ya[t].y);
+                a1[2] = __dadd_rn(a1[2], (double)ya[t].z); a1[3] = __dadd_rn(a1[3], (double)ya[t].w);
+                a1[4] = __dadd_rn(a1[4], (double)yb[t].x); a1[5] = __dadd_rn(a1[5], (double)yb[t].y);
+                a1[6] = __dadd_rn(a1[6], (double)yb[t].z); a1[7] = __dadd_rn(a1[7], (double)yb[t].w);
+            }
+        }
+    }
+    l1_store(a0, m0, A_hi, A_lo, g_hi, g_lo, ovf);
+    if (w1) l1_store(a1, m1, A_hi, A_lo, g_hi, g_lo, ovf);
     __syncwarp();
 }
 
 template <bool kTC>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p)
 {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     Ctl& c = *reinterpret_cast<Ctl*>(sm + kOffCtl);
     uint8_t* win = sm + kOffWin;
     double* rowG = reinterpret_cast<double*>(sm + kOffRowG);
@@ -232,9 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     int* rowC = reinterpret_cast<int*>(sm + kOffRowC);
     uint8_t* A_hi = sm + kOffA;
     uint8_t* A_lo = sm + kOffA + kSplitA;
-    uint8_t* H2_hi = sm + kOffH2;
-    uint8_t* H2_lo = sm + kOffH2 + kSplitH2;
-    double* part_out = reinterpret_cast<double*>(sm + kOffH2);      // [128][8]  (after layer 3)
     double* part_in = reinterpret_cast<double*>(sm + kOffPart);     // [8][16][8]
     ReqHdr* hdr = reinterpret_cast<ReqHdr*>(sm + kOffHdr);
     float* b2s = reinterpret_cast<float*>(sm + kOffB2);
@@ -242,16 +282,21 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffTmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint16_t* l1lst = reinterpret_cast<uint16_t*>(sm + kOffL1) + warp * kWin;
     const uint32_t rank = kTC ? cluster_rank() : 0u;
+    // h2 slice and the layer-3 partials live in this CTA's own row block of A: dead once layer 2 has
+    // completed, and no peer ever writes it (peers' multicasts target their own blocks)
+    const uint32_t own_block = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
+    uint8_t* H2_hi = sm + kOffA + own_block;
+    uint8_t* H2_lo = sm + kOffA + kSplitA + own_block;
+    double* part_out = reinterpret_cast<double*>(H2_hi);            // [128][8]  (after layer 3)
     const uint32_t bar_req = smem_u32(&bars[0]), bar_part = smem_u32(&bars[1]);
     const uint32_t bar_mma = smem_u32(&bars[2]), bar_w = smem_u32(&bars[3]);
     const bool phase_mode = (p.mode == kEnginePhase);
     const bool mlp = (p.model == 1);
     unsigned long long ovf = 0;
-    constexpr uint32_t kStageCta = 2u * 2u * kRowGroupA;            // hi + lo, 16 rows
-    uint8_t* g_hi = kTC ? p.stage + ((size_t)cluster_id() * kClusterN + rank) * kStageCta : nullptr;
-    uint8_t* g_lo = kTC ? g_hi + 2u * kRowGroupA : nullptr;
+    constexpr uint32_t kStageSplitRows = (uint32_t)(kRoundRows / 8) * kRowGroupA;   // one split of a round's rows
+    uint8_t* g_hi = kTC ? p.stage + ((size_t)cluster_id() * kClusterN + rank) * (2u * kStageSplitRows) : nullptr;
+    uint8_t* g_lo = kTC ? g_hi + kStageSplitRows : nullptr;
 
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
@@ -270,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint32_t tmem = 0;
     uint32_t ph_req = 0, ph_part = 0, ph_mma = 0;
     if (kTC) {
-        if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 128);
+        if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 256);
         if (tid < kSliceN) b2s[tid] = p.W.b2[rank * kSliceN + tid];
         if (tid < 8) b3s[tid] = p.W.b3[tid];
         tc_fence_before();
@@ -296,26 +341,37 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
     long long t_mark = t_start;
     auto lap = [&](long long& acc) { const long long t = clock64(); acc += t - t_mark; t_mark = t; };
+    // watchdog progress words (thread 0; mapped host memory, read by the host while the kernel runs)
+    auto wd = [&](int code, int a, int b) {
+        if (p.watch && tid == 0) {
+            volatile int* w = p.watch + blockIdx.x * 8;
+            w[0] = (int)d_it; w[1] = code; w[2] = a; w[3] = b; w[4] = c.nrun; w[5] = c.drained; w[6] = c.npend;
+            w[7] = p.ph ? (int)p.ph->phase : -1;
+            __threadfence_system();
+        }
+    };
 
     for (;;) {
         int own_alive = 0;
         if (phase_mode) {
             // ================= slots: release stopped domains, refill from the segment list =================
             __syncthreads();
-            if (tid < kSlots) {
+            wd(1, 0, 0);
+            if (tid < 64) {
                 // thread = slot; a slot is freed with its domain (head or continuation of a stopped head)
                 const int sl = tid;
-                const int used = c.seg_used[sl];
+                const bool real = sl < kSlots;
+                const int used = real ? c.seg_used[sl] : 3;
                 const int head = used == 2 ? c.seg_head[sl] : sl;
-                const bool rel = used != 0 && !c.seg_run[head];
+                const bool rel = real && used != 0 && !c.seg_run[head];
                 if (rel) {
 #pragma unroll
                     for (int a = 0; a < kSlotCap; ++a) c.mem_act[kSlotCap * sl + a] = 0;
                 }
-                const bool running = used == 1 && c.seg_run[sl];
+                const bool running = real && used == 1 && c.seg_run[sl];
                 __syncwarp();
                 if (rel) c.seg_used[sl] = 0;
-                c.seg_new[sl] = 0;
+                if (real) c.seg_new[sl] = 0;
                 const unsigned fm = __ballot_sync(0xffffffffu, used == 0 || rel);
                 const unsigned rm = __ballot_sync(0xffffffffu, running);
                 if (lane == 0) { c.freew[warp] = fm; c.runw[warp] = rm; }
@@ -338,13 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 }
             }
             __syncthreads();
-            if (tid < c.npend) {                           // carried-over candidates first
-                c.cand_dom[tid] = c.pend_dom[tid]; c.cand_off[tid] = c.pend_off[tid]; c.cand_cnt[tid] = c.pend_cnt[tid];
-            }
             if (c.fetch && tid < c.nnew) {
                 const Segment sg = p.segs[c.s0 + tid];
                 const int q = c.npend + tid;
-                c.cand_dom[q] = sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
+                c.cand_dom[q] = (unsigned)sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
             }
             __syncthreads();
             const int ncand = c.npend + c.nnew;
@@ -399,15 +452,20 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 const bool deferred = q < ncand && c.cand_slot[q] == -2;
                 int ndef = 0;
                 const int pi = block_excl(deferred ? 1 : 0, c.wsum, ndef);
-                if (deferred) { c.pend_dom[pi] = c.cand_dom[q]; c.pend_off[pi] = c.cand_off[q]; c.pend_cnt[pi] = c.cand_cnt[q]; }
-                if (q < ncand && c.cand_slot[q] >= 0) {
-                    const int h = c.cand_slot[q];
+                // carried-over domains are compacted in place to the front of the candidate list (read first)
+                unsigned cdom = 0;
+                int coff = 0, ccnt = 0, cslot = -3;
+                if (q < ncand) { cdom = c.cand_dom[q]; coff = c.cand_off[q]; ccnt = c.cand_cnt[q]; cslot = c.cand_slot[q]; }
+                __syncthreads();
+                if (deferred) { c.cand_dom[pi] = cdom; c.cand_off[pi] = coff; c.cand_cnt[pi] = ccnt; }
+                if (cslot >= 0) {
+                    const int h = cslot;
                     c.seg_used[h] = 1;
-                    c.seg_dom[h] = c.cand_dom[q]; c.seg_goff[h] = c.cand_off[q]; c.seg_cnt[h] = c.cand_cnt[q];
+                    c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
                     c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_run[h] = 1; c.seg_new[h] = 1;
                 }
                 int nplaced = 0;
-                block_excl((q < ncand && c.cand_slot[q] >= 0) ? 1 : 0, c.wsum, nplaced);
+                block_excl(cslot >= 0 ? 1 : 0, c.wsum, nplaced);
                 if (tid == 0) {
                     c.npend = ndef;
                     c.nrun = __popc(c.runw[0]) + __popc(c.runw[1]) + nplaced;
@@ -481,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     if (hit >= 0 && way == hit) {
                         if (k < 8) rowG[r * 8 + k] = gv[q];
                         else if (k == 8) rowR[r] = gv[q];
-                        else if (k == 9) rowC[r] = cv[q];
+                        else if (k == 9 && !kTC) rowC[r] = cv[q];
                     }
                     if (lane == 0) c.row_hit[r] = hit >= 0 ? 1 : 0;
                 }
@@ -494,6 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             if (tid == 0) { c.nmiss = total; c.mrows += (unsigned long long)total; }
             __syncthreads();
+            wd(3, c.nrows, c.nmiss);
         }
         if (tid == 0) { lap(d_x[2]); ++d_it; }
 
@@ -583,16 +642,27 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 int own_n = 0;
                 if (phase_mode) {
                     own_n = min(kRoundRows, max(0, c.nmiss - kRoundRows * k_round));
-                    // layer 1 of this round's own rows; memo way 1 <- way 0, way 0 key <- window
-                    for (int i = warp; i < own_n; i += kWarps) {
-                        const int r = c.miss[kRoundRows * k_round + i];
-                        MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
-                        uint4 t = make_uint4(0, 0, 0, 0);
-                        if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
-                        layer1_row(win + r * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, g_hi, g_lo, ovf);
-                        if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
+                    // layer 1 of this round's own rows (two per warp at a time); memo way 1 <- way 0, key <- window
+                    for (int i = warp; i < own_n; i += 2 * kWarps) {
+                        const int i1 = i + kWarps;
+                        const bool two = i1 < own_n;
+                        const int r0 = c.miss[kRoundRows * k_round + i];
+                        const int r1 = two ? c.miss[kRoundRows * k_round + i1] : r0;
+                        MemoEntry* me0 = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r0]];
+                        MemoEntry* me1 = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r1]];
+                        uint4 t0 = make_uint4(0, 0, 0, 0), t1 = make_uint4(0, 0, 0, 0);
+                        if (lane < 9) { t0 = reinterpret_cast<const uint4*>(&me0[0])[lane]; t1 = reinterpret_cast<const uint4*>(&me1[0])[lane]; }
+                        layer1_rows(win + r0 * kWin, two ? win + r1 * kWin : nullptr, p.W.W1f,
+                                    kRoundRows * (int)rank + i, kRoundRows * (int)rank + i1, A_hi, A_lo, g_hi, g_lo, ovf);
+                        if (lane < 9) {
+                            reinterpret_cast<uint4*>(&me0[1])[lane] = t0;
+                            if (two) reinterpret_cast<uint4*>(&me1[1])[lane] = t1;
+                        }
                         __syncwarp();
-                        if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
+                        if (lane < 16) {
+                            reinterpret_cast<uint32_t*>(me0[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r0 * kWin)[lane];
+                            if (two) reinterpret_cast<uint32_t*>(me1[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r1 * kWin)[lane];
+                        }
                     }
                     if (tid == 0) {
                         hdr[rank].n = own_n;
@@ -617,12 +687,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             win[i * kWin + lane] = site_byte(p.species, p.F, v, p.G.off[lane]);
                             win[i * kWin + lane + 32] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
                         }
-                        __syncwarp();
-                        layer1_row(win + i * kWin, p.W.W1f, l1lst, kRoundRows * (int)rank + i, A_hi, A_lo, g_hi, g_lo, ovf);
+                    }
+                    __syncwarp();
+                    for (int i = warp; i < own_n; i += 2 * kWarps) {
+                        const int i1 = i + kWarps;
+                        const bool two = i1 < own_n;
+                        layer1_rows(win + i * kWin, two ? win + i1 * kWin : nullptr, p.W.W1f,
+                                    kRoundRows * (int)rank + i, kRoundRows * (int)rank + i1, A_hi, A_lo, g_hi, g_lo, ovf);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
                 }
-                // ---- exchange: header (DSMEM) + this CTA's h1 rows (8-row groups 2r, 2r+1), multicast from the
+                wd(4, k_round, own_n);
+                // ---- exchange: header (DSMEM) + this CTA's h1 rows (8-row groups 4r..4r+3), multicast from the
                 //      L2 staging copy into every peer's A (one L2 read, no SM-to-SM bandwidth limit)
                 fence_async_smem();
                 fence_async_global();
@@ -634,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     if (d == rank) {
                         mbar_arrive(bar_req);
                         if (rg) {
-                            const uint32_t aoff = 2u * rank * kRowGroupA;
+                            const uint32_t aoff = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
                             const uint16_t mask = (uint16_t)(((1u << kClusterN) - 1u) & ~(1u << rank));
                             bulk_g2s_multicast(smem_u32(A_hi + aoff), g_hi, rg * kRowGroupA, bar_req, mask);
                             bulk_g2s_multicast(smem_u32(A_lo + aoff), g_lo, rg * kRowGroupA, bar_req, mask);
@@ -648,6 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 }
                 mbar_wait_cluster(bar_req, ph_req);
                 ph_req ^= 1u;
+                wd(5, k_round, own_n);
                 if (tid == 0) { const long long before = d_x[4]; lap(d_x[4]); if (k_round > 0) d_xk += d_x[4] - before; }
                 int n_s[kClusterN];
                 int any_more = 0, any_alive = 0, total = 0;
@@ -660,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 }
                 if (k_round == 0 && !any_alive) all_dead = true;
                 if (total > 0) {
-                    // ---- L2 on tcgen05: D1 (TMEM cols 0-31), D2 (cols 32-63)
+                    // ---- L2 on tcgen05: D1 (TMEM cols [0, 64)), D2 (cols [64, 128))
                     tc_fence_before();
                     __syncthreads();
                     tc_fence_after();
@@ -673,39 +750,43 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             const uint64_t dbh = umma_desc(wb + (uint32_t)ks * 2u * kW2Split, (kSliceN / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(wb + (uint32_t)ks * 2u * kW2Split + kW2Split, (kSliceN / 8) * 128, 128);
                             umma_f16(tmem + 0, dah, dbh, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + 32, dah, dbl, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + 32, dal, dbh, idesc, 1u);
+                            umma_f16(tmem + kSliceN, dah, dbl, idesc, ks > 0 ? 1u : 0u);
+                            umma_f16(tmem + kSliceN, dal, dbh, idesc, 1u);
                         }
                         umma_commit(bar_mma);
                     }
                     mbar_wait(bar_mma, ph_mma);
                     ph_mma ^= 1u;
                     tc_fence_after();
-                    // ---- E2: h2 slice -> H2 (fp16 split, K = 32)
+                    // ---- E2: h2 slice -> H2 (fp16 split, K = 64); warp = (TMEM lane quadrant, 32-column half)
                     {
                         const int q4 = warp & 3, hc = warp >> 2;
-                        if (n_s[2 * q4] > 0 || n_s[2 * q4 + 1] > 0) {
-                            uint32_t d1[16], d2[16];
+                        if (quad_has_rows(n_s, q4)) {
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-                            tmem_ld16(tl + (uint32_t)(16 * hc), d1);
-                            tmem_ld16(tl + (uint32_t)(32 + 16 * hc), d2);
-                            tmem_wait_ld();
                             const int m = 32 * q4 + lane;
                             const float inv = 1.0f / kLo;
 #pragma unroll
-                            for (int g = 0; g < 2; ++g) {
-                                __half hi[8], lo[8];
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const int c0 = 32 * hc + 16 * hh;
+                                uint32_t d1[16], d2[16];
+                                tmem_ld16(tl + (uint32_t)c0, d1);
+                                tmem_ld16(tl + (uint32_t)(kSliceN + c0), d2);
+                                tmem_wait_ld();
 #pragma unroll
-                                for (int t = 0; t < 8; ++t) {
-                                    const int cl = 16 * hc + 8 * g + t;
-                                    float z = __fmaf_rn(__uint_as_float(d2[8 * g + t]), inv, __uint_as_float(d1[8 * g + t]));
-                                    z = __fmaf_rn(z, p.W.s2u, b2s[cl]);
-                                    z = z > 0.0f ? z : 0.0f;
-                                    split_h(z, hi[t], lo[t], ovf);
+                                for (int g = 0; g < 2; ++g) {
+                                    __half hi[8], lo[8];
+#pragma unroll
+                                    for (int t = 0; t < 8; ++t) {
+                                        const int cl = c0 + 8 * g + t;
+                                        float z = __fmaf_rn(__uint_as_float(d2[8 * g + t]), inv, __uint_as_float(d1[8 * g + t]));
+                                        z = __fmaf_rn(z, p.W.s2u, b2s[cl]);
+                                        z = z > 0.0f ? z : 0.0f;
+                                        split_h(z, hi[t], lo[t], ovf);
+                                    }
+                                    const uint32_t off = h2_off(m, c0 + 8 * g);
+                                    *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
+                                    *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
                                 }
-                                const uint32_t off = h2_off(m, 16 * hc + 8 * g);
-                                *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
-                                *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
                             }
                         }
                     }
@@ -714,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     __syncthreads();
                     tc_fence_after();
                     if (tid == 0) lap(d_x[5]);
-                    // ---- L3 on tcgen05: partial outputs of this CTA's 32 h2 columns, Da (64-79), Db (80-95)
+                    // ---- L3 on tcgen05: partial outputs of this CTA's 64 h2 columns, Da / Db in TMEM
                     if (tid == 0) {
                         const uint32_t idesc = idesc_f16(kTileRows, 16);
                         const uint32_t hh = smem_u32(H2_hi), hl = smem_u32(H2_lo), w3 = smem_u32(sm + kOffW3);
@@ -723,9 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             const uint64_t dal = umma_desc(hl + (uint32_t)ks * 2u * kCoreColH2, kCoreColH2, 128);
                             const uint64_t dbh = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split, (16 / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split + kW3Split, (16 / 8) * 128, 128);
-                            umma_f16(tmem + 64, dah, dbh, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + 80, dah, dbl, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + 80, dal, dbh, idesc, 1u);
+                            umma_f16(tmem + kTmemDa, dah, dbh, idesc, ks > 0 ? 1u : 0u);
+                            umma_f16(tmem + kTmemDa + 16, dah, dbl, idesc, ks > 0 ? 1u : 0u);
+                            umma_f16(tmem + kTmemDa + 16, dal, dbh, idesc, 1u);
                         }
                         umma_commit(bar_mma);
                     }
@@ -734,11 +815,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     tc_fence_after();
                     if (warp < 4) {
                         const int q4 = warp;
-                        if (n_s[2 * q4] > 0 || n_s[2 * q4 + 1] > 0) {
+                        if (quad_has_rows(n_s, q4)) {
                             uint32_t da[8], db[8];
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-                            tmem_ld8(tl + 64u, da);
-                            tmem_ld8(tl + 80u, db);
+                            tmem_ld8(tl + (uint32_t)kTmemDa, da);
+                            tmem_ld8(tl + (uint32_t)(kTmemDa + 16), db);
                             tmem_wait_ld();
                             const int m = 32 * q4 + lane;
                             double pv[8];
@@ -766,8 +847,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                         smem_u32(part_out + s * kRoundRows * 8), bytes, cb);
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                    wd(6, k_round, own_n);
                     mbar_wait_cluster(bar_part, ph_part);
                     ph_part ^= 1u;
+                    wd(7, k_round, own_n);
                     if (tid == 0) lap(d_x[6]);
                     // ---- E3 for this CTA's own rows: thread (row i, hop k)
                     if (tid < kRoundRows * 8) {
@@ -791,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                 rowG[r * 8 + k] = Gk;
                                 MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                                 me[0].G[k] = Gk;
-                                if (k == 0) { rowR[r] = R; rowC[r] = 0; me[0].R = R; me[0].clamps = 0; }
+                                if (k == 0) { rowR[r] = R; me[0].R = R; me[0].clamps = 0; }
                             } else {
                                 const int g = c.ebase + i;
                                 const int slot = p.windows ? g : (p.rows ? p.rows[g] : g);
@@ -818,6 +901,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 
         // ================= BKL step per running domain (thread per head slot) =================
         __syncthreads();
+        wd(9, 0, 0);
         if (tid == 0) lap(d_cr);
         if (tid < kSlots && c.seg_used[tid] == 1 && c.seg_run[tid]) {
             const int i = tid;
@@ -833,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 if (c.mem_act[moff + a]) {
                     const int r = c.mem_row[moff + a];
                     buf[m] = rowR[r];
-                    cl += (unsigned long long)rowC[r];
+                    if (!kTC) cl += (unsigned long long)rowC[r];
                     idx[m] = a;
                     ++m;
                 }
@@ -876,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         long long d2;
                         int sec2;
                         dom_sector(nv, p.S, d2, sec2);
-                        if (d2 != c.seg_dom[i] || sec2 != p.ph->sector) c.mem_act[moff + a] = 0;
+                        if (d2 != (long long)c.seg_dom[i] || sec2 != p.ph->sector) c.mem_act[moff + a] = 0;
                         if (p.S.log) {
                             if (near_face(p.F, ov.y, ov.z, ov.w))
                                 log_entry(p.S.log, p.S.nlog, p.S.logcap, ov.y, ov.z, ov.w, tn);
@@ -922,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 
     // ---- teardown
     if (ovf && p.overflow) atomicAdd(p.overflow, ovf);
-    if (phase_mode && tid < kSlots) {
+    if (phase_mode && tid < 64) {                 // whole warps (slot threads are tid < kSlots <= 64)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             my_events += __shfl_xor_sync(0xffffffffu, my_events, o);
@@ -943,7 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         cluster_sync();
         if (warp == 2) {
             tc_fence_after();
-            tmem_dealloc(tmem, 128);
+            tmem_dealloc(tmem, 256);
         }
     }
 }

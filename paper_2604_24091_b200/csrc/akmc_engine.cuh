@@ -7,17 +7,17 @@
 // grid-synchronous inner loop pays one full barrier-network latency per event of the slowest domain.
 // Here every CTA owns a handful of domains and iterates them independently; the 8 CTAs of a cluster
 // share one barrier-network evaluator whose weights stay resident in shared memory (each CTA holds a
-// 32-column slice of W2 and W3), and results are memoised per vacancy (exact: the rates are a pure
+// 64-column slice of W2 and the matching 64 rows of W3), and results are memoised per vacancy (exact: the rates are a pure
 // function of the 64-byte window).
 #pragma once
 #include "akmc_kernels.cuh"
 
 namespace akmc {
 
-constexpr int kClusterN = 8;                   // CTAs per cluster; CTA r owns hidden columns [32r, 32r+32)
-constexpr int kSliceN = kHid / kClusterN;      // 32
-constexpr int kRoundRows = 16;                 // rows a CTA contributes per evaluation round (tile M = 128)
-constexpr int kSlots = 64;                     // domain slots per CTA (a domain with > 2 vacancies spans several)
+constexpr int kClusterN = 4;                   // CTAs per cluster; CTA r owns hidden columns [64r, 64r+64)
+constexpr int kSliceN = kHid / kClusterN;      // 64
+constexpr int kRoundRows = 128 / kClusterN;    // rows a CTA contributes per evaluation round (tile M = 128)
+constexpr int kSlots = 48;                     // domain slots per CTA (a domain with > 2 vacancies spans several)
 constexpr int kSlotCap = 2;                    // vacancies per slot
 constexpr int kRowCap = kSlots * kSlotCap;     // vacancies a CTA holds at once (128)
 constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
@@ -34,8 +34,8 @@ static_assert(sizeof(MemoEntry) == 144, "memo entry layout");
 
 struct EngineWeights {
     const float* W1f;       // [385][256] FP32: row 0 = b1' = b1 + sum_slot W1[slot,Fe]; row 1+(s-1)*64+slot = W1'
-    const uint8_t* W2img;   // [8 CTAs][16 K-steps][hi 1 KiB | lo 1 KiB] fp16 UMMA images of W2^T slices * 2^s2
-    const uint8_t* W3img;   // [8 CTAs][2 K-steps][hi 512 B | lo 512 B] of W3 rows [32r,32r+32) (N padded 16) * 2^s3
+    const uint8_t* W2img;   // [4 CTAs][16 K-steps][hi 2 KiB | lo 2 KiB] fp16 UMMA images of W2^T column slices * 2^s2
+    const uint8_t* W3img;   // [4 CTAs][4 K-steps][hi 512 B | lo 512 B] of W3 rows [64r,64r+64) (N padded 16) * 2^s3
     const float* b2;        // [256]
     const double* b3;       // [8]
     float s2u;              // 2^-s2
@@ -72,9 +72,10 @@ struct EngineParams {
     double* Rsum;
     double* E;
     EngineWeights W;
-    uint8_t* stage;         // [clusters][8 CTAs][hi 8 KiB | lo 8 KiB] h1 rows staged in L2 for the multicast
+    uint8_t* stage;         // [clusters][4 CTAs][hi | lo] h1 rows staged in L2 for the multicast
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
+    int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)
 };
 
 size_t engine_smem_bytes();

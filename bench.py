@@ -373,6 +373,7 @@ def run_ours(args):
 
 
 def main():
+    os.environ.pop("NCCL_DEBUG", None)              # keep NCCL's version banner off stdout (one JSON line)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

@@ -569,7 +569,9 @@ int init_multi(akmc_handle* h)
     ncclUniqueId id;
     static_assert(sizeof(ncclUniqueId) <= sizeof(c.nccl_id), "nccl id size");
     std::memcpy(&id, c.nccl_id, sizeof(id));
+    const auto tv0 = std::chrono::steady_clock::now();
     NCK(h, ncclCommInitRank(&h->comm, c.world, id, c.rank));
+    const auto tv1 = std::chrono::steady_clock::now();
     // peers: distinct ranks at the 26 neighbour offsets along decomposed (non-wrap) axes
     int np = 0;
     for (int dz = -1; dz <= 1; ++dz)
@@ -646,7 +648,14 @@ int init_multi(akmc_handle* h)
     for (int64_t i = 0; i < h->nvac; ++i)
         gid[(size_t)i] = (int)(std::lower_bound(all.begin(), all.end(), mine[(size_t)i]) - all.begin());
     if (h->nvac) CK(h, cudaMemcpy(h->d_gid, gid.data(), (size_t)h->nvac * sizeof(int), cudaMemcpyHostToDevice));
-    return halo_fill(h);
+    const auto tv2 = std::chrono::steady_clock::now();
+    const int rc = halo_fill(h);
+    const auto tv3 = std::chrono::steady_clock::now();
+    if (std::getenv("AKMC_VERBOSE"))
+        std::fprintf(stderr, "[akmc init_multi rank %d] comm init %.3f s, ids %.3f s, halo fill %.3f s\n", c.rank,
+                     std::chrono::duration<double>(tv1 - tv0).count(), std::chrono::duration<double>(tv2 - tv1).count(),
+                     std::chrono::duration<double>(tv3 - tv2).count());
+    return rc;
 }
 
 } // namespace

@@ -684,8 +684,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         } else {
                             const int slot = p.rows ? p.rows[g] : g;
                             const int4 v = p.vac[slot];
-                            win[i * kWin + lane] = site_byte(p.species, p.F, v, p.G.off[lane]);
-                            win[i * kWin + lane + 32] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
+                            const bool live = v.x >= 0;                 // departed slot (multi-rank): any window
+                            win[i * kWin + lane] = live ? site_byte(p.species, p.F, v, p.G.off[lane]) : (uint8_t)kFe;
+                            win[i * kWin + lane + 32] = live ? site_byte(p.species, p.F, v, p.G.off[lane + 32]) : (uint8_t)kFe;
                         }
                     }
                     __syncwarp();

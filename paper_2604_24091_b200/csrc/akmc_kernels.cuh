@@ -51,7 +51,13 @@ static __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, con
             for (int j = 0; j < kWin; ++j) w[j] = windows[(size_t)g * kWin + j];
         } else {
             slot = rows ? rows[g] : g;
-            gather_window(species, F, G, vac[slot], w);
+            const int4 v = vac[slot];
+            if (v.x < 0) {                               // departed slot (multi-rank): nothing to evaluate
+#pragma unroll
+                for (int j = 0; j < kWin; ++j) w[j] = kFe;
+            } else {
+                gather_window(species, F, G, v, w);
+            }
         }
         double R = 0.0;
 #pragma unroll
@@ -100,7 +106,7 @@ static __global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
                 w[j] = windows[(size_t)g * kWin + j];
             } else {
                 const int4 v = vac[slot];
-                w[j] = __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
+                w[j] = v.x < 0 ? (uint8_t)kFe : __ldg(species + neighbour_site(F, v, G.off[j][0], G.off[j][1], G.off[j][2]));
             }
         }
         __syncthreads();

@@ -54,7 +54,7 @@ enum { AKMC_MODEL_PAIR = 0, AKMC_MODEL_MLP = 1 };
 enum { AKMC_PREC_FP64 = 0, AKMC_PREC_FP32 = 1 };
 
 typedef struct akmc_config {
-    int32_t  cells[3];        /* Lx,Ly,Lz bcc cells per voxel; each even and >= 4            */
+    int32_t  cells[3];        /* Lx,Ly,Lz bcc cells per voxel; each even, >= 4 and <= 4096   */
     int32_t  n_voxels;        /* >= 1 independent periodic voxels                          */
     int32_t  n_species;       /* must be 7 (A6); vacancy code 6                                    */
     int32_t  barrier_model;   /* AKMC_MODEL_PAIR or AKMC_MODEL_MLP        */

@@ -241,8 +241,10 @@ void free_all(akmc_handle* h)
 
 int validate(const akmc_config* c, const double* eps, const double* E0, const double* mlp, std::string& why)
 {
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < 3; ++a) {
         if (c->cells[a] < 4 || (c->cells[a] & 1)) { why = "cells must be even and >= 4 (S:30)"; return AKMC_ERR_INVALID; }
+        if (c->cells[a] > 4096) { why = "cells must be <= 4096 per axis (32-bit brick index)"; return AKMC_ERR_INVALID; }
+    }
     if (c->n_voxels < 1) { why = "n_voxels must be >= 1"; return AKMC_ERR_INVALID; }
     if (c->n_species != kSpecies) { why = "n_species must be 7 (Fe Cu Ni Mn Si P V)"; return AKMC_ERR_INVALID; }
     if (!(c->temperature_K > 0.0) || !std::isfinite(c->temperature_K)) { why = "temperature must be > 0 (S:154)"; return AKMC_ERR_INVALID; }

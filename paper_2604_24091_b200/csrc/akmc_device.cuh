@@ -136,9 +136,10 @@ __device__ __forceinline__ int wrap2(int p, int twoL) { return p < 0 ? p + twoL 
 __device__ __forceinline__ int64_t site_of(const Frame& F, int vox, int px, int py, int pz)
 {
     const int cx = (px >> 1) + kHalo, cy = (py >> 1) + kHalo, cz = (pz >> 1) + kHalo;
-    const int64_t brick = (int64_t)(cx >> 2) + (int64_t)F.NB[0] * ((int64_t)(cy >> 2) + (int64_t)F.NB[1] * (int64_t)(cz >> 2));
+    // brick index < 2^25 for any allowed block (32-bit math); only the byte offset needs 64 bits
+    const uint32_t brick = (uint32_t)(cx >> 2) + (uint32_t)F.NB[0] * ((uint32_t)(cy >> 2) + (uint32_t)F.NB[1] * (uint32_t)(cz >> 2));
     const int inb = ((((cz & 3) << 2) | (cy & 3)) << 3) | ((cx & 3) << 1) | (px & 1);
-    return (int64_t)vox * F.sites + (brick << 7) + inb;
+    return (int64_t)vox * F.sites + ((int64_t)brick << 7) + inb;
 }
 
 // window site of an owned vacancy: no wrap needed, the halo holds the periodic images

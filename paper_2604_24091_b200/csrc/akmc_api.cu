@@ -1169,8 +1169,10 @@ static int step_sublattice(akmc_handle* h, int64_t n)
         } else {
             for (int q = 0; q < 8; ++q) {
                 CK(h, cudaGraphLaunch(h->phase_exec[q], h->stream));
+                watchdog_wait(h, "phase graph");
                 const int rc = exchange_deltas(h);
                 if (rc != AKMC_OK) return rc;
+                watchdog_wait(h, "exchange");
             }
             add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, h->stream>>>(h->d_clock, h->nvox, h->cfg.window_s);
             CK(h, cudaGetLastError());

@@ -72,6 +72,7 @@ struct Ctl {
     uint8_t mem_act[kRowCap];
     uint8_t mem_seg[kRowCap];       // head slot of the member's domain
     uint8_t row_hit[kRowCap];
+    uint8_t row_way[kRowCap];       // memo way that holds the row's current rates (read by the selection)
     unsigned long long events, evals, mrows, clamps;
 };
 
@@ -82,8 +83,7 @@ constexpr uint32_t kOffW3 = kOffW2 + kW2Bytes;
 constexpr uint32_t kOffHdr = kOffW3 + kW3Bytes;                      // [8 sources] ReqHdr
 constexpr uint32_t kOffPart = kOffHdr + kClusterN * 16;              // [8 sources][16 rows][8] double
 constexpr uint32_t kOffWin = kOffPart + kClusterN * kRoundRows * 8 * 8;   // own rows' windows [128][64]
-constexpr uint32_t kOffRowG = kOffWin + kRowCap * kWin;              // [128][8] double
-constexpr uint32_t kOffRowR = kOffRowG + kRowCap * 8 * 8;            // [128] double
+constexpr uint32_t kOffRowR = kOffWin + kRowCap * kWin;              // [kRowCap] double (a row's 8 rates stay in the memo)
 constexpr uint32_t kOffRowC = kOffA + 16384;                         // [kRowCap] int, FP64 mode only (A is scratch there)
 constexpr uint32_t kOffB2 = kOffRowR + kRowCap * 8;                  // float [kSliceN]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
@@ -270,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint8_t* sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     Ctl& c = *reinterpret_cast<Ctl*>(sm + kOffCtl);
     uint8_t* win = sm + kOffWin;
-    double* rowG = reinterpret_cast<double*>(sm + kOffRowG);
     double* rowR = reinterpret_cast<double*>(sm + kOffRowR);
     int* rowC = reinterpret_cast<int*>(sm + kOffRowC);
     uint8_t* A_hi = sm + kOffA;
@@ -537,11 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     const unsigned eq = __ballot_sync(0xffffffffu, ww == kw[q]);
                     const int hit = (eq & 0xFFFFu) == 0xFFFFu ? 0 : ((eq >> 16) == 0xFFFFu ? 1 : -1);
                     if (hit >= 0 && way == hit) {
-                        if (k < 8) rowG[r * 8 + k] = gv[q];
-                        else if (k == 8) rowR[r] = gv[q];
+                        if (k == 8) rowR[r] = gv[q];
                         else if (k == 9 && !kTC) rowC[r] = cv[q];
                     }
-                    if (lane == 0) c.row_hit[r] = hit >= 0 ? 1 : 0;
+                    if (lane == 0) { c.row_hit[r] = hit >= 0 ? 1 : 0; c.row_way[r] = hit > 0 ? 1 : 0; }
                 }
             }
             __syncthreads();
@@ -561,10 +559,24 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (!kTC) {
             if (!own_alive) break;
             const int nmiss = c.nmiss;
+            // memo insert, part 1: way 1 <- way 0, way 0 key <- window (the evaluator fills way 0's rates)
+            for (int q = warp; q < nmiss; q += kWarps) {
+                const int r = c.miss[q];
+                MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
+                uint4 t = make_uint4(0, 0, 0, 0);
+                if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
+                __syncwarp();
+                if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
+                __syncwarp();
+                if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
+                if (lane == 0) c.row_way[r] = 0;
+            }
+            __syncthreads();
             if (!mlp) {
                 for (int q = tid; q < nmiss; q += kThreads) {
                     const int r = c.miss[q];
                     const uint8_t* w = win + r * kWin;
+                    MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                     double R = 0.0;
                     int cl = 0;
                     for (int k = 0; k < kHops; ++k) {
@@ -574,10 +586,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             Gk = arrhenius(E, p.P);
                         }
                         R = __dadd_rn(R, Gk);
-                        rowG[r * 8 + k] = Gk;
+                        me[0].G[k] = Gk;
                     }
                     rowR[r] = R;
                     rowC[r] = cl;
+                    me[0].R = R;
+                    me[0].clamps = cl;
                 }
             } else {
                 double* h1 = reinterpret_cast<double*>(sm + kOffA);
@@ -608,33 +622,22 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     }
                     __syncthreads();
                     if (j == 0) {
+                        MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                         double R = 0.0;
                         for (int k = 0; k < kHops; ++k) {
                             const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], p.P) : 0.0;
                             R = __dadd_rn(R, Gk);
-                            rowG[r * 8 + k] = Gk;
+                            me[0].G[k] = Gk;
                         }
                         rowR[r] = R;
                         rowC[r] = 0;
+                        me[0].R = R;
+                        me[0].clamps = 0;
                     }
                     __syncthreads();
                 }
             }
             __syncthreads();
-            // memo insert: way 1 <- way 0, way 0 <- (window, rates)
-            for (int q = warp; q < nmiss; q += kWarps) {
-                const int r = c.miss[q];
-                MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
-                uint4 t = make_uint4(0, 0, 0, 0);
-                if (lane < 9) t = reinterpret_cast<const uint4*>(&me[0])[lane];
-                __syncwarp();
-                if (lane < 9) reinterpret_cast<uint4*>(&me[1])[lane] = t;
-                __syncwarp();
-                if (lane < 16) reinterpret_cast<uint32_t*>(me[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
-                else if (lane < 24) me[0].G[lane - 16] = rowG[r * 8 + lane - 16];
-                else if (lane == 24) me[0].R = rowR[r];
-                else if (lane == 25) me[0].clamps = rowC[r];
-            }
         } else {
             // ---- FP32-equivalent evaluator: rounds in lockstep over the cluster
             int k_round = 0;
@@ -872,10 +875,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         for (int kk = 0; kk < 8; ++kk) R = __dadd_rn(R, __shfl_sync(0xffffffffu, Gk, (lane & ~7) + kk));
                         if (valid) {
                             if (phase_mode) {
-                                rowG[r * 8 + k] = Gk;
                                 MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
                                 me[0].G[k] = Gk;
-                                if (k == 0) { rowR[r] = R; me[0].R = R; me[0].clamps = 0; }
+                                if (k == 0) { rowR[r] = R; c.row_way[r] = 0; me[0].R = R; me[0].clamps = 0; }
                             } else {
                                 const int g = c.ebase + i;
                                 const int slot = p.windows ? g : (p.rows ? p.rows[g] : g);
@@ -946,7 +948,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const int a = idx[leaf];
                         const int slot = c.mem_slot[moff + a];
                         const int r = c.mem_row[moff + a];
-                        const int k = pick_hop(rowG + (size_t)r * 8, rr);
+                        const MemoEntry& mrow = p.memo[2 * (size_t)slot + c.row_way[r]];   // the row's rates
+                        const int k = pick_hop(mrow.G, rr);
                         // hop: the target's species is window slot k (1NN slots are 0..7)
                         const int4 ov = c.mem_vac[moff + a];
                         int4 nv = ov;

@@ -160,6 +160,7 @@ struct akmc_handle {
     unsigned int* d_cursor = nullptr;
     uint8_t* d_stage = nullptr;       // [clusters][8][16 KiB] L2 staging of h1 rows (multicast)
     uint8_t* d_canon = nullptr;       // canonical-order lattice for akmc_state readbacks (lazy)
+    uint8_t* d_wstore = nullptr;      // engine: per-CTA window scratch
     int* h_watch = nullptr;           // AKMC_WATCHDOG: engine progress words (mapped host memory)
     int* d_watch = nullptr;
     int profile = 0;
@@ -221,7 +222,7 @@ void free_all(akmc_handle* h)
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
                     h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
-                    h->d_stage, h->d_canon};
+                    h->d_stage, h->d_canon, h->d_wstore};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -436,6 +437,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
     p.stage = h->d_stage;
+    p.wstore = h->d_wstore;
     p.watch = h->d_watch;
     p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
     return p;
@@ -859,6 +861,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     {
         const int ncl = std::max(h->n_clusters, 1) + 1;
         CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
+        CKI(cudaMalloc(&h->d_wstore, (size_t)std::max(h->num_sms, ncl * kClusterN) * kRowCap * kWin));
     }
     if (h->sub) {
         CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));

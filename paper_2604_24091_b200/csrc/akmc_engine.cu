@@ -44,6 +44,8 @@ constexpr float kLo = 2048.0f;
 
 struct ReqHdr { int n, more, alive, pad; };
 
+constexpr int kMaskWords = (kSlots + 31) / 32;
+
 struct Ctl {
     unsigned seg_dom[kSlots];       // domain ids are < 2^32 (checked at init)
     double seg_t[kSlots];
@@ -59,9 +61,10 @@ struct Ctl {
     int cand_cnt[2 * kSlots];
     short cand_slot[2 * kSlots];    // placement: slot, or -1 (single-slot, parallel) / -2 (deferred)
     int nmulti_def, nfree_single;
-    unsigned long long freem_single;
+    unsigned frees[kMaskWords];     // free slots left for single-slot domains, and their prefix counts
+    int fpre[kMaskWords + 1];
     int npend, nnew, fetch, drained, ntot, s0;
-    unsigned freew[2], runw[2];
+    unsigned freew[kMaskWords], runw[kMaskWords];
     int nrows, nmiss, nrun, ebase;
     int wsum[kWarps];
     int4 mem_vac[kRowCap];          // positions of the held vacancies (this CTA is their only writer)
@@ -82,8 +85,8 @@ constexpr uint32_t kOffW2 = kOffA + 2 * kSplitA;
 constexpr uint32_t kOffW3 = kOffW2 + kW2Bytes;
 constexpr uint32_t kOffHdr = kOffW3 + kW3Bytes;                      // [8 sources] ReqHdr
 constexpr uint32_t kOffPart = kOffHdr + kClusterN * 16;              // [8 sources][16 rows][8] double
-constexpr uint32_t kOffWin = kOffPart + kClusterN * kRoundRows * 8 * 8;   // own rows' windows [128][64]
-constexpr uint32_t kOffRowR = kOffWin + kRowCap * kWin;              // [kRowCap] double (a row's 8 rates stay in the memo)
+constexpr uint32_t kOffWin = kOffPart + kClusterN * kRoundRows * 8 * 8;   // rows' 1NN window bytes [kRowCap][8]
+constexpr uint32_t kOffRowR = kOffWin + kRowCap * 8;                 // [kRowCap] double (a row's 8 rates stay in the memo)
 constexpr uint32_t kOffRowC = kOffA + 16384;                         // [kRowCap] int, FP64 mode only (A is scratch there)
 constexpr uint32_t kOffB2 = kOffRowR + kRowCap * 8;                  // float [kSliceN]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
@@ -98,7 +101,7 @@ static_assert(kSplitH2 == (kRoundRows / 8) * kRowGroupA && kTileRows * 8 * 8 <= 
               "h2 (one split per half) and the partials fit in the CTA's own row block of A");
 static_assert(kOffHdr % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
 static_assert(kRowCap <= 256, "row scan covers one element per thread");
-static_assert(kSlots <= 64, "slot threads are warps 0-1");
+static_assert(kSlots <= kThreads && 2 * kSlots <= kThreads, "slot and candidate threads fit the CTA");
 
 __device__ __forceinline__ uint32_t lanemask_lt()
 {
@@ -269,7 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     Ctl& c = *reinterpret_cast<Ctl*>(sm + kOffCtl);
-    uint8_t* win = sm + kOffWin;
+    // full 64-byte windows of the held rows live in a per-CTA global scratch (L1/L2-resident); shared memory
+    // keeps the 8 first-shell bytes the rates mask and the hop need
+    uint8_t* win = p.wstore + (size_t)blockIdx.x * kRowCap * kWin;
+    uint8_t* win8 = sm + kOffWin;
     double* rowR = reinterpret_cast<double*>(sm + kOffRowR);
     int* rowC = reinterpret_cast<int*>(sm + kOffRowC);
     uint8_t* A_hi = sm + kOffA;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             // ================= slots: release stopped domains, refill from the segment list =================
             __syncthreads();
             wd(1, 0, 0);
-            if (tid < 64) {
+            if (tid < 32 * kMaskWords) {
                 // thread = slot; a slot is freed with its domain (head or continuation of a stopped head)
                 const int sl = tid;
                 const bool real = sl < kSlots;
@@ -377,9 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             if (tid == 0) {
-                const unsigned long long freem = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
-                const int nfree = __popcll(freem);
-                const int nrun0 = __popc(c.runw[0]) + __popc(c.runw[1]);
+                int nfree = 0, nrun0 = 0;
+#pragma unroll
+                for (int w = 0; w < kMaskWords; ++w) { nfree += __popc(c.freew[w]); nrun0 += __popc(c.runw[w]); }
                 c.fetch = 0;
                 c.nnew = 0;
                 if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
@@ -404,30 +410,33 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (tid < ncand) c.cand_slot[tid] = -1;
             const int any_multi = __syncthreads_or(multi ? 1 : 0);
             if (tid == 0) {
-                c.freem_single = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
-                c.nfree_single = __popcll(c.freem_single);
-            }
-            if (tid == 0 && any_multi) {
-                // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
-                // single-slot domains are placed in parallel below
-                unsigned long long freem = ((unsigned long long)c.freew[1] << 32) | c.freew[0];
-                int nd = 0;
-                for (int q = 0; q < ncand; ++q) {
-                    const int cnt = c.cand_cnt[q];
-                    if (cnt <= kSlotCap) continue;
-                    if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
-                    const int need = (cnt + kSlotCap - 1) / kSlotCap;
-                    unsigned long long runs = freem;          // bit i set: slots i .. i+need-1 all free
-                    for (int t = 1; t < need; ++t) runs &= freem >> t;
-                    if (!runs) { c.cand_slot[q] = -2; ++nd; continue; }
-                    const int h = __ffsll((long long)runs) - 1;
-                    freem &= ~(((need >= 64) ? ~0ull : ((1ull << need) - 1ull)) << h);
-                    c.cand_slot[q] = (short)h;
-                    for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
+#pragma unroll
+                for (int w = 0; w < kMaskWords; ++w) c.frees[w] = c.freew[w];
+                if (any_multi) {
+                    // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
+                    // single-slot domains are placed in parallel below
+                    int nd = 0;
+                    for (int q = 0; q < ncand; ++q) {
+                        const int cnt = c.cand_cnt[q];
+                        if (cnt <= kSlotCap) continue;
+                        if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
+                        const int need = (cnt + kSlotCap - 1) / kSlotCap;
+                        int h = -1;
+                        for (int i = 0, run = 0; i < kSlots; ++i) {
+                            run = ((c.frees[i >> 5] >> (i & 31)) & 1u) ? run + 1 : 0;
+                            if (run == need) { h = i - need + 1; break; }
+                        }
+                        if (h < 0) { c.cand_slot[q] = -2; ++nd; continue; }
+                        for (int t = 0; t < need; ++t) c.frees[(h + t) >> 5] &= ~(1u << ((h + t) & 31));
+                        c.cand_slot[q] = (short)h;
+                        for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
+                    }
+                    c.nmulti_def = nd;
                 }
-                c.nmulti_def = nd;
-                c.freem_single = freem;
-                c.nfree_single = __popcll(freem);
+                c.fpre[0] = 0;
+#pragma unroll
+                for (int w = 0; w < kMaskWords; ++w) c.fpre[w + 1] = c.fpre[w] + __popc(c.frees[w]);
+                c.nfree_single = c.fpre[kMaskWords];
             }
             __syncthreads();
             {
@@ -435,13 +444,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 const bool single = tid < ncand && c.cand_slot[tid] == -1;
                 int nsingle = 0;
                 const int j = block_excl(single ? 1 : 0, c.wsum, nsingle);
-                const unsigned long long fm = c.freem_single;
                 const int nf = c.nfree_single;
                 if (single) {
                     if (j < nf) {
-                        const unsigned lo = (unsigned)fm, hi = (unsigned)(fm >> 32);
-                        const int nlo = __popc(lo);
-                        c.cand_slot[tid] = (short)(j < nlo ? __fns(lo, 0, j + 1) : 32 + __fns(hi, 0, j - nlo + 1));
+                        int w = 0;
+#pragma unroll
+                        for (int t = 1; t < kMaskWords; ++t)
+                            if (c.fpre[t] <= j) w = t;
+                        c.cand_slot[tid] = (short)(32 * w + (int)__fns(c.frees[w], 0, j - c.fpre[w] + 1));
                     } else {
                         c.cand_slot[tid] = -2;
                     }
@@ -466,20 +476,28 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 int nplaced = 0;
                 block_excl(cslot >= 0 ? 1 : 0, c.wsum, nplaced);
                 if (tid == 0) {
+                    int nr = 0;
+#pragma unroll
+                    for (int w = 0; w < kMaskWords; ++w) nr += __popc(c.runw[w]);
                     c.npend = ndef;
-                    c.nrun = __popc(c.runw[0]) + __popc(c.runw[1]) + nplaced;
+                    c.nrun = nr + nplaced;
                 }
             }
             __syncthreads();
-            // members of newly placed domains: slot ids and positions (parallel loads)
-            for (int i = warp; i < kSlots; i += kWarps) {
-                if (!c.seg_new[i]) continue;
-                const int cnt = c.seg_cnt[i], goff = c.seg_goff[i];
-                for (int a = lane; a < cnt; a += 32) {
-                    c.mem_slot[kSlotCap * i + a] = p.members[goff + a];
-                    c.mem_vac[kSlotCap * i + a] = p.mpos[goff + a];
-                    c.mem_act[kSlotCap * i + a] = 1;
-                    c.mem_seg[kSlotCap * i + a] = (uint8_t)i;
+            // members of newly placed domains: slot ids and positions, one member position per thread (all
+            // loads in flight at once)
+            for (int pm = tid; pm < kRowCap; pm += kThreads) {
+                const int sl = pm / kSlotCap;
+                const int h = c.seg_used[sl] == 2 ? c.seg_head[sl] : sl;
+                const int a = pm - kSlotCap * h;
+                if (c.seg_used[sl] != 0 && c.seg_new[h] && a < c.seg_cnt[h]) {
+                    const int goff = c.seg_goff[h];
+                    const int slot = p.members[goff + a];
+                    const int4 pos = p.mpos[goff + a];
+                    c.mem_slot[pm] = slot;
+                    c.mem_vac[pm] = pos;
+                    c.mem_act[pm] = 1;
+                    c.mem_seg[pm] = (uint8_t)h;
                 }
             }
             __syncthreads();
@@ -525,14 +543,25 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 #pragma unroll
                 for (int q = 0; q < kGR; ++q) {
                     const int r = r0 + q * kWarps;
-                    if (r < nrows) { win[r * kWin + lane] = b0[q]; win[r * kWin + lane + 32] = b1[q]; }
+                    if (r < nrows) {
+                        win[r * kWin + lane] = b0[q];
+                        win[r * kWin + lane + 32] = b1[q];
+                        if (lane < 8) win8[r * 8 + lane] = b0[q];
+                    }
                 }
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < kGR; ++q) {
                     const int r = r0 + q * kWarps;
                     if (r >= nrows) break;
-                    const uint32_t ww = reinterpret_cast<const uint32_t*>(win + r * kWin)[k];
+                    // window word k (slots 4k..4k+3) assembled from the lanes holding those slots
+                    uint32_t ww = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t v0 = __shfl_sync(0xffffffffu, (uint32_t)b0[q], 4 * (k & 7) + j);
+                        const uint32_t v1 = __shfl_sync(0xffffffffu, (uint32_t)b1[q], 4 * (k & 7) + j);
+                        ww |= (k < 8 ? v0 : v1) << (8 * j);
+                    }
                     const unsigned eq = __ballot_sync(0xffffffffu, ww == kw[q]);
                     const int hit = (eq & 0xFFFFu) == 0xFFFFu ? 0 : ((eq >> 16) == 0xFFFFu ? 1 : -1);
                     if (hit >= 0 && way == hit) {
@@ -684,12 +713,15 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         if (p.windows) {
                             win[i * kWin + lane] = p.windows[(size_t)g * kWin + lane];
                             win[i * kWin + lane + 32] = p.windows[(size_t)g * kWin + lane + 32];
+                            if (lane < 8) win8[i * 8 + lane] = p.windows[(size_t)g * kWin + lane];
                         } else {
                             const int slot = p.rows ? p.rows[g] : g;
                             const int4 v = p.vac[slot];
                             const bool live = v.x >= 0;                 // departed slot (multi-rank): any window
-                            win[i * kWin + lane] = live ? site_byte(p.species, p.F, v, p.G.off[lane]) : (uint8_t)kFe;
+                            const uint8_t a0 = live ? site_byte(p.species, p.F, v, p.G.off[lane]) : (uint8_t)kFe;
+                            win[i * kWin + lane] = a0;
                             win[i * kWin + lane + 32] = live ? site_byte(p.species, p.F, v, p.G.off[lane + 32]) : (uint8_t)kFe;
+                            if (lane < 8) win8[i * 8 + lane] = a0;
                         }
                     }
                     __syncwarp();
@@ -868,7 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             for (int s = 0; s < kClusterN; ++s) acc = __dadd_rn(acc, part_in[(s * kRoundRows + i) * 8 + k]);
                             const double out = __dadd_rn(b3s[k], __dmul_rn(acc, p.W.s3u));
                             Ek = out > 0.0 ? out : 0.0;
-                            Gk = (win[r * kWin + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P) : 0.0;
+                            Gk = (win8[r * 8 + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P) : 0.0;
                         }
                         double R = 0.0;
 #pragma unroll
@@ -956,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         nv.y = p.F.wrap[0] ? wrap2(ov.y + p.G.off[k][0], 2 * p.F.L[0]) : ov.y + p.G.off[k][0];
                         nv.z = p.F.wrap[1] ? wrap2(ov.z + p.G.off[k][1], 2 * p.F.L[1]) : ov.z + p.G.off[k][1];
                         nv.w = p.F.wrap[2] ? wrap2(ov.w + p.G.off[k][2], 2 * p.F.L[2]) : ov.w + p.G.off[k][2];
-                        const uint8_t tn = win[r * kWin + k];
+                        const uint8_t tn = win8[r * 8 + k];
                         write_site(p.species, p.F, ov.x, ov.y, ov.z, ov.w, tn);
                         write_site(p.species, p.F, nv.x, nv.y, nv.z, nv.w, (uint8_t)kVac);
                         p.vac[slot] = nv;
@@ -1010,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 
     // ---- teardown
     if (ovf && p.overflow) atomicAdd(p.overflow, ovf);
-    if (phase_mode && tid < 64) {                 // whole warps (slot threads are tid < kSlots <= 64)
+    if (phase_mode && tid < 32 * kMaskWords) {   // whole warps (slot threads are tid < kSlots)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             my_events += __shfl_xor_sync(0xffffffffu, my_events, o);

@@ -17,7 +17,7 @@ namespace akmc {
 constexpr int kClusterN = 4;                   // CTAs per cluster; CTA r owns hidden columns [64r, 64r+64)
 constexpr int kSliceN = kHid / kClusterN;      // 64
 constexpr int kRoundRows = 128 / kClusterN;    // rows a CTA contributes per evaluation round (tile M = 128)
-constexpr int kSlots = 64;                     // domain slots per CTA (a domain with > 2 vacancies spans several)
+constexpr int kSlots = 128;                    // domain slots per CTA (a domain with > 2 vacancies spans several)
 constexpr int kSlotCap = 2;                    // vacancies per slot
 constexpr int kRowCap = kSlots * kSlotCap;     // vacancies a CTA holds at once (128)
 constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
@@ -73,6 +73,7 @@ struct EngineParams {
     double* E;
     EngineWeights W;
     uint8_t* stage;         // [clusters][4 CTAs][hi | lo] h1 rows staged in L2 for the multicast
+    uint8_t* wstore;        // [CTAs][kRowCap][64] full windows of the rows a CTA holds
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
     int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)

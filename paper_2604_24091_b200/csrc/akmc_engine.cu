@@ -178,6 +178,7 @@ __device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame
 // non-Fe slots of a window as two ballot masks (slots 0-31, 32-63); entry e of the slot-ordered list is the
 // e-th set bit (no list is stored: the masks are warp-uniform registers)
 struct L1Masks { unsigned m0, m1; int c0, n; };
+constexpr int kL1Batch = 4;                  // W1' rows per row in flight (a dilute window has ~6 non-Fe slots)
 __device__ __forceinline__ L1Masks l1_masks(const uint8_t* w)
 {
     const int lane = threadIdx.x & 31;
@@ -232,10 +233,10 @@ __device__ __forceinline__ void layer1_rows(const uint8_t* w0, const uint8_t* w1
         for (int c = 0; c < 8; ++c) a1[c] = a0[c];
     }
     const int nmax = k0.n > k1.n ? k0.n : k1.n;
-    for (int e = 0; e < nmax; e += 4) {
-        float4 xa[4], xb[4], ya[4], yb[4];
+    for (int e = 0; e < nmax; e += kL1Batch) {
+        float4 xa[kL1Batch], xb[kL1Batch], ya[kL1Batch], yb[kL1Batch];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < kL1Batch; ++t) {
             if (e + t < k0.n) {
                 const float4* rp = base + (size_t)l1_row_index(w0, k0, e + t) * (kHid / 4);
                 xa[t] = __ldg(rp); xb[t] = __ldg(rp + 1);
@@ -246,7 +247,7 @@ __device__ __forceinline__ void layer1_rows(const uint8_t* w0, const uint8_t* w1
             }
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < kL1Batch; ++t) {
             if (e + t < k0.n) {
                 a0[0] = __dadd_rn(a0[0], (double)xa[t].x); a0[1] = __dadd_rn(a0[1], (double)xa[t].y);
                 a0[2] = __dadd_rn(a0[2], (double)xa[t].z); a0[3] = __dadd_rn(a0[3], (double)xa[t].w);

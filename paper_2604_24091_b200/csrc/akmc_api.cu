@@ -152,6 +152,7 @@ struct akmc_handle {
     // phase engine (akmc_engine.cuh)
     bool engine = true;               // false: legacy grid-synchronous inner loop (AKMC_LEGACY_LOOP=1)
     bool tc = false;                  // MLP at FP32 precision: cluster tensor-core evaluator
+    bool serial_engine = false;       // serial / voxel-batch mode runs through the engine (voxel = domain)
     int n_clusters = 0;
     MemoEntry* d_memo = nullptr;      // [vcap][2]
     float* d_W1f = nullptr;           // [385][256]
@@ -431,6 +432,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.mode = mode;
     p.model = h->cfg.barrier_model;
     p.species = h->d_species; p.vac = h->d_vac; p.F = h->F; p.G = h->G; p.P = h->P; p.S = h->S;
+    p.S.seed = h->cfg.seed;                        // (serial handles leave the sublattice block unset)
     p.segs = h->d_segs; p.members = h->d_members; p.mpos = h->d_mpos; p.ctr = h->d_ctr; p.memo = h->d_memo;
     p.scratch = h->d_scratch; p.iscratch = h->d_iscratch; p.cursor = h->d_cursor;
     p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
@@ -863,9 +865,25 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
         CKI(cudaMalloc(&h->d_wstore, (size_t)std::max(h->num_sms, ncl * kClusterN) * kRowCap * kWin));
     }
-    if (h->sub) {
-        CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
-        CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
+    CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
+    CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
+    if (!h->sub) {
+        // serial / voxel-batch mode through the engine: one segment per voxel, members = its slots in order
+        std::vector<int> vs((size_t)h->nvox + 1);
+        CKI(cudaMemcpy(vs.data(), h->d_vstart, vs.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        std::vector<Segment> sg((size_t)h->nvox);
+        int maxm = 0;
+        for (int v = 0; v < h->nvox; ++v) {
+            sg[(size_t)v] = Segment{(long long)v, vs[(size_t)v], vs[(size_t)v + 1] - vs[(size_t)v], 0.0, 0u, 1};
+            maxm = std::max(maxm, sg[(size_t)v].cnt);
+        }
+        h->serial_engine = h->engine && maxm <= kRowCap;     // a voxel must fit one CTA's member capacity
+        std::vector<int> mem((size_t)std::max<int64_t>(h->nvac, 1));
+        for (int64_t i = 0; i < h->nvac; ++i) mem[(size_t)i] = (int)i;
+        CKI(cudaMalloc(&h->d_segs, sg.size() * sizeof(Segment)));
+        CKI(cudaMalloc(&h->d_members, mem.size() * sizeof(int)));
+        CKI(cudaMemcpy(h->d_segs, sg.data(), sg.size() * sizeof(Segment), cudaMemcpyHostToDevice));
+        CKI(cudaMemcpy(h->d_members, mem.data(), mem.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     CKI(cudaStreamSynchronize(h->stream));
 #undef CKI
@@ -890,6 +908,41 @@ int akmc_set_profiling(akmc_handle* h, int32_t profile)
 
 static int step_serial(akmc_handle* h, int64_t n)
 {
+    if (h->serial_engine) {
+        // all n events of every voxel in one persistent launch (a10; per-voxel Philox counters keep the
+        // trajectory identical to event-by-event stepping)
+        for (int64_t done = 0; done < n;) {
+            const int chunk = (int)std::min<int64_t>(n - done, 1 << 30);
+            EngineParams p = engine_params(h, kEnginePhase);
+            p.serial = 1;
+            p.nseg_host = h->nvox;
+            p.n_events = chunk;
+            p.nev = h->d_nev;
+            p.term = h->d_term;
+            p.clock = h->d_clock;
+            p.ph = nullptr;
+            CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, chunk), 0,
+                                  sizeof(unsigned long long), h->stream));
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (h->profile) {
+                if (h->ev_used + 2 > h->ev.size())
+                    for (int i = 0; i < 64; ++i) {
+                        cudaEvent_t e;
+                        CK(h, cudaEventCreate(&e));
+                        h->ev.push_back(e);
+                    }
+                e0 = h->ev[h->ev_used++];
+                e1 = h->ev[h->ev_used++];
+                CK(h, cudaEventRecord(e0, h->stream));
+            }
+            CK(h, launch_engine(p, h->tc, h->n_clusters, h->num_sms, h->stream));
+            if (h->profile) CK(h, cudaEventRecord(e1, h->stream));
+            h->total.kernel_launches += 2;
+            h->total.mlp_launches += 1;
+            done += chunk;
+        }
+        return AKMC_OK;
+    }
     const int nv = (int)h->nvac;
     for (int64_t it = 0; it < n; ++it) {
         int rc = eval_rows(h, nullptr, nullptr, nv, nv, nullptr, h->cfg.precision, h->d_rates, h->d_R, h->d_E);
@@ -1207,7 +1260,8 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
     const auto t1 = std::chrono::steady_clock::now();
     h->total.events += (int64_t)(c1.events - c0.events);
     h->total.hop_evals += (int64_t)(c1.hop_evals - c0.hop_evals);
-    h->total.mlp_rows += (h->engine && h->sub) ? (int64_t)(c1.mrows - c0.mrows) : (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
+    h->total.mlp_rows += ((h->engine && h->sub) || h->serial_engine) ? (int64_t)(c1.mrows - c0.mrows)
+                                                                      : (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
     h->total.clamps += (int64_t)(c1.clamps - c0.clamps);
     h->total.terminal_voxels += (int64_t)(c1.terminal - c0.terminal);
     h->total.wall_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();

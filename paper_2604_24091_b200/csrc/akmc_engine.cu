@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
-        c.ntot = phase_mode ? (int)p.ctr->nseg : 0;
+        c.ntot = phase_mode ? (p.serial ? p.nseg_host : (int)p.ctr->nseg) : 0;
         c.events = 0; c.evals = 0; c.mrows = 0; c.clamps = 0;
         if (kTC) {
             mbar_init(bar_req, kClusterN);
@@ -389,12 +389,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 for (int w = 0; w < kMaskWords; ++w) { nfree += __popc(c.freew[w]); nrun0 += __popc(c.runw[w]); }
                 c.fetch = 0;
                 c.nnew = 0;
+                // claim at most a fair share of the segment list at a time (few, large domains -- voxels --
+                // must not pile up in a handful of CTAs)
+                const int share = max(1, (c.ntot + (int)gridDim.x - 1) / (int)gridDim.x);
+                const int claim = min(nfree, share);
                 if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
-                    const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)nfree);
+                    const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)claim);
                     if (s0 >= c.ntot) {
                         c.drained = 1;
                     } else {
-                        c.fetch = 1; c.s0 = s0; c.nnew = min(nfree, c.ntot - s0);
+                        c.fetch = 1; c.s0 = s0; c.nnew = min(claim, c.ntot - s0);
                         ++d_refill;
                     }
                 }
@@ -472,7 +476,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     const int h = cslot;
                     c.seg_used[h] = 1;
                     c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
-                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_run[h] = 1; c.seg_new[h] = 1;
+                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_new[h] = 1;
+                    c.seg_run[h] = (p.serial && p.term[cdom]) ? 0 : 1;   // a terminal voxel stays frozen
                 }
                 int nplaced = 0;
                 block_excl(cslot >= 0 ? 1 : 0, c.wsum, nplaced);
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 if (c.seg_used[sl] != 0 && c.seg_new[h] && a < c.seg_cnt[h]) {
                     const int goff = c.seg_goff[h];
                     const int slot = p.members[goff + a];
-                    const int4 pos = p.mpos[goff + a];
+                    const int4 pos = p.serial ? p.vac[slot] : p.mpos[goff + a];
                     c.mem_slot[pm] = slot;
                     c.mem_vac[pm] = pos;
                     c.mem_act[pm] = 1;
@@ -960,6 +965,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             bool stop = false;
             if (m == 0) {
                 stop = true;
+                if (p.serial) {                               // a voxel without vacancies: terminal
+                    p.term[c.seg_dom[i]] = 1;
+                    atomicAdd(&p.ctr->terminal, 1ull);
+                }
             } else {
                 my_evals += 8ull * (unsigned long long)m;
                 my_clamps += cl;
@@ -967,14 +976,29 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 const double Rd = tree_build(buf, m, P, nlev);
                 if (!(Rd > 0.0)) {
                     stop = true;
+                    if (p.serial) {                           // no feasible event in this voxel
+                        p.term[c.seg_dom[i]] = 1;
+                        p.nev[c.seg_dom[i]] += c.seg_it[i];
+                        atomicAdd(&p.ctr->terminal, 1ull);
+                    }
                 } else {
-                    const unsigned long long ph = (unsigned long long)p.ph->phase;
-                    double u_sel, u_t;
-                    philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
-                                    u_sel, u_t);
-                    const double dt = __ddiv_rn(-det_log(u_t), Rd);
-                    if (__dadd_rn(c.seg_t[i], dt) > p.S.window) {
-                        stop = true;                          // overshooting draw discarded
+                    double u_sel, u_t, dt;
+                    bool go;
+                    if (p.serial) {
+                        // serial BKL (a10): counter (event index of the voxel, voxel), clock += dt after the hop
+                        const unsigned long long n = (unsigned long long)p.nev[c.seg_dom[i]] + c.seg_it[i];
+                        philox_uniforms(p.S.seed, make_uint4((uint32_t)n, (uint32_t)(n >> 32), c.seg_dom[i], 0u), u_sel, u_t);
+                        dt = __ddiv_rn(-det_log(u_t), Rd);
+                        go = true;
+                    } else {
+                        const unsigned long long ph = (unsigned long long)p.ph->phase;
+                        philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
+                                        u_sel, u_t);
+                        dt = __ddiv_rn(-det_log(u_t), Rd);
+                        go = !(__dadd_rn(c.seg_t[i], dt) > p.S.window);   // else the overshooting draw is discarded
+                    }
+                    if (!go) {
+                        stop = true;
                     } else {
                         double rr = __dmul_rn(u_sel, Rd);
                         const int leaf = tree_descend(buf, m, P, nlev, rr);
@@ -994,10 +1018,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         write_site(p.species, p.F, nv.x, nv.y, nv.z, nv.w, (uint8_t)kVac);
                         p.vac[slot] = nv;
                         c.mem_vac[moff + a] = nv;
-                        long long d2;
-                        int sec2;
-                        dom_sector(nv, p.S, d2, sec2);
-                        if (d2 != (long long)c.seg_dom[i] || sec2 != p.ph->sector) c.mem_act[moff + a] = 0;
+                        long long d2 = 0;
+                        int sec2 = 0;
+                        if (!p.serial) dom_sector(nv, p.S, d2, sec2);
+                        if (!p.serial && (d2 != (long long)c.seg_dom[i] || sec2 != p.ph->sector)) c.mem_act[moff + a] = 0;
                         if (p.S.log) {
                             if (near_face(p.F, ov.y, ov.z, ov.w))
                                 log_entry(p.S.log, p.S.nlog, p.S.logcap, ov.y, ov.z, ov.w, tn);
@@ -1015,6 +1039,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         c.seg_t[i] = __dadd_rn(c.seg_t[i], dt);
                         c.seg_it[i] += 1u;
                         my_events += 1ull;
+                        if (p.serial) {
+                            const unsigned v = c.seg_dom[i];
+                            p.clock[v] = __dadd_rn(p.clock[v], dt);
+                            if ((int)c.seg_it[i] >= p.n_events) {   // this launch's events done
+                                p.nev[v] += c.seg_it[i];
+                                stop = true;
+                            }
+                        }
                     }
                 }
             }

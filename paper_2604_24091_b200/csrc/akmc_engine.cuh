@@ -74,6 +74,13 @@ struct EngineParams {
     EngineWeights W;
     uint8_t* stage;         // [clusters][4 CTAs][hi | lo] h1 rows staged in L2 for the multicast
     uint8_t* wstore;        // [CTAs][kRowCap][64] full windows of the rows a CTA holds
+    // serial / voxel-batch mode (a10): a "domain" is a whole voxel, each runs n_events BKL events per launch
+    int serial;             // 1: segments = voxels, no window/sector; 0: sublattice phase
+    int nseg_host;          // serial: number of voxels (segments)
+    int n_events;           // serial: events per voxel in this launch
+    long long* nev;         // serial: per-voxel event counters (Philox counter, P:294-298 / S:195-203)
+    int* term;              // serial: per-voxel terminal flags
+    double* clock;          // serial: per-voxel clocks
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
     int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)

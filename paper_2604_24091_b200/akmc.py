@@ -10,7 +10,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libakmc.so")
+# AKMC_LIB: an alternative in-tree build of the same library (A/B timing of kernel variants, tools/ab_probe.py)
+LIB_PATH = os.environ.get("AKMC_LIB") or os.path.join(HERE, "lib", "libakmc.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "akmc.h")
 
 AKMC_OK, AKMC_ERR_RUNTIME, AKMC_ERR_INVALID, AKMC_TERMINAL, AKMC_ERR_CUDA, AKMC_ERR_NCCL = range(6)

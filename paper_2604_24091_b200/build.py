@@ -36,18 +36,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Build LIB (or `out`, an A/B variant compiled with extra -D `defines`)."""
+    target = out or LIB
+    if not force and not defines and target == LIB and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(target), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], *nccl_flags(), "-o", tmp]
+    tmp = target + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, *["-D" + d for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], *nccl_flags(),
+           "-o", tmp]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

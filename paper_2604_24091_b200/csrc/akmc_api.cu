@@ -23,6 +23,7 @@ using namespace akmc;
 namespace {
 
 thread_local std::string g_init_error;
+constexpr int kDiagWords = 128 + 512 + 64;   // AKMC_PHASE_TIMING: sums, engine sums, iteration trace
 
 // ------------------------------------------------------------------ host geometry (independent of the oracle)
 // window: bcc vectors within 6.0 A at a0 = 2.866 A, sorted by (|h|^2, hx, hy, hz)  (A3, A4)
@@ -177,7 +178,7 @@ struct akmc_handle {
     cudaGraphExec_t sweep_exec = nullptr;
     cudaStream_t graph_stream = nullptr;   // stream the graph was instantiated for
     int graph_launches_per_sweep = 0;
-    unsigned long long* d_phase_cycles = nullptr;   // AKMC_PHASE_TIMING diagnostics
+    unsigned long long* d_phase_cycles = nullptr;   // AKMC_PHASE_TIMING diagnostics (kDiagWords)
     int vcap = 1;                     // vacancy slot capacity (multi-rank: arrivals append)
     // multi-rank spatial decomposition (C5); see akmc_dist.cuh
     bool multi = false;
@@ -420,8 +421,8 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     CK(h, mlp_tc_setup());
     if (std::getenv("AKMC_PHASE_TIMING")) {
-        CK(h, cudaMalloc(&h->d_phase_cycles, 128 * sizeof(unsigned long long)));
-        CK(h, cudaMemset(h->d_phase_cycles, 0, 128 * sizeof(unsigned long long)));
+        CK(h, cudaMalloc(&h->d_phase_cycles, kDiagWords * sizeof(unsigned long long)));
+        CK(h, cudaMemset(h->d_phase_cycles, 0, kDiagWords * sizeof(unsigned long long)));
     }
     return AKMC_OK;
 }
@@ -1443,7 +1444,8 @@ void akmc_free(akmc_handle* h)
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->d_phase_cycles) {
-        unsigned long long c[128] = {0};
+        static unsigned long long c[kDiagWords];
+        std::memset(c, 0, sizeof(c));
         cudaMemcpy(c, h->d_phase_cycles, sizeof(c), cudaMemcpyDeviceToHost);
         const double t = c[7] ? (double)c[7] : 1.0;
         if (c[7])
@@ -1464,6 +1466,27 @@ void akmc_free(akmc_handle* h)
             std::fprintf(stderr, "[akmc engine] cycles/CTA: refill %.0f rows %.0f gather+memo %.0f | L1 %.0f exchange %.0f"
                          " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
                          d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);
+            std::fprintf(stderr, "[akmc engine] L1 split: memo move %.0f layer 1 %.0f async fences + barrier %.0f\n",
+                         d[20] / n, d[21] / n, d[22] / n);
+            if (d[24] + d[25] + d[26] + d[27])
+                std::fprintf(stderr, "[akmc engine] layer-1 probe (warp 0): index %.0f b1 %.0f loads+adds %.0f store %.0f\n",
+                             d[24] / n, d[25] / n, d[26] / n, d[27] / n);
+        }
+        // per-iteration trace: iteration index -> CTA count, mean rows / misses / running domains, cycles
+        const unsigned long long* tr = c + 128;
+        if (tr[0]) {
+            std::fprintf(stderr, "[akmc iter trace] it: ctas rows miss run | cyc ctl rounds sel | rounds\n");
+            for (int i = 0; i < 64; ++i) {
+                const unsigned long long* t = tr + 8 * i;
+                if (!t[0]) continue;
+                const double n = (double)t[0];
+                std::fprintf(stderr, "[akmc iter trace] %2d: %6llu %6.1f %6.1f %6.1f | %7.0f %7.0f %7.0f | %.2f\n", i, t[0],
+                             t[1] / n, t[2] / n, t[3] / n, t[4] / n, t[5] / n, t[6] / n, t[7] / n);
+            }
+            std::fprintf(stderr, "[akmc iter trace] iterations per CTA launch:");
+            for (int i = 0; i < 64; ++i)
+                if (c[128 + 512 + i]) std::fprintf(stderr, " %d:%llu", i, c[128 + 512 + i]);
+            std::fprintf(stderr, "\n");
         }
         cudaFree(h->d_phase_cycles);
         h->d_phase_cycles = nullptr;

@@ -90,7 +90,10 @@ constexpr uint32_t kOffRowR = kOffWin + kRowCap * 8;                 // [kRowCap
 constexpr uint32_t kOffRowC = kOffA + 16384;                         // [kRowCap] int, FP64 mode only (A is scratch there)
 constexpr uint32_t kOffB2 = kOffRowR + kRowCap * 8;                  // float [kSliceN]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
-constexpr uint32_t kOffCtl = kOffB3 + 8 * 8;
+constexpr int kL1List = 6;                                           // W1' row indices kept per row (RPV: ~1.6)
+constexpr uint32_t kOffL1N = kOffB3 + 8 * 8;                         // [kRowCap] uint8 non-Fe slot count
+constexpr uint32_t kOffL1L = kOffL1N + kRowCap;                      // [kRowCap][kL1List] uint16 W1' row index
+constexpr uint32_t kOffCtl = (kOffL1L + kRowCap * kL1List * 2 + 15u) & ~15u;
 constexpr uint32_t kOffBar = (kOffCtl + (uint32_t)sizeof(Ctl) + 7u) & ~7u;
 constexpr int kNumBars = 4;                                          // req, part, mma, weights
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
@@ -165,10 +168,17 @@ __device__ __forceinline__ uint32_t h2_off(int m, int k)
     return (uint32_t)(k >> 3) * kCoreColH2 + (uint32_t)(m >> 3) * 128u + (uint32_t)(m & 7) * 16u + (uint32_t)(k & 7) * 2u;
 }
 
-// window byte of an owned vacancy: plain (coherent) load -- the lattice is written by this kernel
-__device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame& F, const int4& v, const int8_t* o)
+// window byte of an owned vacancy (plain coherent load -- the lattice is written by this kernel), with the
+// offset packed into a register (bytes dx, dy, dz): a lane-dependent index into the kernel
+// parameters would be a divergent constant-cache load (serialised over the 32 addresses)
+__device__ __forceinline__ uint32_t pack_off(const int8_t* o)
 {
-    return species[neighbour_site(F, v, o[0], o[1], o[2])];
+    return (uint32_t)(uint8_t)o[0] | ((uint32_t)(uint8_t)o[1] << 8) | ((uint32_t)(uint8_t)o[2] << 16);
+}
+__device__ __forceinline__ uint8_t site_byte_pk(const uint8_t* species, const Frame& F, const int4& v, uint32_t pk)
+{
+    return species[neighbour_site(F, v, (int)(int8_t)(pk & 0xFFu), (int)(int8_t)((pk >> 8) & 0xFFu),
+                                  (int)(int8_t)((pk >> 16) & 0xFFu))];
 }
 
 // layer 1 of up to two rows, all 256 columns (lane = columns 8*lane .. 8*lane+7): FP64 sum of b1' and the
@@ -178,7 +188,10 @@ __device__ __forceinline__ uint8_t site_byte(const uint8_t* species, const Frame
 // non-Fe slots of a window as two ballot masks (slots 0-31, 32-63); entry e of the slot-ordered list is the
 // e-th set bit (no list is stored: the masks are warp-uniform registers)
 struct L1Masks { unsigned m0, m1; int c0, n; };
-constexpr int kL1Batch = 4;                  // W1' rows per row in flight (a dilute window has ~6 non-Fe slots)
+#ifndef AKMC_L1_BATCH
+#define AKMC_L1_BATCH 2
+#endif
+constexpr int kL1Batch = AKMC_L1_BATCH;                  // W1' rows per row in flight (an RPV window has ~1.6 non-Fe slots)
 __device__ __forceinline__ L1Masks l1_masks(const uint8_t* w)
 {
     const int lane = threadIdx.x & 31;
@@ -193,6 +206,27 @@ __device__ __forceinline__ int l1_row_index(const uint8_t* w, const L1Masks& k, 
 {
     const int slot = e < k.c0 ? (int)__fns(k.m0, 0, e + 1) : 32 + (int)__fns(k.m1, 0, e - k.c0 + 1);
     return 1 + ((int)w[slot] - 1) * kWin + slot;
+}
+
+// the gather's by-product for layer 1: the row's non-Fe slots as W1' row indices, in slot order, from the
+// window bytes held by the lanes (lane = slots lane, lane + 32); rows with more than kL1List fall back to the
+// window in the global scratch
+__device__ __forceinline__ void l1_list_store(int r, uint8_t b0, uint8_t b1, uint8_t* l1n, uint16_t* l1l)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned m0 = __ballot_sync(0xffffffffu, b0 != (uint8_t)kFe);
+    const unsigned m1 = __ballot_sync(0xffffffffu, b1 != (uint8_t)kFe);
+    const unsigned lt = lanemask_lt();
+    const int c0 = __popc(m0);
+    if (lane == 0) l1n[r] = (uint8_t)(c0 + __popc(m1));
+    if (b0 != (uint8_t)kFe) {
+        const int e = __popc(m0 & lt);
+        if (e < kL1List) l1l[r * kL1List + e] = (uint16_t)(1 + ((int)b0 - 1) * kWin + lane);
+    }
+    if (b1 != (uint8_t)kFe) {
+        const int e = c0 + __popc(m1 & lt);
+        if (e < kL1List) l1l[r * kL1List + e] = (uint16_t)(1 + ((int)b1 - 1) * kWin + lane + 32);
+    }
 }
 
 __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi,
@@ -216,55 +250,94 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
     *reinterpret_cast<uint4*>(g_lo + goff) = vl;
 }
 
-__device__ __forceinline__ void layer1_rows(const uint8_t* w0, const uint8_t* w1, const float* __restrict__ W1f,
-                                            int m0, int m1, uint8_t* A_hi, uint8_t* A_lo,
-                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf)
+// layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once
+#ifndef AKMC_L1_ROWS
+#define AKMC_L1_ROWS 2
+#endif
+#ifndef AKMC_W1_EVICT_LAST
+#define AKMC_W1_EVICT_LAST 0
+#endif
+#ifndef AKMC_L1_PROBE
+#define AKMC_L1_PROBE 0
+#endif
+#ifndef AKMC_REFILL_FAST
+#define AKMC_REFILL_FAST 1
+#endif
+#ifndef AKMC_GATHER_ROWS
+#define AKMC_GATHER_ROWS 8
+#endif
+constexpr int kL1Rows = AKMC_L1_ROWS;
+__device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
+                                            const uint16_t* l1l, const float* __restrict__ W1f,
+                                            const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
+                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf,
+                                            long long* lp = nullptr)
 {
     const int lane = threadIdx.x & 31;
-    const L1Masks k0 = l1_masks(w0);
-    L1Masks k1{0u, 0u, 0, 0};
-    if (w1) k1 = l1_masks(w1);
+    long long t0 = lp ? clock64() : 0;
+    auto plap = [&](int i) { if (lp) { const long long t = clock64(); lp[i] += t - t0; t0 = t; } };
+    int n[kL1Rows];
+    L1Masks k[kL1Rows];
+    int nmax = 0;
+#pragma unroll
+    for (int r = 0; r < kL1Rows; ++r) {
+        n[r] = r < nv ? (int)l1n[rr[r]] : 0;
+        nmax = n[r] > nmax ? n[r] : nmax;
+        k[r].m0 = 0u; k[r].m1 = 0u; k[r].c0 = 0; k[r].n = n[r];
+        if (n[r] > kL1List) k[r] = l1_masks(win + rr[r] * kWin);    // rare crowded window (warp-uniform)
+    }
+    plap(0);
     const float4* base = reinterpret_cast<const float4*>(W1f) + 2 * lane;
-    double a0[8], a1[8];
+#if AKMC_W1_EVICT_LAST
+    const uint64_t pol = policy_evict_last();
+#endif
+    double a[kL1Rows][8];
     {
         const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
-        a0[0] = x0.x; a0[1] = x0.y; a0[2] = x0.z; a0[3] = x0.w; a0[4] = x1.x; a0[5] = x1.y; a0[6] = x1.z; a0[7] = x1.w;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) a1[c] = a0[c];
+        for (int r = 0; r < kL1Rows; ++r) {
+            a[r][0] = x0.x; a[r][1] = x0.y; a[r][2] = x0.z; a[r][3] = x0.w;
+            a[r][4] = x1.x; a[r][5] = x1.y; a[r][6] = x1.z; a[r][7] = x1.w;
+        }
     }
-    const int nmax = k0.n > k1.n ? k0.n : k1.n;
+    plap(1);
     for (int e = 0; e < nmax; e += kL1Batch) {
-        float4 xa[kL1Batch], xb[kL1Batch], ya[kL1Batch], yb[kL1Batch];
+        float4 xa[kL1Rows][kL1Batch], xb[kL1Rows][kL1Batch];
 #pragma unroll
         for (int t = 0; t < kL1Batch; ++t) {
-            if (e + t < k0.n) {
-                const float4* rp = base + (size_t)l1_row_index(w0, k0, e + t) * (kHid / 4);
-                xa[t] = __ldg(rp); xb[t] = __ldg(rp + 1);
-            }
-            if (e + t < k1.n) {
-                const float4* rp = base + (size_t)l1_row_index(w1, k1, e + t) * (kHid / 4);
-                ya[t] = __ldg(rp); yb[t] = __ldg(rp + 1);
+#pragma unroll
+            for (int r = 0; r < kL1Rows; ++r) {
+                if (e + t < n[r]) {
+                    const int ix = n[r] <= kL1List ? (int)l1l[rr[r] * kL1List + e + t]
+                                                   : l1_row_index(win + rr[r] * kWin, k[r], e + t);
+                    const float4* rp = base + (size_t)ix * (kHid / 4);
+#if AKMC_W1_EVICT_LAST
+                    xa[r][t] = ldg_f4_hint(rp, pol); xb[r][t] = ldg_f4_hint(rp + 1, pol);
+#else
+                    xa[r][t] = __ldg(rp); xb[r][t] = __ldg(rp + 1);
+#endif
+                }
             }
         }
 #pragma unroll
         for (int t = 0; t < kL1Batch; ++t) {
-            if (e + t < k0.n) {
-                a0[0] = __dadd_rn(a0[0], (double)xa[t].x); a0[1] = __dadd_rn(a0[1], (double)xa[t].y);
-                a0[2] = __dadd_rn(a0[2], (double)xa[t].z); a0[3] = __dadd_rn(a0[3], (double)xa[t].w);
-                a0[4] = __dadd_rn(a0[4], (double)xb[t].x); a0[5] = __dadd_rn(a0[5], (double)xb[t].y);
-                a0[6] = __dadd_rn(a0[6], (double)xb[t].z); a0[7] = __dadd_rn(a0[7], (double)xb[t].w);
-            }
-            if (e + t < k1.n) {
-                a1[0] = __dadd_rn(a1[0], (double)ya[t].x); a1[1] = __dadd_rn(a1[1], (double)ya[t].y);
-                a1[2] = __dadd_rn(a1[2], (double)ya[t].z); a1[3] = __dadd_rn(a1[3], (double)ya[t].w);
-                a1[4] = __dadd_rn(a1[4], (double)yb[t].x); a1[5] = __dadd_rn(a1[5], (double)yb[t].y);
-                a1[6] = __dadd_rn(a1[6], (double)yb[t].z); a1[7] = __dadd_rn(a1[7], (double)yb[t].w);
+#pragma unroll
+            for (int r = 0; r < kL1Rows; ++r) {
+                if (e + t < n[r]) {
+                    a[r][0] = __dadd_rn(a[r][0], (double)xa[r][t].x); a[r][1] = __dadd_rn(a[r][1], (double)xa[r][t].y);
+                    a[r][2] = __dadd_rn(a[r][2], (double)xa[r][t].z); a[r][3] = __dadd_rn(a[r][3], (double)xa[r][t].w);
+                    a[r][4] = __dadd_rn(a[r][4], (double)xb[r][t].x); a[r][5] = __dadd_rn(a[r][5], (double)xb[r][t].y);
+                    a[r][6] = __dadd_rn(a[r][6], (double)xb[r][t].z); a[r][7] = __dadd_rn(a[r][7], (double)xb[r][t].w);
+                }
             }
         }
     }
-    l1_store(a0, m0, A_hi, A_lo, g_hi, g_lo, ovf);
-    if (w1) l1_store(a1, m1, A_hi, A_lo, g_hi, g_lo, ovf);
+    plap(2);
+#pragma unroll
+    for (int r = 0; r < kL1Rows; ++r)
+        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf);
     __syncwarp();
+    plap(3);
 }
 
 template <bool kTC>
@@ -277,6 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     // keeps the 8 first-shell bytes the rates mask and the hop need
     uint8_t* win = p.wstore + (size_t)blockIdx.x * kRowCap * kWin;
     uint8_t* win8 = sm + kOffWin;
+    uint8_t* l1n = sm + kOffL1N;
+    uint16_t* l1l = reinterpret_cast<uint16_t*>(sm + kOffL1L);
     double* rowR = reinterpret_cast<double*>(sm + kOffRowR);
     int* rowC = reinterpret_cast<int*>(sm + kOffRowC);
     uint8_t* A_hi = sm + kOffA;
@@ -289,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffTmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = kTC ? cluster_rank() : 0u;
+    const uint32_t off_lo = pack_off(p.G.off[lane]), off_hi = pack_off(p.G.off[lane + 32]);   // this lane's window slots
     // h2 slice and the layer-3 partials live in this CTA's own row block of A: dead once layer 2 has
     // completed, and no peer ever writes it (peers' multicasts target their own blocks)
     const uint32_t own_block = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
@@ -342,6 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     unsigned long long d_it = 0, d_rounds = 0, d_erounds = 0, d_refill = 0;
     long long d_cc = 0, d_cr = 0, d_cs = 0;
     long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long d_y[4] = {0, 0, 0, 0};
+    long long d_z[4] = {0, 0, 0, 0};              // AKMC_L1_PROBE: layer-1 sub-steps of warp 0              // L1 lap split: memo move | layer 1 | async fences + barrier
     long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)   // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
     const long long t_start = clock64();
     unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
@@ -357,8 +435,35 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         }
     };
 
+    // per-iteration trace (AKMC_PHASE_TIMING): thread 0 snapshots its counters at the top of every iteration
+    long long tr_ctl = 0, tr_rd = 0, tr_sel = 0, tr_t0 = 0;
+    unsigned long long tr_rounds = 0;
+    int tr_it = 0;
+    auto trace_begin = [&]() {
+        if (p.diag && tid == 0) {
+            tr_ctl = d_x[0] + d_x[1] + d_x[2];
+            tr_rd = d_y[0] + d_y[1] + d_y[2] + d_x[4] + d_x[5] + d_x[6] + d_x[7] + d_cr;
+            tr_sel = d_cs; tr_rounds = d_rounds; tr_t0 = clock64();
+        }
+    };
+    auto trace_end = [&]() {
+        if (p.diag && tid == 0 && phase_mode) {
+            unsigned long long* t = p.diag + 96 + 8 * (size_t)min(tr_it, 63);
+            atomicAdd(t + 0, 1ull);
+            atomicAdd(t + 1, (unsigned long long)c.nrows);
+            atomicAdd(t + 2, (unsigned long long)c.nmiss);
+            atomicAdd(t + 3, (unsigned long long)c.nrun);
+            atomicAdd(t + 4, (unsigned long long)(d_x[0] + d_x[1] + d_x[2] - tr_ctl));
+            atomicAdd(t + 5, (unsigned long long)(d_y[0] + d_y[1] + d_y[2] + d_x[4] + d_x[5] + d_x[6] + d_x[7] + d_cr - tr_rd));
+            atomicAdd(t + 6, (unsigned long long)(d_cs - tr_sel));
+            atomicAdd(t + 7, d_rounds - tr_rounds);
+            ++tr_it;
+        }
+    };
+
     for (;;) {
         int own_alive = 0;
+        trace_begin();
         if (phase_mode) {
             // ================= slots: release stopped domains, refill from the segment list =================
             __syncthreads();
@@ -410,100 +515,113 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 c.cand_dom[q] = (unsigned)sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
             }
             __syncthreads();
-            const int ncand = c.npend + c.nnew;
-            const bool multi = tid < ncand && c.cand_cnt[tid] > kSlotCap;
-            if (tid < ncand) c.cand_slot[tid] = -1;
-            const int any_multi = __syncthreads_or(multi ? 1 : 0);
-            if (tid == 0) {
-#pragma unroll
-                for (int w = 0; w < kMaskWords; ++w) c.frees[w] = c.freew[w];
-                if (any_multi) {
-                    // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
-                    // single-slot domains are placed in parallel below
-                    int nd = 0;
-                    for (int q = 0; q < ncand; ++q) {
-                        const int cnt = c.cand_cnt[q];
-                        if (cnt <= kSlotCap) continue;
-                        if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
-                        const int need = (cnt + kSlotCap - 1) / kSlotCap;
-                        int h = -1;
-                        for (int i = 0, run = 0; i < kSlots; ++i) {
-                            run = ((c.frees[i >> 5] >> (i & 31)) & 1u) ? run + 1 : 0;
-                            if (run == need) { h = i - need + 1; break; }
-                        }
-                        if (h < 0) { c.cand_slot[q] = -2; ++nd; continue; }
-                        for (int t = 0; t < need; ++t) c.frees[(h + t) >> 5] &= ~(1u << ((h + t) & 31));
-                        c.cand_slot[q] = (short)h;
-                        for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
-                    }
-                    c.nmulti_def = nd;
-                }
-                c.fpre[0] = 0;
-#pragma unroll
-                for (int w = 0; w < kMaskWords; ++w) c.fpre[w + 1] = c.fpre[w] + __popc(c.frees[w]);
-                c.nfree_single = c.fpre[kMaskWords];
-            }
-            __syncthreads();
-            {
-                // the j-th single-slot candidate takes the j-th free slot; the rest are deferred
-                const bool single = tid < ncand && c.cand_slot[tid] == -1;
-                int nsingle = 0;
-                const int j = block_excl(single ? 1 : 0, c.wsum, nsingle);
-                const int nf = c.nfree_single;
-                if (single) {
-                    if (j < nf) {
-                        int w = 0;
-#pragma unroll
-                        for (int t = 1; t < kMaskWords; ++t)
-                            if (c.fpre[t] <= j) w = t;
-                        c.cand_slot[tid] = (short)(32 * w + (int)__fns(c.frees[w], 0, j - c.fpre[w] + 1));
-                    } else {
-                        c.cand_slot[tid] = -2;
-                    }
-                }
-                __syncthreads();
-                const int q = tid;
-                const bool deferred = q < ncand && c.cand_slot[q] == -2;
-                int ndef = 0;
-                const int pi = block_excl(deferred ? 1 : 0, c.wsum, ndef);
-                // carried-over domains are compacted in place to the front of the candidate list (read first)
-                unsigned cdom = 0;
-                int coff = 0, ccnt = 0, cslot = -3;
-                if (q < ncand) { cdom = c.cand_dom[q]; coff = c.cand_off[q]; ccnt = c.cand_cnt[q]; cslot = c.cand_slot[q]; }
-                __syncthreads();
-                if (deferred) { c.cand_dom[pi] = cdom; c.cand_off[pi] = coff; c.cand_cnt[pi] = ccnt; }
-                if (cslot >= 0) {
-                    const int h = cslot;
-                    c.seg_used[h] = 1;
-                    c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
-                    c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_new[h] = 1;
-                    c.seg_run[h] = (p.serial && p.term[cdom]) ? 0 : 1;   // a terminal voxel stays frozen
-                }
-                int nplaced = 0;
-                block_excl(cslot >= 0 ? 1 : 0, c.wsum, nplaced);
+            const int ncand = c.npend + c.nnew;     // block-uniform (shared, after a barrier)
+#if AKMC_REFILL_FAST
+            if (ncand == 0) {                        // nothing to place: running set unchanged
                 if (tid == 0) {
                     int nr = 0;
 #pragma unroll
                     for (int w = 0; w < kMaskWords; ++w) nr += __popc(c.runw[w]);
-                    c.npend = ndef;
-                    c.nrun = nr + nplaced;
+                    c.npend = 0;
+                    c.nrun = nr;
                 }
-            }
-            __syncthreads();
-            // members of newly placed domains: slot ids and positions, one member position per thread (all
-            // loads in flight at once)
-            for (int pm = tid; pm < kRowCap; pm += kThreads) {
-                const int sl = pm / kSlotCap;
-                const int h = c.seg_used[sl] == 2 ? c.seg_head[sl] : sl;
-                const int a = pm - kSlotCap * h;
-                if (c.seg_used[sl] != 0 && c.seg_new[h] && a < c.seg_cnt[h]) {
-                    const int goff = c.seg_goff[h];
-                    const int slot = p.members[goff + a];
-                    const int4 pos = p.serial ? p.vac[slot] : p.mpos[goff + a];
-                    c.mem_slot[pm] = slot;
-                    c.mem_vac[pm] = pos;
-                    c.mem_act[pm] = 1;
-                    c.mem_seg[pm] = (uint8_t)h;
+            } else
+#endif
+            {
+                const bool multi = tid < ncand && c.cand_cnt[tid] > kSlotCap;
+                if (tid < ncand) c.cand_slot[tid] = -1;
+                const int any_multi = __syncthreads_or(multi ? 1 : 0);
+                if (tid == 0) {
+    #pragma unroll
+                    for (int w = 0; w < kMaskWords; ++w) c.frees[w] = c.freew[w];
+                    if (any_multi) {
+                        // domains needing several consecutive slots (> 2 vacancies, rare): first fit, sequentially;
+                        // single-slot domains are placed in parallel below
+                        int nd = 0;
+                        for (int q = 0; q < ncand; ++q) {
+                            const int cnt = c.cand_cnt[q];
+                            if (cnt <= kSlotCap) continue;
+                            if (cnt > kRowCap) { atomicAdd(p.overflow, 1ull); c.cand_slot[q] = -3; continue; }
+                            const int need = (cnt + kSlotCap - 1) / kSlotCap;
+                            int h = -1;
+                            for (int i = 0, run = 0; i < kSlots; ++i) {
+                                run = ((c.frees[i >> 5] >> (i & 31)) & 1u) ? run + 1 : 0;
+                                if (run == need) { h = i - need + 1; break; }
+                            }
+                            if (h < 0) { c.cand_slot[q] = -2; ++nd; continue; }
+                            for (int t = 0; t < need; ++t) c.frees[(h + t) >> 5] &= ~(1u << ((h + t) & 31));
+                            c.cand_slot[q] = (short)h;
+                            for (int t = 1; t < need; ++t) { c.seg_used[h + t] = 2; c.seg_head[h + t] = (uint8_t)h; }
+                        }
+                        c.nmulti_def = nd;
+                    }
+                    c.fpre[0] = 0;
+    #pragma unroll
+                    for (int w = 0; w < kMaskWords; ++w) c.fpre[w + 1] = c.fpre[w] + __popc(c.frees[w]);
+                    c.nfree_single = c.fpre[kMaskWords];
+                }
+                __syncthreads();
+                {
+                    // the j-th single-slot candidate takes the j-th free slot; the rest are deferred
+                    const bool single = tid < ncand && c.cand_slot[tid] == -1;
+                    int nsingle = 0;
+                    const int j = block_excl(single ? 1 : 0, c.wsum, nsingle);
+                    const int nf = c.nfree_single;
+                    if (single) {
+                        if (j < nf) {
+                            int w = 0;
+    #pragma unroll
+                            for (int t = 1; t < kMaskWords; ++t)
+                                if (c.fpre[t] <= j) w = t;
+                            c.cand_slot[tid] = (short)(32 * w + (int)__fns(c.frees[w], 0, j - c.fpre[w] + 1));
+                        } else {
+                            c.cand_slot[tid] = -2;
+                        }
+                    }
+                    __syncthreads();
+                    const int q = tid;
+                    const bool deferred = q < ncand && c.cand_slot[q] == -2;
+                    int ndef = 0;
+                    const int pi = block_excl(deferred ? 1 : 0, c.wsum, ndef);
+                    // carried-over domains are compacted in place to the front of the candidate list (read first)
+                    unsigned cdom = 0;
+                    int coff = 0, ccnt = 0, cslot = -3;
+                    if (q < ncand) { cdom = c.cand_dom[q]; coff = c.cand_off[q]; ccnt = c.cand_cnt[q]; cslot = c.cand_slot[q]; }
+                    __syncthreads();
+                    if (deferred) { c.cand_dom[pi] = cdom; c.cand_off[pi] = coff; c.cand_cnt[pi] = ccnt; }
+                    if (cslot >= 0) {
+                        const int h = cslot;
+                        c.seg_used[h] = 1;
+                        c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
+                        c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_new[h] = 1;
+                        c.seg_run[h] = (p.serial && p.term[cdom]) ? 0 : 1;   // a terminal voxel stays frozen
+                    }
+                    int nplaced = 0;
+                    block_excl(cslot >= 0 ? 1 : 0, c.wsum, nplaced);
+                    if (tid == 0) {
+                        int nr = 0;
+    #pragma unroll
+                        for (int w = 0; w < kMaskWords; ++w) nr += __popc(c.runw[w]);
+                        c.npend = ndef;
+                        c.nrun = nr + nplaced;
+                    }
+                }
+                __syncthreads();
+                // members of newly placed domains: slot ids and positions, one member position per thread (all
+                // loads in flight at once)
+                for (int pm = tid; pm < kRowCap; pm += kThreads) {
+                    const int sl = pm / kSlotCap;
+                    const int h = c.seg_used[sl] == 2 ? c.seg_head[sl] : sl;
+                    const int a = pm - kSlotCap * h;
+                    if (c.seg_used[sl] != 0 && c.seg_new[h] && a < c.seg_cnt[h]) {
+                        const int goff = c.seg_goff[h];
+                        const int slot = p.members[goff + a];
+                        const int4 pos = p.serial ? p.vac[slot] : p.mpos[goff + a];
+                        c.mem_slot[pm] = slot;
+                        c.mem_vac[pm] = pos;
+                        c.mem_act[pm] = 1;
+                        c.mem_seg[pm] = (uint8_t)h;
+                    }
                 }
             }
             __syncthreads();
@@ -522,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             if (tid == 0) lap(d_x[1]);
             // ================= gather + memo lookup: warp per row, lanes = window slots j and j+32 =================
             const int nrows = c.nrows;
-            constexpr int kGR = 8;     // rows per warp in flight
+            constexpr int kGR = AKMC_GATHER_ROWS;     // rows per warp in flight
             for (int r0 = warp; r0 < nrows; r0 += kGR * kWarps) {
                 // kGR rows per warp in flight: memo ways (lanes 0-15 way 0, 16-31 way 1) and window bytes
                 const int k = lane & 15, way = lane >> 4;
@@ -542,8 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         if (k < 8) gv[q] = e.G[k];
                         else if (k == 8) gv[q] = e.R;
                         else if (k == 9) cv[q] = e.clamps;
-                        b0[q] = site_byte(p.species, p.F, v, p.G.off[lane]);
-                        b1[q] = site_byte(p.species, p.F, v, p.G.off[lane + 32]);
+                        b0[q] = site_byte_pk(p.species, p.F, v, off_lo);
+                        b1[q] = site_byte_pk(p.species, p.F, v, off_hi);
                     }
                 }
 #pragma unroll
@@ -575,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         else if (k == 9 && !kTC) rowC[r] = cv[q];
                     }
                     if (lane == 0) { c.row_hit[r] = hit >= 0 ? 1 : 0; c.row_way[r] = hit > 0 ? 1 : 0; }
+                    if (kTC && hit < 0) l1_list_store(r, b0[q], b1[q], l1n, l1l);
                 }
             }
             __syncthreads();
@@ -675,32 +794,53 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             __syncthreads();
         } else {
             // ---- FP32-equivalent evaluator: rounds in lockstep over the cluster
+            if (phase_mode) {
+                // memo insert, part 1, for every miss of this iteration: way 1 <- way 0, way 0 key <- window
+                // (E3 fills way 0's rates); a warp moves kL1Rows entries at a time
+                const int nmiss = c.nmiss;
+                for (int q0 = warp; q0 < nmiss; q0 += kL1Rows * kWarps) {
+                    MemoEntry* me[kL1Rows];
+                    uint4 tm[kL1Rows];
+                    uint32_t kw[kL1Rows];
+#pragma unroll
+                    for (int q = 0; q < kL1Rows; ++q) {
+                        const int qq = q0 + q * kWarps;
+                        tm[q] = make_uint4(0, 0, 0, 0);
+                        kw[q] = 0;
+                        me[q] = nullptr;
+                        if (qq < nmiss) {
+                            const int r = c.miss[qq];
+                            me[q] = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
+                            if (lane < 9) tm[q] = reinterpret_cast<const uint4*>(&me[q][0])[lane];
+                            if (lane < 16) kw[q] = reinterpret_cast<const uint32_t*>(win + r * kWin)[lane];
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < kL1Rows; ++q)
+                        if (me[q] && lane < 9) reinterpret_cast<uint4*>(&me[q][1])[lane] = tm[q];
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < kL1Rows; ++q)
+                        if (me[q] && lane < 16) reinterpret_cast<uint32_t*>(me[q][0].key)[lane] = kw[q];
+                }
+            }
+            if (tid == 0) lap(d_y[0]);
             int k_round = 0;
             for (;;) {
                 int own_n = 0;
                 if (phase_mode) {
                     own_n = min(kRoundRows, max(0, c.nmiss - kRoundRows * k_round));
                     // layer 1 of this round's own rows (two per warp at a time); memo way 1 <- way 0, key <- window
-                    for (int i = warp; i < own_n; i += 2 * kWarps) {
-                        const int i1 = i + kWarps;
-                        const bool two = i1 < own_n;
-                        const int r0 = c.miss[kRoundRows * k_round + i];
-                        const int r1 = two ? c.miss[kRoundRows * k_round + i1] : r0;
-                        MemoEntry* me0 = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r0]];
-                        MemoEntry* me1 = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r1]];
-                        uint4 t0 = make_uint4(0, 0, 0, 0), t1 = make_uint4(0, 0, 0, 0);
-                        if (lane < 9) { t0 = reinterpret_cast<const uint4*>(&me0[0])[lane]; t1 = reinterpret_cast<const uint4*>(&me1[0])[lane]; }
-                        layer1_rows(win + r0 * kWin, two ? win + r1 * kWin : nullptr, p.W.W1f,
-                                    kRoundRows * (int)rank + i, kRoundRows * (int)rank + i1, A_hi, A_lo, g_hi, g_lo, ovf);
-                        if (lane < 9) {
-                            reinterpret_cast<uint4*>(&me0[1])[lane] = t0;
-                            if (two) reinterpret_cast<uint4*>(&me1[1])[lane] = t1;
+                    for (int i = warp; i < own_n; i += kL1Rows * kWarps) {
+                        const int nv = min(kL1Rows, (own_n - i + kWarps - 1) / kWarps);
+                        int rr[kL1Rows], mr[kL1Rows];
+#pragma unroll
+                        for (int q = 0; q < kL1Rows; ++q) {
+                            rr[q] = c.miss[kRoundRows * k_round + (q < nv ? i + q * kWarps : i)];
+                            mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        __syncwarp();
-                        if (lane < 16) {
-                            reinterpret_cast<uint32_t*>(me0[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r0 * kWin)[lane];
-                            if (two) reinterpret_cast<uint32_t*>(me1[0].key)[lane] = reinterpret_cast<const uint32_t*>(win + r1 * kWin)[lane];
-                        }
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                                    (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) {
                         hdr[rank].n = own_n;
@@ -716,36 +856,44 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     own_n = min(kRoundRows, max(0, nrows_eval - base));
                     for (int i = warp; i < own_n; i += kWarps) {
                         const int g = base + i;
+                        uint8_t a0, a1;
                         if (p.windows) {
-                            win[i * kWin + lane] = p.windows[(size_t)g * kWin + lane];
-                            win[i * kWin + lane + 32] = p.windows[(size_t)g * kWin + lane + 32];
-                            if (lane < 8) win8[i * 8 + lane] = p.windows[(size_t)g * kWin + lane];
+                            a0 = p.windows[(size_t)g * kWin + lane];
+                            a1 = p.windows[(size_t)g * kWin + lane + 32];
                         } else {
                             const int slot = p.rows ? p.rows[g] : g;
                             const int4 v = p.vac[slot];
                             const bool live = v.x >= 0;                 // departed slot (multi-rank): any window
-                            const uint8_t a0 = live ? site_byte(p.species, p.F, v, p.G.off[lane]) : (uint8_t)kFe;
-                            win[i * kWin + lane] = a0;
-                            win[i * kWin + lane + 32] = live ? site_byte(p.species, p.F, v, p.G.off[lane + 32]) : (uint8_t)kFe;
-                            if (lane < 8) win8[i * 8 + lane] = a0;
+                            a0 = live ? site_byte_pk(p.species, p.F, v, off_lo) : (uint8_t)kFe;
+                            a1 = live ? site_byte_pk(p.species, p.F, v, off_hi) : (uint8_t)kFe;
                         }
+                        win[i * kWin + lane] = a0;
+                        win[i * kWin + lane + 32] = a1;
+                        if (lane < 8) win8[i * 8 + lane] = a0;
+                        l1_list_store(i, a0, a1, l1n, l1l);
                     }
                     __syncwarp();
-                    for (int i = warp; i < own_n; i += 2 * kWarps) {
-                        const int i1 = i + kWarps;
-                        const bool two = i1 < own_n;
-                        layer1_rows(win + i * kWin, two ? win + i1 * kWin : nullptr, p.W.W1f,
-                                    kRoundRows * (int)rank + i, kRoundRows * (int)rank + i1, A_hi, A_lo, g_hi, g_lo, ovf);
+                    for (int i = warp; i < own_n; i += kL1Rows * kWarps) {
+                        const int nv = min(kL1Rows, (own_n - i + kWarps - 1) / kWarps);
+                        int rr[kL1Rows], mr[kL1Rows];
+#pragma unroll
+                        for (int q = 0; q < kL1Rows; ++q) {
+                            rr[q] = q < nv ? i + q * kWarps : i;
+                            mr[q] = kRoundRows * (int)rank + i + q * kWarps;
+                        }
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                                    (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
                 }
                 wd(4, k_round, own_n);
+                if (tid == 0) lap(d_y[1]);
                 // ---- exchange: header (DSMEM) + this CTA's h1 rows (8-row groups 4r..4r+3), multicast from the
                 //      L2 staging copy into every peer's A (one L2 read, no SM-to-SM bandwidth limit)
                 fence_async_smem();
                 fence_async_global();
                 __syncthreads();
-                if (tid == 0) lap(d_x[3]);
+                if (tid == 0) lap(d_y[2]);
                 if (warp == 0 && lane < kClusterN) {        // lane d signals CTA d
                     const uint32_t d = (uint32_t)lane;
                     const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
@@ -1054,9 +1202,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         }
         __syncthreads();
         if (tid == 0) lap(d_cs);
+        trace_end();
     }
+    if (tid == 0 && p.diag && phase_mode) atomicAdd(p.diag + 96 + 512 + min(tr_it, 63), 1ull);
     if (tid == 0 && p.diag) {
         d_cc = d_x[0] + d_x[1] + d_x[2];
+        d_x[3] = d_y[0] + d_y[1] + d_y[2];
         d_cr += d_x[3] + d_x[4] + d_x[5] + d_x[6] + d_x[7];
         atomicAdd(p.diag + 0, d_it);
         atomicMax(p.diag + 1, d_it);
@@ -1070,6 +1221,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         atomicAdd(p.diag + 9, (unsigned long long)(clock64() - t_start));
         atomicAdd(p.diag + 10, 1ull * (phase_mode ? 1 : 0));
         for (int q = 0; q < 8; ++q) atomicAdd(p.diag + 11 + q, (unsigned long long)d_x[q]);
+        for (int q = 0; q < 3; ++q) atomicAdd(p.diag + 20 + q, (unsigned long long)d_y[q]);
+        for (int q = 0; q < 4; ++q) atomicAdd(p.diag + 24 + q, (unsigned long long)d_z[q]);
         atomicAdd(p.diag + 19, (unsigned long long)d_xk);
     }
 

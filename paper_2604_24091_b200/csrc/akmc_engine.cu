@@ -24,6 +24,33 @@
 #include "akmc_engine.cuh"
 #include "akmc_ptx.cuh"
 
+// Compile-time variants (A/B builds via build.build(out=..., defines=...) and AKMC_LIB; tools/ab_probe.py).
+// Defaults are the measured best on B200 (C5, same box, profiles/r01_engine_timing.md):
+#ifndef AKMC_L1_ROWS
+#define AKMC_L1_ROWS 2          // layer-1 rows per warp in flight (4: register spills, slower)
+#endif
+#ifndef AKMC_L1_BATCH
+#define AKMC_L1_BATCH 2         // W1' rows per layer-1 row in flight
+#endif
+#ifndef AKMC_REFILL_FAST
+#define AKMC_REFILL_FAST 1      // skip slot placement when nothing is pending (-2 %)
+#endif
+#ifndef AKMC_GATHER_ROWS
+#define AKMC_GATHER_ROWS 8      // gather rows per warp in flight
+#endif
+#ifndef AKMC_W1_EVICT_LAST
+#define AKMC_W1_EVICT_LAST 0    // L2 evict_last policy on W1' loads (no effect measured)
+#endif
+#ifndef AKMC_PREFETCH
+#define AKMC_PREFETCH 0         // L2 prefetch of the next window/memo at hop/placement (+1.6 %, slower)
+#endif
+#ifndef AKMC_XCHG_DSMEM
+#define AKMC_XCHG_DSMEM 0       // h1 rows by DSMEM bulk copies instead of L2-staged multicast (+5 %, slower)
+#endif
+#ifndef AKMC_L1_PROBE
+#define AKMC_L1_PROBE 0         // cycle laps inside layer 1 (diagnostic)
+#endif
+
 namespace akmc {
 
 namespace {
@@ -185,12 +212,31 @@ __device__ __forceinline__ uint8_t site_byte_pk(const uint8_t* species, const Fr
 // W1' rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
 // row m of the A operand (M-major no-swizzle: 8-row group g at g*4096, core column c at c*128) and into the
 // CTA's L2 staging block.  The two rows' loads are interleaved (independent latency chains).
+// L2 prefetch of what the next gather of a vacancy reads: the <= 8 bricks its window touches (reach 2 cells)
+// and its two memo ways
+__device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr)); }
+__device__ __forceinline__ void prefetch_vacancy(const uint8_t* species, const Frame& F, const int4& v, const void* memo2)
+{
+    // (clamped to the storage: a vacancy that just left a decomposed block may sit half a cell outside it)
+    const int pv[3] = {v.y, v.z, v.w};
+    int b0[3], b1[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        b0[a] = max(0, (((pv[a] - 4) >> 1) + kHalo) >> 2);
+        b1[a] = min(F.NB[a] - 1, (((pv[a] + 4) >> 1) + kHalo) >> 2);
+    }
+    const uint8_t* vb = species + (int64_t)v.x * F.sites;
+    for (int bz = b0[2]; bz <= b1[2]; ++bz)
+        for (int by = b0[1]; by <= b1[1]; ++by)
+            for (int bx = b0[0]; bx <= b1[0]; ++bx)
+                prefetch_l2(vb + ((int64_t)((uint32_t)bx + (uint32_t)F.NB[0] * ((uint32_t)by + (uint32_t)F.NB[1] * (uint32_t)bz)) << 7));
+    const uint8_t* m = reinterpret_cast<const uint8_t*>(memo2);
+    prefetch_l2(m); prefetch_l2(m + 128); prefetch_l2(m + 256);
+}
+
 // non-Fe slots of a window as two ballot masks (slots 0-31, 32-63); entry e of the slot-ordered list is the
 // e-th set bit (no list is stored: the masks are warp-uniform registers)
 struct L1Masks { unsigned m0, m1; int c0, n; };
-#ifndef AKMC_L1_BATCH
-#define AKMC_L1_BATCH 2
-#endif
 constexpr int kL1Batch = AKMC_L1_BATCH;                  // W1' rows per row in flight (an RPV window has ~1.6 non-Fe slots)
 __device__ __forceinline__ L1Masks l1_masks(const uint8_t* w)
 {
@@ -246,26 +292,13 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
     *reinterpret_cast<uint4*>(A_lo + off) = vl;
     // the same 16 B into the L2 staging block of this CTA (row m % kRoundRows of its block)
     const uint32_t goff = (uint32_t)((m % kRoundRows) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
+#if !AKMC_XCHG_DSMEM
     *reinterpret_cast<uint4*>(g_hi + goff) = vh;
     *reinterpret_cast<uint4*>(g_lo + goff) = vl;
+#endif
 }
 
 // layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once
-#ifndef AKMC_L1_ROWS
-#define AKMC_L1_ROWS 2
-#endif
-#ifndef AKMC_W1_EVICT_LAST
-#define AKMC_W1_EVICT_LAST 0
-#endif
-#ifndef AKMC_L1_PROBE
-#define AKMC_L1_PROBE 0
-#endif
-#ifndef AKMC_REFILL_FAST
-#define AKMC_REFILL_FAST 1
-#endif
-#ifndef AKMC_GATHER_ROWS
-#define AKMC_GATHER_ROWS 8
-#endif
 constexpr int kL1Rows = AKMC_L1_ROWS;
 __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
                                             const uint16_t* l1l, const float* __restrict__ W1f,
@@ -417,10 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     // diagnostics (thread 0): iterations, rounds, evaluation rounds, cycles in control / rounds / selection
     unsigned long long d_it = 0, d_rounds = 0, d_erounds = 0, d_refill = 0;
     long long d_cc = 0, d_cr = 0, d_cs = 0;
-    long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long d_y[4] = {0, 0, 0, 0};
-    long long d_z[4] = {0, 0, 0, 0};              // AKMC_L1_PROBE: layer-1 sub-steps of warp 0              // L1 lap split: memo move | layer 1 | async fences + barrier
-    long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)   // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
+    long long d_x[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // sub-phase cycles: refill, rows, gather | L1, xchg, L2+E2, L3+part, E3
+    long long d_y[4] = {0, 0, 0, 0};              // L1 lap split: memo move | layer 1 | async fences + barrier
+    long long d_z[4] = {0, 0, 0, 0};              // AKMC_L1_PROBE: layer-1 sub-steps of warp 0
+    long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)
     const long long t_start = clock64();
     unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
     long long t_mark = t_start;
@@ -617,6 +650,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const int goff = c.seg_goff[h];
                         const int slot = p.members[goff + a];
                         const int4 pos = p.serial ? p.vac[slot] : p.mpos[goff + a];
+#if AKMC_PREFETCH
+                        prefetch_vacancy(p.species, p.F, pos, p.memo + 2 * (size_t)slot);
+#endif
                         c.mem_slot[pm] = slot;
                         c.mem_vac[pm] = pos;
                         c.mem_act[pm] = 1;
@@ -891,12 +927,29 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 // ---- exchange: header (DSMEM) + this CTA's h1 rows (8-row groups 4r..4r+3), multicast from the
                 //      L2 staging copy into every peer's A (one L2 read, no SM-to-SM bandwidth limit)
                 fence_async_smem();
+#if !AKMC_XCHG_DSMEM
                 fence_async_global();
+#endif
                 __syncthreads();
                 if (tid == 0) lap(d_y[2]);
                 if (warp == 0 && lane < kClusterN) {        // lane d signals CTA d
                     const uint32_t d = (uint32_t)lane;
                     const uint32_t rg = (uint32_t)((own_n + 7) >> 3);
+#if AKMC_XCHG_DSMEM
+                    // h1 rows straight from this CTA's A into each peer's A (SM-to-SM, no L2 round trip)
+                    if (d == rank) {
+                        mbar_arrive(bar_req);
+                    } else {
+                        const uint32_t cb = map_to(bar_req, d);
+                        const uint32_t aoff = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
+                        mbar_remote_expect_tx(cb, 16u + 2u * rg * kRowGroupA);
+                        bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
+                        if (rg) {
+                            bulk_s2peer(map_to(smem_u32(A_hi + aoff), d), smem_u32(A_hi + aoff), rg * kRowGroupA, cb);
+                            bulk_s2peer(map_to(smem_u32(A_lo + aoff), d), smem_u32(A_lo + aoff), rg * kRowGroupA, cb);
+                        }
+                    }
+#else
                     if (d == rank) {
                         mbar_arrive(bar_req);
                         if (rg) {
@@ -910,10 +963,15 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         mbar_remote_expect_tx(cb, 16u + 2u * rg * kRowGroupA);
                         bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
                     }
+#endif
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 mbar_wait_cluster(bar_req, ph_req);
                 ph_req ^= 1u;
+#if AKMC_XCHG_DSMEM
+                // the outgoing copies read this CTA's row block, which E2 overwrites with h2
+                if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
                 wd(5, k_round, own_n);
                 if (tid == 0) { const long long before = d_x[4]; lap(d_x[4]); if (k_round > 0) d_xk += d_x[4] - before; }
                 int n_s[kClusterN];
@@ -1164,6 +1222,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const uint8_t tn = win8[r * 8 + k];
                         write_site(p.species, p.F, ov.x, ov.y, ov.z, ov.w, tn);
                         write_site(p.species, p.F, nv.x, nv.y, nv.z, nv.w, (uint8_t)kVac);
+#if AKMC_PREFETCH
+                        prefetch_vacancy(p.species, p.F, nv, p.memo + 2 * (size_t)slot);
+#endif
                         p.vac[slot] = nv;
                         c.mem_vac[moff + a] = nv;
                         long long d2 = 0;

@@ -220,7 +220,15 @@ def run_ours(args):
     sim.set_stream(stream.cuda_stream)
     cs = ClockSampler(local).__enter__()
     t_ramp = time.perf_counter()                      # untimed clock ramp before the warm-up steps
-    while time.perf_counter() - t_ramp < args.ramp_s:
+    flag = torch.ones(1, dtype=torch.int32, device=dev)
+    while True:
+        # every rank must run the same number of steps (each sweep exchanges halo deltas with the peers):
+        # rank 0's clock decides when the ramp ends
+        flag.fill_(1 if time.perf_counter() - t_ramp < args.ramp_s else 0)
+        if world > 1:
+            dist.broadcast(flag, src=0)
+        if not int(flag.item()):
+            break
         sim.step(1)
     for _ in range(args.warmup):
         sim.step(1)

@@ -124,7 +124,7 @@ def make_inputs(name: str, rank: int, device):
 
 def sim_config(name: str, precision: int, model: int, lam: float, E0, rank: int = 0, world: int = 1, nccl_id=b""):
     """C3/C5 (sublattice) at N > 1: the global lattice is grid_for(N) blocks of `cells`, one per rank, with
-    NCCL halo deltas between phases; C1/C2/C4 (serial BKL): independent voxels per rank, no collective."""
+    halo deltas between phases over NVLink peer memory; C1/C2/C4 (serial BKL): independent voxels per rank, no collective."""
     import paper_2604_24091_b200 as akmc
     from paper_2604_24091_b200 import dist as D
     pr, cells, nvox = workload(name)
@@ -355,8 +355,8 @@ def run_ours(args):
                            "domain_cells": list(cfg.domain_cells), "lambda": args.lam, "window_s": cfg.window_s,
                            "model": "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA",
                            "parallelism": ("1 GPU" if world == 1 else
-                                           (f"spatial blocks {'x'.join(map(str, cfg.gpu_grid))}, NCCL halo deltas "
-                                            "between phases" if cfg.world > 1 else f"independent voxels x{world}")),
+                                           (f"spatial blocks {'x'.join(map(str, cfg.gpu_grid))}, halo deltas between "
+                                            "phases written into the peers' mailboxes over NVLink (CUDA IPC)" if cfg.world > 1 else f"independent voxels x{world}")),
                            "l2": "inputs > L2 (lattice %.2f GB per GPU)" % (sites / 1e9)},
                 "sim_seconds_per_wall_second": (sim_s * world / world) / (ms_max / 1e3),
                 "events_per_s": float(sm[2]) / (ms_max / 1e3),

@@ -194,6 +194,16 @@ struct akmc_handle {
     int* d_dist_overflow = nullptr;
     cudaGraphExec_t phase_exec[8] = {};
     int64_t exchanges = 0, exchange_bytes = 0;
+    // per-phase exchange over NVLink peer memory (CUDA IPC mailboxes; AKMC_EXCHANGE=nccl selects NCCL p2p)
+    bool p2p = false;
+    int4* d_mbox = nullptr;                    // [npeer][2][cap + 1]
+    unsigned long long* d_mflag = nullptr;     // [kMaxPeers]
+    int* d_pcnt = nullptr;
+    unsigned int* d_pdone = nullptr;
+    PeerBoxes PB{};
+    void* ipc_box[kMaxPeers] = {};
+    void* ipc_flag[kMaxPeers] = {};
+    unsigned long long epoch = 0;
 };
 
 namespace {
@@ -233,7 +243,12 @@ void free_all(akmc_handle* h)
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     if (h->h_watch) cudaFreeHost(h->h_watch);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
-    void* dptrs[] = {h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow};
+    for (int r = 0; r < kMaxPeers; ++r) {
+        if (h->ipc_box[r]) cudaIpcCloseMemHandle(h->ipc_box[r]);
+        if (h->ipc_flag[r]) cudaIpcCloseMemHandle(h->ipc_flag[r]);
+    }
+    void* dptrs[] = {h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
+                     h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     for (int q = 0; q < 8; ++q)
@@ -570,6 +585,75 @@ int halo_fill(akmc_handle* h)
     return AKMC_OK;
 }
 
+// distinct ranks at the 26 neighbour offsets along decomposed (non-wrap) axes of the block at grid coords rc
+int peer_list(const akmc_config& c, const int rc[3], const int wrap[3], int* out)
+{
+    int np = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int d[3] = {dx, dy, dz};
+                bool skip = dx == 0 && dy == 0 && dz == 0;
+                for (int a = 0; a < 3; ++a)
+                    if (wrap[a] && d[a] != 0) skip = true;
+                if (skip) continue;
+                const int r = rank_of(c, rc[0] + dx, rc[1] + dy, rc[2] + dz);
+                if (r == rank_of(c, rc[0], rc[1], rc[2])) continue;
+                bool seen = false;
+                for (int i = 0; i < np; ++i) seen |= (out[i] == r);
+                if (!seen) out[np++] = r;
+            }
+    return np;
+}
+
+// mailboxes for the per-phase exchange, mapped into every peer by CUDA IPC (handles all-gathered over NCCL)
+int setup_p2p(akmc_handle* h)
+{
+    const akmc_config& c = h->cfg;
+    const int np = h->DP.npeer;
+    const size_t per = (size_t)(h->DP.cap + 1);
+    CK(h, cudaMalloc(&h->d_mbox, std::max<size_t>(1, (size_t)np * 2 * per) * sizeof(int4)));
+    CK(h, cudaMalloc(&h->d_mflag, kMaxPeers * sizeof(unsigned long long)));
+    CK(h, cudaMalloc(&h->d_pcnt, kMaxPeers * sizeof(int)));
+    CK(h, cudaMalloc(&h->d_pdone, sizeof(unsigned int)));
+    CK(h, cudaMemset(h->d_mbox, 0, std::max<size_t>(1, (size_t)np * 2 * per) * sizeof(int4)));
+    CK(h, cudaMemset(h->d_mflag, 0, kMaxPeers * sizeof(unsigned long long)));
+    CK(h, cudaMemset(h->d_pcnt, 0, kMaxPeers * sizeof(int)));
+    CK(h, cudaMemset(h->d_pdone, 0, sizeof(unsigned int)));
+    cudaIpcMemHandle_t mine[2];
+    CK(h, cudaIpcGetMemHandle(&mine[0], h->d_mbox));
+    CK(h, cudaIpcGetMemHandle(&mine[1], h->d_mflag));
+    const size_t hb = sizeof(mine);
+    uint8_t *d_h = nullptr, *d_all = nullptr;
+    CK(h, cudaMalloc(&d_h, hb));
+    CK(h, cudaMalloc(&d_all, hb * c.world));
+    CK(h, cudaMemcpy(d_h, mine, hb, cudaMemcpyHostToDevice));
+    NCK(h, ncclAllGather(d_h, d_all, hb, ncclChar, h->comm, h->stream));
+    std::vector<cudaIpcMemHandle_t> all((size_t)2 * c.world);
+    CK(h, cudaMemcpyAsync(all.data(), d_all, hb * c.world, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    cudaFree(d_h);
+    cudaFree(d_all);
+    for (int r = 0; r < np; ++r) {
+        const int pr = h->peer_rank[r];
+        const int prc[3] = {pr % c.gpu_grid[0], (pr / c.gpu_grid[0]) % c.gpu_grid[1], pr / (c.gpu_grid[0] * c.gpu_grid[1])};
+        int theirs[kMaxPeers];
+        const int tn = peer_list(c, prc, h->F.wrap, theirs);
+        int me = -1;
+        for (int i = 0; i < tn; ++i)
+            if (theirs[i] == c.rank) me = i;
+        if (me < 0) return fail(h, AKMC_ERR_RUNTIME, "peer lists are not symmetric");
+        CK(h, cudaIpcOpenMemHandle(&h->ipc_box[r], all[(size_t)2 * pr], cudaIpcMemLazyEnablePeerAccess));
+        CK(h, cudaIpcOpenMemHandle(&h->ipc_flag[r], all[(size_t)2 * pr + 1], cudaIpcMemLazyEnablePeerAccess));
+        h->PB.box[r] = reinterpret_cast<int4*>(h->ipc_box[r]) + (size_t)me * 2 * per;
+        h->PB.flag[r] = reinterpret_cast<unsigned long long*>(h->ipc_flag[r]) + me;
+    }
+    h->PB.cnt = h->d_pcnt;
+    h->PB.done = h->d_pdone;
+    h->p2p = true;
+    return AKMC_OK;
+}
+
 int init_multi(akmc_handle* h)
 {
     const akmc_config& c = h->cfg;
@@ -580,26 +664,13 @@ int init_multi(akmc_handle* h)
     NCK(h, ncclCommInitRank(&h->comm, c.world, id, c.rank));
     const auto tv1 = std::chrono::steady_clock::now();
     // peers: distinct ranks at the 26 neighbour offsets along decomposed (non-wrap) axes
-    int np = 0;
-    for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int d[3] = {dx, dy, dz};
-                bool skip = dx == 0 && dy == 0 && dz == 0;
-                for (int a = 0; a < 3; ++a)
-                    if (h->F.wrap[a] && d[a] != 0) skip = true;
-                if (skip) continue;
-                const int r = rank_of(c, h->rc[0] + dx, h->rc[1] + dy, h->rc[2] + dz);
-                if (r == c.rank) continue;
-                bool seen = false;
-                for (int i = 0; i < np; ++i) seen |= (h->peer_rank[i] == r);
-                if (seen) continue;
-                h->peer_rank[np] = r;
-                h->DP.peerO[np][0] = (r % c.gpu_grid[0]) * c.cells[0];
-                h->DP.peerO[np][1] = ((r / c.gpu_grid[0]) % c.gpu_grid[1]) * c.cells[1];
-                h->DP.peerO[np][2] = (r / (c.gpu_grid[0] * c.gpu_grid[1])) * c.cells[2];
-                ++np;
-            }
+    const int np = peer_list(c, h->rc, h->F.wrap, h->peer_rank);
+    for (int i = 0; i < np; ++i) {
+        const int r = h->peer_rank[i];
+        h->DP.peerO[i][0] = (r % c.gpu_grid[0]) * c.cells[0];
+        h->DP.peerO[i][1] = ((r / c.gpu_grid[0]) % c.gpu_grid[1]) * c.cells[1];
+        h->DP.peerO[i][2] = (r / (c.gpu_grid[0] * c.gpu_grid[1])) * c.cells[2];
+    }
     h->DP.npeer = np;
     h->DP.cap = 8192;
     h->S.logcap = 1 << 17;
@@ -655,6 +726,11 @@ int init_multi(akmc_handle* h)
     for (int64_t i = 0; i < h->nvac; ++i)
         gid[(size_t)i] = (int)(std::lower_bound(all.begin(), all.end(), mine[(size_t)i]) - all.begin());
     if (h->nvac) CK(h, cudaMemcpy(h->d_gid, gid.data(), (size_t)h->nvac * sizeof(int), cudaMemcpyHostToDevice));
+    const char* ex = std::getenv("AKMC_EXCHANGE");
+    if (!(ex && std::strcmp(ex, "nccl") == 0)) {
+        const int prc = setup_p2p(h);
+        if (prc != AKMC_OK) return prc;
+    }
     const auto tv2 = std::chrono::steady_clock::now();
     const int rc = halo_fill(h);
     const auto tv3 = std::chrono::steady_clock::now();
@@ -1095,6 +1171,18 @@ static int exchange_deltas(akmc_handle* h)
 {
     const int np = h->DP.npeer;
     const size_t per = (size_t)(h->DP.cap + 1);
+    if (h->p2p) {
+        // deltas straight into the peers' mailboxes over NVLink, flag per peer; wait + apply (akmc_dist.cuh)
+        h->epoch += 1;
+        pack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
+                                                          h->PB, h->epoch, h->d_dist_overflow);
+        unpack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
+                                                            h->d_vac, h->d_gid, h->d_nvac, h->vcap, h->d_dist_overflow);
+        CK(h, cudaGetLastError());
+        h->total.kernel_launches += 2;
+        h->exchanges += 1;
+        return AKMC_OK;
+    }
     pack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP,
                                                           h->d_species, h->d_send,
                                                           h->d_dist_overflow);

@@ -1,4 +1,4 @@
-"""Multi-GPU parity (C5 spatial decomposition, NCCL halo deltas between phases): the same global problem
+"""Multi-GPU parity (C5 spatial decomposition, halo deltas between phases over NVLink peer memory, NCCL only at init): the same global problem
 on 2 ranks and on 1 rank gives bit-identical lattices, vacancy lists, clocks and event counts (GPU-count
 invariance, SURVEY 8(c) decomposition pin), and equals the FP64 oracle.  Needs >= 2 GPUs."""
 import json

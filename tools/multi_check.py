@@ -1,5 +1,5 @@
 """Multi-GPU spatial decomposition check (C5 path): run the same global problem on
-`world` ranks (NCCL halo deltas between phases) and on one rank, and compare the final global lattices,
+`world` ranks (halo deltas between phases) and on one rank, and compare the final global lattices,
 vacancy lists, clocks and event counts bit for bit (GPU-count invariance); optionally also against the
 FP64 CPU oracle.  Launch:  torchrun --nproc-per-node N tools/multi_check.py --grid gx gy gz ..."""
 import argparse

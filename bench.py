@@ -217,6 +217,11 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     # ---------------- device-resident timing ("value"): production path (per-sweep CUDA graph)
     sim = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    vT = None
+    if args.voxel_T:
+        # C4 variant: per-voxel T uniform in 558-577 K, distinct per rank
+        vT = synth.voxel_temperatures(cfg.n_voxels, seed=pr.seed + 1000 * rank + 7)
+        sim.set_voxel_temperatures(vT)
     sim.set_stream(stream.cuda_stream)
     cs = ClockSampler(local).__enter__()
     t_ramp = time.perf_counter()                      # untimed clock ramp before the warm-up steps
@@ -288,6 +293,8 @@ def run_ours(args):
         dist.barrier()
     t0 = time.perf_counter()
     sim2 = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    if vT is not None:
+        sim2.set_voxel_temperatures(vT)
     t_init = time.perf_counter() - t0
     hop_e2e = 0
     for _ in range(args.steps):
@@ -353,6 +360,7 @@ def run_ours(args):
                            "voxels_per_gpu": cfg.n_voxels, "sites_per_gpu": sites,
                            "vacancies_per_gpu": pr.n_vac_per_voxel * cfg.n_voxels,
                            "domain_cells": list(cfg.domain_cells), "lambda": args.lam, "window_s": cfg.window_s,
+                           "temperature_K": ("per voxel, uniform 558-577" if vT is not None else cfg.temperature_K),
                            "model": "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA",
                            "parallelism": ("1 GPU" if world == 1 else
                                            (f"spatial blocks {'x'.join(map(str, cfg.gpu_grid))}, halo deltas between "
@@ -392,6 +400,7 @@ def main():
     ap.add_argument("--model", default="mlp", choices=["mlp", "pair"])
     ap.add_argument("--lam", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--voxel-T", action="store_true", help="per-voxel temperature uniform in 558-577 K (C4 variant)")
     ap.add_argument("--ramp-s", type=float, default=1.0, help="untimed clock ramp before the warm-up steps")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -141,6 +141,14 @@ int akmc_rates(akmc_handle* h, double* rates_out, double* barriers_out);
  * (mask not applied).  Uses the handle's weights/parameters; state untouched.                   */
 int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t precision, double* E_out);
 
+/* Per-voxel temperature (SURVEY 8(d) C4 variant "per-voxel T uniform in 558-577 K"; the voxels
+ * of a mesoscopic model see different local conditions).  T_K: host [n] Kelvin, n == n_voxels, each
+ * finite and > 0, copied.  Every later rate of a vacancy in voxel v is nu0 exp(-E/(kB*T_v))
+ * (Eq. 8) with kB*T_v formed as one IEEE product, as for the uniform T; the barrier memo is cleared
+ * (its rates were formed at the old T).  akmc_eval_windows keeps the configured temperature_K.
+ * Callable between steps in any mode; AKMC_ERR_INVALID on a wrong n or a bad T (state unchanged). */
+int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n);
+
 /* Launch the library's kernels on this CUDA stream (cudaStream_t as void*; NULL = the handle's
  * own stream).  profile != 0 records CUDA events around every barrier-kernel launch (mlp_ms).  */
 int akmc_set_stream(akmc_handle* h, void* stream);

@@ -34,7 +34,7 @@ class _Cfg(C.Structure):
     _fields_ = [("cells", C.c_int32 * 3), ("n_voxels", C.c_int32), ("T", C.c_double),
                 ("nu0", C.c_double), ("kB", C.c_double), ("model", C.c_int32),
                 ("domain", C.c_int32 * 3), ("window_s", C.c_double), ("seed", C.c_uint64),
-                ("strict", C.c_int32)]
+                ("strict", C.c_int32), ("voxel_T", C.c_void_p)]
 
 
 _lib = None
@@ -83,6 +83,7 @@ class Config:
     window_s: float = 0.0
     seed: int = 1
     strict: int = 0
+    voxel_T: tuple = None    # per-voxel temperature K (C4 variant) or None = T everywhere
 
     def c(self) -> _Cfg:
         s = _Cfg()
@@ -94,6 +95,11 @@ class Config:
         s.window_s = float(self.window_s)
         s.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
         s.strict = int(self.strict)
+        if self.voxel_T is not None:
+            vt = np.ascontiguousarray(self.voxel_T, dtype=np.float64)
+            assert vt.shape == (self.n_voxels,), vt.shape
+            s._vt = vt                          # keeps the array alive with the struct
+            s.voxel_T = vt.ctypes.data
         return s
 
     @property

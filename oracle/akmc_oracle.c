@@ -51,6 +51,8 @@ typedef struct {
     double  window_s;     /* Delta_win per phase */
     uint64_t seed;        /* Philox key */
     int32_t strict;       /* 1: recompute active sets by full scan (slow, checks A20) */
+    const double* voxel_T;/* [n_voxels] K per voxel or NULL (= T everywhere): the C4 variant with
+                             per-voxel temperature ("temperatures ... vary") */
 } orc_cfg;
 
 /* ------------------------------------------------------------------ */
@@ -382,7 +384,7 @@ static int vac_rates(const orc_cfg* c, const geom* g, const uint8_t* sp, int64_t
         window_of(g, sp, vsite, sigma);
         orc_mlp_fp64(sigma, mlp, E);
     }
-    double kT = c->kB * c->T;
+    double kT = c->kB * (c->voxel_T ? c->voxel_T[vox] : c->T);   /* the vacancy's voxel's T */
     for (int k = 0; k < 8; ++k) {
         int pn[3] = {pv[0] + g_win[k][0], pv[1] + g_win[k][1], pv[2] + g_win[k][2]};
         int64_t nsite = pos_site(g, vox, pn);

@@ -67,13 +67,15 @@ def load() -> C.CDLL:
     lib.akmc_debug_extended.argtypes = [P, P]
     lib.akmc_set_stream.argtypes = [P, P]
     lib.akmc_set_profiling.argtypes = [P, C.c_int32]
+    lib.akmc_set_voxel_temperatures.argtypes = [P, P, C.c_int32]
     lib.akmc_free.argtypes = [P]
     lib.akmc_free.restype = None
     lib.akmc_last_error.argtypes = [P]
     lib.akmc_last_error.restype = C.c_char_p
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
-              "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended"):
+              "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
+              "akmc_set_voxel_temperatures"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -209,6 +211,11 @@ class Simulation:
 
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.akmc_set_stream(self.h, C.c_void_p(int(stream_ptr)) if stream_ptr else None))
+
+    def set_voxel_temperatures(self, T_K):
+        """Per-voxel temperature in K, one per voxel (C4 variant); clears the barrier memo."""
+        t = np.ascontiguousarray(T_K, dtype=np.float64).reshape(-1)
+        self._check(self.lib.akmc_set_voxel_temperatures(self.h, _ptr(t), int(t.size)))
 
     def set_profiling(self, on: bool):
         self._check(self.lib.akmc_set_profiling(self.h, 1 if on else 0))

@@ -156,6 +156,7 @@ struct akmc_handle {
     bool serial_engine = false;       // serial / voxel-batch mode runs through the engine (voxel = domain)
     int n_clusters = 0;
     MemoEntry* d_memo = nullptr;      // [vcap][2]
+    double* d_kT = nullptr;           // [n_voxels] kB * T_v (per-voxel temperature, C4 variant)
     float* d_W1f = nullptr;           // [385][256]
     uint8_t* d_W2e = nullptr;         // [8][32 KiB]
     uint8_t* d_W3e = nullptr;         // [8][2 KiB]
@@ -234,7 +235,7 @@ void free_all(akmc_handle* h)
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
                     h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
-                    h->d_stage, h->d_canon, h->d_wstore};
+                    h->d_stage, h->d_canon, h->d_wstore, h->d_kT};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->d_phase) cudaFree(h->d_phase);
@@ -944,6 +945,14 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
     CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
+    {
+        // per-voxel kT (uniform until akmc_set_voxel_temperatures); the pointer is fixed for the handle's
+        // life, so kernel parameters captured in graphs stay valid when the values change
+        const std::vector<double> kT((size_t)h->nvox, h->P.kT);
+        CKI(cudaMalloc(&h->d_kT, kT.size() * sizeof(double)));
+        CKI(cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
+        h->P.kT_vox = h->d_kT;
+    }
     if (!h->sub) {
         // serial / voxel-batch mode through the engine: one segment per voxel, members = its slots in order
         std::vector<int> vs((size_t)h->nvox + 1);
@@ -973,6 +982,22 @@ int akmc_set_stream(akmc_handle* h, void* stream)
     if (!h) return AKMC_ERR_RUNTIME;
     CK(h, cudaStreamSynchronize(h->stream));
     h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+    return AKMC_OK;
+}
+
+int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (!T_K || n != h->nvox) return fail(h, AKMC_ERR_INVALID, "voxel temperatures: need one per voxel");
+    std::vector<double> kT((size_t)n);
+    for (int v = 0; v < n; ++v) {
+        if (!(T_K[v] > 0.0) || !std::isfinite(T_K[v])) return fail(h, AKMC_ERR_INVALID, "temperature must be > 0 (S:154)");
+        kT[(size_t)v] = h->cfg.kB * T_K[v];                  // the same IEEE product as the uniform kT
+    }
+    CK(h, cudaStreamSynchronize(h->stream));
+    CK(h, cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // memoised rates were formed at the old temperatures (R7: the memo maps window -> rates at fixed T)
+    CK(h, cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
     return AKMC_OK;
 }
 

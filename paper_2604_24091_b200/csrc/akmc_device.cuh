@@ -34,6 +34,7 @@ struct PhysParams {
     double kT;                           // kB * T (IEEE product, computed once on the host)
     double nu0;
     double inv_kT;                       // 1 / kT (FP32-equivalent mode only; FP64 mode divides, A29)
+    const double* kT_vox;                // [n_voxels] kB * T_v (C4 per-voxel temperature; always set by init)
 };
 
 // Lattice frame of one voxel.  The voxel's L^3 owned cells are stored inside a halo of kHalo cells
@@ -122,10 +123,17 @@ __device__ __forceinline__ double det_log(double u)
     return __fma_rn(de, ln2_hi, __fma_rn(de, ln2_lo, lm));
 }
 
-// Gamma = nu0 * det_exp(-(E / kT)), masked -> exactly 0 (Eq. 1; Eq. 8)
-__device__ __forceinline__ double arrhenius(double E, const PhysParams& P)
+// kT of the voxel a vacancy lives in (SURVEY 8(d) C4 variant: per-voxel T); vox < 0 (a bare
+// window, akmc_eval_windows) -> the configured T
+__device__ __forceinline__ double kT_of(const PhysParams& P, int vox)
 {
-    return __dmul_rn(P.nu0, det_exp(-__ddiv_rn(E, P.kT)));
+    return vox >= 0 ? __ldg(P.kT_vox + vox) : P.kT;
+}
+
+// Gamma = nu0 * det_exp(-(E / kT_v)), masked -> exactly 0 (Eq. 1; Eq. 8)
+__device__ __forceinline__ double arrhenius(double E, const PhysParams& P, int vox)
+{
+    return __dmul_rn(P.nu0, det_exp(-__ddiv_rn(E, kT_of(P, vox))));
 }
 
 // ------------------------------------------------------------------ lattice addressing

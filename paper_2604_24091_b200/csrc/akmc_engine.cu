@@ -767,13 +767,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     const int r = c.miss[q];
                     const uint8_t* w = win + r * kWin;
                     MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
+                    const int vox = c.mem_vac[c.row_mem[r]].x;
                     double R = 0.0;
                     int cl = 0;
                     for (int k = 0; k < kHops; ++k) {
                         double E = 0.0, Gk = 0.0;
                         if (w[k] != kVac) {
                             cl += pair_barrier(w, k, p.G, p.P, E);
-                            Gk = arrhenius(E, p.P);
+                            Gk = arrhenius(E, p.P, vox);
                         }
                         R = __dadd_rn(R, Gk);
                         me[0].G[k] = Gk;
@@ -813,9 +814,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     __syncthreads();
                     if (j == 0) {
                         MemoEntry* me = p.memo + 2 * (size_t)c.mem_slot[c.row_mem[r]];
+                        const int vox = c.mem_vac[c.row_mem[r]].x;
                         double R = 0.0;
                         for (int k = 0; k < kHops; ++k) {
-                            const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], p.P) : 0.0;
+                            const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], p.P, vox) : 0.0;
                             R = __dadd_rn(R, Gk);
                             me[0].G[k] = Gk;
                         }
@@ -1112,7 +1114,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             for (int s = 0; s < kClusterN; ++s) acc = __dadd_rn(acc, part_in[(s * kRoundRows + i) * 8 + k]);
                             const double out = __dadd_rn(b3s[k], __dmul_rn(acc, p.W.s3u));
                             Ek = out > 0.0 ? out : 0.0;
-                            Gk = (win8[r * 8 + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P) : 0.0;
+                            int vox = -1;
+                            if (phase_mode) vox = c.mem_vac[c.row_mem[r]].x;
+                            else if (!p.windows) vox = max(p.vac[p.rows ? p.rows[c.ebase + i] : c.ebase + i].x, 0);
+                            Gk = (win8[r * 8 + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P, vox) : 0.0;
                         }
                         double R = 0.0;
 #pragma unroll

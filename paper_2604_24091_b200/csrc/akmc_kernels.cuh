@@ -59,13 +59,14 @@ static __global__ void eval_pair_kernel(const uint8_t* __restrict__ species, con
                 gather_window(species, F, G, v, w);
             }
         }
+        const int vox = windows ? -1 : max(vac[slot].x, 0);
         double R = 0.0;
 #pragma unroll
         for (int k = 0; k < kHops; ++k) {
             double E = 0.0, Gk = 0.0;
             if (w[k] != kVac) {
                 clamps += pair_barrier(w, k, G, P, E);
-                Gk = arrhenius(E, P);
+                Gk = arrhenius(E, P, vox);
             }
             R = __dadd_rn(R, Gk);
             if (rates) rates[(size_t)slot * 8 + k] = Gk;
@@ -125,9 +126,10 @@ static __global__ void __launch_bounds__(256) eval_mlp_fp64_kernel(
         }
         __syncthreads();
         if (j == 0) {
+            const int vox = windows ? -1 : max(vac[slot].x, 0);
             double R = 0.0;
             for (int k = 0; k < kHops; ++k) {
-                const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], P) : 0.0;
+                const double Gk = (w[k] != kVac) ? arrhenius(Ek[k], P, vox) : 0.0;
                 R = __dadd_rn(R, Gk);
                 if (rates) rates[(size_t)slot * 8 + k] = Gk;
                 if (Eout) Eout[(size_t)slot * 8 + k] = Ek[k];

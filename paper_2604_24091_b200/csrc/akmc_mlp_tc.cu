@@ -500,13 +500,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_tc_kernel(const __grid_consta
             double Gk[4];
             if (slot >= 0) {
                 const int mask = smask[row];
+                const double ikT = p.windows ? p.P.inv_kT : 1.0 / kT_of(p.P, max(p.vac[slot].x, 0));
                 double Ek[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int kk = 4 * half + k;
                     const double out = __ldg(p.b3 + kk) + accE[k] * p.s3_unscale;
                     Ek[k] = out > 0.0 ? out : 0.0;
-                    Gk[k] = ((mask >> kk) & 1) ? p.P.nu0 * det_exp(-(Ek[k] * p.P.inv_kT)) : 0.0;
+                    Gk[k] = ((mask >> kk) & 1) ? p.P.nu0 * det_exp(-(Ek[k] * ikT)) : 0.0;
                 }
                 if (p.E) {
                     double2* e2 = reinterpret_cast<double2*>(p.E + (size_t)slot * 8 + 4 * half);

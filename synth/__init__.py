@@ -293,6 +293,12 @@ def window_seconds(lam: float, E0_fe: float, T: float = T_DEFAULT, nu0: float = 
     return lam / (8.0 * nu0 * math.exp(-E0_fe / (kB * T)))
 
 
+def voxel_temperatures(n: int, seed: int, lo: float = 558.0, hi: float = 577.0) -> np.ndarray:
+    """Per-voxel temperatures for the C4 heterogeneous-T variant (uniform in 558-577 K)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.uniform(lo, hi, size=n)
+
+
 def random_windows(n: int, seed: int, solute: float = 0.3, vac: float = 0.02) -> np.ndarray:
     """Random 64-slot windows (uint8 species codes) for network-precision studies:
     each slot is V with prob `vac`, else a solute (Cu..P uniform) with prob `solute`, else Fe."""

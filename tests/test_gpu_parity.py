@@ -150,6 +150,61 @@ def test_voxel_batch_bitexact(akmc, orc):
     assert gctr["events"] == ost.counters[0]
 
 
+@pytest.mark.parametrize("model", ["pair", "mlp"])
+def test_voxel_batch_heterogeneous_T_bitexact(akmc, orc, model):
+    """C4 variant: per-voxel T uniform in 558-577 K; FP64 trajectories bit-exact vs the
+    oracle with the same per-voxel T, including a temperature change between steps (memo cleared)."""
+    eps, E0 = _params()
+    L = 16
+    nvox = 10
+    sp = synth.make_lattice((L, L, L), nvox, synth.a508_atomic_fractions(), 10, seed=33)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=4) if model == "mlp" else None
+    T1 = synth.voxel_temperatures(nvox, seed=2608)
+    T2 = synth.voxel_temperatures(nvox, seed=2609)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, precision=akmc.PREC_FP64, seed=6,
+                      barrier_model=akmc.MODEL_PAIR if model == "pair" else akmc.MODEL_MLP)
+    n = 200 if model == "pair" else 40
+    oc1 = orc.Config(**{**_ocfg(orc, cfg).__dict__, "voxel_T": T1})
+    oc2 = orc.Config(**{**_ocfg(orc, cfg).__dict__, "voxel_T": T2})
+    ost = orc.State.from_species(oc1, sp)
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        sim.set_voxel_temperatures(T1)
+        sim.step(n)
+        R, _ = sim.rates()
+        orc.run(oc1, ost, n, eps, E0, mlp)
+        Ro, _ = orc.rates(oc1, ost.species, ost.vac, eps, E0, mlp)
+        assert np.array_equal(R, Ro)
+        sim.set_voxel_temperatures(T2)
+        sim.step(n)
+        orc.run(oc2, ost, n, eps, E0, mlp)
+        gsp, gvac, gclock, gctr = sim.state()
+        with pytest.raises(akmc.AkmcError):
+            sim.set_voxel_temperatures(T2[:-1])
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+
+
+def test_rates_fp32_heterogeneous_T(akmc, orc):
+    """Tensor-core FP32 rates at per-voxel T within 1e-5 of the FP64 oracle at the same T."""
+    eps, E0 = _params()
+    L = 16
+    nvox = 6
+    sp = synth.make_lattice((L, L, L), nvox, synth.a508_atomic_fractions(), 40, seed=34)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=5)
+    T = synth.voxel_temperatures(nvox, seed=2610)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg, sp, mlp=mlp) as sim:
+        sim.set_voxel_temperatures(T)
+        R, _ = sim.rates()
+        _, vac, _, _ = sim.state(species=False)
+    Ro, _ = orc.rates(orc.Config(**{**_ocfg(orc, cfg).__dict__, "voxel_T": T}), sp, vac, None, None, mlp)
+    assert np.array_equal(R == 0, Ro == 0)
+    m = Ro > 0
+    assert np.max(np.abs(R[m] / Ro[m] - 1)) <= RTOL_FAST
+
+
 @pytest.mark.parametrize("lam,driver", [(1.0, "graph"), (0.25, "graph"), (1.0, "host")])
 def test_sublattice_bitexact(akmc, orc, lam, driver):
     """Windowed synchronous sublattice (reading A19), domains 8^3: bit-exact vs the oracle, with the

@@ -215,3 +215,31 @@ def test_sector_permutation_is_permutation(orc):
     for p in perms:
         assert sorted(p) == list(range(8))
     assert len(set(perms)) > 30
+
+
+def test_per_voxel_temperature(orc):
+    """C4 variant: each voxel's rates follow Eq. 8 at ITS temperature.
+    Pure-Fe voxels with one vacancy: every rate = nu0 exp(-E0[Fe]/(kB T_v)) and the mean
+    residence time of voxel v is 1/(8 nu0 exp(-E0/kB T_v)); voxels are independent."""
+    L = 6
+    nvox = 3
+    one, v = _pure_fe_with_vacancy(L)
+    sp = np.concatenate([one] * nvox)
+    eps, E0 = synth.illustrative_pair_params()
+    T = np.array([450.0, 563.0, 700.0])
+    cfg = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=41, voxel_T=T)
+    st = orc.State.from_species(cfg, sp)
+    R, E = orc.rates(cfg, st.species, st.vac, eps, E0)
+    for i in range(nvox):
+        g = cfg.nu0 * math.exp(-E0[0] / (cfg.kB * T[i]))
+        assert np.allclose(R[i], g, rtol=1e-14, atol=0.0), (i, R[i], g)
+    # uniform T through voxel_T == the scalar path, bit for bit
+    cu = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=41, T=563.0)
+    cv = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=41, voxel_T=np.full(nvox, 563.0))
+    assert np.array_equal(orc.rates(cu, sp, st.vac, eps, E0)[0], orc.rates(cv, sp, st.vac, eps, E0)[0])
+    n = 3000
+    orc.run(cfg, st, n, eps, E0)
+    for i in range(nvox):
+        gtot = 8 * cfg.nu0 * math.exp(-E0[0] / (cfg.kB * T[i]))
+        mean = st.clock[i] / n * gtot                 # mean of Exp(1) draws
+        assert abs(mean - 1.0) < 5.0 / math.sqrt(n), (i, mean)

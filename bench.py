@@ -214,6 +214,9 @@ def run_ours(args):
     sp_host, sp_keep = make_inputs(args.workload, rank, dev)
     sites = sp_host.size
 
+    # one step = one sweep of 8 phases (sublattice) or `--events` BKL events of every voxel in one engine
+    # launch (serial C1/C2/C4: the per-launch setup is amortised as in a production run of 1e4-1e5 events)
+    nstep = 1 if pr.domain[0] else max(1, args.events)
     stream = torch.cuda.Stream(device=dev)
     # ---------------- device-resident timing ("value"): production path (per-sweep CUDA graph)
     sim = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
@@ -234,9 +237,9 @@ def run_ours(args):
             dist.broadcast(flag, src=0)
         if not int(flag.item()):
             break
-        sim.step(1)
+        sim.step(nstep)
     for _ in range(args.warmup):
-        sim.step(1)
+        sim.step(nstep)
     torch.cuda.synchronize()
     _, _, clock0, tot0 = sim.state(species=False)
     if world > 1:
@@ -246,7 +249,7 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        sim.step(1)
+        sim.step(nstep)
     e1.record(stream)
     torch.cuda.synchronize()
     cs.__exit__()
@@ -266,7 +269,7 @@ def run_ours(args):
     pe1 = torch.cuda.Event(enable_timing=True)
     pe0.record(stream)
     for _ in range(args.steps):
-        sim.step(1)
+        sim.step(nstep)
     pe1.record(stream)
     torch.cuda.synchronize()
     _, _, _, p1 = sim.state(species=False)
@@ -298,7 +301,7 @@ def run_ours(args):
     t_init = time.perf_counter() - t0
     hop_e2e = 0
     for _ in range(args.steps):
-        c = sim2.step(1)
+        c = sim2.step(nstep)
         hop_e2e += c["hop_evals"]
         sim2.counters()                                  # the step's result: counters read back to the host
     t_steps = time.perf_counter() - t0 - t_init
@@ -360,6 +363,8 @@ def run_ours(args):
                            "voxels_per_gpu": cfg.n_voxels, "sites_per_gpu": sites,
                            "vacancies_per_gpu": pr.n_vac_per_voxel * cfg.n_voxels,
                            "domain_cells": list(cfg.domain_cells), "lambda": args.lam, "window_s": cfg.window_s,
+                           "step": ("one sweep (8 sublattice phases)" if pr.domain[0] else
+                                    f"{nstep} BKL events per voxel (one engine launch)"),
                            "temperature_K": ("per voxel, uniform 558-577" if vT is not None else cfg.temperature_K),
                            "model": "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA",
                            "parallelism": ("1 GPU" if world == 1 else
@@ -400,6 +405,7 @@ def main():
     ap.add_argument("--model", default="mlp", choices=["mlp", "pair"])
     ap.add_argument("--lam", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--events", type=int, default=100, help="serial workloads: BKL events per voxel per step")
     ap.add_argument("--voxel-T", action="store_true", help="per-voxel temperature uniform in 558-577 K (C4 variant)")
     ap.add_argument("--ramp-s", type=float, default=1.0, help="untimed clock ramp before the warm-up steps")
     args = ap.parse_args()

@@ -1579,6 +1579,7 @@ void akmc_free(akmc_handle* h)
             std::fprintf(stderr, "[akmc engine] cycles/CTA: refill %.0f rows %.0f gather+memo %.0f | L1 %.0f exchange %.0f"
                          " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
                          d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);
+            if (d[29]) std::fprintf(stderr, "[akmc engine] memo-hit chain: %llu events of %llu checks (%.1f per CTA-launch)\n", d[29], d[30], d[29] / n);
             std::fprintf(stderr, "[akmc engine] L1 split: memo move %.0f layer 1 %.0f async fences + barrier %.0f\n",
                          d[20] / n, d[21] / n, d[22] / n);
             if (d[24] + d[25] + d[26] + d[27])

@@ -47,6 +47,12 @@
 #ifndef AKMC_XCHG_DSMEM
 #define AKMC_XCHG_DSMEM 0       // h1 rows by DSMEM bulk copies instead of L2-staged multicast (+5 %, slower)
 #endif
+#ifndef AKMC_CHAIN_MAX
+#define AKMC_CHAIN_MAX 0        // memo-hit chain: extra BKL steps a single-member domain may take per iteration
+#endif                          // (bit-exact; C5: 30 % of checks hit, -0.7 iterations/CTA, but 1.86 -> 2.51 ms
+#ifndef AKMC_CHAIN_NRUN         //  per sweep with 64; gated to the tail (<= 4 / 16 running domains) 1.97 / 2.04)
+#define AKMC_CHAIN_NRUN 1024    // ... only while the CTA holds at most this many running domains
+#endif
 #ifndef AKMC_L1_PROBE
 #define AKMC_L1_PROBE 0         // cycle laps inside layer 1 (diagnostic)
 #endif
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)
     const long long t_start = clock64();
     unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
+    unsigned long long my_chain = 0, my_check = 0;                    // memo-hit chain: events taken, checks
     long long t_mark = t_start;
     auto lap = [&](long long& acc) { const long long t = clock64(); acc += t - t_mark; t_mark = t; };
     // watchdog progress words (thread 0; mapped host memory, read by the host while the kernel runs)
@@ -1193,30 +1200,43 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         atomicAdd(&p.ctr->terminal, 1ull);
                     }
                 } else {
+                    // Memo-hit chain (R7 + R6): a domain with ONE active member is the only writer of the sites its
+                    // windows read in this phase (A20; the other members do not move), so after its hop the next
+                    // iteration would gather exactly the window the hop left.  If that window is already a key of
+                    // the vacancy's memo (a back-hop restores an earlier configuration exactly), the next
+                    // iteration would be a pure memo hit and its BKL step can run here at once, with the same
+                    // Philox counter (the domain's own event index) -- bit-identical to waiting for the
+                    // iteration, without its gather + evaluation round.  The window comparison is the full
+                    // 64-byte key, so nothing is assumed about which configuration recurs.
                     double u_sel, u_t, dt;
                     bool go;
+                    double Rc = Rd;
+                    const MemoEntry* src = nullptr;      // chained step: the memo way that holds the rates
+                    int a = 0;
+                    const bool may_chain = m == 1 && AKMC_CHAIN_MAX > 0 && c.nrun <= AKMC_CHAIN_NRUN;
+                    for (int chain = 0;; ++chain) {
                     if (p.serial) {
                         // serial BKL (a10): counter (event index of the voxel, voxel), clock += dt after the hop
                         const unsigned long long n = (unsigned long long)p.nev[c.seg_dom[i]] + c.seg_it[i];
                         philox_uniforms(p.S.seed, make_uint4((uint32_t)n, (uint32_t)(n >> 32), c.seg_dom[i], 0u), u_sel, u_t);
-                        dt = __ddiv_rn(-det_log(u_t), Rd);
+                        dt = __ddiv_rn(-det_log(u_t), Rc);
                         go = true;
                     } else {
                         const unsigned long long ph = (unsigned long long)p.ph->phase;
                         philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
                                         u_sel, u_t);
-                        dt = __ddiv_rn(-det_log(u_t), Rd);
+                        dt = __ddiv_rn(-det_log(u_t), Rc);
                         go = !(__dadd_rn(c.seg_t[i], dt) > p.S.window);   // else the overshooting draw is discarded
                     }
                     if (!go) {
                         stop = true;
+                        break;
                     } else {
-                        double rr = __dmul_rn(u_sel, Rd);
-                        const int leaf = tree_descend(buf, m, P, nlev, rr);
-                        const int a = idx[leaf];
+                        double rr = __dmul_rn(u_sel, Rc);
+                        if (chain == 0) a = idx[tree_descend(buf, m, P, nlev, rr)];   // m == 1 in a chain: rr as is
                         const int slot = c.mem_slot[moff + a];
                         const int r = c.mem_row[moff + a];
-                        const MemoEntry& mrow = p.memo[2 * (size_t)slot + c.row_way[r]];   // the row's rates
+                        const MemoEntry& mrow = chain ? *src : p.memo[2 * (size_t)slot + c.row_way[r]];   // the rates
                         const int k = pick_hop(mrow.G, rr);
                         // hop: the target's species is window slot k (1NN slots are 0..7)
                         const int4 ov = c.mem_vac[moff + a];
@@ -1224,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         nv.y = p.F.wrap[0] ? wrap2(ov.y + p.G.off[k][0], 2 * p.F.L[0]) : ov.y + p.G.off[k][0];
                         nv.z = p.F.wrap[1] ? wrap2(ov.z + p.G.off[k][1], 2 * p.F.L[1]) : ov.z + p.G.off[k][1];
                         nv.w = p.F.wrap[2] ? wrap2(ov.w + p.G.off[k][2], 2 * p.F.L[2]) : ov.w + p.G.off[k][2];
-                        const uint8_t tn = win8[r * 8 + k];
+                        const uint8_t tn = chain ? mrow.key[k] : win8[r * 8 + k];
                         write_site(p.species, p.F, ov.x, ov.y, ov.z, ov.w, tn);
                         write_site(p.species, p.F, nv.x, nv.y, nv.z, nv.w, (uint8_t)kVac);
 #if AKMC_PREFETCH
@@ -1261,6 +1281,55 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                 stop = true;
                             }
                         }
+                        // ---- chain test: is the window the hop left a key of the vacancy's memo?
+                        if (stop || !may_chain || chain >= AKMC_CHAIN_MAX || !c.mem_act[moff + a] || p.vac[slot].x < 0) break;
+                        my_check += 1ull;
+                        uint32_t ww[kWin / 4];
+                        // stage 1: the 8 first-shell bytes against both ways (most failing checks end here)
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            uint32_t wq = 0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                wq |= (uint32_t)p.species[neighbour_site(p.F, nv, p.G.off[4 * q + j][0], p.G.off[4 * q + j][1],
+                                                                         p.G.off[4 * q + j][2])] << (8 * j);
+                            ww[q] = wq;
+                        }
+                        {
+                            const uint2 k0 = *reinterpret_cast<const uint2*>(p.memo[2 * (size_t)slot].key);
+                            const uint2 k1 = *reinterpret_cast<const uint2*>(p.memo[2 * (size_t)slot + 1].key);
+                            if (!((k0.x == ww[0] && k0.y == ww[1]) || (k1.x == ww[0] && k1.y == ww[1]))) break;
+                        }
+#pragma unroll
+                        for (int q = 2; q < kWin / 4; ++q) {
+                            uint32_t wq = 0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                wq |= (uint32_t)p.species[neighbour_site(p.F, nv, p.G.off[4 * q + j][0], p.G.off[4 * q + j][1],
+                                                                         p.G.off[4 * q + j][2])] << (8 * j);
+                            ww[q] = wq;
+                        }
+                        int hw = -1;
+#pragma unroll
+                        for (int w = 0; w < 2; ++w) {
+                            const uint4* kq = reinterpret_cast<const uint4*>(p.memo[2 * (size_t)slot + w].key);
+                            bool eq = true;
+#pragma unroll
+                            for (int q = 0; q < kWin / 16; ++q) {
+                                const uint4 t = kq[q];
+                                eq = eq && t.x == ww[4 * q] && t.y == ww[4 * q + 1] && t.z == ww[4 * q + 2] && t.w == ww[4 * q + 3];
+                            }
+                            if (eq && hw < 0) hw = w;
+                        }
+                        if (hw < 0) break;
+                        src = &p.memo[2 * (size_t)slot + hw];
+                        Rc = src->R;
+                        if (!(Rc > 0.0)) break;                  // the next iteration handles a dead vacancy
+                        // the chained step is one more logical evaluation of this vacancy (R4 accounting)
+                        my_evals += 8ull;
+                        if (!kTC) my_clamps += (unsigned long long)src->clamps;
+                        my_chain += 1ull;
+                    }
                     }
                 }
             }
@@ -1300,7 +1369,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             my_events += __shfl_xor_sync(0xffffffffu, my_events, o);
             my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
             my_clamps += __shfl_xor_sync(0xffffffffu, my_clamps, o);
+            my_chain += __shfl_xor_sync(0xffffffffu, my_chain, o);
+            my_check += __shfl_xor_sync(0xffffffffu, my_check, o);
         }
+        if (lane == 0 && p.diag && my_chain) atomicAdd(p.diag + 29, my_chain);
+        if (lane == 0 && p.diag && my_check) atomicAdd(p.diag + 30, my_check);
         if (lane == 0) { atomicAdd(&c.events, my_events); atomicAdd(&c.evals, my_evals); atomicAdd(&c.clamps, my_clamps); }
     }
     __syncthreads();

@@ -168,7 +168,7 @@ def cpu_baseline(name: str, steps: int, lam: float, seconds_target: float = 15.0
         if el >= seconds_target or done >= max(steps, 1) * 1000:
             break
     hop = int(st.counters[1])
-    return {"value": hop / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": hop / el, "unit": UNIT, "cores": 1, "kind": "oracle", "steps": done,
             "sample": f"{sample}; {done} step(s), {hop} hop evals in {el:.1f} s"}, st, el
 
 
@@ -179,9 +179,11 @@ def run_reference(args):
     t_all = time.perf_counter()
     cb, st, el = cpu_baseline(args.workload, args.steps, args.lam, seconds_target=max(10.0, 4.0 * args.steps))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / max(cb["steps"], 1),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload.upper(), "impl": "CPU FP64 oracle (oracle/akmc_oracle.c)"},
+            "config": {"workload": args.workload.upper(), "impl": "CPU FP64 oracle (oracle/akmc_oracle.c)",
+                       "step": "one oracle step of the bounded sample named in cpu_baseline.sample"},
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t_all}

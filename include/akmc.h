@@ -113,6 +113,17 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
  * unchanged from that point); other voxels still advance. */
 int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr);
 
+/* Voxel-ensemble mode (voxels evolved independently to a common physical time; serial mode
+ * only): every voxel runs BKL events until its next event would happen after t_end_s, or
+ * max_events events of this call, or Gamma_tot == 0.  The draw whose event time clock + dt exceeds
+ * t_end_s is discarded and its Philox counter (the voxel's event index) is not consumed, so splitting a
+ * run at any horizons gives the trajectory of the unsplit run; voxel clocks stay at their last event
+ * (raw AKMC time, <= t_end_s).  Voxels run concurrently in one persistent engine launch (each CTA pulls
+ * voxels as slots free up).  Returns like akmc_step; AKMC_ERR_INVALID in sublattice mode, for a
+ * non-finite t_end_s or max_events outside [0, 2^30] (one launch per call), and when the legacy
+ * (non-engine) serial path is active.                                                                   */
+int akmc_run_until(akmc_handle* h, double t_end_s, int64_t max_events, akmc_counters* ctr);
+
 /* Read back the state.  species_out: n_voxels*sites bytes (may be NULL); vac_sites_out: global
  * site index of each vacancy slot (may be NULL) with *n_vac_inout = capacity in / count out
  * (a short buffer returns AKMC_ERR_INVALID without writing); clock_s_out: [n_voxels] simulated

@@ -59,6 +59,8 @@ def lib():
                                       C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_run.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.orc_run_until.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_void_p]
         _lib.orc_rates.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_cluster_stats.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_int, C.c_int,
@@ -201,6 +203,16 @@ def run(cfg: Config, st: State, n: int, eps=None, E0=None, mlp=None) -> int:
     m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
     return lib().orc_run(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
                          _ptr(st.nev), _ptr(st.sweep), _ptr(e), _ptr(e0), _ptr(m), int(n), _ptr(st.counters))
+
+
+def run_until(cfg: Config, st: State, t_end: float, max_events: int, eps=None, E0=None, mlp=None) -> int:
+    """Serial mode: every voxel advances to physical time t_end (<= max_events events each)."""
+    e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
+    e0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
+    m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
+    return lib().orc_run_until(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
+                               _ptr(st.nev), _ptr(e), _ptr(e0), _ptr(m), float(t_end), int(max_events),
+                               _ptr(st.counters))
 
 
 def rates(cfg: Config, species, vac, eps=None, E0=None, mlp=None):

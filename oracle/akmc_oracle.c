@@ -510,10 +510,13 @@ static void apply_hop(const geom* g, uint8_t* sp, int64_t* vac, int i, int k)
 }
 
 /* serial BKL, one competing set per voxel (P:294-298 with A15).
- * Each voxel runs n events (or until Gamma_tot == 0 -> terminal). */
+ * Each voxel runs n events (or until Gamma_tot == 0 -> terminal).  With a horizon (t_end finite; the
+ * voxel-ensemble mode of P:453-455, every voxel advanced to a common physical time) a voxel also stops
+ * at the first draw whose event time clock + dt exceeds t_end; that draw is discarded and its counter
+ * is not consumed, so horizons split a run without changing the trajectory. */
 static int run_serial(const orc_cfg* c, uint8_t* sp, int64_t* vac, int64_t nvac, double* clock,
                       int64_t* nev, const double* Dp, const double* E0, const double* mlp,
-                      int64_t n, orc_ctr* ctr)
+                      int64_t n, double t_end, orc_ctr* ctr)
 {
     geom g = mk_geom(c);
     int* members = (int*)malloc(sizeof(int) * (size_t)(nvac + 1));
@@ -544,11 +547,12 @@ static int run_serial(const orc_cfg* c, uint8_t* sp, int64_t* vac, int64_t nvac,
             double u_sel, u_t;
             draw_uniforms(c->seed, (uint32_t)nev[v], (uint32_t)((uint64_t)nev[v] >> 32), (uint32_t)v, 0u,
                           &u_sel, &u_t);
+            double dt = (-orc_det_log(u_t)) / tot;
+            if (clock[v] + dt > t_end) break;   /* horizon: the event would happen after t_end */
             double r = u_sel * tot;
             int a = tree_descend(buf, R, m, P, &r);
             int k = pick_hop(&G[8 * a], r);
             apply_hop(&g, sp, vac, members[a], k);
-            double dt = (-orc_det_log(u_t)) / tot;
             clock[v] = clock[v] + dt;
             nev[v] += 1;
             ctr->events += 1;
@@ -703,9 +707,33 @@ int orc_run(const orc_cfg* c, uint8_t* species, int64_t* vac, int64_t nvac, doub
     orc_ctr ctr = {0, 0, 0, 0};
     int rc;
     if (c->domain[0] == 0)
-        rc = run_serial(c, species, vac, nvac, clock, nev, Dp, E0, mlp, n, &ctr);
+        rc = run_serial(c, species, vac, nvac, clock, nev, Dp, E0, mlp, n, INFINITY, &ctr);
     else
         rc = run_sublattice(c, species, vac, nvac, clock, sweep, Dp, E0, mlp, n, &ctr);
+    if (ctr_out) {
+        ctr_out[0] += ctr.events; ctr_out[1] += ctr.hop_evals;
+        ctr_out[2] += ctr.terminal_voxels; ctr_out[3] += ctr.clamps;
+    }
+    return rc;
+}
+
+/* serial mode: advance every voxel to the common physical time t_end (at most max_events events per
+ * voxel); same counters as orc_run */
+int orc_run_until(const orc_cfg* c, uint8_t* species, int64_t* vac, int64_t nvac, double* clock,
+                  int64_t* nev, const double* eps, const double* E0, const double* mlp,
+                  double t_end, int64_t max_events, int64_t* ctr_out)
+{
+    build_window();
+    if (g_win_ready != 1 || c->domain[0] != 0) return ORC_INVALID;
+    double Dp[2 * NSPEC * NSPEC];
+    if (c->model == 0) {
+        if (!eps || !E0) return ORC_INVALID;
+        build_dp(eps, Dp);
+    } else if (!mlp) {
+        return ORC_INVALID;
+    }
+    orc_ctr ctr = {0, 0, 0, 0};
+    int rc = run_serial(c, species, vac, nvac, clock, nev, Dp, E0, mlp, max_events, t_end, &ctr);
     if (ctr_out) {
         ctr_out[0] += ctr.events; ctr_out[1] += ctr.hop_evals;
         ctr_out[2] += ctr.terminal_voxels; ctr_out[3] += ctr.clamps;

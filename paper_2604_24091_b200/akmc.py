@@ -59,6 +59,7 @@ def load() -> C.CDLL:
     P = C.c_void_p
     lib.akmc_init.argtypes = [C.POINTER(CConfig), P, P, P, P, C.POINTER(P)]
     lib.akmc_step.argtypes = [P, C.c_int64, C.POINTER(CCounters)]
+    lib.akmc_run_until.argtypes = [P, C.c_double, C.c_int64, C.POINTER(CCounters)]
     lib.akmc_state.argtypes = [P, P, P, C.POINTER(C.c_int64), P, C.POINTER(CCounters)]
     lib.akmc_rates.argtypes = [P, P, P]
     lib.akmc_eval_windows.argtypes = [P, P, C.c_int64, C.c_int32, P]
@@ -75,7 +76,7 @@ def load() -> C.CDLL:
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
-              "akmc_set_voxel_temperatures"):
+              "akmc_set_voxel_temperatures", "akmc_run_until"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -159,6 +160,15 @@ class Simulation:
     def step(self, n: int) -> dict:
         ctr = CCounters()
         rc = self._check(self.lib.akmc_step(self.h, int(n), C.byref(ctr)), allow=(AKMC_OK, AKMC_TERMINAL))
+        d = ctr.as_dict()
+        d["status"] = rc
+        return d
+
+    def run_until(self, t_end: float, max_events: int = 1 << 30) -> dict:
+        """Voxel-ensemble mode: every voxel advances to physical time t_end (serial mode)."""
+        ctr = CCounters()
+        rc = self._check(self.lib.akmc_run_until(self.h, float(t_end), int(max_events), C.byref(ctr)),
+                         allow=(AKMC_OK, AKMC_TERMINAL))
         d = ctr.as_dict()
         d["status"] = rc
         return d

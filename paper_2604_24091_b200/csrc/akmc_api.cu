@@ -1008,7 +1008,7 @@ int akmc_set_profiling(akmc_handle* h, int32_t profile)
     return AKMC_OK;
 }
 
-static int step_serial(akmc_handle* h, int64_t n)
+static int step_serial(akmc_handle* h, int64_t n, bool horizon = false, double t_end = 0.0)
 {
     if (h->serial_engine) {
         // all n events of every voxel in one persistent launch (a10; per-voxel Philox counters keep the
@@ -1022,6 +1022,8 @@ static int step_serial(akmc_handle* h, int64_t n)
             p.nev = h->d_nev;
             p.term = h->d_term;
             p.clock = h->d_clock;
+            p.horizon = horizon ? 1 : 0;
+            p.t_end = t_end;
             p.ph = nullptr;
             CK(h, cudaMemsetAsync(reinterpret_cast<char*>(h->d_ctr) + offsetof(DevCounters, chunk), 0,
                                   sizeof(unsigned long long), h->stream));
@@ -1355,16 +1357,14 @@ static int step_sublattice(akmc_handle* h, int64_t n)
     return AKMC_OK;
 }
 
-int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
+static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horizon, double t_end)
 {
-    if (!h) return AKMC_ERR_RUNTIME;
-    if (n < 0) return fail(h, AKMC_ERR_INVALID, "n must be >= 0");
     const akmc_counters before = h->total;
     CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     const DevCounters c0 = *h->h_ctr;
     const auto t0 = std::chrono::steady_clock::now();
-    int rc = h->sub ? step_sublattice(h, n) : step_serial(h, n);
+    int rc = h->sub ? step_sublattice(h, n) : step_serial(h, n, horizon, t_end);
     if (rc != AKMC_OK) return rc;
     CK(h, cudaMemcpyAsync(h->h_ctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
@@ -1401,6 +1401,24 @@ int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
     }
     if (c1.terminal != c0.terminal) return fail(h, AKMC_TERMINAL, "a competing set has no feasible event (S:199)");
     return AKMC_OK;
+}
+
+int akmc_step(akmc_handle* h, int64_t n, akmc_counters* ctr)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (n < 0) return fail(h, AKMC_ERR_INVALID, "n must be >= 0");
+    return step_common(h, n, ctr, false, 0.0);
+}
+
+int akmc_run_until(akmc_handle* h, double t_end_s, int64_t max_events, akmc_counters* ctr)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (h->sub) return fail(h, AKMC_ERR_INVALID, "akmc_run_until: serial (voxel) mode only");
+    if (!h->serial_engine) return fail(h, AKMC_ERR_INVALID, "akmc_run_until: needs the engine path (AKMC_LEGACY_LOOP unset, "
+                                                            "a voxel's vacancies fit one engine CTA)");
+    if (!std::isfinite(t_end_s) || max_events < 0 || max_events > (1LL << 30))
+        return fail(h, AKMC_ERR_INVALID, "akmc_run_until: bad t_end or max_events (0 .. 2^30)");
+    return step_common(h, max_events, ctr, true, t_end_s);
 }
 
 struct VacRec { int64_t gid, site; int slot; };

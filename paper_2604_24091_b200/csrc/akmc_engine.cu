@@ -1220,7 +1220,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const unsigned long long n = (unsigned long long)p.nev[c.seg_dom[i]] + c.seg_it[i];
                         philox_uniforms(p.S.seed, make_uint4((uint32_t)n, (uint32_t)(n >> 32), c.seg_dom[i], 0u), u_sel, u_t);
                         dt = __ddiv_rn(-det_log(u_t), Rc);
-                        go = true;
+                        go = !(p.horizon && __dadd_rn(p.clock[c.seg_dom[i]], dt) > p.t_end);   // akmc_run_until
                     } else {
                         const unsigned long long ph = (unsigned long long)p.ph->phase;
                         philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
@@ -1230,6 +1230,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     }
                     if (!go) {
                         stop = true;
+                        if (p.serial) p.nev[c.seg_dom[i]] += c.seg_it[i];   // horizon reached in this launch
                         break;
                     } else {
                         double rr = __dmul_rn(u_sel, Rc);

@@ -81,6 +81,8 @@ struct EngineParams {
     long long* nev;         // serial: per-voxel event counters (Philox counter, P:294-298 / S:195-203)
     int* term;              // serial: per-voxel terminal flags
     double* clock;          // serial: per-voxel clocks
+    int horizon;            // serial: 1 -> a voxel also stops at its first draw with clock + dt > t_end
+    double t_end;           //   (akmc_run_until; the draw is discarded, its counter not consumed)
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
     int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)

@@ -186,6 +186,40 @@ def test_voxel_batch_heterogeneous_T_bitexact(akmc, orc, model):
     assert gctr["events"] == ost.counters[0]
 
 
+@pytest.mark.parametrize("model", ["pair", "mlp"])
+def test_run_until_voxel_ensemble_bitexact(akmc, orc, model):
+    """Voxel-ensemble mode with per-voxel T: every voxel advanced to a common physical time in
+    two horizons (and an event cap) -- bit-exact vs the oracle's run_until."""
+    eps, E0 = _params()
+    L = 16
+    nvox = 12
+    sp = synth.make_lattice((L, L, L), nvox, synth.a508_atomic_fractions(), 10, seed=35)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=6) if model == "mlp" else None
+    T = synth.voxel_temperatures(nvox, seed=2611)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, precision=akmc.PREC_FP64, seed=8,
+                      barrier_model=akmc.MODEL_PAIR if model == "pair" else akmc.MODEL_MLP)
+    oc = orc.Config(**{**_ocfg(orc, cfg).__dict__, "voxel_T": T})
+    t1, t2 = 5e-9, 1.5e-8                            # ~ 6 / 20 events per voxel
+    ost = orc.State.from_species(oc, sp)
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        sim.set_voxel_temperatures(T)
+        sim.run_until(t1)
+        orc.run_until(oc, ost, t1, 10 ** 9, eps, E0, mlp)
+        _, _, gclock1, _ = sim.state(species=False)
+        assert np.array_equal(gclock1, ost.clock) and np.all(gclock1 <= t1)
+        sim.run_until(t2, max_events=7)              # the cap binds for the busiest voxels
+        orc.run_until(oc, ost, t2, 7, eps, E0, mlp)
+        sim.run_until(t2)
+        orc.run_until(oc, ost, t2, 10 ** 9, eps, E0, mlp)
+        gsp, gvac, gclock, gctr = sim.state()
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert np.all(gclock <= t2)
+    assert gctr["events"] == ost.counters[0] > 10 * nvox
+    assert gctr["hop_evals"] == ost.counters[1]
+
+
 def test_rates_fp32_heterogeneous_T(akmc, orc):
     """Tensor-core FP32 rates at per-voxel T within 1e-5 of the FP64 oracle at the same T."""
     eps, E0 = _params()

@@ -243,3 +243,64 @@ def test_per_voxel_temperature(orc):
         gtot = 8 * cfg.nu0 * math.exp(-E0[0] / (cfg.kB * T[i]))
         mean = st.clock[i] / n * gtot                 # mean of Exp(1) draws
         assert abs(mean - 1.0) < 5.0 / math.sqrt(n), (i, mean)
+
+
+def test_run_until_horizon(orc):
+    """Voxel-ensemble mode: horizons split a run without changing it, and no voxel clock passes
+    the horizon."""
+    L = 8
+    nvox = 3
+    sp = synth.make_lattice((L, L, L), nvox, synth.a508_atomic_fractions(), 4, seed=17)
+    eps, E0 = synth.illustrative_pair_params()
+    cfg = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=23)
+    t1, t2 = 8e-8, 2e-7                # ~ 40 / 100 events per voxel (Gamma_tot ~ 5e8 /s)
+    a = orc.State.from_species(cfg, sp)
+    orc.run_until(cfg, a, t2, 10 ** 6, eps, E0)
+    b = orc.State.from_species(cfg, sp)
+    orc.run_until(cfg, b, t1, 10 ** 6, eps, E0)
+    orc.run_until(cfg, b, t2, 10 ** 6, eps, E0)
+    for f in ("species", "vac", "clock", "nev"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert a.counters[0] == b.counters[0] > 20
+    assert np.all(a.clock <= t2)
+
+
+def test_run_until_single_voxel_bruteforce(orc):
+    """One voxel: run_until(t) stops exactly before the first event with time > t (S:198 clock)."""
+    L = 8
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.03), 2, seed=19)
+    eps, E0 = synth.illustrative_pair_params()
+    cfg = orc.Config(cells=(L, L, L), model=0, seed=29)
+    t = 2e-7
+    a = orc.State.from_species(cfg, sp)
+    orc.run_until(cfg, a, t, 10 ** 6, eps, E0)
+    ref = orc.State.from_species(cfg, sp)
+    n = 0
+    while True:
+        trial = ref.copy()
+        orc.run(cfg, trial, 1, eps, E0)
+        if trial.clock[0] > t:
+            break
+        ref = trial
+        n += 1
+    assert n > 10 and a.nev[0] == n
+    for f in ("species", "vac", "clock", "nev"):
+        assert np.array_equal(getattr(a, f), getattr(ref, f)), f
+
+
+def test_run_until_poisson_counts(orc):
+    """Pure Fe, one vacancy per voxel: Gamma_tot = 8 nu0 e^{-E0/kT} is constant, so the number of events
+    by time t is Poisson(Gamma_tot t); mean over 200 voxels within 4 sigma."""
+    L = 6
+    nvox = 200
+    one, _ = _pure_fe_with_vacancy(L)
+    sp = np.concatenate([one] * nvox)
+    eps, E0 = synth.illustrative_pair_params()
+    cfg = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=31)
+    gtot = 8 * cfg.nu0 * math.exp(-E0[0] / (cfg.kB * cfg.T))
+    lam = 12.0
+    st = orc.State.from_species(cfg, sp)
+    orc.run_until(cfg, st, lam / gtot, 10 ** 6, eps, E0)
+    n = st.nev.astype(float)
+    assert abs(n.mean() - lam) < 4.0 * math.sqrt(lam / nvox), n.mean()
+    assert abs(n.var() / lam - 1.0) < 0.35

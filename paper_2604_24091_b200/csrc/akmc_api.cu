@@ -157,6 +157,8 @@ struct akmc_handle {
     int n_clusters = 0;
     MemoEntry* d_memo = nullptr;      // [vcap][2]
     double* d_kT = nullptr;           // [n_voxels] kB * T_v (per-voxel temperature, C4 variant)
+    double hot_events = 0.0;          // phase engine: domains expecting >= this many events go first (0: off;
+                                      // A/B on C5: no change, profiles/r01_engine_timing.md)
     float* d_W1f = nullptr;           // [385][256]
     uint8_t* d_W2e = nullptr;         // [8][32 KiB]
     uint8_t* d_W3e = nullptr;         // [8][2 KiB]
@@ -459,6 +461,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.wstore = h->d_wstore;
     p.watch = h->d_watch;
     p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
+    p.seg_cap = (h->engine && h->hot_events > 0.0) ? h->vcap : 0;   // hot-first segment list (phase mode)
     return p;
 }
 
@@ -927,6 +930,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     h->tc = cfg->barrier_model == AKMC_MODEL_MLP && cfg->precision == AKMC_PREC_FP32;
     h->engine = std::getenv("AKMC_LEGACY_LOOP") == nullptr;
+    if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
     CKI(engine_setup());
     if (h->tc) {
         h->n_clusters = engine_max_clusters();
@@ -1087,7 +1091,10 @@ static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_
     activate_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
                                                         h->d_ctr);
     segments_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr, h->d_mpos);
+                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr, h->d_mpos,
+                                                        h->engine && h->hot_events > 0.0
+                                                            ? reinterpret_cast<const unsigned char*>(h->d_memo) : nullptr,
+                                                        nv, h->hot_events);
 }
 
 // the whole phase on the device: activate + segments, then the persistent phase engine runs every domain

@@ -96,7 +96,7 @@ struct Ctl {
     int nmulti_def, nfree_single;
     unsigned frees[kMaskWords];     // free slots left for single-slot domains, and their prefix counts
     int fpre[kMaskWords + 1];
-    int npend, nnew, fetch, drained, ntot, s0;
+    int npend, nnew, fetch, drained, ntot, s0, nhot;
     unsigned freew[kMaskWords], runw[kMaskWords];
     int nrows, nmiss, nrun, ebase;
     int wsum[kWarps];
@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
         c.ntot = phase_mode ? (p.serial ? p.nseg_host : (int)p.ctr->nseg) : 0;
+        c.nhot = (phase_mode && !p.serial && p.seg_cap > 0) ? (int)p.ctr->nhot : -1;
         c.events = 0; c.evals = 0; c.mrows = 0; c.clamps = 0;
         if (kTC) {
             mbar_init(bar_req, kClusterN);
@@ -550,7 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             if (c.fetch && tid < c.nnew) {
-                const Segment sg = p.segs[c.s0 + tid];
+                const int si = c.s0 + tid;
+                const Segment sg = p.segs[(c.nhot < 0 || si < c.nhot) ? si : p.seg_cap - 1 - (si - c.nhot)];
                 const int q = c.npend + tid;
                 c.cand_dom[q] = (unsigned)sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
             }

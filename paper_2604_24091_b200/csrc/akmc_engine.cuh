@@ -31,6 +31,7 @@ struct MemoEntry {
     int pad;
 };
 static_assert(sizeof(MemoEntry) == 144, "memo entry layout");
+static_assert(sizeof(MemoEntry) == kMemoBytes && offsetof(MemoEntry, R) == kMemoROff, "memo layout seen by segments_kernel");
 
 struct EngineWeights {
     const float* W1f;       // [385][256] FP32: row 0 = b1' = b1 + sum_slot W1[slot,Fe]; row 1+(s-1)*64+slot = W1'
@@ -81,6 +82,7 @@ struct EngineParams {
     long long* nev;         // serial: per-voxel event counters (Philox counter, P:294-298 / S:195-203)
     int* term;              // serial: per-voxel terminal flags
     double* clock;          // serial: per-voxel clocks
+    int seg_cap;            // phase: > 0 -> hot segments at segs[0, nhot), cold ones at segs[seg_cap-1-i]
     int horizon;            // serial: 1 -> a voxel also stops at its first draw with clock + dt > t_end
     double t_end;           //   (akmc_run_until; the draw is discarded, its counter not consumed)
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)

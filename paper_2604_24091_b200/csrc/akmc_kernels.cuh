@@ -18,7 +18,11 @@ struct DevCounters {                 // device-side counters (unsigned long long
     unsigned long long events, hop_evals, clamps, terminal, nrun, nseg, total, nrows;
     unsigned long long chunk;        // phase engine: next segment to hand out (reset per phase)
     unsigned long long mrows;        // barrier-network rows actually evaluated (memo misses)
+    unsigned long long nhot, ncold;  // phase engine: segments at the front (hot) / back (cold) of the list
 };
+
+// memo layout as seen from the segment builder (MemoEntry lives in akmc_engine.cuh; asserted there)
+constexpr int kMemoBytes = 144, kMemoROff = 128;
 
 // ------------------------------------------------------------------ window gather
 __device__ __forceinline__ void gather_window(const uint8_t* __restrict__ species, const Frame& F, const GeomTables& G,
@@ -294,7 +298,7 @@ static __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, c
                                 const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; ctr->chunk = 0; }
+    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; ctr->chunk = 0; ctr->nhot = 0; ctr->ncold = 0; }
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     if (i >= n) return;
     const int4 v = vac[i];
@@ -338,7 +342,9 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
                                                        const int* __restrict__ nvac_dev, SubParams S,
                                                        const PhaseInfo* __restrict__ ph, int* dmin, int* head,
                                                        const int* __restrict__ next, Segment* segs, int* members,
-                                                       uint8_t* mactive, DevCounters* ctr, int4* mpos)
+                                                       uint8_t* mactive, DevCounters* ctr, int4* mpos,
+                                                       const unsigned char* memo = nullptr, int seg_cap = 0,
+                                                       double hot_events = 0.0)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
@@ -356,7 +362,26 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
         }
     }
     const int off = block_alloc(cnt, &ctr->total);
-    const int seg = block_alloc(owner ? 1 : 0, &ctr->nseg);
+    int seg;
+    if (memo) {
+        // phase engine: order the segment list by expected events (processing order is free, R6).  A domain
+        // whose last memoised rates predict >= hot_events events in the window (R_d * window) goes to the
+        // front, the rest fill the list from the back; CTAs claim the front first, so long event chains
+        // start at the first iteration instead of after a refill (shorter phase tail).
+        double Rd = 0.0;
+        if (owner)
+            for (int j = head[d]; j >= 0; j = next[j]) {
+                const double r = *reinterpret_cast<const double*>(memo + (size_t)(2 * j) * kMemoBytes + kMemoROff);
+                if (r > 0.0) Rd += r;                    // empty entries (NaN) and dead vacancies add nothing
+            }
+        const bool hot = owner && Rd * S.window >= hot_events;
+        const int h = block_alloc(hot ? 1 : 0, &ctr->nhot);
+        const int k = block_alloc(owner && !hot ? 1 : 0, &ctr->ncold);
+        seg = hot ? h : seg_cap - 1 - k;
+        block_alloc(owner ? 1 : 0, &ctr->nseg);
+    } else {
+        seg = block_alloc(owner ? 1 : 0, &ctr->nseg);
+    }
     if (!owner) return;
     int c = 0;
     for (int j = head[d]; j >= 0; j = next[j]) members[off + (c++)] = j;

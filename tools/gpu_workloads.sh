@@ -1,9 +1,7 @@
-# one GPU round-trip: build, the new/changed GPU tests, then bench lines for every workload config
+# one GPU round-trip: build, then bench lines for every workload config (serial: --events per step)
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "heterogeneous or voxel_batch or rates" > gpurun_out/pytest_sel.log 2>&1; echo pytest=$?
-tail -3 gpurun_out/pytest_sel.log
-for w in "c1" "c2" "c3" "c4" "c4 --voxel-T" "c5 --lam 1.0"; do
+for w in "c5" "c1" "c2" "c3" "c4" "c4 --voxel-T" "c5 --lam 1.0"; do
   n=$(echo $w | tr ' ' '_' | tr -d '-')
   timeout 400 python bench.py --workload $w --no-cpu-baseline > gpurun_out/bench_$n.json 2> gpurun_out/bench_$n.err; echo "$w rc=$?"
-  python -c "import json;d=json.load(open('gpurun_out/bench_$n.json'));print('$w', d['value'], d['ms_per_step'], d['events_per_s'], d['sim_seconds_per_wall_second'], d['roofline']['frac'])" 2>&1 | tail -1
+  python -c "import json;d=json.load(open('gpurun_out/bench_$n.json'));print('$w', d['value'], d['ms_per_step'], d['events_per_s'], d['sim_seconds_per_wall_second'], d['roofline']['frac'], d['e2e']['value'])" 2>&1 | tail -1
 done

@@ -823,10 +823,23 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     } while (0)
 
     h->num_sms = prop.multiProcessorCount;
+    // AKMC_VERBOSE: host wall time of the init stages (where bench.py's e2e init time goes)
+    const bool verbose = std::getenv("AKMC_VERBOSE") != nullptr;
+    auto t_lap = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!verbose) return;
+        cudaDeviceSynchronize();
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[akmc init] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_lap).count());
+        t_lap = t;
+    };
     CKI(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
+    lap("context + stream");
     CKI(cudaMalloc(&h->d_species, (size_t)h->sites));        // canonical upload buffer (temporary)
+    lap("malloc canonical buffer");
     CKI(cudaMemcpy(h->d_species, species, (size_t)h->sites, cudaMemcpyHostToDevice));
+    lap("H2D lattice");
     CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
     CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
     CKI(cudaMallocHost(&h->h_ctr, sizeof(DevCounters)));
@@ -867,9 +880,11 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaStreamSynchronize(h->stream));
         cudaFree(d_bc);
         cudaFree(d_max);
+        lap("vacancy scan");
         // storage layout with halo ghosts (periodic images)
         uint8_t* st = nullptr;
         CKI(cudaMalloc(&st, (size_t)h->ssites));
+        lap("malloc storage");
         const long long nlines = 16ll * h->F.NB[0] * h->F.NB[1] * h->F.NB[2] * h->nvox;
         scatter_storage_kernel<<<blocks_for(nlines, 256), 256, 0, h->stream>>>(h->d_species, st, h->F, h->nvox);
         const cudaError_t es = cudaStreamSynchronize(h->stream);
@@ -879,6 +894,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->d_iscratch = nullptr;
         h->d_overflow = nullptr;
     }
+    lap("scatter to bricks");
     const size_t nv = (size_t)h->vcap;
     CKI(cudaMalloc(&h->d_rates, nv * 8 * sizeof(double)));
     CKI(cudaMalloc(&h->d_E, nv * 8 * sizeof(double)));
@@ -917,6 +933,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaMalloc(&h->d_phase, 8 * sizeof(PhaseInfo)));
         CKI(cudaMallocHost(&h->h_phase, 8 * sizeof(PhaseInfo)));
     }
+    lap("per-vacancy / domain buffers");
     if (h->multi) {
         rc = init_multi(h);
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
@@ -928,6 +945,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         rc = prepare_fast_weights(h, mlp);
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
+    lap("multi-rank setup + weights");
     h->tc = cfg->barrier_model == AKMC_MODEL_MLP && cfg->precision == AKMC_PREC_FP32;
     h->engine = std::getenv("AKMC_LEGACY_LOOP") == nullptr;
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
@@ -976,6 +994,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         CKI(cudaMemcpy(h->d_members, mem.data(), mem.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     CKI(cudaStreamSynchronize(h->stream));
+    lap("engine setup + memo + segments");
 #undef CKI
     *out = h;
     return AKMC_OK;

@@ -60,7 +60,14 @@ def full(rep, out):
            "achieved_dram_GBps": (rd + wr) / (dur * 1e-6) / 1e9 if dur else None}
     for k in ["sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
               "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
-              "launch__cluster_dim_x" , "smsp__inst_executed.sum"]:
+              "launch__cluster_dim_x" , "smsp__inst_executed.sum",
+              # tensor pipe (the barrier network's layers 2-3) and L2 (the gather / W1' rows are L2 traffic)
+              "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+              "TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+              "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+              "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+              "lts__t_bytes.sum", "lts__t_sectors_op_read.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+              "l1tex__t_bytes.sum", "sm__cycles_elapsed.avg"]:
         if k in get:
             res[k] = get[k][0]
     stalls = {}

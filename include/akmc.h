@@ -160,6 +160,11 @@ int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t
  * Callable between steps in any mode; AKMC_ERR_INVALID on a wrong n or a bad T (state unchanged). */
 int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n);
 
+/* Diagnostics (no handle; current device): the device's deterministic exp / log (DESIGN.md sec. 5.3,
+ * reading A29) on n host doubles x -> y.  fn 0 = det_exp (rates, Eq. 8), 1 = det_log (residence time,
+ * S:198).  AKMC_ERR_INVALID for another fn or bad pointers, AKMC_ERR_CUDA on a device error.       */
+int akmc_debug_math(int32_t fn, const double* x, int64_t n, double* y);
+
 /* Launch the library's kernels on this CUDA stream (cudaStream_t as void*; NULL = the handle's
  * own stream).  profile != 0 records CUDA events around every barrier-kernel launch (mlp_ms).  */
 int akmc_set_stream(akmc_handle* h, void* stream);

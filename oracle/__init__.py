@@ -48,6 +48,8 @@ def lib():
         _lib.orc_philox.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
         _lib.orc_det_exp.argtypes = [C.c_double]; _lib.orc_det_exp.restype = C.c_double
         _lib.orc_det_log.argtypes = [C.c_double]; _lib.orc_det_log.restype = C.c_double
+        _lib.orc_det_exp_n.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.orc_det_log_n.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
         _lib.orc_window_offsets.argtypes = [P(C.c_int32)]
         _lib.orc_system_energy.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_void_p]
         _lib.orc_system_energy.restype = C.c_double
@@ -123,6 +125,20 @@ def det_exp(x: float) -> float:
 
 def det_log(u: float) -> float:
     return lib().orc_det_log(float(u))
+
+
+def det_exp_n(x) -> np.ndarray:
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(xs)
+    lib().orc_det_exp_n(_ptr(xs), int(xs.size), _ptr(y))
+    return y
+
+
+def det_log_n(x) -> np.ndarray:
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(xs)
+    lib().orc_det_log_n(_ptr(xs), int(xs.size), _ptr(y))
+    return y
 
 
 def window_offsets() -> np.ndarray:

@@ -133,6 +133,10 @@ double orc_det_log(double u)
     return fma(de, LN2_HI, fma(de, LN2_LO, lm));
 }
 
+/* array forms of the two (test convenience: one call instead of n ctypes calls) */
+void orc_det_exp_n(const double* x, int64_t n, double* y) { for (int64_t i = 0; i < n; ++i) y[i] = orc_det_exp(x[i]); }
+void orc_det_log_n(const double* x, int64_t n, double* y) { for (int64_t i = 0; i < n; ++i) y[i] = orc_det_log(x[i]); }
+
 /* ------------------------------------------------------------------ */
 /* geometry                                                             */
 /* ------------------------------------------------------------------ */

@@ -60,6 +60,7 @@ def load() -> C.CDLL:
     lib.akmc_init.argtypes = [C.POINTER(CConfig), P, P, P, P, C.POINTER(P)]
     lib.akmc_step.argtypes = [P, C.c_int64, C.POINTER(CCounters)]
     lib.akmc_run_until.argtypes = [P, C.c_double, C.c_int64, C.POINTER(CCounters)]
+    lib.akmc_debug_math.argtypes = [C.c_int32, P, C.c_int64, P]
     lib.akmc_state.argtypes = [P, P, P, C.POINTER(C.c_int64), P, C.POINTER(CCounters)]
     lib.akmc_rates.argtypes = [P, P, P]
     lib.akmc_eval_windows.argtypes = [P, P, C.c_int64, C.c_int32, P]
@@ -76,7 +77,7 @@ def load() -> C.CDLL:
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
-              "akmc_set_voxel_temperatures", "akmc_run_until"):
+              "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -130,6 +131,17 @@ class Config:
 
 def _ptr(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def debug_math(fn: int, x) -> np.ndarray:
+    """The device's det_exp (fn 0) / det_log (fn 1) on host doubles (diagnostics)."""
+    lib = load()
+    xs = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.empty_like(xs)
+    rc = lib.akmc_debug_math(int(fn), _ptr(xs), int(xs.size), _ptr(y))
+    if rc != AKMC_OK:
+        raise AkmcError(rc, "akmc_debug_math failed")
+    return y
 
 
 class Simulation:

@@ -1008,6 +1008,28 @@ int akmc_set_stream(akmc_handle* h, void* stream)
     return AKMC_OK;
 }
 
+__global__ void debug_math_kernel(int fn, const double* __restrict__ x, long long n, double* __restrict__ y)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = fn == 0 ? det_exp(x[i]) : det_log(x[i]);
+}
+
+int akmc_debug_math(int32_t fn, const double* x, int64_t n, double* y)
+{
+    if ((fn != 0 && fn != 1) || n < 0 || (n > 0 && (!x || !y))) return AKMC_ERR_INVALID;
+    if (n == 0) return AKMC_OK;
+    double* d = nullptr;
+    if (cudaMalloc(&d, (size_t)n * 2 * sizeof(double)) != cudaSuccess) return AKMC_ERR_CUDA;
+    cudaError_t e = cudaMemcpy(d, x, (size_t)n * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        debug_math_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(fn, d, (long long)n, d + n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(y, d + n, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? AKMC_OK : AKMC_ERR_CUDA;
+}
+
 int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n)
 {
     if (!h) return AKMC_ERR_RUNTIME;

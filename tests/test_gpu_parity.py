@@ -34,6 +34,22 @@ def _ocfg(orc, acfg):
                       model=acfg.barrier_model, domain=acfg.domain_cells, window_s=acfg.window_s, seed=acfg.seed)
 
 
+# ----------------------------------------------------------------------------- deterministic exp / log
+def test_det_exp_log_bitexact_vs_oracle(akmc, orc):
+    """the device det_exp / det_log (A29) equal the oracle's bit for bit on 2e7 arguments
+    spanning the ranges the path uses (-E/kT in [-60, 0] plus the tail to -700; u = k 2^-53 in (0, 1])."""
+    rng = np.random.default_rng(2604)
+    n = 10_000_000
+    xe = np.concatenate([-rng.random(n) * 60.0, -rng.random(n // 10) * 700.0, [0.0, -0.0, -1e-300, -5e-324]])
+    ye = akmc.debug_math(0, xe)
+    assert np.array_equal(ye.view(np.uint64), orc.det_exp_n(xe).view(np.uint64))
+    # Philox uniforms are multiples of 2^-53 in (0, 1]
+    u = np.concatenate([(rng.integers(0, 2 ** 53, n, dtype=np.int64) + 1).astype(np.float64) * 2.0 ** -53,
+                        2.0 ** -rng.integers(0, 54, n // 10).astype(np.float64), [1.0, 2.0 ** -53]])
+    yl = akmc.debug_math(1, u)
+    assert np.array_equal(yl.view(np.uint64), orc.det_log_n(u).view(np.uint64))
+
+
 # ----------------------------------------------------------------------------- network evaluation
 @pytest.mark.parametrize("weights", ["random", "physics_residual"])
 def test_eval_windows_fp64_bitexact(akmc, orc, weights):

@@ -304,3 +304,75 @@ def test_run_until_poisson_counts(orc):
     n = st.nev.astype(float)
     assert abs(n.mean() - lam) < 4.0 * math.sqrt(lam / nvox), n.mean()
     assert abs(n.var() / lam - 1.0) < 0.35
+
+
+def _unwrap_step(p0, p1, L):
+    """half-cell displacement of one 1NN hop under the periodic box of L cells (|component| = 1)"""
+    d = (p1 - p0 + L) % (2 * L) - L
+    return d
+
+
+def _half_cell_pos(site, L):
+    cell, b = site // 2, site % 2
+    x = cell % L; y = (cell // L) % L; z = cell // (L * L)
+    return np.stack([2 * x + b, 2 * y + b, 2 * z + b], axis=-1)
+
+
+def test_pure_fe_vacancy_diffusivity(orc):
+    """in pure Fe a vacancy random-walks on the bcc 1NN vectors (a/2)(+-1,+-1,+-1) with 8 equal rates
+    Gamma, so D = (1/6) sum_k Gamma |d_k|^2 = Gamma a^2: after n hops E|R|^2 = n (3/4) a^2 and E t = n/(8 Gamma),
+    i.e. E|R|^2 / (6 E t) = Gamma a^2.  200 independent voxels, 150 hops each."""
+    L = 6
+    nvox, n = 200, 150
+    one, _ = _pure_fe_with_vacancy(L)
+    sp = np.concatenate([one] * nvox)
+    eps, E0 = synth.illustrative_pair_params()
+    cfg = orc.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=37)
+    st = orc.State.from_species(cfg, sp)
+    spv = 2 * L ** 3
+    pos = _half_cell_pos(st.vac - np.arange(nvox) * spv, L)
+    R = np.zeros((nvox, 3))
+    for _ in range(n):
+        orc.run(cfg, st, 1, eps, E0)
+        p1 = _half_cell_pos(st.vac - np.arange(nvox) * spv, L)
+        d = _unwrap_step(pos, p1, L)
+        assert np.all(np.abs(d) == 1)                   # every hop is a 1NN vector (1/2,1/2,1/2) cell
+        R += d
+        pos = p1
+    a = 1.0                                             # lengths in cells: one half-cell unit = a/2
+    msd = np.mean(np.sum((R * a / 2) ** 2, axis=1))
+    gamma = cfg.nu0 * math.exp(-E0[0] / (cfg.kB * cfg.T))
+    D_est = msd / (6.0 * st.clock.mean())
+    # |R|^2 has mean n*3/4 and sd ~ n*3/4*sqrt(2/3); the clock mean is n/(8 Gamma) with relative sd 1/sqrt(n nvox)
+    rel_sd = math.sqrt(2.0 / 3.0) / math.sqrt(nvox) + 1.0 / math.sqrt(n * nvox)
+    assert abs(D_est / (gamma * a * a) - 1.0) < 4.0 * rel_sd, (D_est, gamma)
+
+
+def test_sublattice_time_consistency(orc):
+    """Windowed synchronous sublattice (A19): with configuration-independent rates (all pair
+    energies equal -> dE = 0) every isolated vacancy hops at Gamma_tot = 8 nu0 e^{-E0/kT} in serial
+    BKL.  A sweep advances the clock by the window and runs each vacancy in its sector's phase, so
+    events / (vacancies x Gamma_tot x clock) -> 1 as lambda -> 0, with the O(lambda) deficit of vacancies
+    that leave their sector mid-window (-0.34 % at lambda = 1/4, -3.7 % at lambda = 1)."""
+    L = 48
+    eps, E0 = synth.illustrative_pair_params()
+    eps = np.full_like(eps, -0.5)
+    sp = np.zeros(2 * L ** 3, dtype=np.uint8)
+    cells = [(x, y, z) for x in range(1, L, 8) for y in range(1, L, 8) for z in range(1, L, 8)]
+    for (x, y, z) in cells:                             # one vacancy per 8^3 domain, 8 cells apart
+        sp[2 * (x + L * (y + L * z))] = 6
+    nvac = len(cells)
+    gtot = 8 * 6.0e12 * math.exp(-E0[0] / (8.617333262e-5 * 563.0))
+    ratio = {}
+    for lam, sweeps in ((0.25, 200), (1.0, 60)):
+        cfg = orc.Config(cells=(L, L, L), model=0, domain=(8, 8, 8), window_s=synth.window_seconds(lam, E0[0]),
+                         seed=43)
+        st = orc.State.from_species(cfg, sp)
+        orc.run(cfg, st, sweeps, eps, E0)
+        assert st.clock[0] == pytest.approx(sweeps * cfg.window_s, rel=1e-12)
+        expected = nvac * gtot * st.clock[0]
+        ratio[lam] = (float(st.counters[0]) / expected, 1.0 / math.sqrt(expected))
+    r, sd = ratio[0.25]
+    assert abs(r - 1.0) < 4.0 * sd + 0.005, ratio
+    r1, sd1 = ratio[1.0]
+    assert r1 < 1.0 and abs(r1 - (1.0 - 0.037)) < 4.0 * sd1, ratio

@@ -48,3 +48,35 @@ def test_four_rank_invariance(tmp_path, grid, extra):
     res = json.loads(out.read_text())
     assert res["ok"], res
     assert res["events"] > 20
+
+
+def test_two_rank_nccl_transport(tmp_path):
+    """SURVEY 4.2 L4 (transport equivalence): the per-phase deltas over NCCL send/recv (AKMC_EXCHANGE=nccl)
+    give the same lattices as 1 rank and the oracle, like the default peer-mailbox path above."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = tmp_path / "multi_nccl.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29641", os.path.join(ROOT, "tools", "multi_check.py"),
+           "--grid", "2", "1", "1", "--out", str(out), "--oracle"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, AKMC_EXCHANGE="nccl"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"], res
+    assert res["events"] > 20
+
+
+def test_eight_rank_invariance(tmp_path):
+    """2x2x2 (all three axes decomposed, 7 distinct peers per rank, corner halos): 8 ranks == 1 rank (== oracle)."""
+    if _ngpu() < 8:
+        pytest.skip("needs 8 GPUs")
+    out = tmp_path / "multi8.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8", "--master-addr",
+           "127.0.0.1", "--master-port", "29688", os.path.join(ROOT, "tools", "multi_check.py"),
+           "--grid", "2", "2", "2", "--out", str(out), "--oracle", "--nvac", "120"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"], res
+    assert res["events"] > 20

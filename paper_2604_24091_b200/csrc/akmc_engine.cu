@@ -53,6 +53,9 @@
 #ifndef AKMC_CHAIN_NRUN         //  per sweep with 64; gated to the tail (<= 4 / 16 running domains) 1.97 / 2.04)
 #define AKMC_CHAIN_NRUN 1024    // ... only while the CTA holds at most this many running domains
 #endif
+#ifndef AKMC_SERIAL_CLOCK
+#define AKMC_SERIAL_CLOCK 1     // serial mode: voxel clock cached in the slot (no per-event global load)
+#endif
 #ifndef AKMC_L1_PROBE
 #define AKMC_L1_PROBE 0         // cycle laps inside layer 1 (diagnostic)
 #endif
@@ -635,7 +638,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const int h = cslot;
                         c.seg_used[h] = 1;
                         c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
-                        c.seg_t[h] = 0.0; c.seg_it[h] = 0u; c.seg_new[h] = 1;
+                        // serial mode: seg_t IS the voxel clock for the launch (same sums as p.clock += dt, no
+                        // dependent global load per event); sublattice: the domain's time in the window
+                        c.seg_t[h] = (AKMC_SERIAL_CLOCK && p.serial) ? p.clock[cdom] : 0.0;
+                        c.seg_it[h] = 0u; c.seg_new[h] = 1;
                         c.seg_run[h] = (p.serial && p.term[cdom]) ? 0 : 1;   // a terminal voxel stays frozen
                     }
                     int nplaced = 0;
@@ -1222,7 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         const unsigned long long n = (unsigned long long)p.nev[c.seg_dom[i]] + c.seg_it[i];
                         philox_uniforms(p.S.seed, make_uint4((uint32_t)n, (uint32_t)(n >> 32), c.seg_dom[i], 0u), u_sel, u_t);
                         dt = __ddiv_rn(-det_log(u_t), Rc);
-                        go = !(p.horizon && __dadd_rn(p.clock[c.seg_dom[i]], dt) > p.t_end);   // akmc_run_until
+                        go = !(p.horizon && __dadd_rn(AKMC_SERIAL_CLOCK ? c.seg_t[i] : p.clock[c.seg_dom[i]], dt) > p.t_end);
                     } else {
                         const unsigned long long ph = (unsigned long long)p.ph->phase;
                         philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
@@ -1278,7 +1284,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         my_events += 1ull;
                         if (p.serial) {
                             const unsigned v = c.seg_dom[i];
-                            p.clock[v] = __dadd_rn(p.clock[v], dt);
+                            p.clock[v] = AKMC_SERIAL_CLOCK ? c.seg_t[i] : __dadd_rn(p.clock[v], dt);
                             if ((int)c.seg_it[i] >= p.n_events) {   // this launch's events done
                                 p.nev[v] += c.seg_it[i];
                                 stop = true;

@@ -48,3 +48,27 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(akmc.AkmcError) as e:
         akmc.Simulation(akmc.Config(cells=(4, 4, 4)), np.zeros(128, np.uint8), np.zeros((2, 7, 7)), np.zeros(7))
     assert e.value.code == akmc.AKMC_ERR_CUDA
+
+
+def test_entry_points_reject_bad_arguments_without_device():
+    """Argument checks of the newer entry points happen before any device work (header contracts)."""
+    lib = akmc.load()
+    x = np.zeros(4)
+    y = np.zeros(4)
+    p = ctypes.c_void_p
+    assert lib.akmc_debug_math(7, p(x.ctypes.data), 4, p(y.ctypes.data)) == akmc.AKMC_ERR_INVALID   # unknown fn
+    assert lib.akmc_debug_math(0, None, 4, p(y.ctypes.data)) == akmc.AKMC_ERR_INVALID
+    assert lib.akmc_debug_math(0, None, 0, None) == akmc.AKMC_OK                                    # empty batch
+    ctr = akmc.akmc.CCounters()
+    assert lib.akmc_run_until(None, 1.0, 10, ctypes.byref(ctr)) == 1                                 # AKMC_ERR_RUNTIME
+    assert lib.akmc_set_voxel_temperatures(None, p(x.ctypes.data), 4) == 1
+    assert lib.akmc_step(None, 1, ctypes.byref(ctr)) == 1
+
+
+def test_no_device_math_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(akmc.AkmcError) as e:
+        akmc.debug_math(0, np.zeros(8))
+    assert e.value.code == akmc.AKMC_ERR_CUDA

@@ -50,15 +50,18 @@ enum { AKMC_MODEL_PAIR = 0, AKMC_MODEL_MLP = 1 };
  *  FP32 : "matrix multiplication ... executed in FP32": layer 1 FP64-accumulated sparse
  *         embedding bag rounded to FP32; layer 2 on tcgen05 tensor cores as an FP32-equivalent
  *         3-pass fp16 split (hi*hi + hi*lo + lo*hi, FP32 accumulate in TMEM); layer 3 FP32.
- *         Per-hop rates within 1e-5 relative of FP64 (north star).  Pair model: same as FP64. */
-enum { AKMC_PREC_FP64 = 0, AKMC_PREC_FP32 = 1 };
+ *         Per-hop rates within 1e-5 relative of FP64 (north star).  Pair model: same as FP64.
+ * FP16_FAST : SURVEY 8(b) "fast" mode, for information only: layers 2-3 as ONE fp16 pass (hi parts only,
+ *         FP32 accumulate; 1/3 of the tensor-core work and half the h1 traffic).  Rates ~1e-3 relative:
+ *         it does NOT meet the 1e-5 bar; trajectories are valid AKMC at approximate rates.  MLP only. */
+enum { AKMC_PREC_FP64 = 0, AKMC_PREC_FP32 = 1, AKMC_PREC_FP16_FAST = 2 };
 
 typedef struct akmc_config {
     int32_t  cells[3];        /* Lx,Ly,Lz bcc cells per voxel; each even, >= 4 and <= 4096   */
     int32_t  n_voxels;        /* >= 1 independent periodic voxels                          */
     int32_t  n_species;       /* must be 7 (A6); vacancy code 6                                    */
     int32_t  barrier_model;   /* AKMC_MODEL_PAIR or AKMC_MODEL_MLP        */
-    int32_t  precision;       /* AKMC_PREC_FP64 or AKMC_PREC_FP32                                  */
+    int32_t  precision;       /* AKMC_PREC_FP64, AKMC_PREC_FP32 or AKMC_PREC_FP16_FAST             */
     int32_t  domain_cells[3]; /* sublattice domain edge (reading A19/A21): {0,0,0} => serial BKL,  */
                               /* one competing set per voxel (A15); else each even, >= 6, divides */
                               /* cells (sector = domain/2 >= 3 cells, A20)                          */

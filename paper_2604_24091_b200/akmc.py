@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "akmc.h")
 
 AKMC_OK, AKMC_ERR_RUNTIME, AKMC_ERR_INVALID, AKMC_TERMINAL, AKMC_ERR_CUDA, AKMC_ERR_NCCL = range(6)
 MODEL_PAIR, MODEL_MLP = 0, 1
-PREC_FP64, PREC_FP32 = 0, 1
+PREC_FP64, PREC_FP32, PREC_FP16_FAST = 0, 1, 2
 STATUS = {0: "AKMC_OK", 1: "AKMC_ERR_RUNTIME", 2: "AKMC_ERR_INVALID", 3: "AKMC_TERMINAL", 4: "AKMC_ERR_CUDA",
           5: "AKMC_ERR_NCCL"}
 

@@ -271,7 +271,9 @@ int validate(const akmc_config* c, const double* eps, const double* E0, const do
     if (!(c->temperature_K > 0.0) || !std::isfinite(c->temperature_K)) { why = "temperature must be > 0 (S:154)"; return AKMC_ERR_INVALID; }
     if (!(c->nu0 > 0.0) || !std::isfinite(c->nu0) || !(c->kB > 0.0) || !std::isfinite(c->kB)) { why = "nu0 and kB must be > 0"; return AKMC_ERR_INVALID; }
     if (c->barrier_model != AKMC_MODEL_PAIR && c->barrier_model != AKMC_MODEL_MLP) { why = "unknown barrier_model"; return AKMC_ERR_INVALID; }
-    if (c->precision != AKMC_PREC_FP64 && c->precision != AKMC_PREC_FP32) { why = "unknown precision"; return AKMC_ERR_INVALID; }
+    if (c->precision != AKMC_PREC_FP64 && c->precision != AKMC_PREC_FP32 && c->precision != AKMC_PREC_FP16_FAST) {
+        why = "unknown precision"; return AKMC_ERR_INVALID;
+    }
     const bool sub = c->domain_cells[0] || c->domain_cells[1] || c->domain_cells[2];
     if (sub) {
         for (int a = 0; a < 3; ++a) {
@@ -462,6 +464,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.watch = h->d_watch;
     p.diag = h->d_phase_cycles ? h->d_phase_cycles + 32 : nullptr;
     p.seg_cap = (h->engine && h->hot_events > 0.0) ? h->vcap : 0;   // hot-first segment list (phase mode)
+    p.fast = h->cfg.precision == AKMC_PREC_FP16_FAST ? 1 : 0;
     return p;
 }
 
@@ -497,10 +500,12 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         EngineParams p = engine_params(h, kEngineEval);
         p.windows = windows; p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
         p.rates = rates; p.Rsum = R; p.E = E;
+        p.fast = prec == AKMC_PREC_FP16_FAST ? 1 : 0;
         CK(h, cudaMemsetAsync(h->d_cursor, 0, sizeof(unsigned int), h->stream));
         const int need = (max_rows + kRoundRows * kClusterN - 1) / (kRoundRows * kClusterN);
         CK(h, launch_engine(p, true, std::max(1, std::min(h->n_clusters, need)), h->num_sms, h->stream));
     } else {
+        if (prec == AKMC_PREC_FP16_FAST) return fail(h, AKMC_ERR_INVALID, "FP16 fast mode needs the engine (AKMC_LEGACY_LOOP unset)");
         MlpTcParams p{};
         p.species = h->d_species; p.vac = h->d_vac; p.windows = windows; p.F = h->F; p.G = h->G;
         p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
@@ -946,7 +951,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
     lap("multi-rank setup + weights");
-    h->tc = cfg->barrier_model == AKMC_MODEL_MLP && cfg->precision == AKMC_PREC_FP32;
+    h->tc = cfg->barrier_model == AKMC_MODEL_MLP && (cfg->precision == AKMC_PREC_FP32 || cfg->precision == AKMC_PREC_FP16_FAST);
     h->engine = std::getenv("AKMC_LEGACY_LOOP") == nullptr;
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
     CKI(engine_setup());
@@ -1597,7 +1602,8 @@ int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t
 {
     if (!h) return AKMC_ERR_RUNTIME;
     if (n < 0 || n > (1 << 26) || !windows || !E_out) return fail(h, AKMC_ERR_INVALID, "bad window batch");
-    if (precision != AKMC_PREC_FP64 && precision != AKMC_PREC_FP32) return fail(h, AKMC_ERR_INVALID, "unknown precision");
+    if (precision != AKMC_PREC_FP64 && precision != AKMC_PREC_FP32 && precision != AKMC_PREC_FP16_FAST)
+        return fail(h, AKMC_ERR_INVALID, "unknown precision");
     for (int64_t i = 0; i < n * kWin; ++i)
         if (windows[i] > kVac) return fail(h, AKMC_ERR_INVALID, "species code > 6 in window");
     if (n == 0) return AKMC_OK;

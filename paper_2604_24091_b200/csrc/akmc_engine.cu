@@ -285,7 +285,7 @@ __device__ __forceinline__ void l1_list_store(int r, uint8_t b0, uint8_t b1, uin
 }
 
 __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi,
-                                         uint8_t* g_lo, unsigned long long& ovf)
+                                         uint8_t* g_lo, unsigned long long& ovf, bool fast)
 {
     const int lane = threadIdx.x & 31;
     __half hi[8], lo[8];
@@ -298,12 +298,12 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
     const uint32_t off = (uint32_t)(m >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
     const uint4 vh = pack8(hi), vl = pack8(lo);
     *reinterpret_cast<uint4*>(A_hi + off) = vh;
-    *reinterpret_cast<uint4*>(A_lo + off) = vl;
+    if (!fast) *reinterpret_cast<uint4*>(A_lo + off) = vl;
     // the same 16 B into the L2 staging block of this CTA (row m % kRoundRows of its block)
     const uint32_t goff = (uint32_t)((m % kRoundRows) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
 #if !AKMC_XCHG_DSMEM
     *reinterpret_cast<uint4*>(g_hi + goff) = vh;
-    *reinterpret_cast<uint4*>(g_lo + goff) = vl;
+    if (!fast) *reinterpret_cast<uint4*>(g_lo + goff) = vl;
 #endif
 }
 
@@ -312,7 +312,7 @@ constexpr int kL1Rows = AKMC_L1_ROWS;
 __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
                                             const uint16_t* l1l, const float* __restrict__ W1f,
                                             const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
-                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf,
+                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf, bool fast,
                                             long long* lp = nullptr)
 {
     const int lane = threadIdx.x & 31;
@@ -377,7 +377,7 @@ __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, co
     plap(2);
 #pragma unroll
     for (int r = 0; r < kL1Rows; ++r)
-        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf);
+        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf, fast);
     __syncwarp();
     plap(3);
 }
@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffTmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool fast = kTC && p.fast;                 // AKMC_PREC_FP16_FAST: hi parts only (no lo MMAs / copies)
     const uint32_t rank = kTC ? cluster_rank() : 0u;
     const uint32_t off_lo = pack_off(p.G.off[lane]), off_hi = pack_off(p.G.off[lane + 32]);   // this lane's window slots
     // h2 slice and the layer-3 partials live in this CTA's own row block of A: dead once layer 2 has
@@ -892,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             rr[q] = c.miss[kRoundRows * k_round + (q < nv ? i + q * kWarps : i)];
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) {
@@ -934,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             rr[q] = q < nv ? i + q * kWarps : i;
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
@@ -973,11 +974,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             const uint32_t aoff = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
                             const uint16_t mask = (uint16_t)(((1u << kClusterN) - 1u) & ~(1u << rank));
                             bulk_g2s_multicast(smem_u32(A_hi + aoff), g_hi, rg * kRowGroupA, bar_req, mask);
-                            bulk_g2s_multicast(smem_u32(A_lo + aoff), g_lo, rg * kRowGroupA, bar_req, mask);
+                            if (!fast) bulk_g2s_multicast(smem_u32(A_lo + aoff), g_lo, rg * kRowGroupA, bar_req, mask);
                         }
                     } else {
                         const uint32_t cb = map_to(bar_req, d);
-                        mbar_remote_expect_tx(cb, 16u + 2u * rg * kRowGroupA);
+                        mbar_remote_expect_tx(cb, 16u + (fast ? 1u : 2u) * rg * kRowGroupA);
                         bulk_s2peer(map_to(smem_u32(&hdr[rank]), d), smem_u32(&hdr[rank]), 16u, cb);
                     }
 #endif
@@ -1015,8 +1016,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             const uint64_t dbh = umma_desc(wb + (uint32_t)ks * 2u * kW2Split, (kSliceN / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(wb + (uint32_t)ks * 2u * kW2Split + kW2Split, (kSliceN / 8) * 128, 128);
                             umma_f16(tmem + 0, dah, dbh, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + kSliceN, dah, dbl, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + kSliceN, dal, dbh, idesc, 1u);
+                            if (!fast) {
+                                umma_f16(tmem + kSliceN, dah, dbl, idesc, ks > 0 ? 1u : 0u);
+                                umma_f16(tmem + kSliceN, dal, dbh, idesc, 1u);
+                            }
                         }
                         umma_commit(bar_mma);
                     }
@@ -1035,7 +1038,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                 const int c0 = 32 * hc + 16 * hh;
                                 uint32_t d1[16], d2[16];
                                 tmem_ld16(tl + (uint32_t)c0, d1);
-                                tmem_ld16(tl + (uint32_t)(kSliceN + c0), d2);
+                                if (!fast) tmem_ld16(tl + (uint32_t)(kSliceN + c0), d2);
+                                else
+#pragma unroll
+                                    for (int t = 0; t < 16; ++t) d2[t] = 0u;
                                 tmem_wait_ld();
 #pragma unroll
                                 for (int g = 0; g < 2; ++g) {
@@ -1050,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                     }
                                     const uint32_t off = h2_off(m, c0 + 8 * g);
                                     *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
-                                    *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
+                                    if (!fast) *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
                                 }
                             }
                         }
@@ -1070,8 +1076,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             const uint64_t dbh = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split, (16 / 8) * 128, 128);
                             const uint64_t dbl = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split + kW3Split, (16 / 8) * 128, 128);
                             umma_f16(tmem + kTmemDa, dah, dbh, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + kTmemDa + 16, dah, dbl, idesc, ks > 0 ? 1u : 0u);
-                            umma_f16(tmem + kTmemDa + 16, dal, dbh, idesc, 1u);
+                            if (!fast) {
+                                umma_f16(tmem + kTmemDa + 16, dah, dbl, idesc, ks > 0 ? 1u : 0u);
+                                umma_f16(tmem + kTmemDa + 16, dal, dbh, idesc, 1u);
+                            }
                         }
                         umma_commit(bar_mma);
                     }
@@ -1084,7 +1092,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             uint32_t da[8], db[8];
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
                             tmem_ld8(tl + (uint32_t)kTmemDa, da);
-                            tmem_ld8(tl + (uint32_t)(kTmemDa + 16), db);
+                            if (!fast) tmem_ld8(tl + (uint32_t)(kTmemDa + 16), db);
+                            else
+#pragma unroll
+                                for (int t = 0; t < 8; ++t) db[t] = 0u;
                             tmem_wait_ld();
                             const int m = 32 * q4 + lane;
                             double pv[8];

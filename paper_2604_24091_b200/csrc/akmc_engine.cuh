@@ -49,6 +49,7 @@ enum EngineMode { kEnginePhase = 0, kEngineEval = 1 };
 struct EngineParams {
     int mode;               // kEnginePhase: run the phase's domains; kEngineEval: evaluate a row list
     int model;              // AKMC_MODEL_PAIR (0) / AKMC_MODEL_MLP (1)
+    int fast;               // 1: AKMC_PREC_FP16_FAST -- single-pass fp16 layers 2-3 (hi parts only)
     uint8_t* species;
     int4* vac;
     Frame F;

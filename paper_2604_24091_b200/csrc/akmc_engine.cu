@@ -382,7 +382,7 @@ __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, co
     plap(3);
 }
 
-template <bool kTC>
+template <bool kTC, bool kFast = false>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffTmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool fast = kTC && p.fast;                 // AKMC_PREC_FP16_FAST: hi parts only (no lo MMAs / copies)
+    constexpr bool fast = kTC && kFast;              // AKMC_PREC_FP16_FAST: hi parts only (no lo MMAs / copies);
+                                                     // a separate instantiation, so FP32 mode carries no branch
     const uint32_t rank = kTC ? cluster_rank() : 0u;
     const uint32_t off_lo = pack_off(p.G.off[lane]), off_hi = pack_off(p.G.off[lane + 32]);   // this lane's window slots
     // h2 slice and the layer-3 partials live in this CTA's own row block of A: dead once layer 2 has
@@ -1420,6 +1421,8 @@ size_t engine_smem_bytes() { return kSmemTotal; }
 cudaError_t engine_setup()
 {
     cudaError_t e = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
 }
@@ -1460,7 +1463,7 @@ cudaError_t launch_engine(const EngineParams& p, bool tc, int nclusters, int num
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, engine_kernel<true>, p);
+    return p.fast ? cudaLaunchKernelEx(&cfg, engine_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, engine_kernel<true>, p);
 }
 
 } // namespace akmc

@@ -8,6 +8,9 @@ side: FP64 pair KRA (equal to the physics-embedded network to <= 1e-12 eV) on th
   python tools/stats_longrun.py oracle OUT.npz [--nvox 256] [--events 1000000] [--procs 8]
   python tools/stats_longrun.py compare GPU.npz ORACLE.npz [--md profiles/...md]
 
+--weights residual (SURVEY 8(d) second set): both sides use the physics-embedded network plus a seeded random
+residual (barrier perturbations ~0.02 eV); the oracle evaluates that same network in FP64 (64 seeds x 1e5 events).
+
 The oracle runs the voxels in parallel processes WITHOUT changing any voxel's Philox stream: every process runs
 the full batch geometry (voxel ids fixed) with the vacancies of the voxels it does not own replaced by Fe, so
 those voxels are terminal at once and the owned ones follow exactly the trajectory of the full run (voxels never
@@ -33,10 +36,14 @@ def inputs(nvox):
     return synth.make_lattice((L, L, L), nvox, synth.fe_cu_fractions(0.01), 1, seed=SEED_LATTICE)
 
 
+def weights(kind):
+    eps, E0 = synth.illustrative_pair_params()
+    return eps, E0, (synth.physics_mlp(eps, E0, residual=0.02, seed=1) if kind == "residual" else synth.physics_mlp(eps, E0))
+
+
 def run_gpu(a):
     import paper_2604_24091_b200 as akmc
-    eps, E0 = synth.illustrative_pair_params()
-    mlp = synth.physics_mlp(eps, E0)
+    eps, E0, mlp = weights(a.weights)
     sp = inputs(a.nvox)
     cfg = akmc.Config(cells=(L, L, L), n_voxels=a.nvox, barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32,
                       seed=SEED_PHILOX)
@@ -54,18 +61,18 @@ def run_gpu(a):
 
 
 def _oracle_part(args):
-    nvox, events, own = args
+    nvox, events, own, kind = args
     import oracle
-    eps, E0 = synth.illustrative_pair_params()
+    eps, E0, mlp = weights(kind)
     sp = inputs(nvox)
     n = 2 * L ** 3
     for v in range(nvox):
         if v not in own:
             blk = sp[v * n:(v + 1) * n]
             blk[blk == 6] = 0
-    oc = oracle.Config(cells=(L, L, L), n_voxels=nvox, model=0, seed=SEED_PHILOX)
+    oc = oracle.Config(cells=(L, L, L), n_voxels=nvox, model=1 if kind == "residual" else 0, seed=SEED_PHILOX)
     st = oracle.State.from_species(oc, sp)
-    oracle.run(oc, st, events, eps, E0)
+    oracle.run(oc, st, events, eps, E0, mlp if kind == "residual" else None)
     return own, st.species, st.clock
 
 
@@ -76,7 +83,7 @@ def run_oracle(a):
     parts = [list(range(p, a.nvox, a.procs)) for p in range(a.procs)]
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(a.procs) as pool:
-        res = pool.map(_oracle_part, [(a.nvox, a.events, set(own)) for own in parts])
+        res = pool.map(_oracle_part, [(a.nvox, a.events, set(own), a.weights) for own in parts])
     n = 2 * L ** 3
     sp = inputs(a.nvox)
     clock = np.zeros(a.nvox)
@@ -119,8 +126,10 @@ def compare(a):
     ct = g["clock"].mean() / o["clock"].mean() - 1
     txt = "\n".join([
         f"# Long-run statistics parity (C1 geometry, {nvox} paired voxels x {int(g['events']) // nvox:,} events)", "",
-        "`tools/stats_longrun.py`: GPU = physics-embedded MLP in the tensor-core FP32-equivalent mode "
-        f"({float(g['seconds']):.1f} s on one B200); oracle = FP64 pair KRA on the same inputs and Philox streams "
+        "`tools/stats_longrun.py`: GPU = " + ("physics-embedded MLP + seeded random residual" if a.weights == "residual"
+                                              else "physics-embedded MLP") +
+        f" in the tensor-core FP32-equivalent mode ({float(g['seconds']):.1f} s on one B200); oracle = "
+        + ("the same network in FP64" if a.weights == "residual" else "FP64 pair KRA") + " on the same inputs and Philox streams "
         f"({float(o['seconds']):.1f} s on {os.cpu_count()} host cores).  Bar (north star): ensemble means within 2 % or "
         "the paired difference within 3 standard errors.", "",
         "| statistic (per voxel) | initial | oracle | GPU | rel. diff | paired diff ± s.e. | |", "|---|---|---|---|---|---|---|",
@@ -142,6 +151,7 @@ def main():
     ap.add_argument("--events", type=int, default=1000000)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     ap.add_argument("--md", default="")
+    ap.add_argument("--weights", choices=["physics", "residual"], default="physics")
     a = ap.parse_args()
     if a.mode == "gpu":
         a.out = a.paths[0]

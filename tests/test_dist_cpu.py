@@ -44,7 +44,7 @@ def _worker(rank, world, port, grid, block, q):
     tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("grid", [(2, 1, 1), (1, 2, 1)])
+@pytest.mark.parametrize("grid", [(2, 1, 1), (1, 2, 1), (2, 2, 2)])
 def test_block_decomposition_gloo(grid):
     world = grid[0] * grid[1] * grid[2]
     ctx = mp.get_context("spawn")

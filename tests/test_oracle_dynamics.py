@@ -376,3 +376,74 @@ def test_sublattice_time_consistency(orc):
     assert abs(r - 1.0) < 4.0 * sd + 0.005, ratio
     r1, sd1 = ratio[1.0]
     assert r1 < 1.0 and abs(r1 - (1.0 - 0.037)) < 4.0 * sd1, ratio
+
+
+def test_mfpt_poisson_equation(orc):
+    """P:338-347 (Eq. 5, Dynkin): the mean first-passage time tau(s) to an absorbing set solves
+    sum_a Gamma_a(s) [tau(Phi(s,a)) - tau(s)] + 1 = 0.  Enumerable space: L = 4 (128 sites), 1 V + 1 Cu in Fe,
+    absorbing = V and Cu first neighbours.  tau from the sparse linear solve over all 16,256 (V, Cu) states
+    (rates from the oracle's barriers) must equal the mean absorption time of serial BKL episodes
+    (S:195-198 clock) within 4 standard errors; with it, Eq. 7 with the exact u = Gamma_tot tau gives
+    delta-tau = tau(s) - tau(s') on every transition (plug-in identity)."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.linalg import spsolve
+    L = 4
+    n = 2 * L ** 3
+    eps = np.zeros((2, 7, 7))
+    eps[0] = -0.78; eps[1] = -0.39
+    eps[0, 6, :] = eps[0, :, 6] = -0.20; eps[0, 6, 1] = eps[0, 1, 6] = -0.33
+    eps[1, 6, :] = eps[1, :, 6] = -0.10; eps[1, 6, 1] = eps[1, 1, 6] = -0.18   # V-Cu 2NN binding
+    E0 = np.array([0.62, 0.54, 0.68, 0.60, 0.78, 0.70, 0.0])
+    cfg = orc.Config(cells=(L, L, L), model=0, T=700.0, seed=91)
+    nn = np.array([[_is_1nn(a, b, L) for b in range(n)] for a in range(n)])
+    idx = -np.ones((n, n), dtype=np.int64)          # state (v, c) -> unknown index (non-absorbing only)
+    states = [(v, c) for v in range(n) for c in range(n) if v != c and not nn[v, c]]
+    for i, (v, c) in enumerate(states):
+        idx[v, c] = i
+    offs = synth.window_offsets_np()[:8, :3]        # 1NN half-cell offsets, hop order k = 0..7
+    rows, cols, vals = [], [], []
+    gtot = np.empty(len(states))
+    rate_cache = {}
+    for i, (v, c) in enumerate(states):
+        sp = np.zeros(n, dtype=np.uint8); sp[v] = 6; sp[c] = 1
+        _, G, _ = orc.barriers(cfg, sp, v, eps, E0)
+        gtot[i] = G.sum()
+        rows.append(i); cols.append(i); vals.append(-G.sum())
+        pv = _half_cell_pos(np.array([v]), L)[0]
+        for k in range(8):
+            pn = (pv + offs[k]) % (2 * L)
+            t = int(2 * ((pn[0] // 2) + L * ((pn[1] // 2) + L * (pn[2] // 2))) + pn[0] % 2)
+            j = idx[t, c]                           # the vacancy moves to t (t != c: c is not a 1NN of v)
+            if j >= 0:
+                rows.append(i); cols.append(j); vals.append(G[k])
+        rate_cache[(v, c)] = G
+    A = csr_matrix((vals, (rows, cols)), shape=(len(states), len(states)))
+    tau = spsolve(A.tocsc(), -np.ones(len(states)))
+    assert np.all(tau > 0)
+    # Monte Carlo: absorption times of serial BKL episodes from one start state
+    v0, c0 = 0, 2 * (2 + L * (2 + L * 2))           # Cu two cells away along the body diagonal
+    assert idx[v0, c0] >= 0
+    times = []
+    for ep in range(1500):
+        sp = np.zeros(n, dtype=np.uint8); sp[v0] = 6; sp[c0] = 1
+        c = orc.Config(cells=(L, L, L), model=0, T=700.0, seed=1000 + ep)
+        st = orc.State.from_species(c, sp)
+        while not nn[st.vac[0], c0]:
+            orc.run(c, st, 1, eps, E0)
+        times.append(st.clock[0])
+    times = np.array(times)
+    t_exact = tau[idx[v0, c0]]
+    se = times.std(ddof=1) / math.sqrt(times.size)
+    print("mfpt", times.mean(), t_exact, se)
+    assert abs(times.mean() - t_exact) < 4 * se, (times.mean(), t_exact, se)
+    # Eq. 7 with the exact u = Gamma_tot tau reproduces delta-tau = tau(s) - tau(s') (absorbing: tau = 0)
+    u = gtot * tau
+    i0 = idx[v0, c0]
+    for k in range(8):
+        pv = _half_cell_pos(np.array([v0]), L)[0]
+        pn = (pv + offs[k]) % (2 * L)
+        t = int(2 * ((pn[0] // 2) + L * ((pn[1] // 2) + L * (pn[2] // 2))) + pn[0] % 2)
+        j = idx[t, c0]
+        tau_n, u_n, g_n = (tau[j], u[j], gtot[j]) if j >= 0 else (0.0, 0.0, 1.0)
+        dt_hat = (u[i0] - gtot[i0] / g_n * u_n) / gtot[i0]
+        assert dt_hat == pytest.approx(tau[i0] - tau_n, rel=1e-12, abs=1e-30)

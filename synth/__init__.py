@@ -347,3 +347,24 @@ def preset(name: str) -> Preset:
         return Preset("C5", (1024, 1024, 1024), 1, 214748, rpv, domain=(8, 8, 8), seed=2609,
                       notes="1024^3 per GPU, c_v 1e-4, sublattice D=8, lambda=1/4")
     raise KeyError(name)
+
+
+def with_vacancy_cluster(species: np.ndarray, cells, center) -> tuple:
+    """Degenerate input: a vacancy at basis-0 site `center` = (x, y, z) whose eight first neighbours are
+    also vacancies (the basis-1 sites of cells x-1..x, y-1..y, z-1..z with basis 1 at +(1/2, 1/2, 1/2)).
+    Every hop of the centre is masked (m_k = 0, P:288-289 / A14), so its R_i = 0 leaf sits inside the
+    competing set.  Returns (species copy, centre site id).  Geometry only, none of the method's arithmetic."""
+    Lx, Ly, Lz = cells
+    x, y, z = center
+    sp = np.array(species, dtype=np.uint8, copy=True)
+
+    def site(cx, cy, cz, b):
+        return 2 * ((cx % Lx) + Lx * ((cy % Ly) + Ly * (cz % Lz))) + b
+
+    c = site(x, y, z, 0)
+    sp[c] = 6
+    for dx in (-1, 0):
+        for dy in (-1, 0):
+            for dz in (-1, 0):
+                sp[site(x + dx, y + dy, z + dz, 1)] = 6
+    return sp, c

@@ -198,6 +198,45 @@ def test_voxel_batch_bitexact(akmc, orc):
     assert gctr["events"] == ost.counters[0]
 
 
+@pytest.mark.parametrize("mode", ["serial", "voxels", "sublattice"])
+def test_zero_rate_vacancy_bitexact(akmc, orc, mode):
+    """Degenerate input: a vacancy whose eight first neighbours are vacancies (every hop masked, R_i = 0,
+    A14) inside the competing set -- the zero leaf of the pairwise tree and the descent guards (A17).
+    FP64 pair trajectories bit-exact vs the oracle in serial, voxel-batch and sublattice mode; FP32
+    tensor-core rates have the oracle's masks (the centre's row all zero) and stay within 1e-5."""
+    eps, E0 = _params()
+    L = 16
+    nvox = 4 if mode == "voxels" else 1
+    base = synth.make_lattice((L, L, L), nvox, synth.fe_cu_fractions(0.05), 3, seed=61)
+    S = 2 * L ** 3
+    sp = base.copy()
+    for v in range(nvox):
+        sp[v * S:(v + 1) * S], _ = synth.with_vacancy_cluster(base[v * S:(v + 1) * S], (L, L, L), (5 + v, 6, 7))
+    dom, win = ((8, 8, 8), synth.window_seconds(1.0, E0[0])) if mode == "sublattice" else ((0, 0, 0), 0.0)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64,
+                      seed=17, domain_cells=dom, window_s=win)
+    n = 10 if mode == "sublattice" else 400
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, n, eps, E0, chunks=2)
+    assert ost.counters[0] > 20
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+    assert gctr["hop_evals"] == ost.counters[1]
+    if mode != "serial":
+        return
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=9)
+    cfg32 = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg32, sp, mlp=mlp) as sim:
+        R, _ = sim.rates()
+        _, vac, _, _ = sim.state(species=False)
+    Ro, _ = orc.rates(_ocfg(orc, cfg32), sp, vac, None, None, mlp)
+    assert np.array_equal(R == 0, Ro == 0)
+    assert np.any(np.all(Ro == 0, axis=1))           # the centre row is fully masked
+    m = Ro > 0
+    assert np.max(np.abs(R[m] / Ro[m] - 1)) <= RTOL_FAST
+
+
 @pytest.mark.parametrize("model", ["pair", "mlp"])
 def test_voxel_batch_heterogeneous_T_bitexact(akmc, orc, model):
     """C4 variant: per-voxel T uniform in 558-577 K; FP64 trajectories bit-exact vs the

@@ -132,6 +132,37 @@ def _is_1nn(a, b, L):
     return bool(np.all(d == 1))
 
 
+def test_zero_rate_vacancy_never_selected(orc):
+    """Degenerate case of the method: a vacancy whose eight first neighbours are all vacancies has every
+    hop masked (m_k = 0; Gamma = 0 exactly, A14), so its leaf R_i = 0 lies inside the competing
+    set.  Pins: brute-force geometry (the eight sites at half-cell distance (1,1,1) are V), all eight rates
+    of that vacancy are exactly 0 while its neighbours have positive rates, and over 300 seeds the first
+    BKL event never moves it and always takes a hop of positive rate."""
+    L = 8
+    eps, E0 = synth.illustrative_pair_params()
+    base = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), 2, seed=5)
+    sp, c = synth.with_vacancy_cluster(base, (L, L, L), (4, 4, 4))
+    nn = [j for j in range(sp.size) if _is_1nn(c, j, L)]
+    assert len(nn) == 8 and all(sp[j] == 6 for j in nn)
+    cfg = orc.Config(cells=(L, L, L), model=0)
+    st0 = orc.State.from_species(cfg, sp)
+    R, _ = orc.rates(cfg, st0.species, st0.vac, eps, E0)
+    ic = int(np.flatnonzero(st0.vac == c)[0])
+    assert np.all(R[ic] == 0.0)
+    assert all(R[int(np.flatnonzero(st0.vac == j)[0])].sum() > 0 for j in nn)
+    for seed in range(300):
+        cfg = orc.Config(cells=(L, L, L), model=0, seed=seed)
+        st = st0.copy()
+        assert orc.run(cfg, st, 1, eps, E0) == 0
+        moved = np.flatnonzero(st.vac != st0.vac)
+        assert moved.size == 1 and int(moved[0]) != ic
+        i = int(moved[0])
+        assert _is_1nn(int(st0.vac[i]), int(st.vac[i]), L)
+        d = (_bcc_pos(int(st.vac[i]), L) - _bcc_pos(int(st0.vac[i]), L)) % (2 * L)   # +1 or 2L-1 per axis
+        k = 4 * (d[0] == 1) + 2 * (d[1] == 1) + (d[2] == 1)                           # A4: k = 4[hx>0]+2[hy>0]+[hz>0]
+        assert R[i, k] > 0
+
+
 @pytest.mark.slow
 def test_boltzmann_stationarity_enumeration(orc):
     """North star / SURVEY 8(c): Boltzmann stationary distribution by exact enumeration on a tiny

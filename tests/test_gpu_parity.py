@@ -375,6 +375,24 @@ def test_terminal_and_conservation(akmc):
         assert np.array_equal(gsp, sp) and clock[0] == 0.0
 
 
+def test_sublattice_no_vacancy(akmc, orc):
+    """Empty input in sublattice mode: no vacancy in any domain.  Every phase is empty, each sweep still
+    advances the global clock by the window (A19/A22), no event, lattice unchanged -- as the oracle does."""
+    eps, E0 = _params()
+    L = 16
+    sp = np.zeros(2 * L ** 3, np.uint8)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=3,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(1.0, E0[0]))
+    ost = orc.State.from_species(_ocfg(orc, cfg), sp)
+    orc_rc = orc.run(_ocfg(orc, cfg), ost, 3, eps, E0)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        c = sim.step(3)
+        gsp, gvac, gclock, gctr = sim.state()
+    assert orc_rc == 0 and c["status"] == akmc.AKMC_OK
+    assert np.array_equal(gsp, sp) and gvac.size == 0
+    assert np.array_equal(gclock, ost.clock) and gctr["events"] == 0
+
+
 # ----------------------------------------------------------------------------- phase engine specifics
 def _crowded_lattice(L, n_spread, cluster_center, n_cluster, seed):
     """Fe-5%Cu lattice with n_spread random vacancies plus n_cluster vacancies packed around one site, so

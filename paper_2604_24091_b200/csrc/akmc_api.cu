@@ -878,6 +878,9 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->vcap = (int)std::max<int64_t>(h->nvac, 1);
         if (cfg->world > 1) h->vcap = (int)std::min<int64_t>(INT32_MAX / 16, 2 * h->nvac + 65536);
         CKI(cudaMalloc(&h->d_vac, (size_t)h->vcap * sizeof(int4)));
+        // slots beyond nvac (vcap >= 1 even with no vacancy; multi-rank spare capacity) start departed (x < 0):
+        // the activation reads vcap slots and must never see an uninitialised record as a vacancy
+        CKI(cudaMemsetAsync(h->d_vac, 0xFF, (size_t)h->vcap * sizeof(int4), h->stream));
         scan_write_kernel<<<nblk, kScanThreads, 0, h->stream>>>(sp4, nwords, d_bc, h->F, h->d_vac);
         CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
         vstart_kernel<<<blocks_for(h->nvox + 1, 128), 128, 0, h->stream>>>(h->d_vac, (int)h->nvac, h->nvox, h->d_vstart);

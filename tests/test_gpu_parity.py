@@ -237,6 +237,30 @@ def test_zero_rate_vacancy_bitexact(akmc, orc, mode):
     assert np.max(np.abs(R[m] / Ro[m] - 1)) <= RTOL_FAST
 
 
+def test_voxel_batch_empty_voxel(akmc, orc):
+    """Ragged voxel batch: the middle voxel holds no vacancy (empty competing set) while its
+    neighbours in the batch keep stepping.  The call reports AKMC_TERMINAL like the oracle, the empty voxel's
+    clock stays 0, and the other voxels' trajectories are bit-exact."""
+    eps, E0 = _params()
+    L, nvox = 8, 3
+    S = 2 * L ** 3
+    sp = synth.make_lattice((L, L, L), nvox, synth.fe_cu_fractions(0.05), 3, seed=5)
+    mid = sp[S:2 * S]
+    mid[mid == 6] = 0
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=4)
+    ost = orc.State.from_species(_ocfg(orc, cfg), sp)
+    orc_rc = orc.run(_ocfg(orc, cfg), ost, 50, eps, E0)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        c = sim.step(50)
+        gsp, gvac, gclock, gctr = sim.state()
+    assert orc_rc == akmc.AKMC_TERMINAL and c["status"] == akmc.AKMC_TERMINAL
+    assert ost.counters[0] == 100 and gctr["events"] == 100
+    assert gclock[1] == 0.0
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+
+
 @pytest.mark.parametrize("model", ["pair", "mlp"])
 def test_voxel_batch_heterogeneous_T_bitexact(akmc, orc, model):
     """C4 variant: per-voxel T uniform in 558-577 K; FP64 trajectories bit-exact vs the
@@ -391,6 +415,43 @@ def test_sublattice_no_vacancy(akmc, orc):
     assert orc_rc == 0 and c["status"] == akmc.AKMC_OK
     assert np.array_equal(gsp, sp) and gvac.size == 0
     assert np.array_equal(gclock, ost.clock) and gctr["events"] == 0
+    # the tensor-core evaluator path with zero rows: FP32 MLP sublattice step and akmc_rates
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=9)
+    cfg32 = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32, seed=3,
+                        domain_cells=(8, 8, 8), window_s=synth.window_seconds(1.0, E0[0]))
+    with akmc.Simulation(cfg32, sp, mlp=mlp) as sim:
+        c = sim.step(2)
+        R, E = sim.rates()
+        gsp, gvac, gclock, gctr = sim.state()
+    assert c["status"] == akmc.AKMC_OK and R.shape == (0, 8) and E.shape == (0, 8)
+    assert np.array_equal(gsp, sp) and gvac.size == 0 and gctr["events"] == 0
+    assert gclock[0] == 2 * cfg32.window_s
+
+
+@pytest.mark.parametrize("mode", ["serial", "sublattice"])
+def test_vacancy_cap_bitexact(akmc, orc, mode):
+    """Maximum size of the vacancy list: exactly 1 % of the sites (one more is AKMC_ERR_INVALID).
+    16^3 cells, 81 vacancies: ~10 per 8^3 domain (multi-slot competing sets) in sublattice mode, one
+    81-member competing set in serial mode.  FP64 pair trajectories bit-exact vs the oracle."""
+    eps, E0 = _params()
+    L = 16
+    nv = int(0.01 * 2 * L ** 3)
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), nv, seed=73)
+    dom, win = ((8, 8, 8), synth.window_seconds(0.25, E0[0])) if mode == "sublattice" else ((0, 0, 0), 0.0)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=29,
+                      domain_cells=dom, window_s=win)
+    n = 6 if mode == "sublattice" else 500
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, n, eps, E0, chunks=2)
+    assert gvac.size == nv and ost.counters[0] > 50
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+    assert gctr["hop_evals"] == ost.counters[1]
+    sp2 = sp.copy()
+    sp2[np.flatnonzero(sp2 != 6)[0]] = 6
+    with pytest.raises(akmc.AkmcError):
+        akmc.Simulation(cfg, sp2, eps, E0)
 
 
 # ----------------------------------------------------------------------------- phase engine specifics

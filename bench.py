@@ -46,6 +46,7 @@ def _traffic():
 
 
 TRAFFIC_PER_LAUNCH = _traffic()
+GATHER_BYTES_PER_VAC = 64 + 16      # SURVEY 8(d) algorithmic work per vac: window + vacancy record
 
 
 def env_rank():
@@ -355,6 +356,18 @@ def run_ours(args):
                                  "set by dependent event latency, not by tensor throughput (DESIGN.md sec. 8)",
                 "timing": "CUDA events around each engine launch in an instrumented pass of K further sweeps "
                           f"(host-stepped, {prof_ms:.2f} ms); share = kernel ms / graph-mode step ms"}
+        if mlp_ms > 0:
+            # north star: achieved HBM GB/s of the gather/encode/select work, beside the tensor roofline.
+            # Algorithmic bytes per vac: 64 B window + 16 B vacancy record; measured DRAM bytes per
+            # launch from the committed ncu capture (cold caches) over the warm average launch time.
+            hbm_peak = peaks.get("hbm_gbs", 6552.0)
+            alg_gbs = logical_rows * GATHER_BYTES_PER_VAC / mlp_s / 1e9
+            dram_gbs = (TRAFFIC_PER_LAUNCH / (1e-3 * mlp_ms / max(mlp_launch, 1)) / 1e9) if TRAFFIC_PER_LAUNCH else None
+            roof["hbm"] = {"achieved": alg_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": alg_gbs / hbm_peak,
+                           "bytes_per_vac": GATHER_BYTES_PER_VAC,
+                           "dram_achieved": dram_gbs, "dram_frac": (dram_gbs / hbm_peak) if dram_gbs else None,
+                           "what": "gather/encode/select bytes (64 B window + 16 B record per vac) / engine time; "
+                                   "dram_achieved = ncu DRAM bytes per launch / warm average launch time"}
         if executed:
             roof["executed"] = {"rows": int(mlp_rows), "achieved": executed, "frac": executed / tc_peak,
                                 "what": "network rows actually run (memo misses) x algorithmic FLOPs / engine time; the "

@@ -364,3 +364,61 @@ def test_softmax_equals_factorised(orc):
     for w, ix in ctx.items():
         for i in ix:
             assert np.allclose(num[w] / den / len(ix), p_soft[i], rtol=1e-12, atol=1e-15)
+
+
+def _half_cell_positions(L):
+    i = np.arange(2 * L ** 3)
+    b = i & 1
+    c = i >> 1
+    return np.stack([2 * (c % L) + b, 2 * ((c // L) % L) + b, 2 * (c // (L * L)) + b], axis=1)
+
+
+def _brute_cu_components(sp, L, cu=1):
+    """Cu clusters by brute force: all Cu pairs at min-image half-cell distance (1, 1, 1) are bonded (1NN,
+    S:222-225); components by scipy's graph routine."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    pos = _half_cell_positions(L)[sp == cu]
+    d = np.abs(pos[:, None, :] - pos[None, :, :]) % (2 * L)
+    d = np.minimum(d, 2 * L - d)
+    adj = np.all(d == 1, axis=2)
+    n, lab = connected_components(coo_matrix(adj), directed=False)
+    sizes = np.bincount(lab, minlength=n)
+    return sizes, int(adj.sum()) // 2
+
+
+def test_cluster_stats_bruteforce(orc):
+    """Pins the statistics the 2 % bar is measured with: the oracle's Cu cluster statistics equal a
+    brute-force 1NN graph + connected components on random lattices, and a hand-built case (a monomer, a
+    dimer, a straight <111> 4-chain = one precipitate, n* = 4) gives the counts written out here."""
+    L = 6
+    cfg = orc.Config(cells=(L, L, L), model=0)
+    S = 2 * L ** 3
+    pos = _half_cell_positions(L)
+
+    def site(h):
+        h = np.asarray(h) % (2 * L)
+        return int(np.flatnonzero(np.all(pos == h, axis=1))[0])
+
+    sp = np.zeros(S, np.uint8)
+    for h in [(0, 0, 0),                                         # monomer
+              (4, 4, 4), (5, 5, 5),                              # dimer (1NN)
+              (0, 6, 2), (1, 7, 3), (2, 8, 4), (3, 9, 5)]:        # straight <111> chain of 4
+        sp[site(h)] = 1
+    st = orc.cluster_stats(cfg, sp)
+    assert (st["n_cu"], st["n_clusters"], st["n_clusters2"], st["largest"], st["monomers"], st["precipitates"],
+            st["mean_size2"], st["cucu_bonds"]) == (7, 3, 2, 4, 1, 1, 3.0, 4)
+    assert list(st["hist"][:6]) == [0, 1, 1, 0, 1, 0]
+    rng = np.random.default_rng(11)
+    for frac in (0.05, 0.15, 0.3):
+        sp = np.where(rng.random(S) < frac, 1, rng.integers(0, 2, S) * 2).astype(np.uint8)   # Cu among Fe/Ni
+        sizes, bonds = _brute_cu_components(sp, L)
+        st = orc.cluster_stats(cfg, sp)
+        big = sizes[sizes >= 2]
+        assert st["n_cu"] == sizes.sum() and st["n_clusters"] == sizes.size
+        assert st["n_clusters2"] == big.size and st["largest"] == sizes.max()
+        assert st["monomers"] == np.sum(sizes == 1) and st["precipitates"] == np.sum(sizes >= 4)
+        assert st["mean_size2"] == (big.sum() / big.size if big.size else 0.0)
+        assert st["cucu_bonds"] == bonds
+        h = np.bincount(sizes, minlength=64)[:64]
+        assert np.array_equal(st["hist"], h)

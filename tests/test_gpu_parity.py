@@ -375,6 +375,28 @@ def test_sublattice_bitexact(akmc, orc, lam, driver):
     assert gctr["hop_evals"] == ost.counters[1]
 
 
+def test_sublattice_bitexact_1e4_events(akmc, orc):
+    """North-star bar in sublattice mode: >= 10^4 events (200 sweeps, 300 vacancies in the A508 alloy, 8^3
+    domains, lambda = 1) bit-exact vs the oracle -- lattice, vacancy registry, clock and counters -- with the
+    state compared after every 40 sweeps."""
+    eps, E0 = _params()
+    L = 32
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), 300, seed=91)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=12,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(1.0, E0[0]))
+    ost = orc.State.from_species(_ocfg(orc, cfg), sp)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        for _ in range(5):
+            sim.step(40)
+            orc.run(_ocfg(orc, cfg), ost, 40, eps, E0)
+            gsp, gvac, gclock, gctr = sim.state()
+            assert np.array_equal(gsp, ost.species)
+            assert np.array_equal(gvac, ost.vac)
+            assert np.array_equal(gclock, ost.clock)
+            assert gctr["events"] == ost.counters[0] and gctr["hop_evals"] == ost.counters[1]
+    assert ost.counters[0] >= 10_000
+
+
 def test_sublattice_mlp_fp64_bitexact(akmc, orc):
     eps, E0 = _params()
     L = 24

@@ -198,6 +198,44 @@ def test_voxel_batch_bitexact(akmc, orc):
     assert gctr["events"] == ost.counters[0]
 
 
+@pytest.mark.parametrize("model", ["pair", "mlp"])
+def test_anisotropic_cells_serial_bitexact(akmc, orc, model):
+    """Geometry edge case: Lx != Ly != Lz and none a multiple of the 4-cell brick (S:30 asks only even,
+    >= 4), so the last brick along every axis is ragged and a transposed axis or stride in the periodic
+    wrap / brick index would move a hop to the wrong site.  Three voxels, FP64, bit-exact vs the oracle."""
+    eps, E0 = _params()
+    cells, nvox = (6, 10, 14), 3
+    sp = synth.make_lattice(cells, nvox, synth.a508_atomic_fractions(), 4, seed=71)
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=7) if model == "mlp" else None
+    cfg = akmc.Config(cells=cells, n_voxels=nvox, barrier_model=akmc.MODEL_PAIR if model == "pair" else akmc.MODEL_MLP,
+                      precision=akmc.PREC_FP64, seed=23)
+    if mlp is None:
+        ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 400, eps, E0, chunks=2)
+    else:
+        ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 200, mlp=mlp, chunks=2)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0]
+
+
+def test_anisotropic_domains_sublattice_bitexact(akmc, orc):
+    """Sublattice mode on a non-cubic lattice with non-cubic domains (18 x 24 x 30 cells, 6 x 8 x 10-cell
+    domains, so 3 x 3 x 3 domains with sectors of 3 x 4 x 5 cells, A20) and ragged bricks along x and z:
+    the sector permutation, activation and window bookkeeping per axis.  FP64 pair, 6 sweeps, bit-exact."""
+    eps, E0 = _params()
+    cells = (18, 24, 30)
+    sp = synth.make_lattice(cells, 1, synth.a508_atomic_fractions(), 60, seed=73)
+    cfg = akmc.Config(cells=cells, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=29,
+                      domain_cells=(6, 8, 10), window_s=synth.window_seconds(1.0, E0[0]))
+    ost, (gsp, gvac, gclock, gctr) = _run_both(akmc, orc, cfg, sp, 6, eps, E0, chunks=2)
+    assert np.array_equal(gsp, ost.species)
+    assert np.array_equal(gvac, ost.vac)
+    assert np.array_equal(gclock, ost.clock)
+    assert gctr["events"] == ost.counters[0] and gctr["hop_evals"] == ost.counters[1]
+    assert ost.counters[0] > 0
+
+
 @pytest.mark.parametrize("mode", ["serial", "voxels", "sublattice"])
 def test_zero_rate_vacancy_bitexact(akmc, orc, mode):
     """Degenerate input: a vacancy whose eight first neighbours are vacancies (every hop masked, R_i = 0,

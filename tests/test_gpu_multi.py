@@ -18,13 +18,14 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("grid,extra", [((2, 1, 1), ["--oracle"]), ((1, 2, 1), []),
-                                        ((2, 1, 1), ["--model", "mlp", "--precision", "fp32"])])
+                                        ((2, 1, 1), ["--model", "mlp", "--precision", "fp32"]),
+                                        ((2, 1, 1), ["--oracle", "--cells", "18", "16", "30", "--domain", "6", "8", "10"])])
 def test_two_rank_invariance(tmp_path, grid, extra):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     out = tmp_path / "multi.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
-           "127.0.0.1", "--master-port", str(29600 + grid[1]), os.path.join(ROOT, "tools", "multi_check.py"),
+           "127.0.0.1", "--master-port", str(29600 + grid[1] + 3 * len(extra)), os.path.join(ROOT, "tools", "multi_check.py"),
            "--grid", *map(str, grid), "--out", str(out), *extra]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

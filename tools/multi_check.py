@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--cells", type=int, nargs=3, default=[16, 16, 16])
     ap.add_argument("--sweeps", type=int, default=6)
     ap.add_argument("--nvac", type=int, default=40)
+    ap.add_argument("--domain", type=int, nargs=3, default=[8, 8, 8])
     ap.add_argument("--lam", type=float, default=1.0)
     ap.add_argument("--model", default="pair", choices=["pair", "mlp"])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
@@ -46,13 +47,13 @@ def main():
     prec = akmc.PREC_FP32 if a.precision == "fp32" else akmc.PREC_FP64
     win = synth.window_seconds(a.lam, E0[0])
     nid = D.broadcast_nccl_id(rank, device=torch.device("cuda", local))
-    cfg = akmc.Config(cells=block, barrier_model=model, precision=prec, domain_cells=(8, 8, 8), window_s=win, seed=5,
+    cfg = akmc.Config(cells=block, barrier_model=model, precision=prec, domain_cells=tuple(a.domain), window_s=win, seed=5,
                       gpu_grid=grid, rank=rank, world=world, nccl_id=nid)
     sim = akmc.Simulation(cfg, D.block_of(glob, block, grid, rank), eps, E0, mlp)
     if a.debug:
         # lockstep with a single-rank reference; after every sweep each rank's extended block (halo
         # included) must equal the reference global lattice around its block (periodic images)
-        ref = akmc.Simulation(akmc.Config(cells=G, barrier_model=model, precision=prec, domain_cells=(8, 8, 8),
+        ref = akmc.Simulation(akmc.Config(cells=G, barrier_model=model, precision=prec, domain_cells=tuple(a.domain),
                                           window_s=win, seed=5), glob, eps, E0, mlp)
         cx, cy, cz = D.rank_coords(rank, grid)
         O = (cx * block[0], cy * block[1], cz * block[2])
@@ -91,7 +92,7 @@ def main():
         order = np.argsort(gids)
         events = sum(p[4] for p in parts)
         hop = sum(p[5] for p in parts)
-        ref_cfg = akmc.Config(cells=G, barrier_model=model, precision=prec, domain_cells=(8, 8, 8), window_s=win, seed=5)
+        ref_cfg = akmc.Config(cells=G, barrier_model=model, precision=prec, domain_cells=tuple(a.domain), window_s=win, seed=5)
         ref = akmc.Simulation(ref_cfg, glob, eps, E0, mlp)
         rc = ref.step(a.sweeps)
         rsp, rvac, rclock, _ = ref.state()
@@ -104,7 +105,7 @@ def main():
                   "clock_equal": all(p[3] == float(rclock[0]) for p in parts)}
         if a.oracle:
             import oracle
-            oc = oracle.Config(cells=G, model=model, domain=(8, 8, 8), window_s=win, seed=5)
+            oc = oracle.Config(cells=G, model=model, domain=tuple(a.domain), window_s=win, seed=5)
             st = oracle.State.from_species(oc, glob)
             oracle.run(oc, st, a.sweeps, eps, E0, mlp)
             result["oracle_species_equal"] = bool(np.array_equal(gsp, st.species))

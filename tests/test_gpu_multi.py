@@ -35,14 +35,16 @@ def test_two_rank_invariance(tmp_path, grid, extra):
 
 
 @pytest.mark.parametrize("grid,extra", [((2, 2, 1), ["--oracle", "--nvac", "60"]), ((1, 2, 2), ["--oracle", "--nvac", "60"]),
-                                        ((2, 2, 1), ["--model", "mlp", "--precision", "fp32", "--nvac", "60"])])
+                                        ((2, 2, 1), ["--model", "mlp", "--precision", "fp32", "--nvac", "60"]),
+                                        ((1, 2, 2), ["--oracle", "--nvac", "60", "--cells", "12", "18", "14",
+                                                     "--domain", "6", "6", "14"])])
 def test_four_rank_invariance(tmp_path, grid, extra):
     """Two decomposed axes (edge and corner halos, 3 distinct peers per rank): 4 ranks == 1 rank (== oracle)."""
     if _ngpu() < 4:
         pytest.skip("needs 4 GPUs")
     out = tmp_path / "multi4.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4", "--master-addr",
-           "127.0.0.1", "--master-port", str(29670 + grid[0] + 2 * grid[2]), os.path.join(ROOT, "tools", "multi_check.py"),
+           "127.0.0.1", "--master-port", str(29670 + grid[0] + 2 * grid[2] + 3 * len(extra)), os.path.join(ROOT, "tools", "multi_check.py"),
            "--grid", *map(str, grid), "--out", str(out), *extra]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

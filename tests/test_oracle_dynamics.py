@@ -478,3 +478,36 @@ def test_mfpt_poisson_equation(orc):
         tau_n, u_n, g_n = (tau[j], u[j], gtot[j]) if j >= 0 else (0.0, 0.0, 1.0)
         dt_hat = (u[i0] - gtot[i0] / g_n * u_n) / gtot[i0]
         assert dt_hat == pytest.approx(tau[i0] - tau_n, rel=1e-12, abs=1e-30)
+
+
+def test_anisotropic_hops_are_first_neighbours(orc):
+    """Geometry pin on a non-cubic box (each Lx, Ly, Lz even and >= 4, not necessarily equal):
+    every event the oracle applies moves one vacancy by a bcc first-neighbour vector (+-1/2, +-1/2, +-1/2)
+    cells under the periodic metric of EACH axis (hops go to the 8 first neighbours), composition is
+    conserved, and all 8 directions occur.  Brute force from site coordinates, so a transposed axis or a
+    stride of the wrong length in the oracle's neighbour table fails here."""
+    cells = (6, 10, 14)
+    Lx, Ly, Lz = cells
+    sp = synth.make_lattice(cells, 1, synth.fe_cu_fractions(0.1), 3, seed=17)
+    cfg = orc.Config(cells=cells, model=0, seed=31)
+    eps, E0 = synth.illustrative_pair_params()
+    st = orc.State.from_species(cfg, sp)
+    counts0 = np.bincount(sp, minlength=7)
+
+    def pos2(i):                       # doubled coordinates: 2*cell + basis
+        b, c = i % 2, i // 2
+        return np.array([2 * (c % Lx) + b, 2 * ((c // Lx) % Ly) + b, 2 * (c // (Lx * Ly)) + b])
+
+    seen = set()
+    for _ in range(600):
+        before = st.vac.copy()
+        assert orc.run(cfg, st, 1, eps, E0) == orc.ORC_OK
+        moved = np.flatnonzero(st.vac != before)
+        assert moved.size == 1
+        d = pos2(st.vac[moved[0]]) - pos2(before[moved[0]])
+        d = (d + np.array([Lx, Ly, Lz])) % (2 * np.array([Lx, Ly, Lz])) - np.array([Lx, Ly, Lz])
+        assert np.array_equal(np.abs(d), [1, 1, 1]), d
+        seen.add(tuple(d))
+    assert len(seen) == 8
+    assert np.array_equal(np.bincount(st.species, minlength=7), counts0)
+    assert np.array_equal(np.sort(st.vac), np.flatnonzero(st.species == 6))

@@ -20,14 +20,17 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 ORC_OK, ORC_INVALID, ORC_TERMINAL = 0, 2, 3
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle: plain C11, -O2, no SIMD intrinsics, no FP contraction."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+def build(force: bool = False, mutant: int = 0) -> str:
+    """Compile the oracle: plain C11, -O2, no SIMD intrinsics, no FP contraction.  mutant != 0 builds a
+    separate fault-injected copy (liboracle_mutant<k>.so, -DORC_MUTANT=k) that the selection-law tests
+    must reject; the real library is always built with ORC_MUTANT = 0."""
+    out = _LIB if not mutant else os.path.join(_HERE, f"liboracle_mutant{int(mutant)}.so")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-o", _LIB + ".tmp", _SRC, "-lm"]
+               f"-DORC_MUTANT={int(mutant)}", "-o", out + ".tmp", _SRC, "-lm"]
         subprocess.run(cmd, check=True)
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
 class _Cfg(C.Structure):
@@ -68,7 +71,43 @@ def lib():
         _lib.orc_cluster_stats.argtypes = [P(_Cfg), C.c_void_p, C.c_int64, C.c_int, C.c_int,
                                            C.c_void_p, C.c_void_p, C.c_int64]
         _lib.orc_sector_perm.argtypes = [C.c_uint64, C.c_int64, P(C.c_int)]
+        _declare_selection(_lib)
     return _lib
+
+
+def _declare_selection(L):
+    P = C.POINTER
+    L.orc_bkl_select_u.argtypes = [C.c_void_p, C.c_int, C.c_double, P(C.c_int), P(C.c_int)]
+    L.orc_bkl_select_u.restype = C.c_double
+    L.orc_draw_uniforms.argtypes = [C.c_uint64, P(C.c_uint32), P(C.c_double), P(C.c_double)]
+
+
+def bkl_select_u(G, u_sel: float, L=None):
+    """One residence-time selection (the oracle's tree + descent + pick_hop) over hop rates G[n][8] with a
+    given u_sel; returns (Gamma_tot, vacancy i, hop k).  L: an alternative build (mutant tests)."""
+    g = np.ascontiguousarray(G, dtype=np.float64).reshape(-1, 8)
+    i, k = C.c_int(), C.c_int()
+    tot = (L or lib()).orc_bkl_select_u(_ptr(g), int(g.shape[0]), float(u_sel), C.byref(i), C.byref(k))
+    return tot, i.value, k.value
+
+
+def draw_uniforms(seed: int, ctr) -> tuple:
+    c = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    us, ut = C.c_double(), C.c_double()
+    lib().orc_draw_uniforms(int(seed) & 0xFFFFFFFFFFFFFFFF, c, C.byref(us), C.byref(ut))
+    return us.value, ut.value
+
+
+def load_variant(path: str):
+    """ctypes handle of an alternative oracle build (fault-injected copies for the selection tests)."""
+    L = C.CDLL(path)
+    _declare_selection(L)
+    P = C.POINTER
+    L.orc_run.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    L.orc_rates.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                            C.c_void_p, C.c_void_p, C.c_void_p]
+    return L
 
 
 def _ptr(a):
@@ -213,11 +252,11 @@ class State:
                      self.sweep.copy(), self.counters.copy())
 
 
-def run(cfg: Config, st: State, n: int, eps=None, E0=None, mlp=None) -> int:
+def run(cfg: Config, st: State, n: int, eps=None, E0=None, mlp=None, L=None) -> int:
     e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
     e0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
     m = None if mlp is None else np.ascontiguousarray(mlp, dtype=np.float64)
-    return lib().orc_run(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
+    return (L or lib()).orc_run(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
                          _ptr(st.nev), _ptr(st.sweep), _ptr(e), _ptr(e0), _ptr(m), int(n), _ptr(st.counters))
 
 

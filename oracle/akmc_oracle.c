@@ -31,6 +31,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#ifndef ORC_MUTANT
+#define ORC_MUTANT 0   /* test-only fault injection (tests/test_oracle_selection.py); 0 in every real build */
+#endif
+
 #define NSPEC 7   /* Fe0 Cu1 Ni2 Mn3 Si4 P5 V6 (A6) */
 #define VAC 6
 #define FE 0
@@ -438,7 +442,11 @@ static double tree_build(const double* R, int n, double* buf, int* P_out, int* l
 {
     int P = 1, levels = 0;
     while (P < n) { P <<= 1; ++levels; }
+#if ORC_MUTANT == 3   /* test-only mutant: the padded tree drops the last real leaf */
+    for (int i = 0; i < P; ++i) buf[i] = (i < n - 1) ? R[i] : 0.0;
+#else
     for (int i = 0; i < P; ++i) buf[i] = (i < n) ? R[i] : 0.0;
+#endif
     int off = 0, width = P;
     while (width > 1) {
         for (int i = 0; i < width / 2; ++i) buf[off + width + i] = buf[off + 2 * i] + buf[off + 2 * i + 1];
@@ -462,12 +470,18 @@ static int tree_descend(const double* buf, const double* R, int n, int P, double
     int idx = 0;
     for (int l = nlev; l >= 1; --l) {
         double left = buf[offs[l - 1] + 2 * idx];
+#if ORC_MUTANT == 1   /* test-only mutant: right turn keeps r (no subtraction of the left mass) */
+        if (r < left) idx = 2 * idx; else idx = 2 * idx + 1;
+#elif ORC_MUTANT == 2 /* test-only mutant: wrong child offset (children swapped) */
+        if (r < left) { idx = 2 * idx + 1; } else { r = r - left; idx = 2 * idx; }
+#else
         if (r < left) {
             idx = 2 * idx;
         } else {
             r = r - left;
             idx = 2 * idx + 1;
         }
+#endif
     }
     if (idx >= n || !(R[idx] > 0.0)) {
         int last = -1;
@@ -489,6 +503,39 @@ static int pick_hop(const double G[8], double r)
     int last = -1;
     for (int k = 0; k < 8; ++k) if (G[k] > 0.0) last = k;
     return last;
+}
+
+/* One residence-time selection over n competing vacancies (Eq. 2 with log-rate logits, P:294-298;
+ * S:195-198): R_i = sequential sum of the 8 hop rates G[i][0..7] (A17); Gamma_tot = canonical pairwise tree
+ * over R_0..R_{n-1}; r = u_sel * Gamma_tot; descend to the vacancy, then pick_hop inside it.  This is exactly
+ * the code path of run_serial / run_sublattice (they call tree_build / tree_descend / pick_hop in this order).
+ * Returns Gamma_tot; *i_out = *k_out = -1 when Gamma_tot == 0 (terminal). */
+double orc_bkl_select_u(const double* G, int n, double u_sel, int* i_out, int* k_out)
+{
+    double* R = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    double* buf = (double*)malloc(sizeof(double) * 4 * (size_t)(n + 2));
+    for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < 8; ++k) s = s + G[8 * i + k];
+        R[i] = s;
+    }
+    int P = 1, lev = 0;
+    double tot = (n > 0) ? tree_build(R, n, buf, &P, &lev) : 0.0;
+    *i_out = -1; *k_out = -1;
+    if (tot > 0.0) {
+        double r = u_sel * tot;
+        int a = tree_descend(buf, R, n, P, &r);
+        *i_out = a;
+        *k_out = pick_hop(&G[8 * a], r);
+    }
+    free(R); free(buf);
+    return tot;
+}
+
+/* the serial-mode uniforms of one event (A16/A18): Philox4x32-10(key = seed; ctr = (c0, c1, c2, c3)) */
+void orc_draw_uniforms(uint64_t seed, const uint32_t ctr[4], double* u_sel, double* u_t)
+{
+    draw_uniforms(seed, ctr[0], ctr[1], ctr[2], ctr[3], u_sel, u_t);
 }
 
 /* ------------------------------------------------------------------ */

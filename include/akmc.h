@@ -139,6 +139,21 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
  * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
 int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
 
+/* Checkpoint / resume (lattice + vacancy list + clock + counters is a full checkpoint; the
+ * counter-based RNG needs no state).  akmc_progress reads the rest of the run position: nev_out [n_voxels]
+ * (may be NULL) = each voxel's serial event index (the Philox counter of its next event, S:195-198 / A16),
+ * sweep_out (may be NULL) = sublattice sweeps done (the next sweep's sector permutation and phase counters).
+ * akmc_restore, on a handle freshly created by akmc_init from a checkpointed lattice, re-establishes that
+ * position: vac_sites [n_vac] (may be NULL) = the checkpoint's vacancy sites in SLOT order (akmc_state's
+ * vac_sites_out), which fixes the slot ids and therefore every competing-set tree order (A17); clock_s
+ * [n_voxels] and nev [n_voxels] may be NULL; sweep >= 0.  The resumed run is bit-identical to the unsplit
+ * one.  AKMC_ERR_INVALID (state unchanged) when vac_sites is not a permutation of the lattice's vacancy
+ * sites, slots are not grouped by voxel in ascending order, a clock is negative or non-finite, a counter is
+ * negative, or the handle is multi-rank (world > 1).                                                     */
+int akmc_progress(akmc_handle* h, int64_t* nev_out, int64_t* sweep_out);
+int akmc_restore(akmc_handle* h, const int64_t* vac_sites, int64_t n_vac, const double* clock_s, const int64_t* nev,
+                 int64_t sweep);
+
 /* Diagnostics: the voxel-0 block INCLUDING its halo, cells [-2, L+2) per axis, canonical order
  * (2*(x + (Lx+4)*(y + (Ly+4)*z)) + b over the extended box); out holds 2*(Lx+4)*(Ly+4)*(Lz+4) bytes.  */
 int akmc_debug_extended(akmc_handle* h, uint8_t* out);

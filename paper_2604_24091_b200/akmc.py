@@ -70,6 +70,8 @@ def load() -> C.CDLL:
     lib.akmc_set_stream.argtypes = [P, P]
     lib.akmc_set_profiling.argtypes = [P, C.c_int32]
     lib.akmc_set_voxel_temperatures.argtypes = [P, P, C.c_int32]
+    lib.akmc_progress.argtypes = [P, P, P]
+    lib.akmc_restore.argtypes = [P, P, C.c_int64, P, P, C.c_int64]
     lib.akmc_free.argtypes = [P]
     lib.akmc_free.restype = None
     lib.akmc_last_error.argtypes = [P]
@@ -77,7 +79,7 @@ def load() -> C.CDLL:
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
-              "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math"):
+              "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math", "akmc_progress", "akmc_restore"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -211,6 +213,21 @@ class Simulation:
         n = C.c_int64(cap)
         self._check(self.lib.akmc_vacancies(self.h, _ptr(gid), _ptr(site), C.byref(n)))
         return gid[: n.value], site[: n.value]
+
+    def progress(self):
+        """(per-voxel serial event counters, sublattice sweeps done): with state(), a full checkpoint."""
+        nev = np.empty(self.cfg.n_voxels, dtype=np.int64)
+        sw = C.c_int64(0)
+        self._check(self.lib.akmc_progress(self.h, _ptr(nev), C.byref(sw)))
+        return nev, int(sw.value)
+
+    def restore(self, vac_sites=None, clock=None, nev=None, sweep: int = 0):
+        """Resume a checkpoint on a handle created from its lattice (akmc_restore)."""
+        v = None if vac_sites is None else np.ascontiguousarray(vac_sites, dtype=np.int64)
+        c = None if clock is None else np.ascontiguousarray(clock, dtype=np.float64)
+        n = None if nev is None else np.ascontiguousarray(nev, dtype=np.int64)
+        self._check(self.lib.akmc_restore(self.h, _ptr(v), 0 if v is None else int(v.size), _ptr(c), _ptr(n),
+                                          int(sweep)))
 
     def debug_extended(self) -> np.ndarray:
         """Voxel-0 block including its 2-cell halo, canonical over the extended box (diagnostics)."""

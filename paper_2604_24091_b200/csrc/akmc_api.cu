@@ -14,7 +14,6 @@
 
 #include "../../include/akmc.h"
 #include "akmc_kernels.cuh"
-#include "akmc_mlp_tc.cuh"
 #include "akmc_engine.cuh"
 #include <nccl.h>
 
@@ -143,12 +142,11 @@ struct akmc_handle {
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;     // pinned
     double* d_mlp = nullptr;
-    uint8_t* d_Bimg = nullptr;        // ring image: W1'^T (24 chunks) + W2^T (16 chunks), fp16 hi/lo
-    uint8_t* d_W3img = nullptr;       // W3^T hi/lo, N padded to 16
     float* d_b2 = nullptr;
     double* d_b3 = nullptr;
-    float s1u = 1.0f, s2u = 1.0f;
+    float s2u = 1.0f, h1s = 1.0f, h2s = 1.0f;
     double s3u = 1.0;
+    int act_shift[2] = {0, 0};        // t1, t2: activation scales 2^-t (prepare_engine_weights)
     unsigned long long* d_overflow = nullptr;
     // phase engine (akmc_engine.cuh)
     bool engine = true;               // false: legacy grid-synchronous inner loop (AKMC_LEGACY_LOOP=1)
@@ -189,6 +187,8 @@ struct akmc_handle {
     int rc[3] = {0, 0, 0};            // this rank's block coordinates
     DistParams DP{};
     int peer_rank[kMaxPeers] = {};
+    int* d_free = nullptr;            // free local slots (departures), reused by arrivals
+    int* d_fcnt = nullptr;            // [0] free count [1] pops [2] unpack blocks done
     int* d_gid = nullptr;             // global slot id per local slot
     int* d_nvac = nullptr;            // live local slot count (device)
     int4* d_log = nullptr;
@@ -235,7 +235,7 @@ void free_all(akmc_handle* h)
 {
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
-                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp, h->d_Bimg, h->d_W3img,
+                    h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp,
                     h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
                     h->d_stage, h->d_canon, h->d_wstore, h->d_kT};
     for (void* p : ptrs)
@@ -250,7 +250,7 @@ void free_all(akmc_handle* h)
         if (h->ipc_box[r]) cudaIpcCloseMemHandle(h->ipc_box[r]);
         if (h->ipc_flag[r]) cudaIpcCloseMemHandle(h->ipc_flag[r]);
     }
-    void* dptrs[] = {h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
+    void* dptrs[] = {h->d_free, h->d_fcnt, h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
                      h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone};
     for (void* p : dptrs)
         if (p) cudaFree(p);
@@ -311,8 +311,9 @@ int validate(const akmc_config* c, const double* eps, const double* E0, const do
     return AKMC_OK;
 }
 
-// fast-mode weight preparation
-int prepare_fast_weights(akmc_handle* h, const double* mlp)
+// FP32-equivalent evaluator weights: Fe-referenced layer-1 table, fp16 hi/lo UMMA images
+// of the per-CTA W2 / W3 slices, and the power-of-two scales of weights and activations
+int prepare_engine_weights(akmc_handle* h, const double* mlp)
 {
     const double* W1 = mlp;
     const double* b1 = W1 + 448 * kHid;
@@ -320,95 +321,70 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
     const double* b2 = W2 + kHid * kHid;
     const double* W3 = b2 + kHid;
     const double* b3 = W3 + kHid * 8;
+    constexpr double kLoScale = 2048.0;           // lo parts are stored * 2^11
     // power-of-two scale so that max|w| * 2^s <= 2^13 (fp16 hi/lo splits stay in range)
     auto scale_exp = [](const double* w, size_t n) {
         double mx = 0.0;
         for (size_t i = 0; i < n; ++i) mx = std::max(mx, std::fabs(w[i]));
         return mx > 0.0 ? 13 - (int)std::ceil(std::log2(mx)) : 0;
     };
-    // UMMA K-major no-swizzle image of B[n][k] (N rows, K cols): core matrices of 8 rows x 16 B
-    auto put = [](uint8_t* img, int N, int n, int k, double w) {
-        const __half hi = __float2half_rn((float)w);
-        const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
-        const size_t off = ((size_t)(k / 8) * (N / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-        const size_t split = (size_t)N * 16 * 2;    // per K-step of 16, hi then lo
-        reinterpret_cast<__half*>(img + (size_t)(k / 16) * 2 * split + (off % split))[0] = hi;
-        reinterpret_cast<__half*>(img + (size_t)(k / 16) * 2 * split + split + (off % split))[0] = lo;
-    };
-    // layer 1: Fe-referenced rows W1'[6*slot + s-1] = W1[7*slot+s] - W1[7*slot+Fe] (s = 1..6), bias
-    // b1' = b1 + sum_slot W1[7*slot+Fe] (exact algebra: one species per slot)
-    // layer-1 K: K-step 0 = bias columns, then species-major one-hot columns
-    // k = 16 + (s-1)*64 + slot (s = 1..6) so that a K-step is all-zero for a tile unless the tile holds
-    // species s in its 16-slot group (skipped exactly: a zero K-step adds exact zeros)
-    std::vector<double> W1p((size_t)kK1 * kHid, 0.0), b1p(kHid);
+    // layer 1, Fe-referenced (exact algebra, one species per slot): b1' = b1 + sum_slot W1[7*slot+Fe],
+    // W1'(s, slot) = W1[7*slot+s] - W1[7*slot+Fe] for s = 1..6; table row 0 = b1', row 1+(s-1)*64+slot = W1'
+    std::vector<double> w1p((size_t)kW1Rows * kHid);
     for (int j = 0; j < kHid; ++j) {
         double acc = b1[j];
         for (int s = 0; s < kWin; ++s) acc += W1[(size_t)(kSpecies * s + kFe) * kHid + j];
-        b1p[j] = acc;
+        w1p[j] = acc;
     }
-    for (int slot = 0; slot < kWin; ++slot)
-        for (int s = 1; s < kSpecies; ++s)
+    for (int s = 1; s < kSpecies; ++s)
+        for (int slot = 0; slot < kWin; ++slot)
             for (int j = 0; j < kHid; ++j)
-                W1p[(size_t)(16 + (s - 1) * kWin + slot) * kHid + j] =
+                w1p[(size_t)(1 + (s - 1) * kWin + slot) * kHid + j] =
                     W1[(size_t)(kSpecies * slot + s) * kHid + j] - W1[(size_t)(kSpecies * slot + kFe) * kHid + j];
-    double mx1 = 0.0;
-    for (int j = 0; j < kHid; ++j) mx1 = std::max(mx1, std::fabs(b1p[j]));
-    for (double w : W1p) mx1 = std::max(mx1, std::fabs(w));
-    const int s1 = mx1 > 0.0 ? 13 - (int)std::ceil(std::log2(mx1)) : 0;
+    // activation bounds over ALL windows: h1_j <= max(0, b1'_j + sum_slot max(0, max_s W1'(s,slot)_j)), and
+    // h2_j <= max(0, b2_j + sum_i max(0, W2_ij) * U1_i); the activation scales 2^-t keep every U * 2^-t <= 2^15,
+    // so the fp16 hi part of an activation can never overflow (t = 0 for O(1) activations: bits unchanged)
+    std::vector<double> U1((size_t)kHid), U2((size_t)kHid);
+    double m1 = 0.0, m2 = 0.0;
+    for (int j = 0; j < kHid; ++j) {
+        double u = w1p[j];
+        for (int slot = 0; slot < kWin; ++slot) {
+            double mx = 0.0;
+            for (int s = 1; s < kSpecies; ++s) mx = std::max(mx, w1p[(size_t)(1 + (s - 1) * kWin + slot) * kHid + j]);
+            u += mx;
+        }
+        U1[(size_t)j] = std::max(0.0, u);
+        m1 = std::max(m1, U1[(size_t)j]);
+    }
+    for (int j = 0; j < kHid; ++j) {
+        double u = b2[j];
+        for (int i = 0; i < kHid; ++i) u += std::max(0.0, W2[(size_t)i * kHid + j]) * U1[(size_t)i];
+        U2[(size_t)j] = std::max(0.0, u);
+        m2 = std::max(m2, U2[(size_t)j]);
+    }
+    // AKMC_NO_ACT_SCALE: fault injection for the overflow guard's test (no activation scaling)
+    const bool no_scale = std::getenv("AKMC_NO_ACT_SCALE") != nullptr;
+    const int t1 = (m1 > 32768.0 && !no_scale) ? (int)std::ceil(std::log2(m1 / 32768.0)) : 0;
+    const int t2 = (m2 > 32768.0 && !no_scale) ? (int)std::ceil(std::log2(m2 / 32768.0)) : 0;
     const int s2 = scale_exp(W2, (size_t)kHid * kHid);
     const int s3 = scale_exp(W3, (size_t)kHid * 8);
-    h->s1u = (float)std::ldexp(1.0, -s1);
-    h->s2u = (float)std::ldexp(1.0, -s2);
-    h->s3u = std::ldexp(1.0, -s3);
-    std::vector<uint8_t> img((size_t)kChunksTile * kStageBytes, 0);
-    for (int k = 16; k < kK1; ++k)                               // chunks 1..24: W1'^T
-        for (int n = 0; n < kHid; ++n) put(img.data(), kHid, n, k, std::ldexp(W1p[(size_t)k * kHid + n], s1));
-    // chunk 0: b1' (scaled) as three fp16 pieces: column 0 carries hi (D1) and mid (D2 = lo*2^11 frame),
-    // column 1 carries the third piece in the D2 frame, so D1 + 2^-11 D2 holds b1' to ~2^-33 relative
-    for (int n = 0; n < kHid; ++n) {
-        const double b = std::ldexp(b1p[n], s1);
-        const __half hi = __float2half_rn((float)b);
-        const double r1 = (b - (double)__half2float(hi)) * (double)kLoScale;
-        const __half mid = __float2half_rn((float)r1);
-        const __half lo2 = __float2half_rn((float)(r1 - (double)__half2float(mid)));
-        const size_t split = (size_t)kHid * 16 * 2;
-        for (int k = 0; k < 2; ++k) {
-            const size_t off = ((size_t)(k / 8) * (kHid / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-            reinterpret_cast<__half*>(img.data() + off)[0] = k == 0 ? hi : __float2half_rn(0.0f);
-            reinterpret_cast<__half*>(img.data() + split + off)[0] = k == 0 ? mid : lo2;
-        }
-    }
-    for (int k = 0; k < kHid; ++k)                               // chunks 25..40: W2^T
-        for (int n = 0; n < kHid; ++n)
-            put(img.data() + (size_t)kChunksL1 * kStageBytes, kHid, n, k, std::ldexp(W2[(size_t)k * kHid + n], s2));
-    // W3^T padded to N = 16: per K-step of 16 the layout above interleaves hi/lo, so build the two
-    // K=256 splits separately (no-swizzle, LBO = 256 B)
-    std::vector<uint8_t> w3img((size_t)2 * kW3SplitBytes, 0);
-    for (int k = 0; k < kHid; ++k)
-        for (int n = 0; n < 8; ++n) {
-            const double w = std::ldexp(W3[(size_t)k * 8 + n], s3);
-            const __half hi = __float2half_rn((float)w);
-            const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
-            const size_t off = ((size_t)(k / 8) * (kN3 / 8) + n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-            reinterpret_cast<__half*>(w3img.data() + off)[0] = hi;
-            reinterpret_cast<__half*>(w3img.data() + kW3SplitBytes + off)[0] = lo;
-        }
+    h->act_shift[0] = t1;
+    h->act_shift[1] = t2;
+    h->s2u = (float)std::ldexp(1.0, t1 - s2);
+    h->s3u = std::ldexp(1.0, t2 - s3);
+    h->h1s = (float)std::ldexp(1.0, -t1);
+    h->h2s = (float)std::ldexp(1.0, -t2);
     std::vector<float> b2f(kHid);
     for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
-    // phase-engine evaluator images (akmc_engine.cu): FP32 layer-1 table (b1' then W1' rows), and per
-    // cluster CTA r the fp16 hi/lo UMMA images of W2^T columns [32r, 32r+32) and W3 rows [32r, 32r+32)
+    // per cluster CTA r: fp16 hi/lo UMMA images of W2^T columns [64r, 64r+64) and W3 rows [64r, 64r+64)
     {
         std::vector<float> w1f((size_t)kW1Rows * kHid);
-        for (int n = 0; n < kHid; ++n) w1f[n] = (float)b1p[n];
-        for (int s = 1; s < kSpecies; ++s)
-            for (int slot = 0; slot < kWin; ++slot)
-                for (int n = 0; n < kHid; ++n)
-                    w1f[(size_t)(1 + (s - 1) * kWin + slot) * kHid + n] = (float)W1p[(size_t)(16 + (s - 1) * kWin + slot) * kHid + n];
+        for (size_t i = 0; i < w1f.size(); ++i) w1f[i] = (float)w1p[i];
         const size_t w2b = (size_t)(kHid / 16) * 2 * kSliceN * 16 * 2, w3b = (size_t)(kSliceN / 16) * 2 * 16 * 16 * 2;
         std::vector<uint8_t> w2e((size_t)kClusterN * w2b, 0), w3e((size_t)kClusterN * w3b, 0);
-        auto put_split = [](uint8_t* stepbase, int N, int n, int kk, double w) {   // one K-step (16), hi then lo
+        auto put_split = [&](uint8_t* stepbase, int N, int n, int kk, double w) {   // one K-step (16), hi then lo
             const __half hi = __float2half_rn((float)w);
-            const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * (double)kLoScale));
+            const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * kLoScale));
             const size_t off = ((size_t)(kk / 8) * (N / 8) + n / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2;
             const size_t split = (size_t)N * 16 * 2;
             reinterpret_cast<__half*>(stepbase + off)[0] = hi;
@@ -431,15 +407,10 @@ int prepare_fast_weights(akmc_handle* h, const double* mlp)
         CK(h, cudaMemcpy(h->d_W2e, w2e.data(), w2e.size(), cudaMemcpyHostToDevice));
         CK(h, cudaMemcpy(h->d_W3e, w3e.data(), w3e.size(), cudaMemcpyHostToDevice));
     }
-    CK(h, cudaMalloc(&h->d_Bimg, img.size()));
-    CK(h, cudaMalloc(&h->d_W3img, w3img.size()));
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
     CK(h, cudaMalloc(&h->d_b3, 8 * 8));
-    CK(h, cudaMemcpy(h->d_Bimg, img.data(), img.size(), cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->d_W3img, w3img.data(), w3img.size(), cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
-    CK(h, mlp_tc_setup());
     if (std::getenv("AKMC_PHASE_TIMING")) {
         CK(h, cudaMalloc(&h->d_phase_cycles, kDiagWords * sizeof(unsigned long long)));
         CK(h, cudaMemset(h->d_phase_cycles, 0, kDiagWords * sizeof(unsigned long long)));
@@ -457,7 +428,7 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.segs = h->d_segs; p.members = h->d_members; p.mpos = h->d_mpos; p.ctr = h->d_ctr; p.memo = h->d_memo;
     p.scratch = h->d_scratch; p.iscratch = h->d_iscratch; p.cursor = h->d_cursor;
     p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
-    p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.mlp64 = h->d_mlp;
+    p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.h1s = h->h1s; p.W.h2s = h->h2s; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
     p.stage = h->d_stage;
     p.wstore = h->d_wstore;
@@ -496,7 +467,9 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         eval_mlp_fp64_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
                                                            h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
         CK(h, cudaGetLastError());
-    } else if (h->engine) {
+    } else {
+        // FP32-equivalent / FP16-fast: the engine's cluster evaluator in eval mode (the same arithmetic, row for
+        // row, as inside the phase engine -- every path that produces a rate produces the same bits, R7)
         EngineParams p = engine_params(h, kEngineEval);
         p.windows = windows; p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
         p.rates = rates; p.Rsum = R; p.E = E;
@@ -504,18 +477,6 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         CK(h, cudaMemsetAsync(h->d_cursor, 0, sizeof(unsigned int), h->stream));
         const int need = (max_rows + kRoundRows * kClusterN - 1) / (kRoundRows * kClusterN);
         CK(h, launch_engine(p, true, std::max(1, std::min(h->n_clusters, need)), h->num_sms, h->stream));
-    } else {
-        if (prec == AKMC_PREC_FP16_FAST) return fail(h, AKMC_ERR_INVALID, "FP16 fast mode needs the engine (AKMC_LEGACY_LOOP unset)");
-        MlpTcParams p{};
-        p.species = h->d_species; p.vac = h->d_vac; p.windows = windows; p.F = h->F; p.G = h->G;
-        p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
-        p.Bimg = reinterpret_cast<const __half*>(h->d_Bimg);
-        p.W3img = reinterpret_cast<const __half*>(h->d_W3img);
-        p.b2 = h->d_b2; p.b3 = h->d_b3;
-        p.s1_unscale = h->s1u; p.s2_unscale = h->s2u; p.s3_unscale = h->s3u;
-        p.P = h->P; p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
-        p.phase_cycles = h->d_phase_cycles;
-        CK(h, launch_mlp_tc(p, max_rows, h->num_sms, h->stream));
     }
     h->total.kernel_launches += 1;
     h->total.mlp_launches += 1;
@@ -691,6 +652,11 @@ int init_multi(akmc_handle* h)
     CK(h, cudaMalloc(&h->d_dist_overflow, sizeof(int)));
     CK(h, cudaMalloc(&h->d_gid, (size_t)h->vcap * sizeof(int)));
     CK(h, cudaMalloc(&h->d_nvac, sizeof(int)));
+    CK(h, cudaMalloc(&h->d_free, (size_t)h->vcap * sizeof(int)));
+    CK(h, cudaMalloc(&h->d_fcnt, 4 * sizeof(int)));
+    CK(h, cudaMemset(h->d_fcnt, 0, 4 * sizeof(int)));
+    h->S.freelist = h->d_free;
+    h->S.fcnt = h->d_fcnt;
     CK(h, cudaMemset(h->d_nlog, 0, sizeof(unsigned long long)));
     CK(h, cudaMemset(h->d_dist_overflow, 0, sizeof(int)));
     CK(h, cudaMemset(h->d_send, 0, std::max<size_t>(1, np * per) * sizeof(int4)));
@@ -876,7 +842,15 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         if ((double)h->nvac > 0.01 * (double)h->sites) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "vacancies exceed 1% of sites (S:48)"); }
         if (h->nvac > INT32_MAX / 8) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies"); }
         h->vcap = (int)std::max<int64_t>(h->nvac, 1);
-        if (cfg->world > 1) h->vcap = (int)std::min<int64_t>(INT32_MAX / 16, 2 * h->nvac + 65536);
+        if (cfg->world > 1) {
+            // arrivals from other ranks need spare slots (departed slots are reused, akmc_dist.cuh FreeList);
+            // AKMC_VCAP_SPARE (tests) shrinks the spare to exercise the reuse
+            int64_t spare = 65536;
+            if (const char* sv = std::getenv("AKMC_VCAP_SPARE")) spare = std::max<int64_t>(0, std::atoll(sv));
+            const int64_t want = h->nvac + std::max<int64_t>(h->nvac, 0) + spare;
+            if (want > INT32_MAX / 16) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies per rank for the slot capacity"); }
+            h->vcap = (int)std::max<int64_t>(want, 1);
+        }
         CKI(cudaMalloc(&h->d_vac, (size_t)h->vcap * sizeof(int4)));
         // slots beyond nvac (vcap >= 1 even with no vacancy; multi-rank spare capacity) start departed (x < 0):
         // the activation reads vcap slots and must never see an uninitialised record as a vacancy
@@ -950,12 +924,19 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
         CKI(cudaMalloc(&h->d_mlp, n * sizeof(double)));
         CKI(cudaMemcpy(h->d_mlp, mlp, n * sizeof(double), cudaMemcpyHostToDevice));
-        rc = prepare_fast_weights(h, mlp);
+        rc = prepare_engine_weights(h, mlp);
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
     lap("multi-rank setup + weights");
     h->tc = cfg->barrier_model == AKMC_MODEL_MLP && (cfg->precision == AKMC_PREC_FP32 || cfg->precision == AKMC_PREC_FP16_FAST);
     h->engine = std::getenv("AKMC_LEGACY_LOOP") == nullptr;
+    if (h->sub) {
+        // the phase engine holds at most kRowCap vacancies of one competing set (domain, active sector) in a CTA;
+        // a sector with more sites than that could exceed it, so such configurations run the grid-synchronous
+        // inner loop (any set size; same selection arithmetic, same evaluator -> same trajectory bits)
+        const long long sec_sites = 2LL * (cfg->domain_cells[0] / 2) * (cfg->domain_cells[1] / 2) * (cfg->domain_cells[2] / 2);
+        if (sec_sites > kRowCap) h->engine = false;
+    }
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
     CKI(engine_setup());
     if (h->tc) {
@@ -1260,7 +1241,8 @@ static int exchange_deltas(akmc_handle* h)
         pack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
                                                           h->PB, h->epoch, h->d_dist_overflow);
         unpack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
-                                                            h->d_vac, h->d_gid, h->d_nvac, h->vcap, h->d_dist_overflow);
+                                                            h->d_vac, h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
+                                                            h->d_dist_overflow);
         CK(h, cudaGetLastError());
         h->total.kernel_launches += 2;
         h->exchanges += 1;
@@ -1277,7 +1259,8 @@ static int exchange_deltas(akmc_handle* h)
     }
     NCK(h, ncclGroupEnd());
     unpack_deltas_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_recv, np, h->F, h->DP, h->d_species, h->d_vac, h->d_gid,
-                                                            h->d_nvac, h->vcap, h->d_dist_overflow);
+                                                            h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
+                                                            h->d_dist_overflow);
     clear_headers_kernel<<<1, 32, 0, h->stream>>>(h->d_send, np, h->DP.cap, h->d_nlog);
     CK(h, cudaGetLastError());
     h->total.kernel_launches += 3;
@@ -1413,6 +1396,22 @@ static int step_sublattice(akmc_handle* h, int64_t n)
     return AKMC_OK;
 }
 
+// The evaluator's fp16 range guard and the engine's capacity guards count into d_overflow ("must stay 0").  A
+// non-zero count means some rate of this call was formed from a clamped activation or some competing set was
+// not run: the call fails loudly instead of returning a wrong trajectory with AKMC_OK.
+static int check_overflow(akmc_handle* h, const char* where)
+{
+    unsigned long long ovf = 0;
+    CK(h, cudaMemcpyAsync(&ovf, h->d_overflow, sizeof(ovf), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (!ovf) return AKMC_OK;
+    CK(h, cudaMemsetAsync(h->d_overflow, 0, sizeof(ovf), h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return fail(h, AKMC_ERR_RUNTIME, std::string(where) + ": " + std::to_string(ovf) +
+                " evaluator range / engine capacity overflow(s) (fp16 activation clamp or a competing set beyond the "
+                "engine's capacity); the results of this call are invalid");
+}
+
 static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horizon, double t_end)
 {
     const akmc_counters before = h->total;
@@ -1450,6 +1449,8 @@ static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horiz
         d.wall_ms = h->total.wall_ms - before.wall_ms;
         *ctr = d;
     }
+    rc = check_overflow(h, "akmc_step");
+    if (rc != AKMC_OK) return rc;
     if (h->multi) {
         int ovf = 0;
         CK(h, cudaMemcpy(&ovf, h->d_dist_overflow, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1548,6 +1549,69 @@ int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t*
     return AKMC_OK;
 }
 
+int akmc_progress(akmc_handle* h, int64_t* nev_out, int64_t* sweep_out)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (nev_out) {
+        static_assert(sizeof(long long) == sizeof(int64_t), "event counter width");
+        CK(h, cudaMemcpy(nev_out, h->d_nev, (size_t)h->nvox * sizeof(long long), cudaMemcpyDeviceToHost));
+    }
+    if (sweep_out) *sweep_out = h->sweep;
+    return AKMC_OK;
+}
+
+int akmc_restore(akmc_handle* h, const int64_t* vac_sites, int64_t n_vac, const double* clock_s, const int64_t* nev,
+                 int64_t sweep)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (h->multi) return fail(h, AKMC_ERR_INVALID, "akmc_restore: single-rank handles only");
+    if (sweep < 0) return fail(h, AKMC_ERR_INVALID, "akmc_restore: sweep must be >= 0");
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (vac_sites) {
+        if (n_vac != h->nvac) return fail(h, AKMC_ERR_INVALID, "akmc_restore: vacancy count differs from the lattice's");
+        std::vector<VacRec> cur;
+        const int rc = collect_vacancies(h, cur);
+        if (rc != AKMC_OK) return rc;
+        std::vector<int64_t> a((size_t)n_vac), b;
+        b.reserve(cur.size());
+        for (const VacRec& r : cur) b.push_back(r.site);
+        std::copy(vac_sites, vac_sites + n_vac, a.begin());
+        std::sort(a.begin(), a.end());
+        std::sort(b.begin(), b.end());
+        if (a != b || std::adjacent_find(a.begin(), a.end()) != a.end())
+            return fail(h, AKMC_ERR_INVALID, "akmc_restore: vac_sites is not the lattice's vacancy set");
+        std::vector<int4> v((size_t)std::max<int64_t>(n_vac, 1));
+        const int Lx = h->F.L[0], Ly = h->F.L[1];
+        for (int64_t i = 0; i < n_vac; ++i) {
+            const int64_t site = vac_sites[i];
+            const int vox = (int)(site / h->csites);
+            const int64_t r = site % h->csites;
+            const int bb = (int)(r & 1);
+            const int64_t c = r >> 1;
+            const int x = (int)(c % Lx), y = (int)((c / Lx) % Ly), z = (int)(c / ((int64_t)Lx * Ly));
+            if (i > 0 && vox < v[(size_t)i - 1].x)
+                return fail(h, AKMC_ERR_INVALID, "akmc_restore: slots must be grouped by voxel in ascending order");
+            v[(size_t)i] = make_int4(vox, 2 * x + bb, 2 * y + bb, 2 * z + bb);
+        }
+        if (n_vac) CK(h, cudaMemcpy(h->d_vac, v.data(), (size_t)n_vac * sizeof(int4), cudaMemcpyHostToDevice));
+    }
+    if (clock_s) {
+        for (int i = 0; i < h->nvox; ++i)
+            if (!std::isfinite(clock_s[i]) || clock_s[i] < 0.0) return fail(h, AKMC_ERR_INVALID, "akmc_restore: bad clock");
+        CK(h, cudaMemcpy(h->d_clock, clock_s, (size_t)h->nvox * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (nev) {
+        for (int i = 0; i < h->nvox; ++i)
+            if (nev[i] < 0) return fail(h, AKMC_ERR_INVALID, "akmc_restore: event counters must be >= 0");
+        CK(h, cudaMemcpy(h->d_nev, nev, (size_t)h->nvox * sizeof(long long), cudaMemcpyHostToDevice));
+    }
+    h->sweep = sweep;
+    CK(h, cudaMemset(h->d_term, 0, (size_t)h->nvox * sizeof(int)));
+    CK(h, cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
+    return AKMC_OK;
+}
+
 int akmc_debug_extended(akmc_handle* h, uint8_t* out)
 {
     if (!h || !out) return AKMC_ERR_INVALID;
@@ -1590,6 +1654,8 @@ int akmc_rates(akmc_handle* h, double* rates_out, double* barriers_out)
     CK(h, cudaStreamSynchronize(h->stream));
     rc = harvest_events(h);
     if (rc != AKMC_OK) return rc;
+    rc = check_overflow(h, "akmc_rates");
+    if (rc != AKMC_OK) return rc;
     std::vector<double> R((size_t)nslots * 8), E((size_t)nslots * 8);
     CK(h, cudaMemcpy(R.data(), h->d_rates, R.size() * sizeof(double), cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(E.data(), h->d_E, E.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1621,6 +1687,7 @@ int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t
         if (e == cudaSuccess) e = cudaMemcpy(E_out, d_e, (size_t)n * 8 * sizeof(double), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) rc = fail(h, AKMC_ERR_CUDA, std::string("eval_windows: ") + cudaGetErrorString(e));
         else rc = harvest_events(h);
+        if (rc == AKMC_OK) rc = check_overflow(h, "akmc_eval_windows");
     }
     cudaFree(d_w);
     cudaFree(d_e);

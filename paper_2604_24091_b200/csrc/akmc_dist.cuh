@@ -63,6 +63,37 @@ __device__ __forceinline__ void log_entry(int4* log, unsigned long long* nlog, i
     if (i < (unsigned long long)cap) log[i] = make_int4(px, py, pz, code);
 }
 
+// Local slot reuse (multi-rank): a departure pushes its slot on the free list (depart_slot, akmc_kernels.cuh);
+// an arrival pops one (FreeList.cnt[1] counts the pops of this exchange against the count nfree0 at kernel
+// start -- no departures happen during an unpack) and only appends a new slot when the list is empty, so the
+// slot range stays bounded by the most vacancies the block ever held at once, not by the migrations so far.
+// The last block of the unpack folds the pops into the count.  The per-vacancy memo of a reused slot is kept:
+// its entries are keyed by the full 64-byte window and rates are a pure function of the window (R7).
+struct FreeList {
+    int* slots;        // [vcap]
+    int* cnt;          // [0] free slots, [1] pops of the running exchange, [2] finished unpack blocks
+};
+
+__device__ __forceinline__ int arrival_slot(const FreeList& FL, int nfree0, int* nvac_local)
+{
+    const int k = atomicAdd(&FL.cnt[1], 1);
+    return k < nfree0 ? FL.slots[nfree0 - 1 - k] : atomicAdd(nvac_local, 1);
+}
+
+__device__ __forceinline__ void unpack_done(const FreeList& FL, int nfree0)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&FL.cnt[2], 1) == (int)gridDim.x - 1) {
+            const int pops = atomicExch(&FL.cnt[1], 0);
+            FL.cnt[0] = max(0, nfree0 - pops);
+            FL.cnt[2] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // pack the phase's log into per-peer send buffers (header entry 0 = count); global half-cell coords
 // A site may be written several times in one phase (a vacancy enters and leaves it), so species entries
 // carry the site's FINAL value, read here after the phase: duplicates are identical and the receiver may
@@ -101,8 +132,9 @@ static __global__ void clear_headers_kernel(int4* sendbuf, int npeer, int cap, u
 
 // apply received entries: species writes into block/halo (with wrap-axis ghosts); vacancy arrivals
 static __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, int npeer, Frame F, DistParams D, uint8_t* species,
-                                     int4* vac, int* gid, int* nvac_local, int vcap, int* overflow)
+                                     int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL, int* overflow)
 {
+    const int nfree0 = *(volatile int*)&FL.cnt[0];
     for (int r = 0; r < npeer; ++r) {
         const int4* buf = recvbuf + (size_t)r * (D.cap + 1);
         const int cnt = min(buf[0].x, D.cap);
@@ -120,7 +152,7 @@ static __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, in
             }
             if (!ok) { atomicAdd(overflow, 1); continue; }
             if (e.w >= kMigrateBase) {
-                const int slot = atomicAdd(nvac_local, 1);
+                const int slot = arrival_slot(FL, nfree0, nvac_local);
                 if (slot < vcap) {
                     vac[slot] = make_int4(0, lp[0], lp[1], lp[2]);
                     gid[slot] = e.w - kMigrateBase;
@@ -132,6 +164,7 @@ static __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, in
             }
         }
     }
+    unpack_done(FL, nfree0);
 }
 
 // ---------------------------------------------------------------- per-phase exchange over NVLink peer memory
@@ -204,8 +237,9 @@ static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned lo
 // wait for every peer's deltas of exchange `epoch`, then apply them (same semantics as unpack_deltas_kernel)
 static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const unsigned long long* mflag, unsigned long long epoch,
                                          Frame F, DistParams D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
-                                         int vcap, int* overflow)
+                                         int vcap, FreeList FL, int* overflow)
 {
+    const int nfree0 = *(volatile int*)&FL.cnt[0];
     if (threadIdx.x < D.npeer)
         while (ld_acquire_sys(&mflag[threadIdx.x]) < epoch) __nanosleep(64);
     __syncthreads();
@@ -227,7 +261,7 @@ static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const un
             }
             if (!ok) { atomicAdd(overflow, 1); continue; }
             if (e.w >= kMigrateBase) {
-                const int slot = atomicAdd(nvac_local, 1);
+                const int slot = arrival_slot(FL, nfree0, nvac_local);
                 if (slot < vcap) {
                     vac[slot] = make_int4(0, lp[0], lp[1], lp[2]);
                     gid[slot] = e.w - kMigrateBase;
@@ -239,6 +273,7 @@ static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const un
             }
         }
     }
+    unpack_done(FL, nfree0);
 }
 
 // dense slab of cells (storage <-> buffer) for the initial halo fill.  Range per axis [lo, hi) in owned

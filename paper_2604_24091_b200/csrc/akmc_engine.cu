@@ -174,6 +174,8 @@ __device__ __forceinline__ int block_excl(int v, int* wsum, int& total)
 }
 
 // fp16 hi/lo split of an FP32 value (lo carries the remainder * 2^11)
+// (the init-time activation scales keep v <= 2^15; a value beyond 60000 would be a bound violation: it is
+// clamped, counted, and the call that produced it returns AKMC_ERR_RUNTIME)
 __device__ __forceinline__ void split_h(float v, __half& hi, __half& lo, unsigned long long& ovf)
 {
     if (v > 60000.0f) { v = 60000.0f; ++ovf; }
@@ -285,7 +287,7 @@ __device__ __forceinline__ void l1_list_store(int r, uint8_t b0, uint8_t b1, uin
 }
 
 __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi,
-                                         uint8_t* g_lo, unsigned long long& ovf, bool fast)
+                                         uint8_t* g_lo, unsigned long long& ovf, bool fast, float sc)
 {
     const int lane = threadIdx.x & 31;
     __half hi[8], lo[8];
@@ -293,7 +295,7 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
     for (int c = 0; c < 8; ++c) {
         float h = (float)acc[c];
         h = h > 0.0f ? h : 0.0f;
-        split_h(h, hi[c], lo[c], ovf);
+        split_h(h * sc, hi[c], lo[c], ovf);          // sc = 2^-t1 (exact; 1 for O(1) activations)
     }
     const uint32_t off = (uint32_t)(m >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
     const uint4 vh = pack8(hi), vl = pack8(lo);
@@ -313,7 +315,7 @@ __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, co
                                             const uint16_t* l1l, const float* __restrict__ W1f,
                                             const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
                                             uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf, bool fast,
-                                            long long* lp = nullptr)
+                                            float sc, long long* lp = nullptr)
 {
     const int lane = threadIdx.x & 31;
     long long t0 = lp ? clock64() : 0;
@@ -377,7 +379,7 @@ __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, co
     plap(2);
 #pragma unroll
     for (int r = 0; r < kL1Rows; ++r)
-        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf, fast);
+        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf, fast, sc);
     __syncwarp();
     plap(3);
 }
@@ -894,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             rr[q] = c.miss[kRoundRows * k_round + (q < nv ? i + q * kWarps : i)];
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast,
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast, p.W.h1s,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) {
@@ -936,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             rr[q] = q < nv ? i + q * kWarps : i;
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast,
+                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast, p.W.h1s,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }
@@ -1053,7 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                         float z = __fmaf_rn(__uint_as_float(d2[8 * g + t]), inv, __uint_as_float(d1[8 * g + t]));
                                         z = __fmaf_rn(z, p.W.s2u, b2s[cl]);
                                         z = z > 0.0f ? z : 0.0f;
-                                        split_h(z, hi[t], lo[t], ovf);
+                                        split_h(z * p.W.h2s, hi[t], lo[t], ovf);
                                     }
                                     const uint32_t off = h2_off(m, c0 + 8 * g);
                                     *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
@@ -1288,7 +1290,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                                 if (!p.F.wrap[ax] && (np[ax] < 0 || np[ax] >= 2 * p.F.L[ax])) out = true;
                             if (out) {
                                 log_entry(p.S.log, p.S.nlog, p.S.logcap, nv.y, nv.z, nv.w, kMigrateBase + p.S.gid[slot]);
-                                p.vac[slot].x = -1;
+                                depart_slot(p.vac, p.S, slot);
                             }
                         }
                         c.seg_t[i] = __dadd_rn(c.seg_t[i], dt);

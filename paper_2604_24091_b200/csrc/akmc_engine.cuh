@@ -39,8 +39,10 @@ struct EngineWeights {
     const uint8_t* W3img;   // [4 CTAs][4 K-steps][hi 512 B | lo 512 B] of W3 rows [64r,64r+64) (N padded 16) * 2^s3
     const float* b2;        // [256]
     const double* b3;       // [8]
-    float s2u;              // 2^-s2
-    double s3u;             // 2^-s3
+    float s2u;              // 2^(t1-s2): undoes the W2 image scale 2^s2 and the h1 scale 2^-t1
+    double s3u;             // 2^(t2-s3): undoes the W3 image scale 2^s3 and the h2 scale 2^-t2
+    float h1s, h2s;         // 2^-t1, 2^-t2: power-of-two activation scales chosen at init from weight bounds so
+                            // that |h| * 2^-t <= 2^15 for every window (the fp16 hi part cannot overflow)
     const double* mlp64;    // FP64 weights (verify precision)
 };
 

@@ -261,7 +261,17 @@ struct SubParams {
     int4* log;
     unsigned long long* nlog;
     int logcap;
+    // multi-rank: local slots freed by departures (reused by arrivals, akmc_dist.cuh); fcnt[0] = free count
+    int* freelist;
+    int* fcnt;
 };
+
+// a vacancy left this rank's block: its local slot is marked departed and pushed on the free list
+__device__ __forceinline__ void depart_slot(int4* vac, const SubParams& S, int slot)
+{
+    vac[slot].x = -1;
+    if (S.freelist) S.freelist[atomicAdd(&S.fcnt[0], 1)] = slot;
+}
 
 __device__ __forceinline__ int imodk(int a, int m) { const int r = a % m; return r < 0 ? r + m : r; }
 
@@ -489,7 +499,7 @@ static __global__ void select_sub_kernel(uint8_t* species, int4* vac, Frame F, G
                             if (!F.wrap[ax] && (np[ax] < 0 || np[ax] >= 2 * F.L[ax])) out = true;
                         if (out) {
                             log_entry(S.log, S.nlog, S.logcap, nv.y, nv.z, nv.w, kMigrateBase + S.gid[slot]);
-                            vac[slot].x = -1;                   // departed: re-created by the owner rank
+                            depart_slot(vac, S, slot);          // departed: re-created by the owner rank
                         }
                     }
                     sg.t = __dadd_rn(sg.t, dt);

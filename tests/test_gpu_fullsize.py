@@ -4,6 +4,9 @@ and properties that hold at any size:
   * species counts are conserved and the vacancy registry equals the set of V sites;
   * every voxel clock advanced by exactly 2 windows (2 sweeps; A19/A25);
   * the rates of sampled vacancies (after the sweeps) equal the FP64 oracle's within 1e-5 relative.
+Plus the FP64 pair-model trajectories at the full C3 (512^3, 26,844 vacancies, 2 sweeps) and C5 (1024^3, 214,748
+vacancies, 1 sweep) sizes, bit-exact against the oracle: the engine's refill from millions of domains, the fair-
+share claims and the hot/cold segment lists run here exactly as in the bench.
 """
 import numpy as np
 import pytest
@@ -55,3 +58,27 @@ def test_c5_fullsize_sweeps(akmc, orc):
         worst = max(worst, float(rel.max()))
         assert np.array_equal(G[i] == 0.0, g_orc == 0.0)          # masks exact
     assert worst <= RTOL_FAST, worst
+
+
+@pytest.mark.parametrize("name,sweeps", [("c3", 2), ("c5", 1)])
+def test_fullsize_fp64_pair_bitexact(akmc, orc, name, sweeps):
+    import torch
+    import bench
+    eps, E0 = synth.illustrative_pair_params()
+    cfg, pr = bench.sim_config(name, akmc.PREC_FP64, akmc.MODEL_PAIR, 0.25, E0)
+    sp, keep = bench.make_inputs(name, 0, torch.device("cuda", 0))
+    sp = np.ascontiguousarray(sp)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        c = sim.step(sweeps)
+        gsp, gvac, gclock, gctr = sim.state()
+    del keep
+    ocfg = orc.Config(cells=cfg.cells, n_voxels=1, T=cfg.temperature_K, nu0=cfg.nu0, kB=cfg.kB, model=0,
+                      domain=cfg.domain_cells, window_s=cfg.window_s, seed=cfg.seed)
+    st = orc.State.from_species(ocfg, sp)
+    del sp
+    orc.run(ocfg, st, sweeps, eps, E0)
+    assert c["events"] > 10000
+    assert gctr["events"] == st.counters[0] and gctr["hop_evals"] == st.counters[1]
+    assert np.array_equal(gvac, st.vac)
+    assert np.array_equal(gclock, st.clock)
+    assert np.array_equal(gsp, st.species)

@@ -83,3 +83,22 @@ def test_eight_rank_invariance(tmp_path):
     res = json.loads(out.read_text())
     assert res["ok"], res
     assert res["events"] > 20
+
+
+def test_two_rank_slot_reuse_long_run(tmp_path):
+    """departed local slots are reused by arrivals (akmc_dist.cuh FreeList).  With the spare slot
+    capacity shrunk to 4 (AKMC_VCAP_SPARE) a long run migrates far more vacancies than the spare holds; it must
+    neither overflow nor change the trajectory (2 ranks == 1 rank == oracle)."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = tmp_path / "multi_reuse.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29653", os.path.join(ROOT, "tools", "multi_check.py"),
+           "--grid", "2", "1", "1", "--out", str(out), "--oracle", "--sweeps", "60", "--cells", "12", "12", "12",
+           "--domain", "6", "6", "6", "--nvac", "30"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, AKMC_VCAP_SPARE="4"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"], res
+    assert res["events"] > 200

@@ -144,9 +144,11 @@ struct akmc_handle {
     double* d_mlp = nullptr;
     float* d_b2 = nullptr;
     double* d_b3 = nullptr;
-    float s2u = 1.0f, h1s = 1.0f, h2s = 1.0f;
-    double s3u = 1.0;
-    int act_shift[2] = {0, 0};        // t1, t2: activation scales 2^-t (prepare_engine_weights)
+    float s2u = 1.0f, h1s = 1.0f;
+    int act_shift = 0;                // t1: h1 scale 2^-t1 (prepare_engine_weights)
+    double* d_W3d = nullptr;          // [256][8] FP64 W3 (layer 3 on CUDA cores)
+    uint8_t* d_W2full = nullptr;      // bulk evaluator: W2^T images, N = 256 per K-step
+    bool bulk = true;                 // FP32 batches through the bulk evaluator (AKMC_EVAL_ENGINE=1: cluster evaluator)
     unsigned long long* d_overflow = nullptr;
     // phase engine (akmc_engine.cuh)
     bool engine = true;               // false: legacy grid-synchronous inner loop (AKMC_LEGACY_LOOP=1)
@@ -159,7 +161,6 @@ struct akmc_handle {
                                       // A/B on C5: no change, profiles/r01_engine_timing.md)
     float* d_W1f = nullptr;           // [385][256]
     uint8_t* d_W2e = nullptr;         // [8][32 KiB]
-    uint8_t* d_W3e = nullptr;         // [8][2 KiB]
     unsigned int* d_cursor = nullptr;
     uint8_t* d_stage = nullptr;       // [clusters][8][16 KiB] L2 staging of h1 rows (multicast)
     uint8_t* d_canon = nullptr;       // canonical-order lattice for akmc_state readbacks (lazy)
@@ -236,7 +237,7 @@ void free_all(akmc_handle* h)
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp,
-                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3e, h->d_cursor,
+                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3d, h->d_W2full, h->d_cursor,
                     h->d_stage, h->d_canon, h->d_wstore, h->d_kT};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -341,11 +342,10 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
             for (int j = 0; j < kHid; ++j)
                 w1p[(size_t)(1 + (s - 1) * kWin + slot) * kHid + j] =
                     W1[(size_t)(kSpecies * slot + s) * kHid + j] - W1[(size_t)(kSpecies * slot + kFe) * kHid + j];
-    // activation bounds over ALL windows: h1_j <= max(0, b1'_j + sum_slot max(0, max_s W1'(s,slot)_j)), and
-    // h2_j <= max(0, b2_j + sum_i max(0, W2_ij) * U1_i); the activation scales 2^-t keep every U * 2^-t <= 2^15,
-    // so the fp16 hi part of an activation can never overflow (t = 0 for O(1) activations: bits unchanged)
-    std::vector<double> U1((size_t)kHid), U2((size_t)kHid);
-    double m1 = 0.0, m2 = 0.0;
+    // activation bound over ALL windows: h1_j <= max(0, b1'_j + sum_slot max(0, max_s W1'(s,slot)_j)); the scale
+    // 2^-t1 keeps every |h1| * 2^-t1 <= 2^15, so the fp16 hi part of an activation can never overflow (t1 = 0 for
+    // O(1) activations: bits unchanged).  h2 is not split any more (layer 3 runs in FP64 on CUDA cores).
+    double m1 = 0.0;
     for (int j = 0; j < kHid; ++j) {
         double u = w1p[j];
         for (int slot = 0; slot < kWin; ++slot) {
@@ -353,35 +353,23 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
             for (int s = 1; s < kSpecies; ++s) mx = std::max(mx, w1p[(size_t)(1 + (s - 1) * kWin + slot) * kHid + j]);
             u += mx;
         }
-        U1[(size_t)j] = std::max(0.0, u);
-        m1 = std::max(m1, U1[(size_t)j]);
-    }
-    for (int j = 0; j < kHid; ++j) {
-        double u = b2[j];
-        for (int i = 0; i < kHid; ++i) u += std::max(0.0, W2[(size_t)i * kHid + j]) * U1[(size_t)i];
-        U2[(size_t)j] = std::max(0.0, u);
-        m2 = std::max(m2, U2[(size_t)j]);
+        m1 = std::max(m1, std::max(0.0, u));
     }
     // AKMC_NO_ACT_SCALE: fault injection for the overflow guard's test (no activation scaling)
     const bool no_scale = std::getenv("AKMC_NO_ACT_SCALE") != nullptr;
     const int t1 = (m1 > 32768.0 && !no_scale) ? (int)std::ceil(std::log2(m1 / 32768.0)) : 0;
-    const int t2 = (m2 > 32768.0 && !no_scale) ? (int)std::ceil(std::log2(m2 / 32768.0)) : 0;
     const int s2 = scale_exp(W2, (size_t)kHid * kHid);
-    const int s3 = scale_exp(W3, (size_t)kHid * 8);
-    h->act_shift[0] = t1;
-    h->act_shift[1] = t2;
+    h->act_shift = t1;
     h->s2u = (float)std::ldexp(1.0, t1 - s2);
-    h->s3u = std::ldexp(1.0, t2 - s3);
     h->h1s = (float)std::ldexp(1.0, -t1);
-    h->h2s = (float)std::ldexp(1.0, -t2);
     std::vector<float> b2f(kHid);
     for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
-    // per cluster CTA r: fp16 hi/lo UMMA images of W2^T columns [64r, 64r+64) and W3 rows [64r, 64r+64)
+    // per cluster CTA r: fp16 hi/lo UMMA images of W2^T columns [64r, 64r+64); W3 stays FP64
     {
         std::vector<float> w1f((size_t)kW1Rows * kHid);
         for (size_t i = 0; i < w1f.size(); ++i) w1f[i] = (float)w1p[i];
-        const size_t w2b = (size_t)(kHid / 16) * 2 * kSliceN * 16 * 2, w3b = (size_t)(kSliceN / 16) * 2 * 16 * 16 * 2;
-        std::vector<uint8_t> w2e((size_t)kClusterN * w2b, 0), w3e((size_t)kClusterN * w3b, 0);
+        const size_t w2b = (size_t)(kHid / 16) * 2 * kSliceN * 16 * 2;
+        std::vector<uint8_t> w2e((size_t)kClusterN * w2b, 0);
         auto put_split = [&](uint8_t* stepbase, int N, int n, int kk, double w) {   // one K-step (16), hi then lo
             const __half hi = __float2half_rn((float)w);
             const __half lo = __float2half_rn((float)((w - (double)__half2float(hi)) * kLoScale));
@@ -390,22 +378,25 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
             reinterpret_cast<__half*>(stepbase + off)[0] = hi;
             reinterpret_cast<__half*>(stepbase + split + off)[0] = lo;
         };
-        for (int r = 0; r < kClusterN; ++r) {
+        for (int r = 0; r < kClusterN; ++r)
             for (int k = 0; k < kHid; ++k)
                 for (int c = 0; c < kSliceN; ++c)
                     put_split(w2e.data() + r * w2b + (size_t)(k / 16) * 2 * kSliceN * 16 * 2, kSliceN, c, k % 16,
                               std::ldexp(W2[(size_t)k * kHid + kSliceN * r + c], s2));
-            for (int kk = 0; kk < kSliceN; ++kk)
-                for (int n = 0; n < 8; ++n)
-                    put_split(w3e.data() + r * w3b + (size_t)(kk / 16) * 2 * 16 * 16 * 2, 16, n, kk % 16,
-                              std::ldexp(W3[(size_t)(kSliceN * r + kk) * 8 + n], s3));
-        }
+        // bulk evaluator: the whole W2^T per K-step (N = 256), [16][hi 8 KiB | lo 8 KiB]
+        const size_t w2s = (size_t)kHid * 16 * 2 * 2;
+        std::vector<uint8_t> w2f((size_t)(kHid / 16) * w2s, 0);
+        for (int k = 0; k < kHid; ++k)
+            for (int n = 0; n < kHid; ++n)
+                put_split(w2f.data() + (size_t)(k / 16) * w2s, kHid, n, k % 16, std::ldexp(W2[(size_t)k * kHid + n], s2));
+        CK(h, cudaMalloc(&h->d_W2full, w2f.size()));
+        CK(h, cudaMemcpy(h->d_W2full, w2f.data(), w2f.size(), cudaMemcpyHostToDevice));
         CK(h, cudaMalloc(&h->d_W1f, w1f.size() * sizeof(float)));
         CK(h, cudaMalloc(&h->d_W2e, w2e.size()));
-        CK(h, cudaMalloc(&h->d_W3e, w3e.size()));
+        CK(h, cudaMalloc(&h->d_W3d, (size_t)kHid * 8 * sizeof(double)));
         CK(h, cudaMemcpy(h->d_W1f, w1f.data(), w1f.size() * sizeof(float), cudaMemcpyHostToDevice));
         CK(h, cudaMemcpy(h->d_W2e, w2e.data(), w2e.size(), cudaMemcpyHostToDevice));
-        CK(h, cudaMemcpy(h->d_W3e, w3e.data(), w3e.size(), cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(h->d_W3d, W3, (size_t)kHid * 8 * sizeof(double), cudaMemcpyHostToDevice));
     }
     CK(h, cudaMalloc(&h->d_b2, kHid * 4));
     CK(h, cudaMalloc(&h->d_b3, 8 * 8));
@@ -427,8 +418,8 @@ EngineParams engine_params(akmc_handle* h, int mode)
     p.S.seed = h->cfg.seed;                        // (serial handles leave the sublattice block unset)
     p.segs = h->d_segs; p.members = h->d_members; p.mpos = h->d_mpos; p.ctr = h->d_ctr; p.memo = h->d_memo;
     p.scratch = h->d_scratch; p.iscratch = h->d_iscratch; p.cursor = h->d_cursor;
-    p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3img = h->d_W3e; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
-    p.W.s2u = h->s2u; p.W.s3u = h->s3u; p.W.h1s = h->h1s; p.W.h2s = h->h2s; p.W.mlp64 = h->d_mlp;
+    p.W.W1f = h->d_W1f; p.W.W2img = h->d_W2e; p.W.W3d = h->d_W3d; p.W.b2 = h->d_b2; p.W.b3 = h->d_b3;
+    p.W.s2u = h->s2u; p.W.h1s = h->h1s; p.W.mlp64 = h->d_mlp;
     p.overflow = h->d_overflow;
     p.stage = h->d_stage;
     p.wstore = h->d_wstore;
@@ -467,9 +458,19 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         eval_mlp_fp64_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->d_vac, windows, h->F, h->G, h->P,
                                                            h->d_mlp, rows, nrows_dev, nrows_host, rates, R, E);
         CK(h, cudaGetLastError());
+    } else if (h->bulk) {
+        // FP32-equivalent / FP16-fast batches: the bulk evaluator (akmc_bulk.cu), row for row the phase engine's
+        // arithmetic (akmc_eval.cuh) -- every path that produces a rate produces the same bits (R7)
+        BulkParams p{};
+        p.species = h->d_species; p.vac = h->d_vac; p.F = h->F; p.G = h->G; p.P = h->P;
+        p.windows = windows; p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
+        p.W = engine_params(h, kEngineEval).W;
+        p.W2full = h->d_W2full;
+        p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
+        p.fast = prec == AKMC_PREC_FP16_FAST ? 1 : 0;
+        CK(h, launch_bulk(p, max_rows, h->num_sms, h->stream));
     } else {
-        // FP32-equivalent / FP16-fast: the engine's cluster evaluator in eval mode (the same arithmetic, row for
-        // row, as inside the phase engine -- every path that produces a rate produces the same bits, R7)
+        // the engine's cluster evaluator in eval mode (AKMC_EVAL_ENGINE=1; same arithmetic as the bulk evaluator)
         EngineParams p = engine_params(h, kEngineEval);
         p.windows = windows; p.rows = rows; p.nrows_dev = nrows_dev; p.nrows_host = nrows_host;
         p.rates = rates; p.Rsum = R; p.E = E;
@@ -939,6 +940,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
     CKI(engine_setup());
+    CKI(bulk_setup());
+    h->bulk = std::getenv("AKMC_EVAL_ENGINE") == nullptr;
     if (h->tc) {
         h->n_clusters = engine_max_clusters();
         if (h->n_clusters <= 0) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_CUDA, "no co-resident 8-CTA cluster for the evaluator"); }

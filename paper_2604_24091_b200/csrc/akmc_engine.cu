@@ -23,23 +23,15 @@
 // FP64 kernels), no cluster.
 #include "akmc_engine.cuh"
 #include "akmc_ptx.cuh"
+#include "akmc_eval.cuh"
 
 // Compile-time variants (A/B builds via build.build(out=..., defines=...) and AKMC_LIB; tools/ab_probe.py).
 // Defaults are the measured best on B200 (C5, same box, profiles/r01_engine_timing.md):
-#ifndef AKMC_L1_ROWS
-#define AKMC_L1_ROWS 2          // layer-1 rows per warp in flight (4: register spills, slower)
-#endif
-#ifndef AKMC_L1_BATCH
-#define AKMC_L1_BATCH 2         // W1' rows per layer-1 row in flight
-#endif
 #ifndef AKMC_REFILL_FAST
 #define AKMC_REFILL_FAST 1      // skip slot placement when nothing is pending (-2 %)
 #endif
 #ifndef AKMC_GATHER_ROWS
 #define AKMC_GATHER_ROWS 8      // gather rows per warp in flight
-#endif
-#ifndef AKMC_W1_EVICT_LAST
-#define AKMC_W1_EVICT_LAST 0    // L2 evict_last policy on W1' loads (no effect measured)
 #endif
 #ifndef AKMC_PREFETCH
 #define AKMC_PREFETCH 0         // L2 prefetch of the next window/memo at hop/placement (+1.6 %, slower)
@@ -68,15 +60,10 @@ using namespace ptx;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileRows = kRoundRows * kClusterN;              // 128
-constexpr uint32_t kRowGroupA = (kHid / 8) * 128;              // 4096 B: one 8-row group of h1 (M-major layout)
 constexpr uint32_t kSplitA = kTileRows * kHid * 2;             // 64 KiB: one fp16 split of h1
-constexpr uint32_t kCoreColH2 = (kTileRows / 8) * 128;         // 2048 B: K-adjacent core matrices of H2
-constexpr uint32_t kSplitH2 = kTileRows * kSliceN * 2;         // 8 KiB: one fp16 split of the h2 slice
 constexpr uint32_t kW2Split = kSliceN * 16 * 2;                // 1 KiB: one split of a W2-slice K-step
 constexpr uint32_t kW2Bytes = (kHid / 16) * 2 * kW2Split;      // 32 KiB
-constexpr uint32_t kW3Split = 16 * 16 * 2;                     // 512 B
-constexpr uint32_t kW3Bytes = (kSliceN / 16) * 2 * kW3Split;   // 2 KiB
-constexpr float kLo = 2048.0f;
+constexpr uint32_t kW3Bytes = kSliceN * 8 * 8;                // 4 KiB: FP64 W3 rows of this CTA's h2 slice
 
 struct ReqHdr { int n, more, alive, pad; };
 
@@ -126,7 +113,6 @@ constexpr uint32_t kOffRowR = kOffWin + kRowCap * 8;                 // [kRowCap
 constexpr uint32_t kOffRowC = kOffA + 16384;                         // [kRowCap] int, FP64 mode only (A is scratch there)
 constexpr uint32_t kOffB2 = kOffRowR + kRowCap * 8;                  // float [kSliceN]
 constexpr uint32_t kOffB3 = kOffB2 + kSliceN * 4;                    // double [8]
-constexpr int kL1List = 6;                                           // W1' row indices kept per row (RPV: ~1.6)
 constexpr uint32_t kOffL1N = kOffB3 + 8 * 8;                         // [kRowCap] uint8 non-Fe slot count
 constexpr uint32_t kOffL1L = kOffL1N + kRowCap;                      // [kRowCap][kL1List] uint16 W1' row index
 constexpr uint32_t kOffCtl = (kOffL1L + kRowCap * kL1List * 2 + 15u) & ~15u;
@@ -136,18 +122,12 @@ constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemUsed = kOffTmem + 16;
 constexpr uint32_t kSmemTotal = kSmemUsed + 128;                     // 128-B alignment slack (no-swizzle layouts)
 static_assert(kSmemTotal <= 232448, "shared memory budget");
-static_assert(kSplitH2 == (kRoundRows / 8) * kRowGroupA && kTileRows * 8 * 8 <= kSplitH2,
-              "h2 (one split per half) and the partials fit in the CTA's own row block of A");
+static_assert(kTileRows * 8 * 8 <= (kRoundRows / 8) * kRowGroupA,
+              "layer-3 partials (and the pair scratch) fit in the CTA's own row block of A (hi / lo)");
 static_assert(kOffHdr % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
 static_assert(kRowCap <= 256, "row scan covers one element per thread");
 static_assert(kSlots <= kThreads && 2 * kSlots <= kThreads, "slot and candidate threads fit the CTA");
 
-__device__ __forceinline__ uint32_t lanemask_lt()
-{
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
 
 // exclusive block prefix of v over threads [0, 256); total gets the sum (all threads)
 __device__ __forceinline__ int block_excl(int v, int* wsum, int& total)
@@ -173,22 +153,7 @@ __device__ __forceinline__ int block_excl(int v, int* wsum, int& total)
     return base + incl - v;
 }
 
-// fp16 hi/lo split of an FP32 value (lo carries the remainder * 2^11)
-// (the init-time activation scales keep v <= 2^15; a value beyond 60000 would be a bound violation: it is
-// clamped, counted, and the call that produced it returns AKMC_ERR_RUNTIME)
-__device__ __forceinline__ void split_h(float v, __half& hi, __half& lo, unsigned long long& ovf)
-{
-    if (v > 60000.0f) { v = 60000.0f; ++ovf; }
-    hi = __float2half_rn(v);
-    lo = __float2half_rn((v - __half2float(hi)) * kLo);
-}
 
-__device__ __forceinline__ uint4 pack8(const __half (&x)[8])
-{
-    return make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]), pack_half2(x[6], x[7]));
-}
-
-constexpr uint32_t kTmemDa = 2 * kSliceN;                          // layer-3 accumulators after D1, D2
 
 // does TMEM lane quadrant q (tile rows [32q, 32q+32)) hold any valid row of this round?
 __device__ __forceinline__ bool quad_has_rows(const int (&n_s)[kClusterN], int q)
@@ -200,24 +165,6 @@ __device__ __forceinline__ bool quad_has_rows(const int (&n_s)[kClusterN], int q
     return any;
 }
 
-// H2 (K = kSliceN): no-swizzle K-major, column-major core matrices (LBO 2048, SBO 128)
-__device__ __forceinline__ uint32_t h2_off(int m, int k)
-{
-    return (uint32_t)(k >> 3) * kCoreColH2 + (uint32_t)(m >> 3) * 128u + (uint32_t)(m & 7) * 16u + (uint32_t)(k & 7) * 2u;
-}
-
-// window byte of an owned vacancy (plain coherent load -- the lattice is written by this kernel), with the
-// offset packed into a register (bytes dx, dy, dz): a lane-dependent index into the kernel
-// parameters would be a divergent constant-cache load (serialised over the 32 addresses)
-__device__ __forceinline__ uint32_t pack_off(const int8_t* o)
-{
-    return (uint32_t)(uint8_t)o[0] | ((uint32_t)(uint8_t)o[1] << 8) | ((uint32_t)(uint8_t)o[2] << 16);
-}
-__device__ __forceinline__ uint8_t site_byte_pk(const uint8_t* species, const Frame& F, const int4& v, uint32_t pk)
-{
-    return species[neighbour_site(F, v, (int)(int8_t)(pk & 0xFFu), (int)(int8_t)((pk >> 8) & 0xFFu),
-                                  (int)(int8_t)((pk >> 16) & 0xFFu))];
-}
 
 // layer 1 of up to two rows, all 256 columns (lane = columns 8*lane .. 8*lane+7): FP64 sum of b1' and the
 // W1' rows of the window's non-Fe slots in slot order, one rounding to FP32, ReLU, fp16 hi/lo split into
@@ -243,145 +190,6 @@ __device__ __forceinline__ void prefetch_vacancy(const uint8_t* species, const F
                 prefetch_l2(vb + ((int64_t)((uint32_t)bx + (uint32_t)F.NB[0] * ((uint32_t)by + (uint32_t)F.NB[1] * (uint32_t)bz)) << 7));
     const uint8_t* m = reinterpret_cast<const uint8_t*>(memo2);
     prefetch_l2(m); prefetch_l2(m + 128); prefetch_l2(m + 256);
-}
-
-// non-Fe slots of a window as two ballot masks (slots 0-31, 32-63); entry e of the slot-ordered list is the
-// e-th set bit (no list is stored: the masks are warp-uniform registers)
-struct L1Masks { unsigned m0, m1; int c0, n; };
-constexpr int kL1Batch = AKMC_L1_BATCH;                  // W1' rows per row in flight (an RPV window has ~1.6 non-Fe slots)
-__device__ __forceinline__ L1Masks l1_masks(const uint8_t* w)
-{
-    const int lane = threadIdx.x & 31;
-    L1Masks r;
-    r.m0 = __ballot_sync(0xffffffffu, w[lane] != (uint8_t)kFe);
-    r.m1 = __ballot_sync(0xffffffffu, w[lane + 32] != (uint8_t)kFe);
-    r.c0 = __popc(r.m0);
-    r.n = r.c0 + __popc(r.m1);
-    return r;
-}
-__device__ __forceinline__ int l1_row_index(const uint8_t* w, const L1Masks& k, int e)
-{
-    const int slot = e < k.c0 ? (int)__fns(k.m0, 0, e + 1) : 32 + (int)__fns(k.m1, 0, e - k.c0 + 1);
-    return 1 + ((int)w[slot] - 1) * kWin + slot;
-}
-
-// the gather's by-product for layer 1: the row's non-Fe slots as W1' row indices, in slot order, from the
-// window bytes held by the lanes (lane = slots lane, lane + 32); rows with more than kL1List fall back to the
-// window in the global scratch
-__device__ __forceinline__ void l1_list_store(int r, uint8_t b0, uint8_t b1, uint8_t* l1n, uint16_t* l1l)
-{
-    const int lane = threadIdx.x & 31;
-    const unsigned m0 = __ballot_sync(0xffffffffu, b0 != (uint8_t)kFe);
-    const unsigned m1 = __ballot_sync(0xffffffffu, b1 != (uint8_t)kFe);
-    const unsigned lt = lanemask_lt();
-    const int c0 = __popc(m0);
-    if (lane == 0) l1n[r] = (uint8_t)(c0 + __popc(m1));
-    if (b0 != (uint8_t)kFe) {
-        const int e = __popc(m0 & lt);
-        if (e < kL1List) l1l[r * kL1List + e] = (uint16_t)(1 + ((int)b0 - 1) * kWin + lane);
-    }
-    if (b1 != (uint8_t)kFe) {
-        const int e = c0 + __popc(m1 & lt);
-        if (e < kL1List) l1l[r * kL1List + e] = (uint16_t)(1 + ((int)b1 - 1) * kWin + lane + 32);
-    }
-}
-
-__device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t* A_hi, uint8_t* A_lo, uint8_t* g_hi,
-                                         uint8_t* g_lo, unsigned long long& ovf, bool fast, float sc)
-{
-    const int lane = threadIdx.x & 31;
-    __half hi[8], lo[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        float h = (float)acc[c];
-        h = h > 0.0f ? h : 0.0f;
-        split_h(h * sc, hi[c], lo[c], ovf);          // sc = 2^-t1 (exact; 1 for O(1) activations)
-    }
-    const uint32_t off = (uint32_t)(m >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
-    const uint4 vh = pack8(hi), vl = pack8(lo);
-    *reinterpret_cast<uint4*>(A_hi + off) = vh;
-    if (!fast) *reinterpret_cast<uint4*>(A_lo + off) = vl;
-    // the same 16 B into the L2 staging block of this CTA (row m % kRoundRows of its block)
-    const uint32_t goff = (uint32_t)((m % kRoundRows) >> 3) * kRowGroupA + (uint32_t)lane * 128u + (uint32_t)(m & 7) * 16u;
-#if !AKMC_XCHG_DSMEM
-    *reinterpret_cast<uint4*>(g_hi + goff) = vh;
-    if (!fast) *reinterpret_cast<uint4*>(g_lo + goff) = vl;
-#endif
-}
-
-// layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once
-constexpr int kL1Rows = AKMC_L1_ROWS;
-__device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
-                                            const uint16_t* l1l, const float* __restrict__ W1f,
-                                            const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
-                                            uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf, bool fast,
-                                            float sc, long long* lp = nullptr)
-{
-    const int lane = threadIdx.x & 31;
-    long long t0 = lp ? clock64() : 0;
-    auto plap = [&](int i) { if (lp) { const long long t = clock64(); lp[i] += t - t0; t0 = t; } };
-    int n[kL1Rows];
-    L1Masks k[kL1Rows];
-    int nmax = 0;
-#pragma unroll
-    for (int r = 0; r < kL1Rows; ++r) {
-        n[r] = r < nv ? (int)l1n[rr[r]] : 0;
-        nmax = n[r] > nmax ? n[r] : nmax;
-        k[r].m0 = 0u; k[r].m1 = 0u; k[r].c0 = 0; k[r].n = n[r];
-        if (n[r] > kL1List) k[r] = l1_masks(win + rr[r] * kWin);    // rare crowded window (warp-uniform)
-    }
-    plap(0);
-    const float4* base = reinterpret_cast<const float4*>(W1f) + 2 * lane;
-#if AKMC_W1_EVICT_LAST
-    const uint64_t pol = policy_evict_last();
-#endif
-    double a[kL1Rows][8];
-    {
-        const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
-#pragma unroll
-        for (int r = 0; r < kL1Rows; ++r) {
-            a[r][0] = x0.x; a[r][1] = x0.y; a[r][2] = x0.z; a[r][3] = x0.w;
-            a[r][4] = x1.x; a[r][5] = x1.y; a[r][6] = x1.z; a[r][7] = x1.w;
-        }
-    }
-    plap(1);
-    for (int e = 0; e < nmax; e += kL1Batch) {
-        float4 xa[kL1Rows][kL1Batch], xb[kL1Rows][kL1Batch];
-#pragma unroll
-        for (int t = 0; t < kL1Batch; ++t) {
-#pragma unroll
-            for (int r = 0; r < kL1Rows; ++r) {
-                if (e + t < n[r]) {
-                    const int ix = n[r] <= kL1List ? (int)l1l[rr[r] * kL1List + e + t]
-                                                   : l1_row_index(win + rr[r] * kWin, k[r], e + t);
-                    const float4* rp = base + (size_t)ix * (kHid / 4);
-#if AKMC_W1_EVICT_LAST
-                    xa[r][t] = ldg_f4_hint(rp, pol); xb[r][t] = ldg_f4_hint(rp + 1, pol);
-#else
-                    xa[r][t] = __ldg(rp); xb[r][t] = __ldg(rp + 1);
-#endif
-                }
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < kL1Batch; ++t) {
-#pragma unroll
-            for (int r = 0; r < kL1Rows; ++r) {
-                if (e + t < n[r]) {
-                    a[r][0] = __dadd_rn(a[r][0], (double)xa[r][t].x); a[r][1] = __dadd_rn(a[r][1], (double)xa[r][t].y);
-                    a[r][2] = __dadd_rn(a[r][2], (double)xa[r][t].z); a[r][3] = __dadd_rn(a[r][3], (double)xa[r][t].w);
-                    a[r][4] = __dadd_rn(a[r][4], (double)xb[r][t].x); a[r][5] = __dadd_rn(a[r][5], (double)xb[r][t].y);
-                    a[r][6] = __dadd_rn(a[r][6], (double)xb[r][t].z); a[r][7] = __dadd_rn(a[r][7], (double)xb[r][t].w);
-                }
-            }
-        }
-    }
-    plap(2);
-#pragma unroll
-    for (int r = 0; r < kL1Rows; ++r)
-        if (r < nv) l1_store(a[r], m[r], A_hi, A_lo, g_hi, g_lo, ovf, fast, sc);
-    __syncwarp();
-    plap(3);
 }
 
 template <bool kTC, bool kFast = false>
@@ -414,9 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     // h2 slice and the layer-3 partials live in this CTA's own row block of A: dead once layer 2 has
     // completed, and no peer ever writes it (peers' multicasts target their own blocks)
     const uint32_t own_block = (uint32_t)(kRoundRows / 8) * rank * kRowGroupA;
-    uint8_t* H2_hi = sm + kOffA + own_block;
-    uint8_t* H2_lo = sm + kOffA + kSplitA + own_block;
-    double* part_out = reinterpret_cast<double*>(H2_hi);            // [128][8]  (after layer 3)
+    double* part_out = reinterpret_cast<double*>(sm + kOffA + own_block);             // [128][8] S_rank per row
+    double* pair_tmp = reinterpret_cast<double*>(sm + kOffA + kSplitA + own_block);    // [128][8] hc = 1 pairs
     const uint32_t bar_req = smem_u32(&bars[0]), bar_part = smem_u32(&bars[1]);
     const uint32_t bar_mma = smem_u32(&bars[2]), bar_w = smem_u32(&bars[3]);
     const bool phase_mode = (p.mode == kEnginePhase);
@@ -454,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (tid == 0) {
             mbar_expect_tx(bar_w, kW2Bytes + kW3Bytes);
             bulk_g2s(smem_u32(sm + kOffW2), p.W.W2img + (size_t)rank * kW2Bytes, kW2Bytes, bar_w);
-            bulk_g2s(smem_u32(sm + kOffW3), p.W.W3img + (size_t)rank * kW3Bytes, kW3Bytes, bar_w);
+            bulk_g2s(smem_u32(sm + kOffW3), p.W.W3d + (size_t)rank * kSliceN * 8, kW3Bytes, bar_w);
         }
         mbar_wait(bar_w, 0);
     } else {
@@ -1029,13 +836,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     mbar_wait(bar_mma, ph_mma);
                     ph_mma ^= 1u;
                     tc_fence_after();
-                    // ---- E2: h2 slice -> H2 (fp16 split, K = 64); warp = (TMEM lane quadrant, 32-column half)
+                    // ---- E2 + layer 3 (FP64, CUDA cores): warp = (TMEM lane quadrant q4 = source block, 32-column
+                    //      half hc); a thread holds one row and 2 chunks of 16 h2 columns: P_q, their pair sum
                     {
                         const int q4 = warp & 3, hc = warp >> 2;
-                        if (quad_has_rows(n_s, q4)) {
+                        const int m = 32 * q4 + lane;
+                        const bool rows_here = quad_has_rows(n_s, q4);
+                        double pr[8];
+                        if (rows_here) {
                             const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-                            const int m = 32 * q4 + lane;
-                            const float inv = 1.0f / kLo;
+                            const double* w3s = reinterpret_cast<const double*>(sm + kOffW3);
 #pragma unroll
                             for (int hh = 0; hh < 2; ++hh) {
                                 const int c0 = 32 * hc + 16 * hh;
@@ -1046,72 +856,32 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
 #pragma unroll
                                     for (int t = 0; t < 16; ++t) d2[t] = 0u;
                                 tmem_wait_ld();
+                                float z[16];
+                                e2_chunk(d1, d2, b2s + c0, p.W.s2u, z);
+                                double P[8];
+                                l3_chunk(z, w3s + c0 * 8, P);
 #pragma unroll
-                                for (int g = 0; g < 2; ++g) {
-                                    __half hi[8], lo[8];
-#pragma unroll
-                                    for (int t = 0; t < 8; ++t) {
-                                        const int cl = c0 + 8 * g + t;
-                                        float z = __fmaf_rn(__uint_as_float(d2[8 * g + t]), inv, __uint_as_float(d1[8 * g + t]));
-                                        z = __fmaf_rn(z, p.W.s2u, b2s[cl]);
-                                        z = z > 0.0f ? z : 0.0f;
-                                        split_h(z * p.W.h2s, hi[t], lo[t], ovf);
-                                    }
-                                    const uint32_t off = h2_off(m, c0 + 8 * g);
-                                    *reinterpret_cast<uint4*>(H2_hi + off) = pack8(hi);
-                                    if (!fast) *reinterpret_cast<uint4*>(H2_lo + off) = pack8(lo);
-                                }
+                                for (int k = 0; k < 8; ++k) pr[k] = hh ? __dadd_rn(pr[k], P[k]) : P[k];
+                            }
+                            if (hc == 1) {
+                                double2* dst = reinterpret_cast<double2*>(pair_tmp + m * 8);
+                                dst[0] = make_double2(pr[0], pr[1]); dst[1] = make_double2(pr[2], pr[3]);
+                                dst[2] = make_double2(pr[4], pr[5]); dst[3] = make_double2(pr[6], pr[7]);
                             }
                         }
-                    }
-                    fence_async_smem();
-                    tc_fence_before();
-                    __syncthreads();
-                    tc_fence_after();
-                    if (tid == 0) lap(d_x[5]);
-                    // ---- L3 on tcgen05: partial outputs of this CTA's 64 h2 columns, Da / Db in TMEM
-                    if (tid == 0) {
-                        const uint32_t idesc = idesc_f16(kTileRows, 16);
-                        const uint32_t hh = smem_u32(H2_hi), hl = smem_u32(H2_lo), w3 = smem_u32(sm + kOffW3);
-                        for (int ks = 0; ks < kSliceN / 16; ++ks) {
-                            const uint64_t dah = umma_desc(hh + (uint32_t)ks * 2u * kCoreColH2, kCoreColH2, 128);
-                            const uint64_t dal = umma_desc(hl + (uint32_t)ks * 2u * kCoreColH2, kCoreColH2, 128);
-                            const uint64_t dbh = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split, (16 / 8) * 128, 128);
-                            const uint64_t dbl = umma_desc(w3 + (uint32_t)ks * 2u * kW3Split + kW3Split, (16 / 8) * 128, 128);
-                            umma_f16(tmem + kTmemDa, dah, dbh, idesc, ks > 0 ? 1u : 0u);
-                            if (!fast) {
-                                umma_f16(tmem + kTmemDa + 16, dah, dbl, idesc, ks > 0 ? 1u : 0u);
-                                umma_f16(tmem + kTmemDa + 16, dal, dbh, idesc, 1u);
-                            }
-                        }
-                        umma_commit(bar_mma);
-                    }
-                    mbar_wait(bar_mma, ph_mma);
-                    ph_mma ^= 1u;
-                    tc_fence_after();
-                    if (warp < 4) {
-                        const int q4 = warp;
-                        if (quad_has_rows(n_s, q4)) {
-                            uint32_t da[8], db[8];
-                            const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-                            tmem_ld8(tl + (uint32_t)kTmemDa, da);
-                            if (!fast) tmem_ld8(tl + (uint32_t)(kTmemDa + 16), db);
-                            else
-#pragma unroll
-                                for (int t = 0; t < 8; ++t) db[t] = 0u;
-                            tmem_wait_ld();
-                            const int m = 32 * q4 + lane;
-                            double pv[8];
-#pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                pv[k] = __dadd_rn((double)__uint_as_float(da[k]), (double)__uint_as_float(db[k]) * (1.0 / 2048.0));
+                        tc_fence_before();
+                        __syncthreads();
+                        if (rows_here && hc == 0) {
+                            const double2* o = reinterpret_cast<const double2*>(pair_tmp + m * 8);
                             double2* dst = reinterpret_cast<double2*>(part_out + m * 8);
-                            dst[0] = make_double2(pv[0], pv[1]);
-                            dst[1] = make_double2(pv[2], pv[3]);
-                            dst[2] = make_double2(pv[4], pv[5]);
-                            dst[3] = make_double2(pv[6], pv[7]);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const double2 b = o[j];
+                                dst[j] = make_double2(__dadd_rn(pr[2 * j], b.x), __dadd_rn(pr[2 * j + 1], b.y));
+                            }
                         }
                     }
+                    if (tid == 0) lap(d_x[5]);
                     // ---- partials of row block s -> CTA s (every CTA arrives on every CTA's barrier)
                     fence_async_smem();
                     tc_fence_before();
@@ -1141,7 +911,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             double acc = 0.0;
 #pragma unroll
                             for (int s = 0; s < kClusterN; ++s) acc = __dadd_rn(acc, part_in[(s * kRoundRows + i) * 8 + k]);
-                            const double out = __dadd_rn(b3s[k], __dmul_rn(acc, p.W.s3u));
+                            const double out = __dadd_rn(b3s[k], acc);
                             Ek = out > 0.0 ? out : 0.0;
                             int vox = -1;
                             if (phase_mode) vox = c.mem_vac[c.row_mem[r]].x;

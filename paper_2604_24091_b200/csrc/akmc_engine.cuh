@@ -36,13 +36,12 @@ static_assert(sizeof(MemoEntry) == kMemoBytes && offsetof(MemoEntry, R) == kMemo
 struct EngineWeights {
     const float* W1f;       // [385][256] FP32: row 0 = b1' = b1 + sum_slot W1[slot,Fe]; row 1+(s-1)*64+slot = W1'
     const uint8_t* W2img;   // [4 CTAs][16 K-steps][hi 2 KiB | lo 2 KiB] fp16 UMMA images of W2^T column slices * 2^s2
-    const uint8_t* W3img;   // [4 CTAs][4 K-steps][hi 512 B | lo 512 B] of W3 rows [64r,64r+64) (N padded 16) * 2^s3
+    const double* W3d;      // [256][8] FP64 W3 (CTA r of a cluster loads rows [64r, 64r+64)); layer 3 runs in FP64
     const float* b2;        // [256]
     const double* b3;       // [8]
     float s2u;              // 2^(t1-s2): undoes the W2 image scale 2^s2 and the h1 scale 2^-t1
-    double s3u;             // 2^(t2-s3): undoes the W3 image scale 2^s3 and the h2 scale 2^-t2
-    float h1s, h2s;         // 2^-t1, 2^-t2: power-of-two activation scales chosen at init from weight bounds so
-                            // that |h| * 2^-t <= 2^15 for every window (the fp16 hi part cannot overflow)
+    float h1s;              // 2^-t1: power-of-two activation scale chosen at init from weight bounds so that
+                            // |h1| * 2^-t1 <= 2^15 for every window (the fp16 hi part cannot overflow)
     const double* mlp64;    // FP64 weights (verify precision)
 };
 
@@ -92,6 +91,28 @@ struct EngineParams {
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
     int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)
 };
+
+// bulk evaluator (akmc_bulk.cu): the same per-row arithmetic on many rows, one persistent CTA per SM
+struct BulkParams {
+    const uint8_t* species;
+    const int4* vac;
+    Frame F;
+    GeomTables G;
+    PhysParams P;
+    const uint8_t* windows; // [n][64] or nullptr (then rows -> vac slots, gathered)
+    const int* rows;        // slot list or nullptr (row i = slot i)
+    const int* nrows_dev;   // device row count or nullptr
+    int nrows_host;
+    EngineWeights W;
+    const uint8_t* W2full;  // [16 K-steps][hi 8 KiB | lo 8 KiB] fp16 UMMA images of W2^T (N = 256) * 2^s2
+    double* rates;          // [.][8] or nullptr
+    double* Rsum;
+    double* E;
+    unsigned long long* overflow;
+    int fast;
+};
+cudaError_t bulk_setup();
+cudaError_t launch_bulk(const BulkParams& p, int max_rows, int num_sms, cudaStream_t s);
 
 size_t engine_smem_bytes();
 cudaError_t engine_setup();

@@ -214,3 +214,43 @@ def test_restore_rejects_bad_checkpoints(akmc):
                 sim.restore(*args)
             assert ei.value.code == akmc.AKMC_ERR_INVALID
         sim.restore(vac, clock, nev, sweep)                  # the real checkpoint is accepted
+
+
+# ----------------------------------------------------------------------------- bulk evaluator (akmc_bulk.cu)
+@pytest.mark.parametrize("weights,prec", [("physics", "fp32"), ("random", "fp32"), ("physics", "fast")])
+def test_bulk_evaluator_bitexact_vs_cluster_evaluator(akmc, monkeypatch, weights, prec):
+    """The warp-specialised bulk evaluator and the phase engine's cluster evaluator (AKMC_EVAL_ENGINE=1) give
+    the same bits for every window (ragged last tile: 3000 = 23 x 128 + 56 rows), FP32-equivalent and FP16-fast:
+    one arithmetic for every path that forms a rate (R7)."""
+    eps, E0 = synth.illustrative_pair_params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=4) if weights == "physics" else synth.random_mlp(seed=9)
+    P = akmc.PREC_FP32 if prec == "fp32" else akmc.PREC_FP16_FAST
+    wins = synth.random_windows(3000, seed=21)
+    cfg = akmc.Config(cells=(8, 8, 8), barrier_model=akmc.MODEL_MLP, precision=P)
+    with akmc.Simulation(cfg, np.zeros(1024, np.uint8), mlp=mlp) as sim:
+        e_bulk = sim.eval_windows(wins, P)
+    monkeypatch.setenv("AKMC_EVAL_ENGINE", "1")
+    with akmc.Simulation(cfg, np.zeros(1024, np.uint8), mlp=mlp) as sim:
+        e_eng = sim.eval_windows(wins, P)
+    assert np.array_equal(e_bulk.view(np.uint64), e_eng.view(np.uint64))
+
+
+def test_bulk_rates_lattice_bitexact_and_within_bar(akmc, orc, monkeypatch):
+    """akmc_rates on a 64^3 RPV voxel with 300 vacancies: bulk == cluster evaluator bit for bit, and within the
+    1e-5 bar of the FP64 oracle with exact masks."""
+    eps, E0 = synth.illustrative_pair_params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=2)
+    L = 64
+    sp = synth.make_lattice((L, L, L), 1, synth.a508_atomic_fractions(), 300, seed=31)
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32)
+    with akmc.Simulation(cfg, sp, mlp=mlp) as sim:
+        G1, E1 = sim.rates()
+        _, vac, _, _ = sim.state(species=False)
+    monkeypatch.setenv("AKMC_EVAL_ENGINE", "1")
+    with akmc.Simulation(cfg, sp, mlp=mlp) as sim:
+        G2, E2 = sim.rates()
+    assert np.array_equal(G1.view(np.uint64), G2.view(np.uint64)) and np.array_equal(E1.view(np.uint64), E2.view(np.uint64))
+    ocfg = orc.Config(cells=cfg.cells, model=1)
+    Go, _ = orc.rates(ocfg, sp, vac, mlp=mlp)
+    assert np.array_equal(G1 == 0.0, Go == 0.0)
+    assert float(_rel(G1, Go).max()) <= RTOL_FAST

@@ -139,6 +139,35 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
  * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
 int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
 
+/* World-model time mode (sec. V.A.1 Eqs. 1-2, sec. V.A.3 Eq. 7;
+ * S:356-409).  Serial / voxel-batch handles with barrier_model AKMC_MODEL_MLP at AKMC_PREC_FP64 whose akmc_init
+ * got eps and E0.  After this call every akmc_step(n) event of a voxel: (1) reads the network's raw outputs
+ * as policy logits z_{i,k}; Eq. 1 masks infeasible hops (weight 0) and divides by tau_act; Eq. 2's softmax over
+ * the voxel's concatenated logits selects (i, k) (weights det_exp(min(z/tau, 700)), canonical tree + descent,
+ * the serial Philox counter); (2) applies the hop; (3) advances the voxel clock by max(dtau_hat, 1e-3 /
+ * Gamma_tot(s)) with Eq. 7 dtau_hat = (uhat(s) - Gamma_tot(s)/Gamma_tot(s') uhat(s')) / Gamma_tot(s), Gamma_tot
+ * = total pair-KRA rate and uhat = softplus of the Poisson-time network on the mean one-hot window
+ * of the voxel's vacancies.  tnet: host FP64 Wt1[448*hidden] (row f = 7*slot + species), bt1[hidden],
+ * wt2[hidden], bt2[1], copied.  A voxel with no feasible event (or Gamma_tot = 0) is terminal.  FP64
+ * throughout: trajectories and clocks are bit-equal to the oracle's orc_run_world.  AKMC_ERR_INVALID (state
+ * unchanged) for a sublattice handle, another model/precision, missing eps/E0, hidden outside [1, 256],
+ * tau_act <= 0, non-finite weights, or more than 64 vacancies in a voxel.  akmc_run_until is not available
+ * in this mode.                                                                                          */
+int akmc_set_world_model(akmc_handle* h, const double* tnet, int32_t hidden, double tau_act);
+
+/* Exact MFPT solver (sec. V.A.3 Eq. 5): tau on the transient states
+ * of an enumerated state space from  sum_a Gamma_a(s) [tau(Phi(s,a)) - tau(s)] + 1 = 0,  tau = 0 on the
+ * absorbing set (no handle; runs on the current CUDA device).  Transitions of transient state i are
+ * row_ptr[i] .. row_ptr[i+1]-1 (host, row_ptr[0] = 0): target col[e] (a transient index, or -1 = into the
+ * absorbing set) with rate rate[e] >= 0 s^-1; every transient state needs a positive total rate.  tau_out [n]
+ * (host, seconds).  Jacobi-preconditioned BiCGSTAB until ||1 - A tau|| <= tol ||1|| or max_iter iterations;
+ * iters_out / resid_out (may be NULL) report the iterations and the final relative residual of Eq. 5.  The
+ * exact u = Gamma_tot tau it yields is the reference of the world model's Eq. 7 (plug-in identity).
+ * AKMC_ERR_INVALID for n <= 0, bad CSR, negative / non-finite rates, a state with no outgoing rate, tol <= 0
+ * or max_iter < 1; AKMC_ERR_CUDA on a device error.                                                         */
+int akmc_mfpt_solve(const int64_t* row_ptr, const int32_t* col, const double* rate, int64_t n, double tol,
+                    int32_t max_iter, double* tau_out, int32_t* iters_out, double* resid_out);
+
 /* Checkpoint / resume (lattice + vacancy list + clock + counters is a full checkpoint; the
  * counter-based RNG needs no state).  akmc_progress reads the rest of the run position: nev_out [n_voxels]
  * (may be NULL) = each voxel's serial event index (the Philox counter of its next event, S:195-198 / A16),

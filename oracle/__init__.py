@@ -72,6 +72,16 @@ def lib():
                                            C.c_void_p, C.c_void_p, C.c_int64]
         _lib.orc_sector_perm.argtypes = [C.c_uint64, C.c_int64, P(C.c_int)]
         _declare_selection(_lib)
+        _lib.orc_softplus.argtypes = [C.c_double]; _lib.orc_softplus.restype = C.c_double
+        _lib.orc_delta_tau_hat.argtypes = [C.c_double] * 4; _lib.orc_delta_tau_hat.restype = C.c_double
+        _lib.orc_poisson_net.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_poisson_net.restype = C.c_double
+        _lib.orc_run_world.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                       C.c_int64, C.c_void_p]
+        _lib.orc_world_eval.argtypes = [P(_Cfg), C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
     return _lib
 
 
@@ -291,3 +301,44 @@ def cluster_stats(cfg: Config, species, vox: int = 0, cu: int = 1, nstar: int = 
     d = {k: float(v) for k, v in zip(keys, out)}
     d["hist"] = hist
     return d
+
+
+# ----------------------------------------------------------------------------- world-model time mode (f2)
+def softplus(y: float) -> float:
+    return lib().orc_softplus(float(y))
+
+
+def delta_tau_hat(u_s: float, g_s: float, u_sp: float, g_sp: float) -> float:
+    """Eq. 7 (P:352-358): (u(s) - Gamma_tot(s)/Gamma_tot(s') u(s')) / Gamma_tot(s)."""
+    return lib().orc_delta_tau_hat(float(u_s), float(g_s), float(u_sp), float(g_sp))
+
+
+def poisson_net(sigmas, tnet, H: int) -> float:
+    s = np.ascontiguousarray(sigmas, dtype=np.uint8).reshape(-1, 64)
+    t = np.ascontiguousarray(tnet, dtype=np.float64)
+    return lib().orc_poisson_net(_ptr(s), int(s.shape[0]), _ptr(t), int(H))
+
+
+def run_world(cfg: Config, st: State, n: int, eps, E0, mlp, tnet, H: int, tau_act: float = 1.0) -> int:
+    """Serial world-model steps (policy-logit selection, Eq. 7 clock), n events per voxel."""
+    e = np.ascontiguousarray(eps, dtype=np.float64)
+    e0 = np.ascontiguousarray(E0, dtype=np.float64)
+    m = np.ascontiguousarray(mlp, dtype=np.float64)
+    t = np.ascontiguousarray(tnet, dtype=np.float64)
+    return lib().orc_run_world(C.byref(cfg.c()), _ptr(st.species), _ptr(st.vac), int(st.vac.size), _ptr(st.clock),
+                               _ptr(st.nev), _ptr(e), _ptr(e0), _ptr(m), _ptr(t), int(H), float(tau_act), int(n),
+                               _ptr(st.counters))
+
+
+def world_eval(cfg: Config, species, vac, vox: int, eps, E0, mlp, tnet, H: int, tau_act: float = 1.0):
+    """(policy weights W[m][8], physical rates G[m][8], wtot, gtot, uhat) of voxel `vox`."""
+    sp = np.ascontiguousarray(species, dtype=np.uint8)
+    v = np.ascontiguousarray(vac, dtype=np.int64)
+    W = np.zeros((v.size + 1, 8)); G = np.zeros((v.size + 1, 8)); o = np.zeros(3)
+    m = lib().orc_world_eval(C.byref(cfg.c()), _ptr(sp), _ptr(v), int(v.size), int(vox),
+                             _ptr(np.ascontiguousarray(eps, dtype=np.float64)),
+                             _ptr(np.ascontiguousarray(E0, dtype=np.float64)),
+                             _ptr(np.ascontiguousarray(mlp, dtype=np.float64)),
+                             _ptr(np.ascontiguousarray(tnet, dtype=np.float64)), int(H), float(tau_act),
+                             _ptr(W), _ptr(G), _ptr(o))
+    return W[:m], G[:m], o[0], o[1], o[2]

@@ -350,7 +350,18 @@ int orc_window(const orc_cfg* c, const uint8_t* sp, int64_t vsite, uint8_t* sigm
 
 /* FP64 MLP 448-256-256-8 (A8): dense loop over all 448 one-hot features
  * in ascending feature order f = 7*slot + species, acc = fma(x_f, W[f][j], acc). */
+static void mlp_forward(const uint8_t sigma[NWIN], const double* mlp, double out[8]);
+
 void orc_mlp_fp64(const uint8_t sigma[NWIN], const double* mlp, double E[8])
+{
+    double out[8];
+    mlp_forward(sigma, mlp, out);
+    for (int k = 0; k < 8; ++k) E[k] = out[k] > 0.0 ? out[k] : 0.0;    /* barrier reading: clamp at 0 (A8) */
+}
+
+/* raw network outputs (no clamp): the barrier reading clamps them, the world-model reading uses them as the
+ * policy logits z_{i,k} of Eq. 1 */
+static void mlp_forward(const uint8_t sigma[NWIN], const double* mlp, double out[8])
 {
     const double* W1 = mlp;
     const double* b1 = W1 + 448 * NHID;
@@ -375,7 +386,7 @@ void orc_mlp_fp64(const uint8_t sigma[NWIN], const double* mlp, double E[8])
     for (int k = 0; k < 8; ++k) {
         double acc = b3[k];
         for (int i = 0; i < NHID; ++i) acc = fma(h2[i], W3[(size_t)i * 8 + k], acc);
-        E[k] = acc > 0.0 ? acc : 0.0;
+        out[k] = acc;
     }
 }
 
@@ -810,6 +821,178 @@ int orc_rates(const orc_cfg* c, const uint8_t* sp, const int64_t* vac, int64_t n
         }
     }
     return clamps;
+}
+
+/* ------------------------------------------------------------------ */
+/* world-model time mode (sec. V.A.1, sec. V.A.3)               */
+/*   selection: the network outputs are the policy logits z_{i,k}; Eq. 1 masks infeasible hops and       */
+/*     divides by tau_act; Eq. 2's global softmax over the competing set (the voxel, A15) picks (i, k)    */
+/*     with probability exp(zhat)/sum exp(zhat) -- realised as the BKL tree/descent over the weights      */
+/*     w = det_exp(min(zhat, 700)) (softmax is shift invariant, so no max subtraction is needed, W1)     */
+/*   time: Eq. 7, dtau_hat = (u(s) - Gamma_tot(s)/Gamma_tot(s') u(s')) / Gamma_tot(s) with Gamma_tot   */
+/*     from the physical (pair KRA) rates and u = uhat from the Poisson-time network on pooled windows   */
+/*     (mean of the per-vacancy one-hot encodings, softplus head); the clock   */
+/*     advances by max(dtau_hat, 1e-3 / Gamma_tot(s)) (S:409 floor, W4)                                 */
+/* Readings W1-W6 are listed in DESIGN.md sec. 3.                                                       */
+/* ------------------------------------------------------------------ */
+
+/* softplus(y) = ln(1 + e^y), the Poisson network's non-negative head */
+double orc_softplus(double y)
+{
+    if (y > 0.0) return y + orc_det_log(1.0 + orc_det_exp(-y));
+    return orc_det_log(1.0 + orc_det_exp(y));
+}
+
+/* Eq. 7: the learned event-time increment; g_sp == 0 (s' has no event) -> u(s') term dropped */
+double orc_delta_tau_hat(double u_s, double g_s, double u_sp, double g_sp)
+{
+    if (!(g_sp > 0.0)) return u_s / g_s;
+    return (u_s - (g_s / g_sp) * u_sp) / g_s;
+}
+
+/* Poisson-time network on the pooled windows of n vacancies: x_f = count_f / n over the one-hot features
+ * f = 7*slot + species; h_j = ReLU(bt1_j + sum_f x_f Wt1[f][j]) (dense fma loop in f order); y = bt2 +
+ * sum_j h_j wt2_j; uhat = softplus(y).  tnet = Wt1[448*H], bt1[H], wt2[H], bt2[1]. */
+double orc_poisson_net(const uint8_t* sigmas /* [n][64] */, int n, const double* tnet, int H)
+{
+    if (n <= 0) return 0.0;
+    const double* Wt1 = tnet;
+    const double* bt1 = Wt1 + 448 * (size_t)H;
+    const double* wt2 = bt1 + H;
+    const double* bt2 = wt2 + H;
+    int cnt[448];
+    memset(cnt, 0, sizeof(cnt));
+    for (int i = 0; i < n; ++i)
+        for (int s = 0; s < NWIN; ++s) cnt[7 * s + sigmas[(size_t)i * NWIN + s]] += 1;
+    double y = bt2[0];
+    for (int j = 0; j < H; ++j) {
+        double acc = bt1[j];
+        for (int f = 0; f < 448; ++f) {
+            double x = (double)cnt[f] / (double)n;
+            acc = fma(x, Wt1[(size_t)f * H + j], acc);
+        }
+        double h = acc > 0.0 ? acc : 0.0;
+        y = fma(h, wt2[j], y);
+    }
+    return orc_softplus(y);
+}
+
+typedef struct { const double* tnet; int H; double tau; } world_par;
+
+/* policy weights W[m][8], physical rates G[m][8] (pair KRA, the voxel's T) of the m members of a voxel, their
+ * trees' totals, and uhat of the voxel's pooled windows */
+static void world_eval(const orc_cfg* c, const geom* g, const uint8_t* sp, const int64_t* vac, const int* members,
+                       int m, const double* Dp, const double* E0, const double* mlp, const world_par* wp,
+                       double* W, double* G, double* Rw, double* Rg, double* buf, uint8_t* sig,
+                       double* wtot, double* gtot, double* uhat, int* P_out)
+{
+    orc_cfg cp = *c;
+    cp.model = 0;                                  /* physical rates: pair KRA */
+    for (int a = 0; a < m; ++a) {
+        int64_t vsite = vac[members[a]];
+        double E[8], z[8];
+        vac_rates(&cp, g, sp, vsite, Dp, E0, NULL, E, &G[8 * a]);
+        window_of(g, sp, vsite, &sig[(size_t)a * NWIN]);
+        mlp_forward(&sig[(size_t)a * NWIN], mlp, z);
+        double sw = 0.0, sg = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            double w = 0.0;
+            if (sig[(size_t)a * NWIN + k] != VAC) {                     /* Eq. 1 mask m_{i,k} */
+                double zh = z[k] / wp->tau;
+                if (zh > 700.0) zh = 700.0;
+                w = orc_det_exp(zh);
+            }
+            W[8 * a + k] = w;
+            sw = sw + w;
+            sg = sg + G[8 * a + k];
+        }
+        Rw[a] = sw;
+        Rg[a] = sg;
+    }
+    int P = 1, lev = 0;
+    *gtot = (m > 0) ? tree_build(Rg, m, buf, &P, &lev) : 0.0;
+    *wtot = (m > 0) ? tree_build(Rw, m, buf, &P, &lev) : 0.0;     /* buf keeps the policy tree */
+    *P_out = P;
+    *uhat = orc_poisson_net(sig, m, wp->tnet, wp->H);
+}
+
+/* serial world-model steps: n events per voxel (or until no feasible event); same Philox counters as BKL */
+int orc_run_world(const orc_cfg* c, uint8_t* sp, int64_t* vac, int64_t nvac, double* clock, int64_t* nev,
+                  const double* eps, const double* E0, const double* mlp, const double* tnet, int H, double tau_act,
+                  int64_t n, int64_t* ctr_out)
+{
+    build_window();
+    if (g_win_ready != 1 || c->domain[0] != 0 || !eps || !E0 || !mlp || !tnet || H < 1 || !(tau_act > 0.0))
+        return ORC_INVALID;
+    double Dp[2 * NSPEC * NSPEC];
+    build_dp(eps, Dp);
+    geom g = mk_geom(c);
+    world_par wp = {tnet, H, tau_act};
+    int* members = (int*)malloc(sizeof(int) * (size_t)(nvac + 1));
+    double* W = (double*)malloc(sizeof(double) * 8 * (size_t)(nvac + 1));
+    double* G = (double*)malloc(sizeof(double) * 8 * (size_t)(nvac + 1));
+    double* Rw = (double*)malloc(sizeof(double) * (size_t)(nvac + 1));
+    double* Rg = (double*)malloc(sizeof(double) * (size_t)(nvac + 1));
+    double* buf = (double*)malloc(sizeof(double) * 4 * (size_t)(nvac + 2));
+    uint8_t* sig = (uint8_t*)malloc((size_t)NWIN * (size_t)(nvac + 1));
+    int rc = ORC_OK;
+    orc_ctr ctr = {0, 0, 0, 0};
+    for (int64_t v = 0; v < c->n_voxels; ++v) {
+        int m = 0;
+        for (int64_t i = 0; i < nvac; ++i)
+            if (vac[i] / g.sites_per_voxel == v) members[m++] = (int)i;
+        double wtot, gtot, uhat;
+        int P;
+        world_eval(c, &g, sp, vac, members, m, Dp, E0, mlp, &wp, W, G, Rw, Rg, buf, sig, &wtot, &gtot, &uhat, &P);
+        for (int64_t e = 0; e < n; ++e) {
+            ctr.hop_evals += 8LL * m;
+            if (!(wtot > 0.0) || !(gtot > 0.0)) { ctr.terminal_voxels += 1; rc = ORC_TERMINAL; break; }
+            double u_sel, u_t;
+            draw_uniforms(c->seed, (uint32_t)nev[v], (uint32_t)((uint64_t)nev[v] >> 32), (uint32_t)v, 0u, &u_sel, &u_t);
+            double r = u_sel * wtot;
+            int a = tree_descend(buf, Rw, m, P, &r);
+            int k = pick_hop(&W[8 * a], r);
+            apply_hop(&g, sp, vac, members[a], k);
+            const double u_s = uhat, g_s = gtot;
+            world_eval(c, &g, sp, vac, members, m, Dp, E0, mlp, &wp, W, G, Rw, Rg, buf, sig, &wtot, &gtot, &uhat, &P);
+            double dt = orc_delta_tau_hat(u_s, g_s, uhat, gtot);
+            double fl = 1e-3 / g_s;
+            clock[v] = clock[v] + (dt > fl ? dt : fl);
+            nev[v] += 1;
+            ctr.events += 1;
+        }
+    }
+    free(members); free(W); free(G); free(Rw); free(Rg); free(buf); free(sig);
+    if (ctr_out) {
+        ctr_out[0] += ctr.events; ctr_out[1] += ctr.hop_evals;
+        ctr_out[2] += ctr.terminal_voxels; ctr_out[3] += ctr.clamps;
+    }
+    return rc;
+}
+
+/* the world-model quantities of one voxel's current state (pins): policy weights W[m][8], physical rates
+ * G[m][8] (slot order of the voxel's members), their totals and uhat */
+int orc_world_eval(const orc_cfg* c, const uint8_t* sp, const int64_t* vac, int64_t nvac, int64_t vox,
+                   const double* eps, const double* E0, const double* mlp, const double* tnet, int H, double tau_act,
+                   double* W, double* G, double* out3 /* wtot, gtot, uhat */)
+{
+    build_window();
+    double Dp[2 * NSPEC * NSPEC];
+    build_dp(eps, Dp);
+    geom g = mk_geom(c);
+    world_par wp = {tnet, H, tau_act};
+    int* members = (int*)malloc(sizeof(int) * (size_t)(nvac + 1));
+    int m = 0;
+    for (int64_t i = 0; i < nvac; ++i)
+        if (vac[i] / g.sites_per_voxel == vox) members[m++] = (int)i;
+    double* Rw = (double*)malloc(sizeof(double) * (size_t)(m + 1));
+    double* Rg = (double*)malloc(sizeof(double) * (size_t)(m + 1));
+    double* buf = (double*)malloc(sizeof(double) * 4 * (size_t)(m + 2));
+    uint8_t* sig = (uint8_t*)malloc((size_t)NWIN * (size_t)(m + 1));
+    int P;
+    world_eval(c, &g, sp, vac, members, m, Dp, E0, mlp, &wp, W, G, Rw, Rg, buf, sig, &out3[0], &out3[1], &out3[2], &P);
+    free(members); free(Rw); free(Rg); free(buf); free(sig);
+    return m;
 }
 
 /* ------------------------------------------------------------------ */

@@ -71,6 +71,9 @@ def load() -> C.CDLL:
     lib.akmc_set_profiling.argtypes = [P, C.c_int32]
     lib.akmc_set_voxel_temperatures.argtypes = [P, P, C.c_int32]
     lib.akmc_progress.argtypes = [P, P, P]
+    lib.akmc_set_world_model.argtypes = [P, P, C.c_int32, C.c_double]
+    lib.akmc_mfpt_solve.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_int32, P, C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_double)]
     lib.akmc_restore.argtypes = [P, P, C.c_int64, P, P, C.c_int64]
     lib.akmc_free.argtypes = [P]
     lib.akmc_free.restype = None
@@ -79,7 +82,8 @@ def load() -> C.CDLL:
     lib.akmc_version.restype = C.c_char_p
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
-              "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math", "akmc_progress", "akmc_restore"):
+              "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math", "akmc_progress", "akmc_restore",
+              "akmc_set_world_model", "akmc_mfpt_solve"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -214,6 +218,12 @@ class Simulation:
         self._check(self.lib.akmc_vacancies(self.h, _ptr(gid), _ptr(site), C.byref(n)))
         return gid[: n.value], site[: n.value]
 
+    def set_world_model(self, tnet, hidden: int, tau_act: float = 1.0):
+        """World-model time mode (akmc_set_world_model): policy-logit selection (Eqs. 1-2), Eq. 7 clock."""
+        t = np.ascontiguousarray(tnet, dtype=np.float64)
+        self._tnet = t
+        self._check(self.lib.akmc_set_world_model(self.h, _ptr(t), int(hidden), float(tau_act)))
+
     def progress(self):
         """(per-voxel serial event counters, sublattice sweeps done): with state(), a full checkpoint."""
         nev = np.empty(self.cfg.n_voxels, dtype=np.int64)
@@ -275,6 +285,23 @@ class Simulation:
 
     def __exit__(self, *a):
         self.close()
+
+
+def mfpt_solve(row_ptr, col, rate, tol: float = 1e-13, max_iter: int = 100000):
+    """Exact MFPT (Eq. 5) on the device: (tau [n], iterations, relative residual) -- akmc_mfpt_solve."""
+    lib = load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    c = np.ascontiguousarray(col, dtype=np.int32)
+    r = np.ascontiguousarray(rate, dtype=np.float64)
+    n = rp.size - 1
+    tau = np.empty(max(n, 1))
+    it = C.c_int32(0)
+    res = C.c_double(0.0)
+    rc = lib.akmc_mfpt_solve(_ptr(rp), _ptr(c), _ptr(r), int(n), float(tol), int(max_iter), _ptr(tau), C.byref(it),
+                             C.byref(res))
+    if rc != AKMC_OK:
+        raise AkmcError(rc, "akmc_mfpt_solve failed")
+    return tau[:n], int(it.value), float(res.value)
 
 
 def nccl_unique_id() -> bytes:

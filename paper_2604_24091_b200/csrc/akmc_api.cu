@@ -15,6 +15,7 @@
 #include "../../include/akmc.h"
 #include "akmc_kernels.cuh"
 #include "akmc_engine.cuh"
+#include "akmc_world.cuh"
 #include <nccl.h>
 
 using namespace akmc;
@@ -149,6 +150,12 @@ struct akmc_handle {
     double* d_W3d = nullptr;          // [256][8] FP64 W3 (layer 3 on CUDA cores)
     uint8_t* d_W2full = nullptr;      // bulk evaluator: W2^T images, N = 256 per K-step
     bool bulk = true;                 // FP32 batches through the bulk evaluator (AKMC_EVAL_ENGINE=1: cluster evaluator)
+    bool have_pair = false;           // eps / E0 given at init (pair tables valid)
+    // world-model time mode (akmc_set_world_model; akmc_world.cu)
+    bool world = false;
+    double* d_tnet = nullptr;
+    int world_H = 0;
+    double world_tau = 1.0;
     unsigned long long* d_overflow = nullptr;
     // phase engine (akmc_engine.cuh)
     bool engine = true;               // false: legacy grid-synchronous inner loop (AKMC_LEGACY_LOOP=1)
@@ -237,7 +244,7 @@ void free_all(akmc_handle* h)
     void* ptrs[] = {h->d_species, h->d_vac, h->d_rates, h->d_R, h->d_E, h->d_scratch, h->d_iscratch, h->d_vstart,
                     h->d_clock, h->d_nev, h->d_term, h->d_dmin, h->d_head, h->d_next, h->d_members, h->d_mpos, h->d_rows,
                     h->d_segs, h->d_mactive, h->d_ctr, h->d_mlp,
-                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3d, h->d_W2full, h->d_cursor,
+                    h->d_b2, h->d_b3, h->d_overflow, h->d_memo, h->d_W1f, h->d_W2e, h->d_W3d, h->d_W2full, h->d_tnet, h->d_cursor,
                     h->d_stage, h->d_canon, h->d_wstore, h->d_kT};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -780,6 +787,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
                 }
     }
     for (int a = 0; a < kSpecies; ++a) h->P.E0[a] = E0 ? E0[a] : 0.0;
+    h->have_pair = eps != nullptr && E0 != nullptr;
     h->P.kT = cfg->kB * cfg->temperature_K;
     h->P.inv_kT = 1.0 / h->P.kT;
     h->P.nu0 = cfg->nu0;
@@ -941,6 +949,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
     CKI(engine_setup());
     CKI(bulk_setup());
+    CKI(world_setup());
     h->bulk = std::getenv("AKMC_EVAL_ENGINE") == nullptr;
     if (h->tc) {
         h->n_clusters = engine_max_clusters();
@@ -1047,6 +1056,22 @@ int akmc_set_profiling(akmc_handle* h, int32_t profile)
 
 static int step_serial(akmc_handle* h, int64_t n, bool horizon = false, double t_end = 0.0)
 {
+    if (h->world) {
+        // world-model time mode: policy-logit selection (Eqs. 1-2) and the Eq. 7 clock, one CTA per voxel
+        for (int64_t done = 0; done < n;) {
+            const int chunk = (int)std::min<int64_t>(n - done, 1 << 30);
+            WorldParams w{};
+            w.species = h->d_species; w.vac = h->d_vac; w.F = h->F; w.G = h->G; w.P = h->P;
+            w.mlp = h->d_mlp; w.tnet = h->d_tnet; w.H = h->world_H; w.tau_act = h->world_tau;
+            w.nvox = h->nvox; w.vstart = h->d_vstart; w.n_events = chunk;
+            w.nev = h->d_nev; w.term = h->d_term; w.clock = h->d_clock; w.seed = h->cfg.seed; w.ctr = h->d_ctr;
+            CK(h, launch_world(w, h->num_sms, h->stream));
+            h->total.kernel_launches += 1;
+            h->total.mlp_launches += 1;
+            done += chunk;
+        }
+        return AKMC_OK;
+    }
     if (h->serial_engine) {
         // all n events of every voxel in one persistent launch (a10; per-voxel Philox counters keep the
         // trajectory identical to event-by-event stepping)
@@ -1474,6 +1499,7 @@ int akmc_run_until(akmc_handle* h, double t_end_s, int64_t max_events, akmc_coun
 {
     if (!h) return AKMC_ERR_RUNTIME;
     if (h->sub) return fail(h, AKMC_ERR_INVALID, "akmc_run_until: serial (voxel) mode only");
+    if (h->world) return fail(h, AKMC_ERR_INVALID, "akmc_run_until: not available in world-model mode");
     if (!h->serial_engine) return fail(h, AKMC_ERR_INVALID, "akmc_run_until: needs the engine path (AKMC_LEGACY_LOOP unset, "
                                                             "a voxel's vacancies fit one engine CTA)");
     if (!std::isfinite(t_end_s) || max_events < 0 || max_events > (1LL << 30))
@@ -1549,6 +1575,33 @@ int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t*
         if (site_out) site_out[i] = vr[i].site;
     }
     *n_inout = (int64_t)vr.size();
+    return AKMC_OK;
+}
+
+int akmc_set_world_model(akmc_handle* h, const double* tnet, int32_t hidden, double tau_act)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (h->sub) return fail(h, AKMC_ERR_INVALID, "world-model mode: serial / voxel-batch mode only (domain_cells = 0)");
+    if (h->cfg.barrier_model != AKMC_MODEL_MLP || h->cfg.precision != AKMC_PREC_FP64)
+        return fail(h, AKMC_ERR_INVALID, "world-model mode: needs the MLP (policy logits) at FP64 precision");
+    if (!h->have_pair) return fail(h, AKMC_ERR_INVALID, "world-model mode: eps and E0 must be given at init (physical rates of Eq. 7)");
+    if (!tnet || hidden < 1 || hidden > kWorldMaxHidden) return fail(h, AKMC_ERR_INVALID, "world-model mode: bad Poisson-net shape");
+    if (!(tau_act > 0.0) || !std::isfinite(tau_act)) return fail(h, AKMC_ERR_INVALID, "world-model mode: tau_act must be > 0 (Eq. 1)");
+    const size_t n = (size_t)448 * hidden + 2 * (size_t)hidden + 1;
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(tnet[i])) return fail(h, AKMC_ERR_INVALID, "world-model mode: non-finite Poisson-net weight");
+    std::vector<int> vs((size_t)h->nvox + 1);
+    CK(h, cudaMemcpy(vs.data(), h->d_vstart, vs.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int v = 0; v < h->nvox; ++v)
+        if (vs[(size_t)v + 1] - vs[(size_t)v] > kWorldMaxVac)
+            return fail(h, AKMC_ERR_INVALID, "world-model mode: more than 64 vacancies in a voxel");
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->d_tnet) { cudaFree(h->d_tnet); h->d_tnet = nullptr; }
+    CK(h, cudaMalloc(&h->d_tnet, n * sizeof(double)));
+    CK(h, cudaMemcpy(h->d_tnet, tnet, n * sizeof(double), cudaMemcpyHostToDevice));
+    h->world_H = hidden;
+    h->world_tau = tau_act;
+    h->world = true;
     return AKMC_OK;
 }
 

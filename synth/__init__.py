@@ -285,6 +285,23 @@ def random_mlp(seed: int, s1: float = 0.05, s2: float = 1.0 / 16.0, s3: float = 
     return pack_mlp(W1, b1, W2, b2, W3, b3)
 
 
+def policy_mlp(mlp: np.ndarray, kT: float) -> np.ndarray:
+    """World-model policy weights from a barrier network (reading W2): the last layer scaled
+    by -1/kT, so the raw outputs are the logits z_k = -E_k/kT and Eq. 2's softmax selects hops with the BKL
+    probabilities Gamma_a / Gamma_tot (nu0 cancels in the softmax)."""
+    W1, b1, W2, b2, W3, b3 = (a.copy() for a in split_mlp(np.asarray(mlp, dtype=np.float64)))
+    return pack_mlp(W1, b1, W2, b2, W3 * (-1.0 / kT), b3 * (-1.0 / kT))
+
+
+def poisson_net(seed: int, H: int = 32, s1: float = 0.3, s2: float = 0.5, bias: float = 0.5) -> np.ndarray:
+    """Synthetic Poisson-time network (no trained weights exist, P:557-563 OUT): Wt1[448*H], bt1[H], wt2[H],
+    bt2[1] with uhat = softplus(...) = O(1) (SPEC S:337-340 shape, reading W3)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    Wt1 = rng.normal(0.0, s1, size=(448, H)); bt1 = rng.normal(0.1, 0.1, size=H)
+    wt2 = rng.normal(0.0, s2, size=H); bt2 = np.array([bias])
+    return np.concatenate([Wt1.ravel(), bt1, wt2, bt2])
+
+
 # ---------------------------------------------------------------------------
 # windows and presets
 # ---------------------------------------------------------------------------

@@ -139,6 +139,19 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
  * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
 int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
 
+/* Multi-rank exchange statistics (C5): out3[0] = per-phase exchanges done, out3[1] = messages this
+ * rank sent (direct exchange: one per distinct peer and phase; AKMC_EXCHANGE=shift: the paper's shift
+ * communication, P:420-427, 2 per decomposed axis -- 1 when two ranks share the axis), out3[2] = bytes sent.  */
+int akmc_exchange_stats(akmc_handle* h, int64_t* out3);
+
+/* Dynamic voxel scheduling (sec. V.C.2, Eq. 10), serial / voxel-batch handles: voxels are
+ * dispatched to the persistent engine's slots in descending workload proxy W_v = M_v exp(-E_v / (kB T_v)),
+ * M_v = 8 x the voxel's vacancies, E_v = the composition-weighted mean base barrier E0 of its atoms (0 without
+ * pair parameters), T_v its temperature (akmc_set_voxel_temperatures recomputes the order); ties keep voxel
+ * order.  The order changes no trajectory, only the makespan of batches larger than the resident slots.
+ * order_out [n_voxels] receives the voxel ids in dispatch order.  AKMC_ERR_INVALID in sublattice mode.     */
+int akmc_voxel_order(akmc_handle* h, int32_t* order_out);
+
 /* World-model time mode (sec. V.A.1 Eqs. 1-2, sec. V.A.3 Eq. 7;
  * S:356-409).  Serial / voxel-batch handles with barrier_model AKMC_MODEL_MLP at AKMC_PREC_FP64 whose akmc_init
  * got eps and E0.  After this call every akmc_step(n) event of a voxel: (1) reads the network's raw outputs

@@ -72,6 +72,8 @@ def load() -> C.CDLL:
     lib.akmc_set_voxel_temperatures.argtypes = [P, P, C.c_int32]
     lib.akmc_progress.argtypes = [P, P, P]
     lib.akmc_set_world_model.argtypes = [P, P, C.c_int32, C.c_double]
+    lib.akmc_voxel_order.argtypes = [P, P]
+    lib.akmc_exchange_stats.argtypes = [P, P]
     lib.akmc_mfpt_solve.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_int32, P, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double)]
     lib.akmc_restore.argtypes = [P, P, C.c_int64, P, P, C.c_int64]
@@ -83,7 +85,8 @@ def load() -> C.CDLL:
     for n in ("akmc_init", "akmc_step", "akmc_state", "akmc_rates", "akmc_eval_windows", "akmc_set_stream",
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
               "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math", "akmc_progress", "akmc_restore",
-              "akmc_set_world_model", "akmc_mfpt_solve"):
+              "akmc_set_world_model", "akmc_mfpt_solve", "akmc_voxel_order",
+              "akmc_exchange_stats"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -223,6 +226,18 @@ class Simulation:
         t = np.ascontiguousarray(tnet, dtype=np.float64)
         self._tnet = t
         self._check(self.lib.akmc_set_world_model(self.h, _ptr(t), int(hidden), float(tau_act)))
+
+    def exchange_stats(self) -> dict:
+        """Multi-rank: per-phase exchanges, messages and bytes this rank sent."""
+        o = np.zeros(3, dtype=np.int64)
+        self._check(self.lib.akmc_exchange_stats(self.h, _ptr(o)))
+        return {"exchanges": int(o[0]), "messages": int(o[1]), "bytes": int(o[2])}
+
+    def voxel_order(self) -> np.ndarray:
+        """Voxel ids in the engine's dispatch order (descending Eq. 10 workload proxy)."""
+        o = np.empty(self.cfg.n_voxels, dtype=np.int32)
+        self._check(self.lib.akmc_voxel_order(self.h, _ptr(o)))
+        return o
 
     def progress(self):
         """(per-voxel serial event counters, sublattice sweeps done): with state(), a full checkpoint."""

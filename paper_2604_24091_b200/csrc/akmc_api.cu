@@ -151,6 +151,11 @@ struct akmc_handle {
     uint8_t* d_W2full = nullptr;      // bulk evaluator: W2^T images, N = 256 per K-step
     bool bulk = true;                 // FP32 batches through the bulk evaluator (AKMC_EVAL_ENGINE=1: cluster evaluator)
     bool have_pair = false;           // eps / E0 given at init (pair tables valid)
+    // dynamic voxel scheduling (Eq. 10): per-voxel species counts and the segment dispatch order
+    std::vector<unsigned long long> comp;   // [nvox][8]
+    std::vector<int> vorder;                // voxel ids in dispatch order (descending W_v, stable)
+    std::vector<double> vT;                 // per-voxel temperature (K)
+    std::vector<int> vstart_host;           // [nvox + 1] slot ranges per voxel
     // world-model time mode (akmc_set_world_model; akmc_world.cu)
     bool world = false;
     double* d_tnet = nullptr;
@@ -207,6 +212,11 @@ struct akmc_handle {
     int64_t exchanges = 0, exchange_bytes = 0;
     // per-phase exchange over NVLink peer memory (CUDA IPC mailboxes; AKMC_EXCHANGE=nccl selects NCCL p2p)
     bool p2p = false;
+    bool shift = false;                        // AKMC_EXCHANGE=shift: shift-staged NCCL exchange
+    int4* d_slist = nullptr;                   // shift: entries of the phase (own + received)
+    int* d_nslist = nullptr;
+    int slistcap = 0;
+    int64_t messages = 0;                      // per-phase messages sent (all phases)
     int4* d_mbox = nullptr;                    // [npeer][2][cap + 1]
     unsigned long long* d_mflag = nullptr;     // [kMaxPeers]
     int* d_pcnt = nullptr;
@@ -218,6 +228,31 @@ struct akmc_handle {
 };
 
 namespace {
+
+// per-voxel species counts of the canonical upload (composition is conserved per voxel in serial mode: vacancies
+// never leave their voxel) -> the workload proxy's effective barrier (Eq. 10)
+__global__ void voxel_comp_kernel(const uint8_t* __restrict__ canon, long long csites, unsigned long long* comp)
+{
+    __shared__ unsigned int cnt[8];
+    if (threadIdx.x < 8) cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const int v = blockIdx.y;
+    const uint4* p = reinterpret_cast<const uint4*>(canon + (long long)v * csites);
+    const long long nw = csites / 16;
+    unsigned int loc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nw; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 w = p[i];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) loc[(ws[j] >> (8 * b)) & 7u] += 1u;
+    }
+    for (int s = 0; s < 8; ++s)
+        if (loc[s]) atomicAdd(&cnt[s], loc[s]);
+    __syncthreads();
+    if (threadIdx.x < 8 && cnt[threadIdx.x]) atomicAdd(&comp[(size_t)v * 8 + threadIdx.x], (unsigned long long)cnt[threadIdx.x]);
+}
 
 int fail(akmc_handle* h, int code, const std::string& msg)
 {
@@ -258,7 +293,7 @@ void free_all(akmc_handle* h)
         if (h->ipc_box[r]) cudaIpcCloseMemHandle(h->ipc_box[r]);
         if (h->ipc_flag[r]) cudaIpcCloseMemHandle(h->ipc_flag[r]);
     }
-    void* dptrs[] = {h->d_free, h->d_fcnt, h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
+    void* dptrs[] = {h->d_slist, h->d_nslist, h->d_free, h->d_fcnt, h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
                      h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone};
     for (void* p : dptrs)
         if (p) cudaFree(p);
@@ -413,6 +448,42 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
         CK(h, cudaMalloc(&h->d_phase_cycles, kDiagWords * sizeof(unsigned long long)));
         CK(h, cudaMemset(h->d_phase_cycles, 0, kDiagWords * sizeof(unsigned long long)));
     }
+    return AKMC_OK;
+}
+
+// Dynamic voxel scheduling (Eq. 10): W_v = M_v exp(-E_v / (kB T_v)) with M_v = 8 x the
+// voxel's vacancies (feasible-event upper bound) and E_v = the composition-weighted mean base barrier E0 of its
+// atoms (SPEC workload_proxy); voxels are dispatched in descending W_v (stable: ties keep voxel order), and the
+// persistent engine's CTAs pull the next voxel from that list as soon as a slot frees (pull-on-finish).  The
+// order changes no trajectory (voxels are independent, R6/R10) -- only the makespan of batches larger than the
+// resident slots.
+int order_voxels(akmc_handle* h)
+{
+    const int nv = h->nvox;
+    std::vector<double> W((size_t)nv, 0.0);
+    for (int v = 0; v < nv; ++v) {
+        const int m = h->vstart_host[(size_t)v + 1] - h->vstart_host[(size_t)v];
+        double e = 0.0, n = 0.0;
+        for (int s = 0; s < kSpecies; ++s) {
+            if (s == kVac) continue;
+            const double c = (double)h->comp[(size_t)v * 8 + s];
+            e += c * h->P.E0[s];
+            n += c;
+        }
+        const double Ev = (n > 0.0 && h->have_pair) ? e / n : 0.0;
+        W[(size_t)v] = 8.0 * m * std::exp(-Ev / (h->cfg.kB * h->vT[(size_t)v]));
+    }
+    h->vorder.resize((size_t)nv);
+    for (int v = 0; v < nv; ++v) h->vorder[(size_t)v] = v;
+    if (!std::getenv("AKMC_VOXEL_FIFO"))                  // A/B knob: FIFO (voxel id) dispatch
+        std::stable_sort(h->vorder.begin(), h->vorder.end(), [&](int a, int b) { return W[(size_t)a] > W[(size_t)b]; });
+    std::vector<Segment> sg((size_t)nv);
+    for (int q = 0; q < nv; ++q) {
+        const int v = h->vorder[(size_t)q];
+        sg[(size_t)q] = Segment{(long long)v, h->vstart_host[(size_t)v], h->vstart_host[(size_t)v + 1] - h->vstart_host[(size_t)v],
+                                0.0, 0u, 1};
+    }
+    CK(h, cudaMemcpy(h->d_segs, sg.data(), sg.size() * sizeof(Segment), cudaMemcpyHostToDevice));
     return AKMC_OK;
 }
 
@@ -655,8 +726,8 @@ int init_multi(akmc_handle* h)
     const size_t per = (size_t)(h->DP.cap + 1);
     CK(h, cudaMalloc(&h->d_log, (size_t)h->S.logcap * sizeof(int4)));
     CK(h, cudaMalloc(&h->d_nlog, sizeof(unsigned long long)));
-    CK(h, cudaMalloc(&h->d_send, std::max<size_t>(1, np * per) * sizeof(int4)));
-    CK(h, cudaMalloc(&h->d_recv, std::max<size_t>(1, np * per) * sizeof(int4)));
+    CK(h, cudaMalloc(&h->d_send, std::max<size_t>(2, np) * per * sizeof(int4)));     // (shift: 2 buffers per axis)
+    CK(h, cudaMalloc(&h->d_recv, std::max<size_t>(2, np) * per * sizeof(int4)));
     CK(h, cudaMalloc(&h->d_dist_overflow, sizeof(int)));
     CK(h, cudaMalloc(&h->d_gid, (size_t)h->vcap * sizeof(int)));
     CK(h, cudaMalloc(&h->d_nvac, sizeof(int)));
@@ -667,7 +738,7 @@ int init_multi(akmc_handle* h)
     h->S.fcnt = h->d_fcnt;
     CK(h, cudaMemset(h->d_nlog, 0, sizeof(unsigned long long)));
     CK(h, cudaMemset(h->d_dist_overflow, 0, sizeof(int)));
-    CK(h, cudaMemset(h->d_send, 0, std::max<size_t>(1, np * per) * sizeof(int4)));
+    CK(h, cudaMemset(h->d_send, 0, std::max<size_t>(2, np) * per * sizeof(int4)));
     const int nloc = (int)h->nvac;
     CK(h, cudaMemcpy(h->d_nvac, &nloc, sizeof(int), cudaMemcpyHostToDevice));
     h->S.log = h->d_log;
@@ -710,7 +781,12 @@ int init_multi(akmc_handle* h)
         gid[(size_t)i] = (int)(std::lower_bound(all.begin(), all.end(), mine[(size_t)i]) - all.begin());
     if (h->nvac) CK(h, cudaMemcpy(h->d_gid, gid.data(), (size_t)h->nvac * sizeof(int), cudaMemcpyHostToDevice));
     const char* ex = std::getenv("AKMC_EXCHANGE");
-    if (!(ex && std::strcmp(ex, "nccl") == 0)) {
+    if (ex && std::strcmp(ex, "shift") == 0) {
+        h->shift = true;
+        h->slistcap = h->S.logcap + 6 * (h->DP.cap + 1);
+        CK(h, cudaMalloc(&h->d_slist, (size_t)h->slistcap * sizeof(int4)));
+        CK(h, cudaMalloc(&h->d_nslist, sizeof(int)));
+    } else if (!(ex && std::strcmp(ex, "nccl") == 0)) {
         const int prc = setup_p2p(h);
         if (prc != AKMC_OK) return prc;
     }
@@ -872,6 +948,18 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         cudaFree(d_bc);
         cudaFree(d_max);
         lap("vacancy scan");
+        if (!h->sub) {
+            unsigned long long* d_comp = nullptr;
+            CKI(cudaMalloc(&d_comp, (size_t)h->nvox * 8 * sizeof(unsigned long long)));
+            CKI(cudaMemsetAsync(d_comp, 0, (size_t)h->nvox * 8 * sizeof(unsigned long long), h->stream));
+            const unsigned bx = (unsigned)std::min<long long>(64, std::max<long long>(1, h->csites / 16 / 256));
+            voxel_comp_kernel<<<dim3(bx, (unsigned)h->nvox), 256, 0, h->stream>>>(h->d_species, h->csites, d_comp);
+            h->comp.assign((size_t)h->nvox * 8, 0ull);
+            CKI(cudaMemcpyAsync(h->comp.data(), d_comp, h->comp.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                h->stream));
+            CKI(cudaStreamSynchronize(h->stream));
+            cudaFree(d_comp);
+        }
         // storage layout with halo ghosts (periodic images)
         uint8_t* st = nullptr;
         CKI(cudaMalloc(&st, (size_t)h->ssites));
@@ -991,8 +1079,11 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         for (int64_t i = 0; i < h->nvac; ++i) mem[(size_t)i] = (int)i;
         CKI(cudaMalloc(&h->d_segs, sg.size() * sizeof(Segment)));
         CKI(cudaMalloc(&h->d_members, mem.size() * sizeof(int)));
-        CKI(cudaMemcpy(h->d_segs, sg.data(), sg.size() * sizeof(Segment), cudaMemcpyHostToDevice));
         CKI(cudaMemcpy(h->d_members, mem.data(), mem.size() * sizeof(int), cudaMemcpyHostToDevice));
+        h->vT.assign((size_t)h->nvox, cfg->temperature_K);
+        h->vstart_host = vs;
+        rc = order_voxels(h);
+        if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
     }
     CKI(cudaStreamSynchronize(h->stream));
     lap("engine setup + memo + segments");
@@ -1044,6 +1135,10 @@ int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n)
     CK(h, cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
     // memoised rates were formed at the old temperatures (R7: the memo maps window -> rates at fixed T)
     CK(h, cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
+    if (!h->sub) {
+        h->vT.assign(T_K, T_K + n);
+        return order_voxels(h);                            // Eq. 10 priority at the new temperatures
+    }
     return AKMC_OK;
 }
 
@@ -1259,10 +1354,60 @@ static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGra
 }
 
 // multi-rank: after a phase, send logged boundary writes / departures to the peers and apply theirs
+// shift-staged exchange of the phase's deltas: stage x, y, z over the decomposed axes, NCCL send /
+// recv with the 1-2 neighbours of the axis; receivers forward what the later stages route on (akmc_route.h)
+static int exchange_shift(akmc_handle* h)
+{
+    const akmc_config& c = h->cfg;
+    const int cap = h->DP.cap;
+    const size_t per = (size_t)(cap + 1);
+    ShiftGeom SG{};
+    for (int a = 0; a < 3; ++a) { SG.P[a] = h->rc[a]; SG.L[a] = c.cells[a]; SG.grid[a] = c.gpu_grid[a]; }
+    shift_collect_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
+                                                            h->d_slist, h->d_nslist, h->d_dist_overflow);
+    CK(h, cudaMemsetAsync(h->d_nlog, 0, sizeof(unsigned long long), h->stream));
+    int launches = 2;
+    int last = -1;
+    for (int a = 0; a < 3; ++a) if (c.gpu_grid[a] > 1) last = a;
+    for (int a = 0; a < 3; ++a) {
+        const int ndir = route::shift_dirs(c.gpu_grid[a]);
+        if (!ndir) continue;
+        CK(h, cudaMemsetAsync(h->d_send, 0, sizeof(int4), h->stream));
+        if (ndir > 1) CK(h, cudaMemsetAsync(h->d_send + per, 0, sizeof(int4), h->stream));
+        shift_pack_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_slist, h->d_nslist, a, SG, h->d_send, cap,
+                                                             h->d_dist_overflow);
+        int e[3] = {0, 0, 0};
+        e[a] = 1;
+        const int plus = rank_of(c, h->rc[0] + e[0], h->rc[1] + e[1], h->rc[2] + e[2]);
+        const int minus = rank_of(c, h->rc[0] - e[0], h->rc[1] - e[1], h->rc[2] - e[2]);
+        NCK(h, ncclGroupStart());
+        NCK(h, ncclSend(h->d_send, per * sizeof(int4), ncclChar, plus, h->comm, h->stream));        // d = +1
+        NCK(h, ncclRecv(h->d_recv, per * sizeof(int4), ncclChar, minus, h->comm, h->stream));       // their d = +1
+        if (ndir > 1) {
+            NCK(h, ncclSend(h->d_send + per, per * sizeof(int4), ncclChar, minus, h->comm, h->stream));   // d = -1
+            NCK(h, ncclRecv(h->d_recv + per, per * sizeof(int4), ncclChar, plus, h->comm, h->stream));
+        }
+        NCK(h, ncclGroupEnd());
+        shift_unpack_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_recv, ndir, cap, h->F, h->DP, h->d_species, h->d_vac,
+                                                               h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
+                                                               h->d_slist, h->d_nslist, h->slistcap, a != last,
+                                                               h->d_dist_overflow);
+        launches += 2;
+        h->messages += ndir;
+        h->exchange_bytes += (int64_t)(2 * ndir * per * sizeof(int4));
+    }
+    CK(h, cudaGetLastError());
+    h->total.kernel_launches += launches;
+    h->exchanges += 1;
+    return AKMC_OK;
+}
+
 static int exchange_deltas(akmc_handle* h)
 {
+    if (h->shift) return exchange_shift(h);
     const int np = h->DP.npeer;
     const size_t per = (size_t)(h->DP.cap + 1);
+    h->messages += np;
     if (h->p2p) {
         // deltas straight into the peers' mailboxes over NVLink, flag per peer; wait + apply (akmc_dist.cuh)
         h->epoch += 1;
@@ -1602,6 +1747,23 @@ int akmc_set_world_model(akmc_handle* h, const double* tnet, int32_t hidden, dou
     h->world_H = hidden;
     h->world_tau = tau_act;
     h->world = true;
+    return AKMC_OK;
+}
+
+int akmc_exchange_stats(akmc_handle* h, int64_t* out3)
+{
+    if (!h || !out3) return AKMC_ERR_INVALID;
+    out3[0] = h->exchanges;
+    out3[1] = h->messages;
+    out3[2] = h->exchange_bytes;
+    return AKMC_OK;
+}
+
+int akmc_voxel_order(akmc_handle* h, int32_t* order_out)
+{
+    if (!h || !order_out) return AKMC_ERR_INVALID;
+    if (h->sub) return fail(h, AKMC_ERR_INVALID, "akmc_voxel_order: serial (voxel) mode only");
+    std::copy(h->vorder.begin(), h->vorder.end(), order_out);
     return AKMC_OK;
 }
 

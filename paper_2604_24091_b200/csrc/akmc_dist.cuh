@@ -8,6 +8,7 @@
 // wrote that lie in a peer's extended region (block + halo), and the vacancies that left its block.
 #pragma once
 #include "akmc_device.cuh"
+#include "akmc_route.h"
 
 namespace akmc {
 
@@ -270,6 +271,102 @@ static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const un
                 }
             } else {
                 write_site(species, F, 0, lp[0], lp[1], lp[2], (uint8_t)e.w);
+            }
+        }
+    }
+    unpack_done(FL, nfree0);
+}
+
+// ---------------------------------------------------------------- shift-staged per-phase exchange (AKMC_EXCHANGE=shift)
+// The paper's shift communication applied to the sparse per-phase deltas: the phase's entries (global
+// half-cell coordinates, final value or migration code) go through the decomposed axes in order; at stage a a
+// holder forwards an entry to the neighbour(s) along a chosen by route::shift_send (akmc_route.h), and every
+// receiver applies what concerns it and keeps the entry for the later stages.  2 messages per axis instead of one
+// per distinct neighbour block (tests/test_route_cpu.py: same deliveries as the direct exchange).
+struct ShiftGeom {
+    int P[3];          // this rank's block coordinates
+    int L[3];          // block cells
+    int grid[3];       // gpu grid
+};
+
+static __global__ void shift_collect_kernel(const int4* __restrict__ log, const unsigned long long* nlog_p, int logcap, Frame F,
+                                            DistParams D, const uint8_t* __restrict__ species, int4* list, int* nlist,
+                                            int* overflow)
+{
+    const int n = (int)min((unsigned long long)logcap, *nlog_p);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *nlist = n;
+        if (*nlog_p > (unsigned long long)logcap) atomicAdd(overflow, 1);
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int4 e = log[i];
+        if (e.w < kMigrateBase) e.w = species[site_of(F, 0, e.x, e.y, e.z)];   // the site's FINAL value
+        const int p[3] = {e.x, e.y, e.z};
+        int gp[3];
+        for (int a = 0; a < 3; ++a) gp[a] = 2 * imod((p[a] >> 1) + D.O[a], D.G[a]) + (p[a] & 1);
+        list[i] = make_int4(gp[0], gp[1], gp[2], e.w);
+    }
+}
+
+static __global__ void shift_pack_kernel(const int4* __restrict__ list, const int* nlist, int axis, ShiftGeom SG,
+                                         int4* sendbuf, int cap, int* overflow)
+{
+    const int n = *nlist;
+    const int ndir = route::shift_dirs(SG.grid[axis]);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 e = list[i];
+        const int g[3] = {e.x >> 1, e.y >> 1, e.z >> 1};
+        const bool mig = e.w >= kMigrateBase;
+        for (int k = 0; k < ndir; ++k) {
+            if (!route::shift_send(g, SG.P, axis, k == 0 ? 1 : -1, SG.L, SG.grid, kHalo, mig)) continue;
+            int4* buf = sendbuf + (size_t)k * (cap + 1);
+            const int q = atomicAdd(&buf[0].x, 1);
+            if (q < cap) buf[1 + q] = e;
+            else atomicAdd(overflow, 1);
+        }
+    }
+}
+
+// apply a stage's arrivals (species writes inside the extended region, vacancies arriving in the block) and keep
+// them for the later stages
+static __global__ void shift_unpack_kernel(const int4* __restrict__ recvbuf, int ndir, int cap, Frame F, DistParams D,
+                                           uint8_t* species, int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL,
+                                           int4* list, int* nlist, int listcap, bool keep, int* overflow)
+{
+    const int nfree0 = *(volatile int*)&FL.cnt[0];
+    for (int k = 0; k < ndir; ++k) {
+        const int4* buf = recvbuf + (size_t)k * (cap + 1);
+        const int cnt = min(buf[0].x, cap);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+            const int4 e = buf[1 + i];
+            const int gp[3] = {e.x, e.y, e.z};
+            int lp[3];
+            bool in_ext = true, in_blk = true;
+            for (int a = 0; a < 3; ++a) {
+                if (F.wrap[a]) { lp[a] = gp[a]; continue; }
+                int d = imod(gp[a] - 2 * D.O[a], 2 * D.G[a]);
+                if (d >= 2 * (F.L[a] + kHalo)) d -= 2 * D.G[a];
+                lp[a] = d;
+                if (d < -2 * kHalo || d >= 2 * (F.L[a] + kHalo)) in_ext = false;
+                if (d < 0 || d >= 2 * F.L[a]) in_blk = false;
+            }
+            if (e.w >= kMigrateBase) {
+                if (in_blk && in_ext) {
+                    const int slot = arrival_slot(FL, nfree0, nvac_local);
+                    if (slot < vcap) {
+                        vac[slot] = make_int4(0, lp[0], lp[1], lp[2]);
+                        gid[slot] = e.w - kMigrateBase;
+                    } else {
+                        atomicAdd(overflow, 1);
+                    }
+                }
+            } else if (in_ext) {
+                write_site(species, F, 0, lp[0], lp[1], lp[2], (uint8_t)e.w);
+            }
+            if (keep) {
+                const int q = atomicAdd(nlist, 1);
+                if (q < listcap) list[q] = e;
+                else atomicAdd(overflow, 1);
             }
         }
     }

@@ -254,3 +254,32 @@ def test_bulk_rates_lattice_bitexact_and_within_bar(akmc, orc, monkeypatch):
     Go, _ = orc.rates(ocfg, sp, vac, mlp=mlp)
     assert np.array_equal(G1 == 0.0, Go == 0.0)
     assert float(_rel(G1, Go).max()) <= RTOL_FAST
+
+
+# ----------------------------------------------------------------------------- dynamic voxel scheduling (Eq. 10)
+def _eq10_order(sp, cells, nvox, E0, T, kB=8.617333262e-5):
+    S = 2 * cells[0] * cells[1] * cells[2]
+    W = []
+    for v in range(nvox):
+        c = np.bincount(sp[v * S:(v + 1) * S], minlength=7)
+        n = c[:6].sum()
+        Ev = float((c[:6] * np.asarray(E0)[:6]).sum() / n)
+        W.append(8.0 * c[6] * np.exp(-Ev / (kB * T[v])))
+    return np.array(sorted(range(nvox), key=lambda v: -W[v]), dtype=np.int32)   # stable on ties
+
+
+def test_voxel_dispatch_order_is_eq10(akmc):
+    """P:481-490 / S:658-670: voxels are dispatched in descending W_v = 8 m_v exp(-E_v / kB T_v) (E_v = the
+    composition-weighted mean E0), recomputed when the voxel temperatures change; ties keep voxel order."""
+    eps, E0 = synth.illustrative_pair_params()
+    L, nvox = 8, 40
+    rng = np.random.default_rng(4)
+    parts = [synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(float(rng.uniform(0.0, 0.3))),
+                                int(rng.integers(1, 6)), seed=100 + v) for v in range(nvox)]
+    sp = np.concatenate(parts)
+    cfg = akmc.Config(cells=(L, L, L), n_voxels=nvox, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64)
+    with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        assert np.array_equal(sim.voxel_order(), _eq10_order(sp, (L, L, L), nvox, E0, [563.0] * nvox))
+        T = synth.voxel_temperatures(nvox, seed=3)
+        sim.set_voxel_temperatures(T)
+        assert np.array_equal(sim.voxel_order(), _eq10_order(sp, (L, L, L), nvox, E0, T))

@@ -102,3 +102,29 @@ def test_two_rank_slot_reuse_long_run(tmp_path):
     res = json.loads(out.read_text())
     assert res["ok"], res
     assert res["events"] > 200
+
+
+@pytest.mark.parametrize("grid,nproc,direct_msgs,shift_msgs", [((2, 1, 1), 2, 1, 1), ((2, 2, 1), 4, 3, 2),
+                                                              ((1, 2, 2), 4, 3, 2), ((2, 2, 2), 8, 7, 3)])
+def test_shift_exchange_equals_direct(tmp_path, grid, nproc, direct_msgs, shift_msgs):
+    """S:766 / P:420-427: the per-phase deltas by shift communication (X -> Y -> Z stages, AKMC_EXCHANGE=shift)
+    give the same global lattice, vacancies and clocks as 1 rank and the oracle -- as the direct exchange does --
+    with fewer messages per rank and phase (2x2x1: 2 vs 3 distinct peers; 2x2x2: 3 vs 7)."""
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    res = {}
+    for mode in ("shift", "p2p"):
+        out = tmp_path / f"multi_{mode}.json"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}", "--master-addr",
+               "127.0.0.1", "--master-port", str(29710 + grid[0] + 3 * grid[1] + 7 * grid[2] + (mode == "p2p")),
+               os.path.join(ROOT, "tools", "multi_check.py"), "--grid", *map(str, grid), "--out", str(out), "--oracle",
+               "--nvac", str(30 * nproc)]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
+                           env=dict(os.environ, AKMC_EXCHANGE=mode))
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        res[mode] = json.loads(out.read_text())
+        assert res[mode]["ok"], res[mode]
+        assert res[mode]["events"] > 20
+    assert res["shift"]["events"] == res["p2p"]["events"]
+    assert all(m == shift_msgs for m in res["shift"]["messages_per_phase"]), res["shift"]["messages_per_phase"]
+    assert all(m == direct_msgs for m in res["p2p"]["messages_per_phase"]), res["p2p"]["messages_per_phase"]

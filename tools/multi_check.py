@@ -81,9 +81,10 @@ def main():
         c = sim.step(a.sweeps)
     sp, _, clock, _ = sim.state()
     gid, site = sim.vacancies()
+    xs = sim.exchange_stats()
     sim.close()
     parts = [None] * world
-    tdist.all_gather_object(parts, (sp, gid, site, float(clock[0]), int(c["events"]), int(c["hop_evals"])))
+    tdist.all_gather_object(parts, (sp, gid, site, float(clock[0]), int(c["events"]), int(c["hop_evals"]), xs))
     result = {}
     if rank == 0:
         gsp = D.assemble([p[0] for p in parts], block, grid)
@@ -98,6 +99,8 @@ def main():
         rsp, rvac, rclock, _ = ref.state()
         ref.close()
         result = {"world": world, "grid": grid, "events": events, "ref_events": int(rc["events"]),
+                  "exchange": os.environ.get("AKMC_EXCHANGE", "p2p"),
+                  "messages_per_phase": [p[6]["messages"] / max(p[6]["exchanges"], 1) for p in parts],
                   "hop_evals": hop, "ref_hop_evals": int(rc["hop_evals"]),
                   "species_equal": bool(np.array_equal(gsp, rsp)),
                   "vacancies_equal": bool(np.array_equal(gids[order], np.arange(gids.size))) and

@@ -23,7 +23,7 @@ using namespace akmc;
 namespace {
 
 thread_local std::string g_init_error;
-constexpr int kDiagWords = 128 + 512 + 64;   // AKMC_PHASE_TIMING: sums, engine sums, iteration trace
+constexpr int kDiagWords = 128 + 512 + 64 + 16;   // AKMC_PHASE_TIMING: sums, engine sums, iteration trace, bulk roles
 
 // ------------------------------------------------------------------ host geometry (independent of the oracle)
 // window: bcc vectors within 6.0 A at a0 = 2.866 A, sorted by (|h|^2, hx, hy, hz)  (A3, A4)
@@ -149,6 +149,8 @@ struct akmc_handle {
     int act_shift = 0;                // t1: h1 scale 2^-t1 (prepare_engine_weights)
     double* d_W3d = nullptr;          // [256][8] FP64 W3 (layer 3 on CUDA cores)
     uint8_t* d_W2full = nullptr;      // bulk evaluator: W2^T images, N = 256 per K-step
+    std::vector<double> W3h, b3h;     // host copies for the bulk evaluator's constant-bank parameters
+    std::vector<float> b2h;
     bool bulk = true;                 // FP32 batches through the bulk evaluator (AKMC_EVAL_ENGINE=1: cluster evaluator)
     bool have_pair = false;           // eps / E0 given at init (pair tables valid)
     // dynamic voxel scheduling (Eq. 10): per-voxel species counts and the segment dispatch order
@@ -406,6 +408,9 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
     h->h1s = (float)std::ldexp(1.0, -t1);
     std::vector<float> b2f(kHid);
     for (int i = 0; i < kHid; ++i) b2f[i] = (float)b2[i];
+    h->W3h.assign(W3, W3 + (size_t)kHid * 8);
+    h->b3h.assign(b3, b3 + 8);
+    h->b2h = b2f;
     // per cluster CTA r: fp16 hi/lo UMMA images of W2^T columns [64r, 64r+64); W3 stays FP64
     {
         std::vector<float> w1f((size_t)kW1Rows * kHid);
@@ -546,6 +551,7 @@ int eval_rows(akmc_handle* h, const int* rows, const int* nrows_dev, int nrows_h
         p.W2full = h->d_W2full;
         p.rates = rates; p.Rsum = R; p.E = E; p.overflow = h->d_overflow;
         p.fast = prec == AKMC_PREC_FP16_FAST ? 1 : 0;
+        p.diag = h->d_phase_cycles ? h->d_phase_cycles + 128 + 512 + 64 : nullptr;   // last 16 diag words
         CK(h, launch_bulk(p, max_rows, h->num_sms, h->stream));
     } else {
         // the engine's cluster evaluator in eval mode (AKMC_EVAL_ENGINE=1; same arithmetic as the bulk evaluator)
@@ -1059,10 +1065,12 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     {
         // per-voxel kT (uniform until akmc_set_voxel_temperatures); the pointer is fixed for the handle's
         // life, so kernel parameters captured in graphs stay valid when the values change
-        const std::vector<double> kT((size_t)h->nvox, h->P.kT);
-        CKI(cudaMalloc(&h->d_kT, kT.size() * sizeof(double)));
+        const std::vector<double> kT((size_t)h->nvox, h->P.kT), ik((size_t)h->nvox, h->P.inv_kT);
+        CKI(cudaMalloc(&h->d_kT, 2 * kT.size() * sizeof(double)));
         CKI(cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CKI(cudaMemcpy(h->d_kT + h->nvox, ik.data(), ik.size() * sizeof(double), cudaMemcpyHostToDevice));
         h->P.kT_vox = h->d_kT;
+        h->P.inv_kT_vox = h->d_kT + h->nvox;
     }
     if (!h->sub) {
         // serial / voxel-batch mode through the engine: one segment per voxel, members = its slots in order
@@ -1131,8 +1139,11 @@ int akmc_set_voxel_temperatures(akmc_handle* h, const double* T_K, int32_t n)
         if (!(T_K[v] > 0.0) || !std::isfinite(T_K[v])) return fail(h, AKMC_ERR_INVALID, "temperature must be > 0 (S:154)");
         kT[(size_t)v] = h->cfg.kB * T_K[v];                  // the same IEEE product as the uniform kT
     }
+    std::vector<double> ik((size_t)n);
+    for (int v = 0; v < n; ++v) ik[(size_t)v] = 1.0 / kT[(size_t)v];
     CK(h, cudaStreamSynchronize(h->stream));
     CK(h, cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_kT + h->nvox, ik.data(), ik.size() * sizeof(double), cudaMemcpyHostToDevice));
     // memoised rates were formed at the old temperatures (R7: the memo maps window -> rates at fixed T)
     CK(h, cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
     if (!h->sub) {
@@ -1627,6 +1638,7 @@ static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horiz
     if (h->multi) {
         int ovf = 0;
         CK(h, cudaMemcpy(&ovf, h->d_dist_overflow, sizeof(int), cudaMemcpyDeviceToHost));
+        if (ovf & kExchangeTimeout) return fail(h, AKMC_ERR_RUNTIME, "halo exchange timeout: a peer rank did not publish its deltas within 30 s");
         if (ovf) return fail(h, AKMC_ERR_RUNTIME, "halo exchange buffer overflow (" + std::to_string(ovf) + " entries)");
     }
     if (c1.terminal != c0.terminal) return fail(h, AKMC_TERMINAL, "a competing set has no feasible event (S:199)");
@@ -1945,6 +1957,16 @@ void akmc_free(akmc_handle* h)
             if (d[24] + d[25] + d[26] + d[27])
                 std::fprintf(stderr, "[akmc engine] layer-1 probe (warp 0): index %.0f b1 %.0f loads+adds %.0f store %.0f\n",
                              d[24] / n, d[25] / n, d[26] / n, d[27] / n);
+        }
+        {
+            const unsigned long long* b = c + 128 + 512 + 64;
+            if (b[4] && b[8] && b[12]) {
+                const double T = (double)b[8];           // tiles (all CTAs); 8 producer / 4 epilogue warps per CTA
+                std::fprintf(stderr, "[akmc bulk] tiles %.0f; cycles per tile -- producer warp: gather %.0f wait-A %.0f "
+                             "layer-1 %.0f wait-meta %.0f | MMA thread: wait-A %.0f wait-TMEM %.0f issue %.0f | epilogue "
+                             "warp: wait %.0f E2+L3 %.0f E3 %.0f\n", T, b[0] / (8 * T), b[1] / (8 * T), b[2] / (8 * T),
+                             b[3] / (8 * T), b[5] / T, b[6] / T, b[7] / T, b[9] / (4 * T), b[10] / (4 * T), b[11] / (4 * T));
+            }
         }
         // per-iteration trace: iteration index -> CTA count, mean rows / misses / running domains, cycles
         const unsigned long long* tr = c + 128;

@@ -23,7 +23,10 @@ using namespace ptx;
 constexpr int kBTile = 128;                                     // rows per tile = TMEM lanes = UMMA M
 constexpr int kBEpiWarps = 4;
 constexpr int kBLoadWarp = 4, kBMmaWarp = 5;
-constexpr int kBProdWarp0 = 6, kBProdWarps = 8;
+#ifndef AKMC_BULK_PROD
+#define AKMC_BULK_PROD 8        // producer warps (A/B knob; 128 / AKMC_BULK_PROD rows each)
+#endif
+constexpr int kBProdWarp0 = 6, kBProdWarps = AKMC_BULK_PROD;
 constexpr int kBThreads = 32 * (kBProdWarp0 + kBProdWarps);    // 448
 constexpr int kBStages = 4;
 constexpr uint32_t kBSplitA = kBTile * kHid * 2;                // 64 KiB: one fp16 split of the A tile
@@ -118,9 +121,13 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             const uint32_t idesc = idesc_f16(kBTile, kHid);
             const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo);
             int i = 0;
+            long long ta = 0, td = 0, tk = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                long long t0 = clock64();
                 mbar_wait(bar_afull, (uint32_t)i & 1u);
+                long long t1 = clock64(); ta += t1 - t0; t0 = t1;
                 if (i > 0) mbar_wait(bar_dempty, (uint32_t)(i - 1) & 1u);
+                t1 = clock64(); td += t1 - t0; t0 = t1;
                 tc_fence_after();
                 for (int ks = 0; ks < kHid / 16; ++ks) {
                     mbar_wait(bar_full + 8 * st, ph);
@@ -140,16 +147,24 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
                 }
                 umma_commit(bar_aempty);                      // A may be overwritten
                 umma_commit(bar_dfull);                       // accumulators complete
+                tk += clock64() - t0;
+            }
+            if (p.diag) {
+                atomicAdd(p.diag + 5, (unsigned long long)ta); atomicAdd(p.diag + 6, (unsigned long long)td);
+                atomicAdd(p.diag + 7, (unsigned long long)tk); atomicAdd(p.diag + 8, (unsigned long long)i);
             }
         }
     } else if (warp >= kBProdWarp0) {
         // ---------------- producers: gather (overlaps the previous tile's MMA), then layer 1 into A
         const int pw = warp - kBProdWarp0;
         const uint32_t off_lo = pack_off(p.G.off[lane]), off_hi = pack_off(p.G.off[lane + 32]);
+        long long tg = 0, tw = 0, tl = 0, tm = 0;          // diag: gather, wait A, layer 1, wait meta
         int i = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int b = i & 1;
+            long long t0 = clock64();
             if (i >= 2) mbar_wait(bar_mempty + 8 * b, (uint32_t)((i >> 1) - 1) & 1u);
+            long long t1 = clock64(); tm += t1 - t0; t0 = t1;
             BulkMeta& M = meta[b];
             // rows pw + 8 q (q = 0..15): lane q < 16 resolves row q's source (slot, position), then all 32 window
             // bytes of the lane's two slots for the 16 rows are in flight at once
@@ -199,8 +214,10 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
                 M.vox[r] = my_vox;
             }
             __syncwarp();
+            t1 = clock64(); tg += t1 - t0; t0 = t1;
             // layer 1 needs the A operand released by the previous tile's MMAs
             if (i > 0) mbar_wait(bar_aempty, (uint32_t)(i - 1) & 1u);
+            t1 = clock64(); tw += t1 - t0; t0 = t1;
 #pragma unroll 1
             for (int q0 = 0; q0 < kBRowsPerProd; q0 += kL1Rows) {
                 int rr[kL1Rows], mr[kL1Rows];
@@ -211,16 +228,25 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             fence_async_smem();                                 // generic-proxy A writes -> the MMA's async proxy
             __syncwarp();
             if (lane == 0) { mbar_arrive(bar_afull); mbar_arrive(bar_mfull + 8 * b); }
+            tl += clock64() - t0;
+        }
+        if (p.diag && lane == 0) {
+            atomicAdd(p.diag + 0, (unsigned long long)tg); atomicAdd(p.diag + 1, (unsigned long long)tw);
+            atomicAdd(p.diag + 2, (unsigned long long)tl); atomicAdd(p.diag + 3, (unsigned long long)tm);
+            atomicAdd(p.diag + 4, 1ull);
         }
     } else {
         // ---------------- epilogue warps 0-3: row m = TMEM lane 32 w + lane
         const int m = 32 * warp + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+        long long tw = 0, tc = 0, te = 0;
         int i = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int b = i & 1;
+            long long t0 = clock64();
             mbar_wait(bar_dfull, (uint32_t)i & 1u);
             mbar_wait(bar_mfull + 8 * b, (uint32_t)(i >> 1) & 1u);
+            long long t1 = clock64(); tw += t1 - t0; t0 = t1;
             tc_fence_after();
             double acc[8];
 #pragma unroll
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_dempty);            // TMEM may be overwritten by the next tile
+            t1 = clock64(); tc += t1 - t0; t0 = t1;
             const int slot = meta[b].slot[m];
             if (slot >= 0) {
                 const int vox = meta[b].vox[m];
@@ -263,7 +290,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
                 for (int k = 0; k < 8; ++k) {
                     const double out = __dadd_rn(b3s[k], acc[k]);
                     const double Ek = out > 0.0 ? out : 0.0;
-                    const double Gk = (meta[b].win8[m][k] != (uint8_t)kVac) ? arrhenius(Ek, p.P, vox) : 0.0;
+                    const double Gk = (meta[b].win8[m][k] != (uint8_t)kVac) ? arrhenius_tc(Ek, p.P, vox) : 0.0;
                     R = __dadd_rn(R, Gk);
                     if (p.rates) p.rates[(size_t)slot * 8 + k] = Gk;
                     if (p.E) p.E[(size_t)slot * 8 + k] = Ek;
@@ -272,6 +299,11 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_mempty + 8 * b);
+            te += clock64() - t0;
+        }
+        if (p.diag && lane == 0) {
+            atomicAdd(p.diag + 9, (unsigned long long)tw); atomicAdd(p.diag + 10, (unsigned long long)tc);
+            atomicAdd(p.diag + 11, (unsigned long long)te); atomicAdd(p.diag + 12, 1ull);
         }
     }
     if (ovf && p.overflow) atomicAdd(p.overflow, ovf);

@@ -35,6 +35,7 @@ struct PhysParams {
     double nu0;
     double inv_kT;                       // 1 / kT (FP32-equivalent mode only; FP64 mode divides, A29)
     const double* kT_vox;                // [n_voxels] kB * T_v (C4 per-voxel temperature; always set by init)
+    const double* inv_kT_vox;            // [n_voxels] 1 / (kB * T_v) (FP32-equivalent evaluators only)
 };
 
 // Lattice frame of one voxel.  The voxel's L^3 owned cells are stored inside a halo of kHalo cells
@@ -128,6 +129,14 @@ __device__ __forceinline__ double det_log(double u)
 __device__ __forceinline__ double kT_of(const PhysParams& P, int vox)
 {
     return vox >= 0 ? __ldg(P.kT_vox + vox) : P.kT;
+}
+
+// FP32-equivalent evaluators (tensor-core paths; the 1e-5 bar, not bit-exact with the oracle): the exponent is
+// E * (1 / kT_v) -- one multiply instead of an FP64 division (relative change of the rate ~|E/kT| ulp ~ 1e-15)
+__device__ __forceinline__ double arrhenius_tc(double E, const PhysParams& P, int vox)
+{
+    const double ik = vox >= 0 ? __ldg(P.inv_kT_vox + vox) : P.inv_kT;
+    return __dmul_rn(P.nu0, det_exp(-__dmul_rn(E, ik)));
 }
 
 // Gamma = nu0 * det_exp(-(E / kT_v)), masked -> exactly 0 (Eq. 1; Eq. 8)

@@ -186,6 +186,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 {
     asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr int kExchangeTimeout = 1 << 30;  // flag bit in the exchange overflow word
+
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
 {
     unsigned long long v;
@@ -241,8 +249,15 @@ static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const un
                                          int vcap, FreeList FL, int* overflow)
 {
     const int nfree0 = *(volatile int*)&FL.cnt[0];
-    if (threadIdx.x < D.npeer)
-        while (ld_acquire_sys(&mflag[threadIdx.x]) < epoch) __nanosleep(64);
+    if (threadIdx.x < D.npeer) {
+        // bounded wait: a peer that never publishes (a crashed or diverged rank) must not hang the GPU -- after
+        // 30 s the exchange is abandoned and reported (kExchangeTimeout in the overflow word -> AKMC_ERR_RUNTIME)
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(&mflag[threadIdx.x]) < epoch) {
+            __nanosleep(64);
+            if (globaltimer_ns() - t0 > 30000000000ull) { atomicOr(overflow, kExchangeTimeout); break; }
+        }
+    }
     __syncthreads();
     const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
     for (int r = 0; r < D.npeer; ++r) {

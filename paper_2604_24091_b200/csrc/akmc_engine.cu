@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                             int vox = -1;
                             if (phase_mode) vox = c.mem_vac[c.row_mem[r]].x;
                             else if (!p.windows) vox = max(p.vac[p.rows ? p.rows[c.ebase + i] : c.ebase + i].x, 0);
-                            Gk = (win8[r * 8 + k] != (uint8_t)kVac) ? arrhenius(Ek, p.P, vox) : 0.0;
+                            Gk = (win8[r * 8 + k] != (uint8_t)kVac) ? arrhenius_tc(Ek, p.P, vox) : 0.0;
                         }
                         double R = 0.0;
 #pragma unroll

@@ -110,6 +110,7 @@ struct BulkParams {
     double* E;
     unsigned long long* overflow;
     int fast;
+    unsigned long long* diag;   // optional [16] per-role cycle sums (AKMC_PHASE_TIMING)
 };
 cudaError_t bulk_setup();
 cudaError_t launch_bulk(const BulkParams& p, int max_rows, int num_sms, cudaStream_t s);

@@ -139,6 +139,16 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
  * be NULL), sorted by gid; *n_inout = capacity in / count out.                                     */
 int akmc_vacancies(akmc_handle* h, int64_t* gid_out, int64_t* site_out, int64_t* n_inout);
 
+/* Dataflow sweeps (the asynchronous sublattice with readiness signals; S:526-529,
+ * S:572-580), single-rank sublattice handles: instead of 8 phases separated by grid-wide boundaries, one engine
+ * launch per sweep in which each tile of domains starts phase q as soon as the 27 tiles around it have finished
+ * phase q-1 (a domain's phase-q reads and writes stay inside its 26 neighbour domains, reading A20), so the tail
+ * of one phase overlaps the next.  The trajectory is the synchronous sweep's, bit for bit (same Philox counters,
+ * same per-domain order).  on = 0 returns to phase-synchronous launches.  AKMC_ERR_INVALID for serial or
+ * multi-rank handles or the legacy loop; a capacity overflow during a sweep (more than 64 vacancies entering one
+ * tile in a sweep) makes that akmc_step return AKMC_ERR_RUNTIME.                                              */
+int akmc_set_dataflow(akmc_handle* h, int32_t on);
+
 /* Multi-rank exchange statistics (C5): out3[0] = per-phase exchanges done, out3[1] = messages this
  * rank sent (direct exchange: one per distinct peer and phase; AKMC_EXCHANGE=shift: the paper's shift
  * communication, P:420-427, 2 per decomposed axis -- 1 when two ranks share the axis), out3[2] = bytes sent.  */

@@ -74,6 +74,7 @@ def load() -> C.CDLL:
     lib.akmc_set_world_model.argtypes = [P, P, C.c_int32, C.c_double]
     lib.akmc_voxel_order.argtypes = [P, P]
     lib.akmc_exchange_stats.argtypes = [P, P]
+    lib.akmc_set_dataflow.argtypes = [P, C.c_int32]
     lib.akmc_mfpt_solve.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_int32, P, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double)]
     lib.akmc_restore.argtypes = [P, P, C.c_int64, P, P, C.c_int64]
@@ -86,7 +87,7 @@ def load() -> C.CDLL:
               "akmc_set_profiling", "akmc_vacancies", "akmc_nccl_unique_id", "akmc_debug_extended",
               "akmc_set_voxel_temperatures", "akmc_run_until", "akmc_debug_math", "akmc_progress", "akmc_restore",
               "akmc_set_world_model", "akmc_mfpt_solve", "akmc_voxel_order",
-              "akmc_exchange_stats"):
+              "akmc_exchange_stats", "akmc_set_dataflow"):
         getattr(lib, n).restype = C.c_int
     _lib = lib
     return lib
@@ -226,6 +227,10 @@ class Simulation:
         t = np.ascontiguousarray(tnet, dtype=np.float64)
         self._tnet = t
         self._check(self.lib.akmc_set_world_model(self.h, _ptr(t), int(hidden), float(tau_act)))
+
+    def set_dataflow(self, on: bool = True):
+        """Dataflow sweeps (akmc_set_dataflow): tiles start a phase when their neighbours finished the previous one."""
+        self._check(self.lib.akmc_set_dataflow(self.h, 1 if on else 0))
 
     def exchange_stats(self) -> dict:
         """Multi-rank: per-phase exchanges, messages and bytes this rank sent."""

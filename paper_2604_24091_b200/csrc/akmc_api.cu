@@ -153,6 +153,15 @@ struct akmc_handle {
     std::vector<float> b2h;
     bool bulk = true;                 // FP32 batches through the bulk evaluator (AKMC_EVAL_ENGINE=1: cluster evaluator)
     bool have_pair = false;           // eps / E0 given at init (pair tables valid)
+    // dataflow sweep (f1; akmc_set_dataflow; akmc_engine.cu): one engine launch per sweep, tile readiness
+    bool df = false;
+    int df_tdom[3] = {1, 1, 1}, df_NT[3] = {1, 1, 1}, df_ntiles = 0, df_ring_cap = 8192, df_grid = 0;
+    long long* d_done_phase = nullptr;
+    int *d_tile_off = nullptr, *d_tile_cnt = nullptr, *d_tile_cur = nullptr, *d_tile_mem = nullptr;
+    int *d_arr_cnt = nullptr, *d_arr_slot = nullptr, *d_ring_slot = nullptr, *d_df_iscratch = nullptr, *d_df_err = nullptr;
+    int4* d_ring_pos = nullptr;
+    unsigned long long* d_ring_key = nullptr;
+    double* d_df_scratch = nullptr;
     // dynamic voxel scheduling (Eq. 10): per-voxel species counts and the segment dispatch order
     std::vector<unsigned long long> comp;   // [nvox][8]
     std::vector<int> vorder;                // voxel ids in dispatch order (descending W_v, stable)
@@ -295,6 +304,11 @@ void free_all(akmc_handle* h)
         if (h->ipc_box[r]) cudaIpcCloseMemHandle(h->ipc_box[r]);
         if (h->ipc_flag[r]) cudaIpcCloseMemHandle(h->ipc_flag[r]);
     }
+    void* dfptrs[] = {h->d_done_phase, h->d_tile_off, h->d_tile_cnt, h->d_tile_cur, h->d_tile_mem, h->d_arr_cnt,
+                      h->d_arr_slot, h->d_ring_slot, h->d_df_iscratch, h->d_df_err, h->d_ring_pos, h->d_ring_key,
+                      h->d_df_scratch};
+    for (void* p : dfptrs)
+        if (p) cudaFree(p);
     void* dptrs[] = {h->d_slist, h->d_nslist, h->d_free, h->d_fcnt, h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
                      h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone};
     for (void* p : dptrs)
@@ -1261,6 +1275,26 @@ static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_
                                                         nv, h->hot_events);
 }
 
+// dataflow sweep (f1): tile base lists, then ONE engine launch that runs all 8 phases of the sweep, every tile
+// starting a phase as soon as its 27 neighbour tiles finished the previous one (akmc_engine.cu)
+static int enqueue_df_sweep(akmc_handle* h, cudaStream_t s)
+{
+    EngineParams p = engine_params(h, kEnginePhase);
+    p.ph = h->d_phase;
+    p.df = 1;
+    p.ntiles = h->df_ntiles;
+    for (int a = 0; a < 3; ++a) { p.tdom[a] = h->df_tdom[a]; p.NT[a] = h->df_NT[a]; }
+    p.done_phase = h->d_done_phase; p.tile_off = h->d_tile_off; p.tile_mem = h->d_tile_mem;
+    p.arr_cnt = h->d_arr_cnt; p.arr_slot = h->d_arr_slot;
+    p.ring_cap = h->df_ring_cap; p.ring_slot = h->d_ring_slot; p.ring_pos = h->d_ring_pos; p.ring_key = h->d_ring_key;
+    p.members = h->d_ring_slot; p.mpos = h->d_ring_pos;          // segment members live in the per-CTA rings
+    p.scratch = h->d_df_scratch; p.iscratch = h->d_df_iscratch;  // trees of > 16 members, by ring index
+    p.df_err = h->d_df_err;
+    CK(h, launch_df_prep(p, h->d_vac, h->vcap, h->d_tile_cnt, h->d_tile_off, h->d_tile_cur, h->d_tile_mem, s));
+    CK(h, launch_engine(p, h->tc, h->n_clusters, h->num_sms, s));
+    return AKMC_OK;
+}
+
 // the whole phase on the device: activate + segments, then the persistent phase engine runs every domain
 // of the phase to the end of its window (a2-a8 without any grid-wide synchronisation)
 static int enqueue_phase_engine(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s)
@@ -1319,6 +1353,11 @@ static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGra
     };
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return done(fail(h, AKMC_ERR_CUDA, "graph capture begin failed"));
+    if (h->df) {
+        rc = enqueue_df_sweep(h, cs);
+        launches += 5;
+        q0 = q1;                                     // (all phases are in the one engine launch)
+    }
     for (int q = q0; q < q1 && rc == AKMC_OK; ++q) {
         const PhaseInfo* ph = h->d_phase + q;
         if (h->engine) {
@@ -1483,6 +1522,24 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
         h->total.kernel_launches += 1;
         for (int q = 0; q < 8; ++q) {
             const PhaseInfo* ph = h->d_phase + q;
+            if (h->df) {
+                if (q > 0) continue;
+                if (h->ev_used + 2 > h->ev.size())
+                    for (int i = 0; i < 64; ++i) {
+                        cudaEvent_t e;
+                        CK(h, cudaEventCreate(&e));
+                        h->ev.push_back(e);
+                    }
+                cudaEvent_t e0 = h->ev[h->ev_used++], e1 = h->ev[h->ev_used++];
+                CK(h, cudaEventRecord(e0, h->stream));
+                const int rc = enqueue_df_sweep(h, h->stream);
+                if (rc != AKMC_OK) return rc;
+                watchdog_wait(h, "dataflow sweep");
+                CK(h, cudaEventRecord(e1, h->stream));
+                h->total.kernel_launches += 5;
+                h->total.mlp_launches += 1;
+                continue;
+            }
             if (h->engine) {
                 cudaEvent_t e0 = nullptr, e1 = nullptr;
                 if (h->ev_used + 2 > h->ev.size()) {
@@ -1635,6 +1692,15 @@ static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horiz
     }
     rc = check_overflow(h, "akmc_step");
     if (rc != AKMC_OK) return rc;
+    if (h->df) {
+        int e = 0;
+        CK(h, cudaMemcpy(&e, h->d_df_err, sizeof(int), cudaMemcpyDeviceToHost));
+        if (e) {
+            CK(h, cudaMemset(h->d_df_err, 0, sizeof(int)));
+            return fail(h, AKMC_ERR_RUNTIME, "dataflow sweep: tile arrival / activation ring capacity exceeded (" +
+                                                 std::to_string(e) + "); the results of this call are invalid");
+        }
+    }
     if (h->multi) {
         int ovf = 0;
         CK(h, cudaMemcpy(&ovf, h->d_dist_overflow, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1759,6 +1825,52 @@ int akmc_set_world_model(akmc_handle* h, const double* tnet, int32_t hidden, dou
     h->world_H = hidden;
     h->world_tau = tau_act;
     h->world = true;
+    return AKMC_OK;
+}
+
+int akmc_set_dataflow(akmc_handle* h, int32_t on)
+{
+    if (!h) return AKMC_ERR_RUNTIME;
+    if (on && (!h->sub || h->multi || !h->engine))
+        return fail(h, AKMC_ERR_INVALID, "dataflow sweeps: single-rank sublattice handles on the phase engine only");
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->sweep_exec) { cudaGraphExecDestroy(h->sweep_exec); h->sweep_exec = nullptr; }
+    if (!on) { h->df = false; return AKMC_OK; }
+    if (!h->d_done_phase) {
+        // tiles of tdom^3 domains: grow the tile edge until every CTA of the persistent grid holds <= kMyTiles tiles
+        const int grid = h->tc ? kClusterN * h->n_clusters : h->num_sms;
+        int td[3] = {1, 1, 1}, NT[3];
+        long long nt = 0;
+        for (;;) {
+            for (int a = 0; a < 3; ++a) NT[a] = (h->S.ND[a] + td[a] - 1) / td[a];
+            nt = (long long)NT[0] * NT[1] * NT[2] * h->nvox;
+            if (nt <= (long long)kMyTiles * grid) break;
+            int a = 0;
+            for (int b = 1; b < 3; ++b) if (NT[b] > NT[a]) a = b;
+            if (td[a] >= h->S.ND[a]) return fail(h, AKMC_ERR_INVALID, "dataflow sweeps: too many voxels for the tile capacity");
+            td[a] *= 2;
+        }
+        for (int a = 0; a < 3; ++a) { h->df_tdom[a] = td[a]; h->df_NT[a] = NT[a]; }
+        h->df_ntiles = (int)nt;
+        h->df_grid = grid;
+        const size_t ring = (size_t)grid * h->df_ring_cap;
+        CK(h, cudaMalloc(&h->d_done_phase, nt * sizeof(long long)));
+        CK(h, cudaMalloc(&h->d_tile_off, (nt + 1) * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_tile_cnt, nt * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_tile_cur, nt * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_tile_mem, (size_t)h->vcap * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_arr_cnt, nt * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_arr_slot, nt * kArrCap * sizeof(int)));
+        CK(h, cudaMemset(h->d_arr_slot, 0xFF, nt * kArrCap * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_ring_slot, ring * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_ring_pos, ring * sizeof(int4)));
+        CK(h, cudaMalloc(&h->d_ring_key, ring * sizeof(unsigned long long)));
+        CK(h, cudaMalloc(&h->d_df_scratch, (4 * ring + 64) * sizeof(double)));
+        CK(h, cudaMalloc(&h->d_df_iscratch, (ring + 16) * sizeof(int)));
+        CK(h, cudaMalloc(&h->d_df_err, sizeof(int)));
+        CK(h, cudaMemset(h->d_df_err, 0, sizeof(int)));
+    }
+    h->df = true;
     return AKMC_OK;
 }
 
@@ -1952,6 +2064,9 @@ void akmc_free(akmc_handle* h)
                          " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
                          d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);
             if (d[29]) std::fprintf(stderr, "[akmc engine] memo-hit chain: %llu events of %llu checks (%.1f per CTA-launch)\n", d[29], d[30], d[29] / n);
+            if (d[56] + d[57] + d[58])
+                std::fprintf(stderr, "[akmc engine] dataflow refill cycles/CTA: candidates %.0f readiness %.0f activation %.0f\n",
+                             d[56] / n, d[57] / n, d[58] / n);
             std::fprintf(stderr, "[akmc engine] L1 split: memo move %.0f layer 1 %.0f async fences + barrier %.0f\n",
                          d[20] / n, d[21] / n, d[22] / n);
             if (d[24] + d[25] + d[26] + d[27])

@@ -100,7 +100,17 @@ struct Ctl {
     uint8_t row_hit[kRowCap];
     uint8_t row_way[kRowCap];       // memo way that holds the row's current rates (read by the selection)
     unsigned long long events, evals, mrows, clamps;
+    // dataflow sweep (p.df): phase (0..7) and my-tile index of each slot / candidate; my tiles' progress
+    uint8_t seg_q[kSlots], seg_tp[kSlots];
+    uint8_t cand_q[2 * kSlots], cand_tp[2 * kSlots];
+    int df_tile[kMyTiles];
+    int df_left[kMyTiles];          // domains of the tile's current phase still running
+    uint8_t df_np[kMyTiles];        // next phase to activate (8 = sweep done for this tile)
+    uint8_t df_ready[kMyTiles];
+    uint8_t df_cand[kMyTiles];
+    int df_ntiles, df_done_all, df_ring_head, df_nready;
 };
+constexpr int kDfCand = 16;         // dataflow: tiles tested for readiness per refill
 
 // shared-memory carve-up (offsets from a 1024-aligned base)
 constexpr uint32_t kOffA = 0;                                        // h1 hi [0,64K) lo [64K,128K); FP64 scratch
@@ -121,7 +131,11 @@ constexpr int kNumBars = 4;                                          // req, par
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemUsed = kOffTmem + 16;
 constexpr uint32_t kSmemTotal = kSmemUsed + 128;                     // 128-B alignment slack (no-swizzle layouts)
-static_assert(kSmemTotal <= 232448, "shared memory budget");
+template <int N> struct SmemIs; static_assert(kSmemTotal <= 232448, "shared memory budget");
+#ifdef AKMC_PRINT_SMEM
+SmemIs<kSmemTotal> smem_is;
+SmemIs<(int)sizeof(Ctl)> ctl_is;
+#endif
 static_assert(kTileRows * 8 * 8 <= (kRoundRows / 8) * kRowGroupA,
               "layer-3 partials (and the pair scratch) fit in the CTA's own row block of A (hi / lo)");
 static_assert(kOffHdr % 16 == 0 && kOffPart % 16 == 0 && kOffW2 % 16 == 0 && kOffW3 % 16 == 0, "bulk alignment");
@@ -192,6 +206,288 @@ __device__ __forceinline__ void prefetch_vacancy(const uint8_t* species, const F
     prefetch_l2(m); prefetch_l2(m + 128); prefetch_l2(m + 256);
 }
 
+// ---------------------------------------------------------------- dataflow sweep helpers (f1)
+// The synchronous sweep (reading A19) runs phase q of every domain after phase q-1 of every domain.  Domain (d, q)
+// reads the lattice within 2.5 cells of its sector and writes within 0.5 cell; both lie inside d and its 26
+// neighbour domains, and a domain's phase-q sector is >= 3 cells from any other domain's phase-q sector (A20).
+// So (d, q) sees exactly the synchronous state as soon as d and its 26 neighbours have finished phase q-1, and it
+// can disturb nothing a neighbour still has to read in phase q-1 (they are done).  Tiles of tdom^3 domains carry
+// that readiness (a tile's 27 neighbour tiles contain every neighbour of its domains): tile T starts phase q once
+// the 27 tiles around it have published done_phase >= q-1 -- the paper's per-sublattice readiness signals
+// (P:405-418), here between tiles of one GPU.  Trajectories are those of the synchronous sweep, bit for bit.
+__device__ __forceinline__ long long ld_acquire_gpu_s64(const long long* ptr)
+{
+    long long v;
+    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_s64(long long* ptr, long long v)
+{
+    asm volatile("st.release.gpu.global.s64 [%0], %1;" :: "l"(ptr), "l"(v) : "memory");
+}
+__device__ __forceinline__ int df_tile_of(const EngineParams& p, long long d)
+{
+    const long long v = d / p.S.ndom_vox;
+    long long r = d - v * p.S.ndom_vox;
+    const int dx = (int)(r % p.S.ND[0]);
+    r /= p.S.ND[0];
+    const int dy = (int)(r % p.S.ND[1]), dz = (int)(r / p.S.ND[1]);
+    const int ntv = p.NT[0] * p.NT[1] * p.NT[2];
+    return (int)v * ntv + dx / p.tdom[0] + p.NT[0] * (dy / p.tdom[1] + p.NT[1] * (dz / p.tdom[2]));
+}
+__device__ __forceinline__ int df_neighbour(const EngineParams& p, int T, int n)
+{
+    const int ntv = p.NT[0] * p.NT[1] * p.NT[2];
+    const int v = T / ntv, r = T - v * ntv;
+    int t[3] = {r % p.NT[0], (r / p.NT[0]) % p.NT[1], r / (p.NT[0] * p.NT[1])};
+    const int dd[3] = {n % 3 - 1, (n / 3) % 3 - 1, n / 9 - 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) t[a] = (t[a] + dd[a] + p.NT[a]) % p.NT[a];
+    return v * ntv + t[0] + p.NT[0] * (t[1] + p.NT[1] * t[2]);
+}
+// warp bitonic sort of up to 64 keys (2 per lane: lane l holds keys l and l + 32), ascending
+__device__ __forceinline__ void warp_sort64(unsigned long long& a, unsigned long long& b)
+{
+    const int lane = threadIdx.x & 31;
+    // element index e: a -> lane, b -> lane + 32
+    for (int k = 2; k <= 64; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                // partners are a <-> b of the same lane
+                const bool up = ((lane & k) == 0);
+                const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+                a = up ? lo : hi; b = up ? hi : lo;
+            } else {
+                const unsigned long long pa = __shfl_xor_sync(0xffffffffu, a, j);
+                const unsigned long long pb = __shfl_xor_sync(0xffffffffu, b, j);
+                const bool lower = (lane & j) == 0;
+                const bool upa = ((lane & k) == 0), upb = (((lane + 32) & k) == 0);
+                a = (lower == upa) ? (a < pa ? a : pa) : (a < pa ? pa : a);
+                b = (lower == upb) ? (b < pb ? b : pb) : (b < pb ? pb : b);
+            }
+        }
+    }
+}
+
+// the general (slow) activation: any number of vacancies in the set; keys sorted in the ring by lane 0
+__device__ __noinline__ void df_activate_slow(const EngineParams& p, Ctl& c, int i)
+{
+    const int lane = threadIdx.x & 31;
+    {
+    const int T = c.df_tile[i], q = c.df_np[i];
+    const int sector = p.ph[q].sector;
+    const long long phase = p.ph[q].phase;
+    const int b0 = p.tile_off[T], nb = p.tile_off[T + 1] - b0;
+    const int na = min(*(volatile int*)(p.arr_cnt + T), kArrCap);
+    // pass 1: count the vacancies now in (tile T, sector of phase q)
+    auto keep = [&](int e, int& slot, long long& d) -> bool {
+        slot = e < nb ? p.tile_mem[b0 + e] : *(volatile int*)(p.arr_slot + (size_t)T * kArrCap + (e - nb));
+        if (slot < 0) return false;
+        const int4 v = __ldcv(p.vac + slot);
+        if (v.x < 0) return false;
+        int sec = 0;
+        dom_sector(v, p.S, d, sec);
+        return sec == sector && df_tile_of(p, d) == T;
+    };
+    int n = 0;
+    for (int e0 = 0; e0 < nb + na; e0 += 32) {
+        int slot; long long d;
+        const bool k = (e0 + lane < nb + na) && keep(e0 + lane, slot, d);
+        n += __popc(__ballot_sync(0xffffffffu, k));
+    }
+    int r0 = 0;
+    if (lane == 0) r0 = atomicAdd(&c.df_ring_head, n);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+    const size_t rb = (size_t)blockIdx.x * p.ring_cap;
+    bool ok = r0 + n <= p.ring_cap;
+    if (!ok && lane == 0) atomicAdd(p.df_err, 1);
+    if (ok) {
+        // pass 2: keys (domain << 32 | slot) into the ring
+        int w = 0;
+        for (int e0 = 0; e0 < nb + na; e0 += 32) {
+            int slot = 0; long long d = 0;
+            const bool k = (e0 + lane < nb + na) && keep(e0 + lane, slot, d);
+            const unsigned bm = __ballot_sync(0xffffffffu, k);
+            if (k) p.ring_key[rb + r0 + w + __popc(bm & lanemask_lt())] =
+                ((unsigned long long)d << 32) | (unsigned long long)(unsigned)slot;
+            w += __popc(bm);
+        }
+        __syncwarp();
+        // sort by (domain, slot): the synchronous order of a competing set (A17)
+        if (n <= 64) {
+            unsigned long long ka = lane < n ? p.ring_key[rb + r0 + lane] : ~0ull;
+            unsigned long long kb = lane + 32 < n ? p.ring_key[rb + r0 + lane + 32] : ~0ull;
+            warp_sort64(ka, kb);
+            if (lane < n) p.ring_key[rb + r0 + lane] = ka;
+            if (lane + 32 < n) p.ring_key[rb + r0 + lane + 32] = kb;
+        } else if (lane == 0) {
+            unsigned long long* kk = p.ring_key + rb + r0;
+            for (int x = 1; x < n; ++x) {
+                const unsigned long long v = kk[x];
+                int y = x - 1;
+                while (y >= 0 && kk[y] > v) { kk[y + 1] = kk[y]; --y; }
+                kk[y + 1] = v;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // distinct entries (a vacancy can be listed twice: base list and arrivals) -> members,
+            // runs of one domain -> candidate segments
+            const unsigned long long* kk = p.ring_key + rb + r0;
+            int nseg = 0, m = 0;
+            unsigned long long prev = ~0ull;
+            long long pd = -1;
+            for (int x = 0; x < n; ++x) {
+                if (kk[x] == prev) continue;
+                prev = kk[x];
+                const long long d = (long long)(kk[x] >> 32);
+                if (d != pd) { ++nseg; pd = d; }
+                ++m;
+            }
+            const int cq = atomicAdd(&c.nnew, nseg);
+            if (cq + nseg > 2 * kSlots) {
+                atomicSub(&c.nnew, nseg);          // no room: the tile stays ready for a later refill
+            } else {
+                int sidx = cq - 1, mi = 0;
+                prev = ~0ull; pd = -1;
+                for (int x = 0; x < n; ++x) {
+                    if (kk[x] == prev) continue;
+                    prev = kk[x];
+                    const long long d = (long long)(kk[x] >> 32);
+                    const int slot = (int)(unsigned)(kk[x] & 0xFFFFFFFFull);
+                    if (d != pd) {
+                        ++sidx; pd = d;
+                        c.cand_dom[sidx] = (unsigned)d;
+                        c.cand_off[sidx] = (int)(rb + r0 + mi);
+                        c.cand_cnt[sidx] = 0;
+                        c.cand_q[sidx] = (uint8_t)q;
+                        c.cand_tp[sidx] = (uint8_t)i;
+                    }
+                    p.ring_slot[rb + r0 + mi] = slot;
+                    p.ring_pos[rb + r0 + mi] = __ldcv(p.vac + slot);
+                    c.cand_cnt[sidx] += 1;
+                    ++mi;
+                }
+                c.df_np[i] = (uint8_t)(q + 1);
+                c.df_left[i] = nseg;
+                if (nseg == 0) st_release_gpu_s64(p.done_phase + T, phase);   // empty: done at once
+            }
+        }
+    }
+                    }
+}
+
+// Activation of my tile i for its next phase (one warp): the vacancies now in (tile, sector of that phase) --
+// the tile's sweep-start members plus the vacancies that entered it -- sorted by (domain, slot), duplicates
+// dropped, one candidate segment per domain (the synchronous phase's competing sets, A17), members and their
+// positions into this CTA's ring.  All loads of up to 256 entries in flight at once; sort and segmentation in
+// registers (<= 64 entries; a larger set takes df_activate_slow).
+__device__ __forceinline__ void df_activate(const EngineParams& p, Ctl& c, int i)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int T = c.df_tile[i], q = c.df_np[i];
+    const int sector = p.ph[q].sector;
+    const long long phase = p.ph[q].phase;
+    const int b0 = p.tile_off[T], nb = p.tile_off[T + 1] - b0;
+    const int na = min(__ldcv(p.arr_cnt + T), kArrCap);
+    const int ntot = nb + na;
+    unsigned long long ka = ~0ull, kb = ~0ull;
+    int n = 0;
+    constexpr int kU = 8;
+    for (int e0 = 0; e0 < ntot; e0 += 32 * kU) {
+        int sl[kU];
+        int4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int e = e0 + 32 * u + lane;
+            sl[u] = e < nb ? p.tile_mem[b0 + e] : (e < ntot ? __ldcv(p.arr_slot + (size_t)T * kArrCap + (e - nb)) : -1);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = sl[u] >= 0 ? __ldcv(p.vac + sl[u]) : make_int4(-1, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            bool k = false;
+            unsigned long long key = 0;
+            if (v[u].x >= 0) {
+                long long d;
+                int sec;
+                dom_sector(v[u], p.S, d, sec);
+                k = sec == sector && df_tile_of(p, d) == T;
+                key = ((unsigned long long)d << 32) | (unsigned long long)(unsigned)sl[u];
+            }
+            const unsigned m = __ballot_sync(full, k);
+            const int ck = __popc(m);
+            if (n + ck <= 64) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pos = lane + 32 * h - n;
+                    const bool mine = pos >= 0 && pos < ck;
+                    const unsigned long long got = __shfl_sync(full, key, mine ? (int)__fns(m, 0, pos + 1) : 0);
+                    if (mine) { if (h == 0) ka = got; else kb = got; }
+                }
+            }
+            n += ck;
+        }
+    }
+    if (n > 64) { df_activate_slow(p, c, i); return; }
+    warp_sort64(ka, kb);
+    const unsigned long long pa = __shfl_up_sync(full, ka, 1), pb0 = __shfl_up_sync(full, kb, 1);
+    const unsigned long long a31 = __shfl_sync(full, ka, 31);      // (every lane executes the shuffles)
+    const unsigned long long pb = lane == 0 ? a31 : pb0;
+    const bool va = lane < n, vb = lane + 32 < n;
+    const bool da = va && lane > 0 && ka == pa, db = vb && kb == pb;
+    const bool keepa = va && !da, keepb = vb && !db;
+    const bool newa = keepa && (lane == 0 || (ka >> 32) != (pa >> 32)), newb = keepb && ((kb >> 32) != (pb >> 32));
+    const unsigned lt = lanemask_lt();
+    const unsigned ma = __ballot_sync(full, keepa), mb = __ballot_sync(full, keepb);
+    const unsigned sa = __ballot_sync(full, newa), sb = __ballot_sync(full, newb);
+    const int mtot = __popc(ma) + __popc(mb), nseg = __popc(sa) + __popc(sb);
+    int r0 = 0, cq = 0, ok = 1;
+    if (lane == 0) {
+        r0 = atomicAdd(&c.df_ring_head, mtot);
+        if (r0 + mtot > p.ring_cap) { atomicAdd(p.df_err, 1); ok = 0; }
+        if (ok) {
+            cq = atomicAdd(&c.nnew, nseg);
+            if (cq + nseg > 2 * kSlots) { atomicSub(&c.nnew, nseg); ok = 0; }   // no room: stays ready for a later refill
+        }
+    }
+    ok = __shfl_sync(full, ok, 0);
+    if (!ok) return;
+    r0 = __shfl_sync(full, r0, 0);
+    cq = __shfl_sync(full, cq, 0);
+    const size_t rb = (size_t)blockIdx.x * p.ring_cap + r0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const bool kp = h ? keepb : keepa, nw = h ? newb : newa;
+        const unsigned long long key = h ? kb : ka;
+        const int mi = h ? __popc(ma) + __popc(mb & lt) : __popc(ma & lt);
+        const int si = h ? __popc(sa) + __popc(sb & lt) : __popc(sa & lt);
+        if (kp) {
+            const int slot = (int)(unsigned)(key & 0xFFFFFFFFull);
+            p.ring_slot[rb + mi] = slot;
+            p.ring_pos[rb + mi] = __ldcv(p.vac + slot);
+        }
+        if (nw) {
+            c.cand_dom[cq + si] = (unsigned)(key >> 32);
+            c.cand_off[cq + si] = (int)(rb + mi);
+            c.cand_q[cq + si] = (uint8_t)q;
+            c.cand_tp[cq + si] = (uint8_t)i;
+        }
+    }
+    __syncwarp();
+    for (int s2 = lane; s2 < nseg; s2 += 32) {
+        const int next = s2 + 1 < nseg ? c.cand_off[cq + s2 + 1] : (int)(rb + mtot);
+        c.cand_cnt[cq + s2] = next - c.cand_off[cq + s2];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        c.df_np[i] = (uint8_t)(q + 1);
+        c.df_left[i] = nseg;
+        if (nseg == 0) st_release_gpu_s64(p.done_phase + T, phase);       // empty: done at once
+    }
+}
+
 template <bool kTC, bool kFast = false>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p)
 {
@@ -246,7 +542,19 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             mbar_fence_init();
         }
     }
-    if (tid < kSlots) { c.seg_used[tid] = 0; c.seg_run[tid] = 0; c.seg_new[tid] = 0; c.seg_head[tid] = 0; }
+    if (tid < kSlots) { c.seg_used[tid] = 0; c.seg_run[tid] = 0; c.seg_new[tid] = 0; c.seg_head[tid] = 0; c.seg_q[tid] = 0; }
+    if (p.df) {
+        if (tid < kMyTiles) {
+            const int T = (int)blockIdx.x + tid * (int)gridDim.x;
+            c.df_tile[tid] = T < p.ntiles ? T : -1;
+            c.df_np[tid] = T < p.ntiles ? 0 : 8;
+            c.df_left[tid] = 0;
+        }
+        if (tid == 0) {
+            c.df_ntiles = min(kMyTiles, max(0, (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x));
+            c.df_done_all = c.df_ntiles == 0;
+        }
+    }
     if (tid < kRowCap) c.mem_act[tid] = 0;
     uint32_t tmem = 0;
     uint32_t ph_req = 0, ph_part = 0, ph_mma = 0;
@@ -275,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     long long d_y[4] = {0, 0, 0, 0};              // L1 lap split: memo move | layer 1 | async fences + barrier
     long long d_z[4] = {0, 0, 0, 0};              // AKMC_L1_PROBE: layer-1 sub-steps of warp 0
     long long d_xk = 0;                            // exchange wait of rounds k > 0 (no control before them)
+    long long d_df[4] = {0, 0, 0, 0};              // dataflow refill: candidates, readiness, activation, placement
     const long long t_start = clock64();
     unsigned long long my_events = 0, my_evals = 0, my_clamps = 0;   // selection counters (slot threads)
     unsigned long long my_chain = 0, my_check = 0;                    // memo-hit chain: events taken, checks
@@ -353,7 +662,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 // must not pile up in a handful of CTAs)
                 const int share = max(1, (c.ntot + (int)gridDim.x - 1) / (int)gridDim.x);
                 const int claim = min(nfree, share);
-                if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
+                if (p.df) {
+                    c.fetch = (!c.df_done_all && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) ? 2 : 0;
+                    c.df_ring_head = 0;
+                    c.df_nready = 0;
+                } else if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
                     const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)claim);
                     if (s0 >= c.ntot) {
                         c.drained = 1;
@@ -364,11 +677,60 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 }
             }
             __syncthreads();
-            if (c.fetch && tid < c.nnew) {
+            if (c.fetch == 2) {
+                long long tdf = clock64();
+                // ---- dataflow activation: which of my tiles may start their next phase, then one tile per warp
+                // candidates: tiles whose previous phase is done, lowest next phase first, at most kDfCand per refill
+                static_assert(kMyTiles == 32, "one warp ballots over my tiles");
+                if (warp == 0) {
+                    const int i = lane;
+                    const bool el = i < c.df_ntiles && c.df_np[i] < 8 && c.df_left[i] == 0;
+                    const int nq = el ? c.df_np[i] : 8;
+                    int nc = 0, mine = -1;
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const unsigned m = __ballot_sync(0xffffffffu, nq == qq);
+                        if (nq == qq) mine = nc + __popc(m & lanemask_lt());
+                        nc += __popc(m);
+                    }
+                    const bool take = mine >= 0 && mine < kDfCand;
+                    c.df_ready[i] = take ? 1 : 0;
+                    if (take) c.df_cand[mine] = (uint8_t)i;
+                    if (lane == 0) c.df_nready = min(nc, kDfCand);
+                }
+                __syncthreads();
+                if (tid == 0) { const long long t = clock64(); d_df[0] += t - tdf; tdf = t; }
+                // readiness: 27 neighbour tiles' done_phase (relaxed loads, all in flight; one acquire fence after)
+                for (int t = tid; t < c.df_nready * 27; t += kThreads) {
+                    const int i = c.df_cand[t / 27], n = t % 27;
+                    const long long need = p.ph[0].phase + (long long)c.df_np[i] - 1;
+                    if (__ldcv(p.done_phase + df_neighbour(p, c.df_tile[i], n)) < need) c.df_ready[i] = 0;
+                }
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) { const long long t = clock64(); d_df[1] += t - tdf; tdf = t; }
+                {
+                    // warp w activates the w-th ready tile
+                    int cnt = 0, pick = -1;
+                    for (int i = 0; i < c.df_ntiles; ++i)
+                        if (c.df_ready[i]) { if (cnt == warp) pick = i; ++cnt; }
+                    if (pick >= 0) df_activate(p, c, pick);
+                }
+                __syncthreads();
+                if (tid == 0) { const long long t = clock64(); d_df[2] += t - tdf; tdf = t; }
+                if (tid == 0) {
+                    int all = 1;
+                    for (int i = 0; i < c.df_ntiles; ++i) all &= (c.df_np[i] >= 8) ? 1 : 0;
+                    c.df_done_all = all;
+                    c.fetch = c.nnew > 0 ? 1 : 0;
+                    if (c.fetch) ++d_refill;
+                }
+            }
+            if (c.fetch == 1 && !p.df && tid < c.nnew) {
                 const int si = c.s0 + tid;
                 const Segment sg = p.segs[(c.nhot < 0 || si < c.nhot) ? si : p.seg_cap - 1 - (si - c.nhot)];
                 const int q = c.npend + tid;
                 c.cand_dom[q] = (unsigned)sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
+                c.cand_q[q] = 0; c.cand_tp[q] = 0;                        // (one phase per launch: p.ph[0])
             }
             __syncthreads();
             const int ncand = c.npend + c.nnew;     // block-uniform (shared, after a barrier)
@@ -442,11 +804,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     // carried-over domains are compacted in place to the front of the candidate list (read first)
                     unsigned cdom = 0;
                     int coff = 0, ccnt = 0, cslot = -3;
-                    if (q < ncand) { cdom = c.cand_dom[q]; coff = c.cand_off[q]; ccnt = c.cand_cnt[q]; cslot = c.cand_slot[q]; }
+                    uint8_t cq = 0, ctp = 0;
+                    if (q < ncand) {
+                        cdom = c.cand_dom[q]; coff = c.cand_off[q]; ccnt = c.cand_cnt[q]; cslot = c.cand_slot[q];
+                        cq = c.cand_q[q]; ctp = c.cand_tp[q];
+                    }
                     __syncthreads();
-                    if (deferred) { c.cand_dom[pi] = cdom; c.cand_off[pi] = coff; c.cand_cnt[pi] = ccnt; }
+                    if (deferred) { c.cand_dom[pi] = cdom; c.cand_off[pi] = coff; c.cand_cnt[pi] = ccnt; c.cand_q[pi] = cq; c.cand_tp[pi] = ctp; }
                     if (cslot >= 0) {
                         const int h = cslot;
+                        c.seg_q[h] = cq; c.seg_tp[h] = ctp;
                         c.seg_used[h] = 1;
                         c.seg_dom[h] = cdom; c.seg_goff[h] = coff; c.seg_cnt[h] = ccnt;
                         // serial mode: seg_t IS the voxel clock for the launch (same sums as p.clock += dt, no
@@ -488,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             if (tid == 0) lap(d_x[0]);
-            own_alive = c.nrun > 0 ? 1 : 0;
+            own_alive = (c.nrun > 0 || (p.df && (!c.df_done_all || c.npend > 0))) ? 1 : 0;
             // ================= rows = active members of running domains, in slot/member order =================
             int total = 0;
             {
@@ -1014,7 +1381,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         dt = __ddiv_rn(-det_log(u_t), Rc);
                         go = !(p.horizon && __dadd_rn(AKMC_SERIAL_CLOCK ? c.seg_t[i] : p.clock[c.seg_dom[i]], dt) > p.t_end);
                     } else {
-                        const unsigned long long ph = (unsigned long long)p.ph->phase;
+                        const unsigned long long ph = (unsigned long long)p.ph[c.seg_q[i]].phase;
                         philox_uniforms(p.S.seed, make_uint4(c.seg_it[i], (uint32_t)c.seg_dom[i], (uint32_t)ph, (uint32_t)(ph >> 32)),
                                         u_sel, u_t);
                         dt = __ddiv_rn(-det_log(u_t), Rc);
@@ -1048,7 +1415,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         long long d2 = 0;
                         int sec2 = 0;
                         if (!p.serial) dom_sector(nv, p.S, d2, sec2);
-                        if (!p.serial && (d2 != (long long)c.seg_dom[i] || sec2 != p.ph->sector)) c.mem_act[moff + a] = 0;
+                        if (!p.serial && (d2 != (long long)c.seg_dom[i] || sec2 != p.ph[c.seg_q[i]].sector)) c.mem_act[moff + a] = 0;
+                        if (p.df) {
+                            // a vacancy entering another tile is announced to it (read at that tile's next activation)
+                            const int Tn = df_tile_of(p, d2);
+                            if (Tn != df_tile_of(p, (long long)c.seg_dom[i])) {
+                                const int k2 = atomicAdd(p.arr_cnt + Tn, 1);
+                                if (k2 < kArrCap) p.arr_slot[(size_t)Tn * kArrCap + k2] = slot;
+                                else atomicAdd(p.df_err, 1);
+                            }
+                        }
                         if (p.S.log) {
                             if (near_face(p.F, ov.y, ov.z, ov.w))
                                 log_entry(p.S.log, p.S.nlog, p.S.logcap, ov.y, ov.z, ov.w, tn);
@@ -1126,7 +1502,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     }
                 }
             }
-            if (stop) c.seg_run[i] = 0;
+            if (stop) {
+                c.seg_run[i] = 0;
+                if (p.df && atomicSub(&c.df_left[c.seg_tp[i]], 1) == 1)    // the tile's phase is complete
+                    st_release_gpu_s64(p.done_phase + c.df_tile[c.seg_tp[i]], p.ph[c.seg_q[i]].phase);
+            }
         }
         __syncthreads();
         if (tid == 0) lap(d_cs);
@@ -1152,6 +1532,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         for (int q = 0; q < 3; ++q) atomicAdd(p.diag + 20 + q, (unsigned long long)d_y[q]);
         for (int q = 0; q < 4; ++q) atomicAdd(p.diag + 24 + q, (unsigned long long)d_z[q]);
         atomicAdd(p.diag + 19, (unsigned long long)d_xk);
+        for (int q = 0; q < 4; ++q) atomicAdd(p.diag + 56 + q, (unsigned long long)d_df[q]);
     }
 
     // ---- teardown
@@ -1186,7 +1567,62 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
 }
 
+// ---- dataflow sweep preparation: every tile's vacancies at the start of the sweep (base lists), no arrivals yet,
+//      done_phase = the phase before the sweep's first
+__global__ void df_count_kernel(const int4* __restrict__ vac, int nv, EngineParams p, int* cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < p.ntiles) { p.arr_cnt[i] = 0; p.done_phase[i] = p.ph[0].phase - 1; }
+    if (i >= nv) return;
+    const int4 v = vac[i];
+    if (v.x < 0) return;
+    long long d; int sec;
+    dom_sector(v, p.S, d, sec);
+    atomicAdd(cnt + df_tile_of(p, d), 1);
+}
+__global__ void __launch_bounds__(1024) df_scan_kernel(const int* cnt, int n, int* off, int* cursor)
+{
+    // single block: exclusive scan of n counts (n <= a few 1e4)
+    __shared__ int part[1024];
+    const int per = (n + 1023) / 1024;
+    const int b = threadIdx.x * per;
+    int sum = 0;
+    for (int k = 0; k < per && b + k < n; ++k) sum += cnt[b + k];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int t = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += t;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - sum;
+    for (int k = 0; k < per && b + k < n; ++k) { off[b + k] = run; cursor[b + k] = run; run += cnt[b + k]; }
+    if (threadIdx.x == 1023) off[n] = part[1023];
+}
+__global__ void df_scatter_kernel(const int4* __restrict__ vac, int nv, EngineParams p, int* cursor, int* mem)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nv) return;
+    const int4 v = vac[i];
+    if (v.x < 0) return;
+    long long d; int sec;
+    dom_sector(v, p.S, d, sec);
+    mem[atomicAdd(cursor + df_tile_of(p, d), 1)] = i;
+}
+
 } // namespace
+
+cudaError_t launch_df_prep(const EngineParams& p, const int4* vac, int nv, int* cnt, int* off, int* cursor, int* mem,
+                           cudaStream_t s)
+{
+    cudaMemsetAsync(cnt, 0, (size_t)p.ntiles * sizeof(int), s);
+    const int n = std::max(nv, p.ntiles);
+    df_count_kernel<<<(n + 255) / 256, 256, 0, s>>>(vac, nv, p, cnt);
+    df_scan_kernel<<<1, 1024, 0, s>>>(cnt, p.ntiles, off, cursor);
+    df_scatter_kernel<<<(nv + 255) / 256, 256, 0, s>>>(vac, nv, p, cursor, mem);
+    return cudaGetLastError();
+}
 
 size_t engine_smem_bytes() { return kSmemTotal; }
 

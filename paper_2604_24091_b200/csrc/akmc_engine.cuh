@@ -21,6 +21,8 @@ constexpr int kSlots = 128;                    // domain slots per CTA (a domain
 constexpr int kSlotCap = 2;                    // vacancies per slot
 constexpr int kRowCap = kSlots * kSlotCap;     // vacancies a CTA holds at once (128)
 constexpr int kW1Rows = 1 + (kSpecies - 1) * kWin;   // b1' then W1'(s, slot) rows: 385
+constexpr int kMyTiles = 32;                   // dataflow: tiles per CTA (tiles are dealt round-robin)
+constexpr int kArrCap = 64;                    // dataflow: arrivals per tile and sweep
 
 // exact memo of the barrier network per vacancy slot (2 ways, most recent first)
 struct MemoEntry {
@@ -87,6 +89,22 @@ struct EngineParams {
     int seg_cap;            // phase: > 0 -> hot segments at segs[0, nhot), cold ones at segs[seg_cap-1-i]
     int horizon;            // serial: 1 -> a voxel also stops at its first draw with clock + dt > t_end
     double t_end;           //   (akmc_run_until; the draw is discarded, its counter not consumed)
+    // dataflow sweep (f1, P:405-418 readiness signals; single rank): one launch runs the 8 phases of a sweep; a
+    // tile of domains starts phase q once the 27 tiles around it have finished phase q-1 (akmc_engine.cu)
+    int df;                 // 1: dataflow sweep
+    int ntiles;             // tiles in all voxels
+    int tdom[3];            // domains per tile edge
+    int NT[3];              // tiles per axis per voxel
+    long long* done_phase;  // [ntiles] last finished global phase (release / acquire)
+    const int* tile_off;    // [ntiles + 1] base member offsets (vacancies in the tile at sweep start)
+    const int* tile_mem;    // base member slots
+    int* arr_cnt;           // [ntiles] vacancies that entered the tile during the sweep
+    int* arr_slot;          // [ntiles][kArrCap]
+    int ring_cap;           // per-CTA capacity of the activation ring (members / positions / keys)
+    int* ring_slot;         // [CTAs][ring_cap]
+    int4* ring_pos;
+    unsigned long long* ring_key;
+    int* df_err;            // capacity overflows (arrivals, ring) -> AKMC_ERR_RUNTIME
     unsigned long long* overflow;   // fp16 range clamps / capacity overflows (diagnostic, must stay 0)
     unsigned long long* diag;       // [16] optional timing/iteration diagnostics (AKMC_PHASE_TIMING)
     int* watch;             // optional [CTAs][8] progress words in mapped host memory (AKMC_WATCHDOG)
@@ -115,6 +133,9 @@ struct BulkParams {
 cudaError_t bulk_setup();
 cudaError_t launch_bulk(const BulkParams& p, int max_rows, int num_sms, cudaStream_t s);
 
+// dataflow sweep: base lists of the tiles (cnt / cursor scratch [ntiles], off [ntiles + 1], mem [vcap])
+cudaError_t launch_df_prep(const EngineParams& p, const int4* vac, int nv, int* cnt, int* off, int* cursor, int* mem,
+                           cudaStream_t s);
 size_t engine_smem_bytes();
 cudaError_t engine_setup();
 // clusters of 8 that can be co-resident (persistent grid); 0 on failure

@@ -28,7 +28,7 @@ using namespace ptx;
 
 constexpr uint32_t kRowGroupA = (kHid / 8) * 128;              // 4096 B: one 8-row group of h1 (K-major no-swizzle)
 constexpr float kLo = 2048.0f;                                 // fp16 lo parts carry the remainder * 2^11
-constexpr int kL1List = 6;                                     // W1' row indices kept per row (RPV: ~1.6)
+constexpr int kL1List = 4;                                     // W1' row indices kept per row (RPV: ~1.6; more -> window path)
 
 __device__ __forceinline__ uint32_t lanemask_lt()
 {

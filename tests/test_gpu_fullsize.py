@@ -60,8 +60,8 @@ def test_c5_fullsize_sweeps(akmc, orc):
     assert worst <= RTOL_FAST, worst
 
 
-@pytest.mark.parametrize("name,sweeps", [("c3", 2), ("c5", 1)])
-def test_fullsize_fp64_pair_bitexact(akmc, orc, name, sweeps):
+@pytest.mark.parametrize("name,sweeps,dataflow", [("c3", 2, False), ("c5", 1, False), ("c5", 1, True)])
+def test_fullsize_fp64_pair_bitexact(akmc, orc, name, sweeps, dataflow):
     import torch
     import bench
     eps, E0 = synth.illustrative_pair_params()
@@ -69,6 +69,8 @@ def test_fullsize_fp64_pair_bitexact(akmc, orc, name, sweeps):
     sp, keep = bench.make_inputs(name, 0, torch.device("cuda", 0))
     sp = np.ascontiguousarray(sp)
     with akmc.Simulation(cfg, sp, eps, E0) as sim:
+        if dataflow:
+            sim.set_dataflow(True)                   # f1: tile readiness instead of phase boundaries
         c = sim.step(sweeps)
         gsp, gvac, gclock, gctr = sim.state()
     del keep

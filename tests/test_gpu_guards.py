@@ -283,3 +283,71 @@ def test_voxel_dispatch_order_is_eq10(akmc):
         T = synth.voxel_temperatures(nvox, seed=3)
         sim.set_voxel_temperatures(T)
         assert np.array_equal(sim.voxel_order(), _eq10_order(sp, (L, L, L), nvox, E0, T))
+
+
+# ----------------------------------------------------------------------------- dataflow sweeps (f1)
+def _df_pair(akmc, cfg, sp, sweeps, eps=None, E0=None, mlp=None):
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        sim.step(sweeps)
+        sync = sim.state()
+    with akmc.Simulation(cfg, sp, eps, E0, mlp) as sim:
+        sim.set_dataflow(True)
+        half = sweeps // 2
+        sim.step(half)
+        sim.step(sweeps - half)
+        df = sim.state()
+    return sync, df
+
+
+@pytest.mark.parametrize("cells,domain,lam", [((32, 32, 32), (8, 8, 8), 1.0), ((48, 32, 40), (8, 8, 8), 0.25),
+                                              ((18, 24, 30), (6, 8, 10), 1.0)])
+def test_dataflow_sweep_bitexact_fp64(akmc, orc, cells, domain, lam):
+    """P:405-418 readiness signals (f1): tiles start a phase when the 27 tiles around them finished the previous
+    one; the FP64 trajectory equals the phase-synchronous one and the oracle's, bit for bit (anisotropic
+    geometry and ragged tiles included)."""
+    eps, E0 = synth.illustrative_pair_params()
+    sp = synth.make_lattice(cells, 1, synth.a508_atomic_fractions(), 80, seed=61)
+    cfg = akmc.Config(cells=cells, barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=7,
+                      domain_cells=domain, window_s=synth.window_seconds(lam, E0[0]))
+    sync, df = _df_pair(akmc, cfg, sp, 6, eps, E0)
+    assert df[3]["events"] > 50
+    for x, y in zip(sync[:3], df[:3]):
+        assert np.array_equal(x, y)
+    assert df[3]["events"] == sync[3]["events"] and df[3]["hop_evals"] == sync[3]["hop_evals"]
+    ocfg = orc.Config(cells=cells, model=0, domain=domain, window_s=cfg.window_s, seed=cfg.seed)
+    st = orc.State.from_species(ocfg, sp)
+    orc.run(ocfg, st, 6, eps, E0)
+    assert np.array_equal(df[0], st.species) and np.array_equal(df[1], st.vac) and np.array_equal(df[2], st.clock)
+
+
+def test_dataflow_sweep_fp32_crowded(akmc):
+    """FP32 tensor-core engine, crowded domains (multi-slot, > 16-member trees): dataflow == synchronous bits."""
+    eps, E0 = synth.illustrative_pair_params()
+    mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=5)
+    L = 32
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), 100, seed=77)
+    sp = _cluster(sp, L, (8, 8, 8), 4, 60, np.random.default_rng(78))
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_MLP, precision=akmc.PREC_FP32, seed=29,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(1.0, E0[0]))
+    sync, df = _df_pair(akmc, cfg, sp, 6, mlp=mlp)
+    assert df[3]["events"] > 50
+    for x, y in zip(sync[:3], df[:3]):
+        assert np.array_equal(x, y)
+
+
+def test_dataflow_sweep_crowded_tile_bitexact(akmc, orc):
+    """A tile-phase with more than 64 vacancies (90 packed into one 4^3-cell sector): the general activation
+    path; FP64 dataflow == synchronous == oracle."""
+    eps, E0 = synth.illustrative_pair_params()
+    L = 32
+    sp = synth.make_lattice((L, L, L), 1, synth.fe_cu_fractions(0.05), 80, seed=91)
+    sp = _cluster(sp, L, (16, 16, 16), 4, 90, np.random.default_rng(92))
+    cfg = akmc.Config(cells=(L, L, L), barrier_model=akmc.MODEL_PAIR, precision=akmc.PREC_FP64, seed=5,
+                      domain_cells=(8, 8, 8), window_s=synth.window_seconds(1.0, E0[0]))
+    sync, df = _df_pair(akmc, cfg, sp, 4, eps, E0)
+    for x, y in zip(sync[:3], df[:3]):
+        assert np.array_equal(x, y)
+    ocfg = orc.Config(cells=(L, L, L), model=0, domain=(8, 8, 8), window_s=cfg.window_s, seed=cfg.seed)
+    st = orc.State.from_species(ocfg, sp)
+    orc.run(ocfg, st, 4, eps, E0)
+    assert np.array_equal(df[0], st.species) and np.array_equal(df[1], st.vac)

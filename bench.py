@@ -35,7 +35,7 @@ UNIT = "hop-evals/s"
 FLOPS_PER_VAC = 2 * (256 * 256 + 256 * 8) + 64 * 256      # layers 2-3 FLOPs + layer-1 adds
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # DRAM bytes (read + write) per engine launch from the committed ncu --set full capture (profiles/)
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_engine_ncu.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_engine_ncu.json")
 
 
 def _traffic():

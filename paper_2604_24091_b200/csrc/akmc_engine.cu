@@ -488,7 +488,7 @@ __device__ __forceinline__ void df_activate(const EngineParams& p, Ctl& c, int i
     }
 }
 
-template <bool kTC, bool kFast = false>
+template <bool kTC, bool kFast = false, bool kDF = false>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         }
     }
     if (tid < kSlots) { c.seg_used[tid] = 0; c.seg_run[tid] = 0; c.seg_new[tid] = 0; c.seg_head[tid] = 0; c.seg_q[tid] = 0; }
-    if (p.df) {
+    if (kDF) {
         if (tid < kMyTiles) {
             const int T = (int)blockIdx.x + tid * (int)gridDim.x;
             c.df_tile[tid] = T < p.ntiles ? T : -1;
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 // must not pile up in a handful of CTAs)
                 const int share = max(1, (c.ntot + (int)gridDim.x - 1) / (int)gridDim.x);
                 const int claim = min(nfree, share);
-                if (p.df) {
+                if (kDF) {
                     c.fetch = (!c.df_done_all && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) ? 2 : 0;
                     c.df_ring_head = 0;
                     c.df_nready = 0;
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 }
             }
             __syncthreads();
-            if (c.fetch == 2) {
+            if (kDF && c.fetch == 2) {
                 long long tdf = clock64();
                 // ---- dataflow activation: which of my tiles may start their next phase, then one tile per warp
                 // candidates: tiles whose previous phase is done, lowest next phase first, at most kDfCand per refill
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     if (c.fetch) ++d_refill;
                 }
             }
-            if (c.fetch == 1 && !p.df && tid < c.nnew) {
+            if (c.fetch == 1 && !kDF && tid < c.nnew) {
                 const int si = c.s0 + tid;
                 const Segment sg = p.segs[(c.nhot < 0 || si < c.nhot) ? si : p.seg_cap - 1 - (si - c.nhot)];
                 const int q = c.npend + tid;
@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             if (tid == 0) lap(d_x[0]);
-            own_alive = (c.nrun > 0 || (p.df && (!c.df_done_all || c.npend > 0))) ? 1 : 0;
+            own_alive = (c.nrun > 0 || (kDF && (!c.df_done_all || c.npend > 0))) ? 1 : 0;
             // ================= rows = active members of running domains, in slot/member order =================
             int total = 0;
             {
@@ -1416,7 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         int sec2 = 0;
                         if (!p.serial) dom_sector(nv, p.S, d2, sec2);
                         if (!p.serial && (d2 != (long long)c.seg_dom[i] || sec2 != p.ph[c.seg_q[i]].sector)) c.mem_act[moff + a] = 0;
-                        if (p.df) {
+                        if (kDF) {
                             // a vacancy entering another tile is announced to it (read at that tile's next activation)
                             const int Tn = df_tile_of(p, d2);
                             if (Tn != df_tile_of(p, (long long)c.seg_dom[i])) {
@@ -1504,7 +1504,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             if (stop) {
                 c.seg_run[i] = 0;
-                if (p.df && atomicSub(&c.df_left[c.seg_tp[i]], 1) == 1)    // the tile's phase is complete
+                if (kDF && atomicSub(&c.df_left[c.seg_tp[i]], 1) == 1)    // the tile's phase is complete
                     st_release_gpu_s64(p.done_phase + c.df_tile[c.seg_tp[i]], p.ph[c.seg_q[i]].phase);
             }
         }
@@ -1628,11 +1628,14 @@ size_t engine_smem_bytes() { return kSmemTotal; }
 
 cudaError_t engine_setup()
 {
-    cudaError_t e = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTotal);
+    const int b = (int)kSmemTotal;
+    cudaError_t e = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(engine_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(engine_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(engine_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return e;
 }
 
 int engine_max_clusters()
@@ -1656,7 +1659,8 @@ int engine_max_clusters()
 cudaError_t launch_engine(const EngineParams& p, bool tc, int nclusters, int num_sms, cudaStream_t s)
 {
     if (!tc) {
-        engine_kernel<false><<<num_sms, kThreads, kSmemTotal, s>>>(p);
+        if (p.df) engine_kernel<false, false, true><<<num_sms, kThreads, kSmemTotal, s>>>(p);
+        else engine_kernel<false><<<num_sms, kThreads, kSmemTotal, s>>>(p);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -1671,6 +1675,8 @@ cudaError_t launch_engine(const EngineParams& p, bool tc, int nclusters, int num
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (p.df) return p.fast ? cudaLaunchKernelEx(&cfg, engine_kernel<true, true, true>, p)
+                            : cudaLaunchKernelEx(&cfg, engine_kernel<true, false, true>, p);
     return p.fast ? cudaLaunchKernelEx(&cfg, engine_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, engine_kernel<true>, p);
 }
 

@@ -54,28 +54,20 @@ __device__ __forceinline__ uint4 pack8(const __half (&x)[8])
 
 // Layer 3 (h2 -> 8 barriers) on CUDA cores in FP64, the contract shared with the bulk evaluator
 // (akmc_bulk.cu): h2 columns are taken in chunks of 16 (chunk q = global columns 16q..16q+15);
-// P_q[k] = (sequential fma over columns 16q..16q+7 from 0) + (the same over 16q+8..16q+15);
+// P_q[k] = sequential fma over the chunk's 16 columns of (double)h2_c * W3[c][k] from 0;
 // S_r = (P_{4r} + P_{4r+1}) + (P_{4r+2} + P_{4r+3}); out_k = b3_k + (((0 + S_0) + S_1) + S_2) + S_3.
 // h2_c is the FP32 value max(0, fma(fma(D2, 2^-11, D1), s2u, b2_c)) -- products and sums in FP64, so layer 3
 // adds no rounding beyond FP64 (it used to be a 3-pass fp16 tcgen05 product with FP32 accumulators).
 __device__ __forceinline__ void l3_chunk(const float (&z)[16], const double* __restrict__ w3, double (&P)[8])
 {
-    // two independent accumulators per output (columns 0-7 and 8-15 of the chunk), P = Pa + Pb: 16 chains of
-    // depth 8 instead of 8 of depth 16 (latency)
-    double Pb[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { P[k] = 0.0; Pb[k] = 0.0; }
+    for (int k = 0; k < 8; ++k) P[k] = 0.0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const double za = (double)z[t], zb = (double)z[t + 8];
+    for (int t = 0; t < 16; ++t) {
+        const double zt = (double)z[t];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            P[k] = __fma_rn(za, w3[t * 8 + k], P[k]);
-            Pb[k] = __fma_rn(zb, w3[(t + 8) * 8 + k], Pb[k]);
-        }
+        for (int k = 0; k < 8; ++k) P[k] = __fma_rn(zt, w3[t * 8 + k], P[k]);
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) P[k] = __dadd_rn(P[k], Pb[k]);
 }
 
 // h2 of 16 columns from the layer-2 accumulators (FP32-equivalent: D1 + 2^-11 D2), the E2 arithmetic

@@ -2076,11 +2076,12 @@ void akmc_free(akmc_handle* h)
         {
             const unsigned long long* b = c + 128 + 512 + 64;
             if (b[4] && b[8] && b[12]) {
-                const double T = (double)b[8];           // tiles (all CTAs); 8 producer / 4 epilogue warps per CTA
-                std::fprintf(stderr, "[akmc bulk] tiles %.0f; cycles per tile -- producer warp: gather %.0f wait-A %.0f "
+                const double T = (double)b[8];           // tiles (all CTAs)
+                const double P = 4.0 * (double)b[4] / (double)b[12];   // producer warps per CTA (4 epilogue warps)
+                std::fprintf(stderr, "[akmc bulk] tiles %.0f; cycles per tile -- producer warp (%.0f): gather %.0f wait-A %.0f "
                              "layer-1 %.0f wait-meta %.0f | MMA thread: wait-A %.0f wait-TMEM %.0f issue %.0f | epilogue "
-                             "warp: wait %.0f E2+L3 %.0f E3 %.0f\n", T, b[0] / (8 * T), b[1] / (8 * T), b[2] / (8 * T),
-                             b[3] / (8 * T), b[5] / T, b[6] / T, b[7] / T, b[9] / (4 * T), b[10] / (4 * T), b[11] / (4 * T));
+                             "warp: wait %.0f E2+L3 %.0f E3 %.0f\n", T, P, b[0] / (P * T), b[1] / (P * T), b[2] / (P * T),
+                             b[3] / (P * T), b[5] / T, b[6] / T, b[7] / T, b[9] / (4 * T), b[10] / (4 * T), b[11] / (4 * T));
             }
         }
         // per-iteration trace: iteration index -> CTA count, mean rows / misses / running domains, cycles

@@ -10,7 +10,7 @@
 //   warp  4     W2 loader: cp.async.bulk of the fp16 hi|lo image of one K-step of W2 (16 KB) into a 4-stage ring;
 //   warp  5     MMA issuer (one thread): 16 K-steps x {D1 += Ahi W2hi, D2 += Ahi W2lo, D2 += Alo W2hi}, M=128
 //               N=256 K=16, accumulators D1 | D2 = all 512 TMEM columns;
-//   warps 6-13  producers: gather the next tile's windows (while the MMA runs on the current tile), then
+//   warps 6-15  producers: gather the next tile's windows (while the MMA runs on the current tile), then
 //               layer 1 into the A operand as soon as the MMA has released it.
 // Layer 1 is a sparse gather-sum of ~1.6 W1' rows per window (the one-hot input has 64 ones in 448 features
 // and ~62 of them are the Fe reference), FP64 on CUDA cores, not a dense GEMM.
@@ -24,15 +24,16 @@ constexpr int kBTile = 128;                                     // rows per tile
 constexpr int kBEpiWarps = 4;
 constexpr int kBLoadWarp = 4, kBMmaWarp = 5;
 #ifndef AKMC_BULK_PROD
-#define AKMC_BULK_PROD 8        // producer warps (A/B knob; 128 / AKMC_BULK_PROD rows each)
+#define AKMC_BULK_PROD 10       // producer warps (A/B knob): 16 warps in all = 4 per SM sub-partition, 128 registers
 #endif
 constexpr int kBProdWarp0 = 6, kBProdWarps = AKMC_BULK_PROD;
-constexpr int kBThreads = 32 * (kBProdWarp0 + kBProdWarps);    // 448
+constexpr int kBThreads = 32 * (kBProdWarp0 + kBProdWarps);    // 512
 constexpr int kBStages = 4;
 constexpr uint32_t kBSplitA = kBTile * kHid * 2;                // 64 KiB: one fp16 split of the A tile
 constexpr uint32_t kBW2Split = kHid * 16 * 2;                   // 8 KiB: one fp16 split of a W2 K-step, N = 256
 constexpr uint32_t kBW2Stage = 2 * kBW2Split;                   // hi | lo
-constexpr int kBRowsPerProd = kBTile / kBProdWarps;             // 16 rows per producer warp
+constexpr int kBRowsPerProd = (kBTile + kBProdWarps - 1) / kBProdWarps;   // rows pw + P q < 128 of producer pw
+static_assert(kBRowsPerProd <= 32, "one lane per row");
 
 struct BulkMeta {                                               // per tile, read by the epilogue
     uint8_t win8[kBTile][8];                                    // first-shell bytes (masks)
@@ -43,7 +44,8 @@ struct BulkMeta {                                               // per tile, rea
 constexpr uint32_t kBOffA = 0;
 constexpr uint32_t kBOffRing = kBOffA + 2 * kBSplitA;
 constexpr uint32_t kBOffW3 = kBOffRing + kBStages * kBW2Stage;   // double [256][8]
-constexpr uint32_t kBOffB2 = kBOffW3 + kHid * 8 * 8;             // float [256]
+constexpr uint32_t kBOffB1 = kBOffW3 + kHid * 8 * 8;             // float [256]: b1'
+constexpr uint32_t kBOffB2 = kBOffB1 + kHid * 4;                 // float [256]
 constexpr uint32_t kBOffB3 = kBOffB2 + kHid * 4;                 // double [8]
 constexpr uint32_t kBOffWin = kBOffB3 + 8 * 8;                   // uint8 [128][64] (producers)
 constexpr uint32_t kBOffL1N = kBOffWin + kBTile * kWin;          // uint8 [128]
@@ -64,6 +66,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
     uint8_t* A_hi = sm + kBOffA;
     uint8_t* A_lo = sm + kBOffA + kBSplitA;
     double* w3s = reinterpret_cast<double*>(sm + kBOffW3);
+    float* b1s = reinterpret_cast<float*>(sm + kBOffB1);
     float* b2s = reinterpret_cast<float*>(sm + kBOffB2);
     double* b3s = reinterpret_cast<double*>(sm + kBOffB3);
     uint8_t* win = sm + kBOffWin;
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
         mbar_fence_init();
     }
     for (int i = tid; i < kHid * 8; i += kBThreads) w3s[i] = p.W.W3d[i];
-    for (int i = tid; i < kHid; i += kBThreads) b2s[i] = p.W.b2[i];
+    for (int i = tid; i < kHid; i += kBThreads) { b1s[i] = p.W.W1f[i]; b2s[i] = p.W.b2[i]; }
     if (tid < 8) b3s[tid] = p.W.b3[tid];
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
     tc_fence_before();
@@ -170,7 +173,8 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             // bytes of the lane's two slots for the 16 rows are in flight at once
             int my_slot = -1, my_vox = -1;
             int4 my_v = make_int4(-1, 0, 0, 0);
-            if (lane < kBRowsPerProd) {
+            const bool row_ok = lane < kBRowsPerProd && pw + kBProdWarps * lane < kBTile;
+            if (row_ok) {
                 const int g = t * kBTile + pw + kBProdWarps * lane;
                 if (g < nrows) {
                     if (p.windows) {
@@ -203,12 +207,13 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
 #pragma unroll
             for (int q = 0; q < kBRowsPerProd; ++q) {
                 const int r = pw + kBProdWarps * q;
+                if (kBTile % kBProdWarps != 0 && r >= kBTile) break;   // warp-uniform
                 win[r * kWin + lane] = b0[q];
                 win[r * kWin + lane + 32] = b1[q];
                 if (lane < 8) M.win8[r][lane] = b0[q];
                 l1_list_store(r, b0[q], b1[q], l1n, l1l);
             }
-            if (lane < kBRowsPerProd) {
+            if (row_ok) {
                 const int r = pw + kBProdWarps * lane;
                 M.slot[r] = my_slot;
                 M.vox[r] = my_vox;
@@ -220,10 +225,15 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
             t1 = clock64(); tw += t1 - t0; t0 = t1;
 #pragma unroll 1
             for (int q0 = 0; q0 < kBRowsPerProd; q0 += kL1Rows) {
-                int rr[kL1Rows], mr[kL1Rows];
+                int rr[kL1Rows], mr[kL1Rows], nv = 0;
 #pragma unroll
-                for (int q = 0; q < kL1Rows; ++q) { rr[q] = pw + kBProdWarps * (q0 + q); mr[q] = rr[q]; }
-                layer1_rows(rr, kL1Rows, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, nullptr, nullptr, ovf, fast, p.W.h1s);
+                for (int q = 0; q < kL1Rows; ++q) {
+                    rr[q] = pw + kBProdWarps * (q0 + q);
+                    if (q0 + q < kBRowsPerProd && rr[q] < kBTile) ++nv; else rr[q] = 0;   // (valid rows first)
+                    mr[q] = rr[q];
+                }
+                layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, nullptr, nullptr, ovf, fast, p.W.h1s,
+                            nullptr, b1s);
             }
             fence_async_smem();                                 // generic-proxy A writes -> the MMA's async proxy
             __syncwarp();
@@ -290,7 +300,8 @@ __global__ void __launch_bounds__(kBThreads, 1) bulk_eval_kernel(const __grid_co
                 for (int k = 0; k < 8; ++k) {
                     const double out = __dadd_rn(b3s[k], acc[k]);
                     const double Ek = out > 0.0 ? out : 0.0;
-                    const double Gk = (meta[b].win8[m][k] != (uint8_t)kVac) ? arrhenius_tc(Ek, p.P, vox) : 0.0;
+                    const double g = arrhenius_tc(Ek, p.P, vox);   // unconditional: the 8 exps run interleaved
+                    const double Gk = (meta[b].win8[m][k] != (uint8_t)kVac) ? g : 0.0;
                     R = __dadd_rn(R, Gk);
                     if (p.rates) p.rates[(size_t)slot * 8 + k] = Gk;
                     if (p.E) p.E[(size_t)slot * 8 + k] = Ek;

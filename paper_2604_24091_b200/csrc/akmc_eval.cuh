@@ -164,13 +164,14 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
 #endif
 }
 
-// layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once
+// layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once; b1s = a shared-memory copy
+// of b1' (row 0 of W1'), or nullptr to read it from W1f (same values, so the same bits)
 constexpr int kL1Rows = AKMC_L1_ROWS;
 __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
                                             const uint16_t* l1l, const float* __restrict__ W1f,
                                             const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
                                             uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf, bool fast,
-                                            float sc, long long* lp = nullptr)
+                                            float sc, long long* lp = nullptr, const float* b1s = nullptr)
 {
     const int lane = threadIdx.x & 31;
     long long t0 = lp ? clock64() : 0;
@@ -192,7 +193,13 @@ __device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, co
 #endif
     double a[kL1Rows][8];
     {
-        const float4 x0 = __ldg(base), x1 = __ldg(base + 1);
+        float4 x0, x1;
+        if (b1s) {
+            x0 = reinterpret_cast<const float4*>(b1s)[2 * lane];
+            x1 = reinterpret_cast<const float4*>(b1s)[2 * lane + 1];
+        } else {
+            x0 = __ldg(base); x1 = __ldg(base + 1);
+        }
 #pragma unroll
         for (int r = 0; r < kL1Rows; ++r) {
             a[r][0] = x0.x; a[r][1] = x0.y; a[r][2] = x0.z; a[r][3] = x0.w;

@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libakmc.so")
 SOURCES = ["akmc_api.cu", "akmc_engine.cu", "akmc_bulk.cu", "akmc_world.cu", "akmc_mfpt.cu"]
-HEADERS = ["akmc_world.cuh", "akmc_eval.cuh", "akmc_device.cuh", "akmc_kernels.cuh", "akmc_dist.cuh", "akmc_engine.cuh", "akmc_ptx.cuh"]
+HEADERS = ["akmc_world.cuh", "akmc_eval.cuh", "akmc_device.cuh", "akmc_kernels.cuh", "akmc_dist.cuh", "akmc_p2p.cuh", "akmc_engine.cuh", "akmc_ptx.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
 

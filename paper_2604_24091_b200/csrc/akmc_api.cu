@@ -14,6 +14,7 @@
 
 #include "../../include/akmc.h"
 #include "akmc_kernels.cuh"
+#include "akmc_p2p.cuh"
 #include "akmc_engine.cuh"
 #include "akmc_world.cuh"
 #include <nccl.h>
@@ -139,6 +140,14 @@ struct akmc_handle {
     int *d_dmin = nullptr, *d_head = nullptr, *d_next = nullptr, *d_members = nullptr, *d_rows = nullptr;
     int4* d_mpos = nullptr;           // member positions (phase engine)
     Segment* d_segs = nullptr;
+    // multi-rank overlap of the per-phase exchange with the next phase's interior domains (step_sublattice_overlap)
+    Segment* d_segs2 = nullptr;       // boundary domains' segments
+    long long* d_bdom = nullptr;      // boundary domains holding active vacancies of the phase
+    cudaStream_t side = nullptr;      // the exchange's receive side + the boundary activation
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool overlap_ok = false;          // p2p transport, phase engine: the overlapped sweep is available
+    bool xpending = false;            // a packed exchange whose unpack has not been enqueued yet
+    unsigned long long xepoch = 0;
     uint8_t* d_mactive = nullptr;
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;     // pinned
@@ -193,6 +202,11 @@ struct akmc_handle {
     int profile = 0;
     std::vector<cudaEvent_t> ev;      // pairs
     size_t ev_used = 0;
+    std::vector<cudaEvent_t> xev;     // AKMC_PHASE_TIMING, multi-rank host-stepped sweeps: (pack start, unpack start,
+    size_t xev_used = 0;              // unpack end) triples around every exchange
+    double xchg_ms[2] = {0.0, 0.0};   // summed pack / unpack (incl. the wait for the peers) ms
+    int64_t xchg_n = 0;
+    cudaEvent_t* xchg_mark = nullptr; // the current triple (exchange_deltas records the middle event)
     akmc_counters total{};
     int64_t sweep = 0;
     std::string err;
@@ -300,6 +314,12 @@ void free_all(akmc_handle* h)
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     if (h->h_watch) cudaFreeHost(h->h_watch);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->xev) cudaEventDestroy(e);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->d_segs2) cudaFree(h->d_segs2);
+    if (h->d_bdom) cudaFree(h->d_bdom);
     for (int r = 0; r < kMaxPeers; ++r) {
         if (h->ipc_box[r]) cudaIpcCloseMemHandle(h->ipc_box[r]);
         if (h->ipc_flag[r]) cudaIpcCloseMemHandle(h->ipc_flag[r]);
@@ -592,6 +612,13 @@ int harvest_events(akmc_handle* h)
         h->total.mlp_ms += ms;
     }
     h->ev_used = 0;
+    for (size_t i = 0; i + 3 <= h->xev_used; i += 3) {
+        float a = 0.f, b = 0.f;
+        CK(h, cudaEventElapsedTime(&a, h->xev[i], h->xev[i + 1]));
+        CK(h, cudaEventElapsedTime(&b, h->xev[i + 1], h->xev[i + 2]));
+        h->xchg_ms[0] += a; h->xchg_ms[1] += b; h->xchg_n += 1;
+    }
+    h->xev_used = 0;
     return AKMC_OK;
 }
 
@@ -806,7 +833,9 @@ int init_multi(akmc_handle* h)
         h->slistcap = h->S.logcap + 6 * (h->DP.cap + 1);
         CK(h, cudaMalloc(&h->d_slist, (size_t)h->slistcap * sizeof(int4)));
         CK(h, cudaMalloc(&h->d_nslist, sizeof(int)));
-    } else if (!(ex && std::strcmp(ex, "nccl") == 0)) {
+    } else if (!(ex && std::strcmp(ex, "nccl") == 0) &&
+               2 * std::max(h->DP.G[0], std::max(h->DP.G[1], h->DP.G[2])) < 65536) {
+        // (the tagged mailbox entries carry 16-bit global half-cell coordinates; larger global lattices use NCCL)
         const int prc = setup_p2p(h);
         if (prc != AKMC_OK) return prc;
     }
@@ -865,6 +894,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->S.Gc[a] = cfg->gpu_grid[a] * cfg->cells[a];
         h->DP.O[a] = h->S.O[a];
         h->DP.G[a] = h->S.Gc[a];
+        h->S.Lb[a] = cfg->cells[a];
+        h->S.dec[a] = cfg->gpu_grid[a] > 1 ? 1 : 0;
     }
     h->F.sites = 128LL * h->F.NB[0] * h->F.NB[1] * h->F.NB[2];          // storage bytes per voxel
     h->csites = 2LL * cfg->cells[0] * cfg->cells[1] * cfg->cells[2];    // canonical sites per voxel
@@ -1055,6 +1086,20 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         if (sec_sites > kRowCap) h->engine = false;
     }
     if (const char* he = std::getenv("AKMC_HOT_EVENTS")) h->hot_events = std::atof(he);   // A/B knob (0: off)
+    if (h->multi && h->p2p && !h->shift && h->engine) {
+        // opt-in (measured slower on C5): AKMC_OVERLAP=1
+        const char* ov = std::getenv("AKMC_OVERLAP");
+        if (ov && std::strcmp(ov, "1") == 0) {
+            int lo = 0, hi = 0;
+            CKI(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CKI(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
+            CKI(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            CKI(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+            CKI(cudaMalloc(&h->d_segs2, (size_t)h->vcap * sizeof(Segment)));
+            CKI(cudaMalloc(&h->d_bdom, (size_t)h->vcap * sizeof(long long)));
+            h->overlap_ok = true;
+        }
+    }
     CKI(engine_setup());
     CKI(bulk_setup());
     CKI(world_setup());
@@ -1461,9 +1506,10 @@ static int exchange_deltas(akmc_handle* h)
     if (h->p2p) {
         // deltas straight into the peers' mailboxes over NVLink, flag per peer; wait + apply (akmc_dist.cuh)
         h->epoch += 1;
-        pack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
+        pack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
                                                           h->PB, h->epoch, h->d_dist_overflow);
-        unpack_p2p_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
+        if (h->xchg_mark) CK(h, cudaEventRecord(h->xchg_mark[1], h->stream));
+        unpack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
                                                             h->d_vac, h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
                                                             h->d_dist_overflow);
         CK(h, cudaGetLastError());
@@ -1559,8 +1605,21 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
                 h->total.kernel_launches += 3;
                 h->total.mlp_launches += 1;
                 if (h->multi) {
+                    const bool xt = h->d_phase_cycles && h->p2p && !h->shift;   // AKMC_PHASE_TIMING: split the exchange
+                    if (xt) {
+                        if (h->xev_used + 3 > h->xev.size())
+                            for (int i = 0; i < 48; ++i) {
+                                cudaEvent_t e;
+                                CK(h, cudaEventCreate(&e));
+                                h->xev.push_back(e);
+                            }
+                        h->xchg_mark = h->xev.data() + h->xev_used;
+                        h->xev_used += 3;
+                        CK(h, cudaEventRecord(h->xchg_mark[0], h->stream));
+                    }
                     const int rc2 = exchange_deltas(h);
                     if (rc2 != AKMC_OK) return rc2;
+                    if (xt) { CK(h, cudaEventRecord(h->xchg_mark[2], h->stream)); h->xchg_mark = nullptr; }
                 }
                 continue;
             }
@@ -1595,9 +1654,93 @@ static int step_sublattice_host(akmc_handle* h, int64_t n)
     return AKMC_OK;
 }
 
+// Multi-rank sweep with the per-phase exchange overlapped.  After phase q the deltas
+// are packed into the peers' mailboxes and every domain list of phase q + 1 is built from the registry as it
+// stands (stream A); then the receive side -- wait for the peers' deltas of q, apply them, put the arriving
+// vacancies into the lists, cut the boundary domains' segments (the first and last domain layer along each
+// decomposed axis: the only domains that read the halo or receive arrivals) -- runs on a second stream while
+// phase q + 1's engine already runs the interior domains on stream A; the engine takes the boundary segments once
+// they are published (ctr->bready, release / acquire).  Domains of a phase are independent (R6): the trajectory is
+// the unoverlapped one bit for bit.
+static void enqueue_unpack_p2p(akmc_handle* h, cudaStream_t s, const PhaseInfo* ph_next)
+{
+    ArrivalActivation act{};
+    if (ph_next) {
+        act.ph = ph_next; act.S = h->S; act.dmin = h->d_dmin; act.head = h->d_head; act.next = h->d_next;
+        act.bdom = h->d_bdom; act.ctr = h->d_ctr;
+    }
+    unpack_p2p_kernel<<<kP2PBlocks, 256, 0, s>>>(h->d_mbox, h->d_mflag, h->xepoch, h->F, h->DP, h->d_species, h->d_vac,
+                                                 h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
+                                                 h->d_dist_overflow, act);
+    h->xpending = false;
+    h->total.kernel_launches += 1;
+}
+
+static int step_sublattice_overlap(akmc_handle* h, int64_t n)
+{
+    const int nv = h->vcap;
+    const int np = h->DP.npeer;
+    cudaStream_t A = h->stream, B = h->side;
+    for (int64_t sw = 0; sw < n; ++sw) {
+        PhaseTable8 t;
+        phase_table(h, h->sweep, t.p);
+        set_phase_kernel<<<1, 32, 0, A>>>(h->d_phase, t);
+        for (int q = 0; q < 8; ++q) {
+            const PhaseInfo* ph = h->d_phase + q;
+            // every domain's member list from the current registry (also resets the phase counters)
+            activate_kernel<<<blocks_for(nv, 256), 256, 0, A>>>(h->d_vac, nv, h->d_nvac, h->S, ph, h->d_dmin, h->d_head,
+                                                                h->d_next, h->d_ctr, 0, h->d_bdom);
+            CK(h, cudaEventRecord(h->ev_fork, A));
+            // receive side of the previous exchange + the boundary segments (few blocks: the engine keeps its SMs)
+            CK(h, cudaStreamWaitEvent(B, h->ev_fork, 0));
+            if (h->xpending) enqueue_unpack_p2p(h, B, ph);
+            segments_boundary_kernel<<<4, 256, 0, B>>>(h->d_bdom, h->S, h->d_vac, h->d_dmin, h->d_head,
+                                                                    h->d_next, h->d_segs2, h->d_members, h->d_mactive,
+                                                                    h->d_ctr, h->d_mpos);
+            publish_boundary_kernel<<<1, 32, 0, B>>>(h->d_ctr, ph);
+            CK(h, cudaEventRecord(h->ev_join, B));
+            // interior segments + the engine on stream A
+            segments_kernel<<<blocks_for(nv, 256), 256, 0, A>>>(h->d_vac, nv, h->d_nvac, h->S, ph, h->d_dmin, h->d_head,
+                                                                h->d_next, h->d_segs, h->d_members, h->d_mactive, h->d_ctr,
+                                                                h->d_mpos,
+                                                                h->hot_events > 0.0
+                                                                    ? reinterpret_cast<const unsigned char*>(h->d_memo) : nullptr,
+                                                                nv, h->hot_events, 1, nullptr);
+            EngineParams p = engine_params(h, kEnginePhase);
+            p.ph = ph;
+            p.overlap = 1;
+            p.segs2 = h->d_segs2;
+            // (the engine leaves >= 16 SMs to the side stream, whose kernels it may be waiting for)
+            const int spare = h->num_sms - 16;
+            CK(h, launch_engine(p, h->tc, std::max(1, std::min(h->n_clusters, spare / 4)), spare, A));
+            CK(h, cudaStreamWaitEvent(A, h->ev_join, 0));
+            // send side of this phase's exchange
+            h->epoch += 1;
+            h->xepoch = h->epoch;
+            pack_p2p_kernel<<<kP2PBlocks, 256, 0, A>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species, h->PB,
+                                                       h->epoch, h->d_dist_overflow);
+            CK(h, cudaGetLastError());
+            h->xpending = true;
+            h->messages += np;
+            h->exchanges += 1;
+            h->total.kernel_launches += 6;
+            h->total.mlp_launches += 1;
+        }
+        add_window_kernel<<<blocks_for(h->nvox, 128), 128, 0, A>>>(h->d_clock, h->nvox, h->cfg.window_s);
+        CK(h, cudaGetLastError());
+        h->total.kernel_launches += 2;
+        h->sweep += 1;
+        h->total.sweeps += 1;
+    }
+    if (h->xpending) enqueue_unpack_p2p(h, A, nullptr);   // leave the halo and the registry complete at the call's end
+    CK(h, cudaGetLastError());
+    return AKMC_OK;
+}
+
 static int step_sublattice(akmc_handle* h, int64_t n)
 {
     if (h->profile) return step_sublattice_host(h, n);
+    if (h->multi && h->overlap_ok && !h->df) return step_sublattice_overlap(h, n);
     int launches_phase = 0;
     if (!h->multi && !h->sweep_exec) {
         const int rc = build_graph(h, 0, 8, true, &h->sweep_exec, &h->graph_launches_per_sweep);
@@ -2040,6 +2183,9 @@ void akmc_free(akmc_handle* h)
 {
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->xchg_n)
+        std::fprintf(stderr, "[akmc exchange] %lld exchanges: pack %.2f us, unpack incl. wait for the peers %.2f us per "
+                     "exchange\n", (long long)h->xchg_n, 1e3 * h->xchg_ms[0] / h->xchg_n, 1e3 * h->xchg_ms[1] / h->xchg_n);
     if (h->d_phase_cycles) {
         static unsigned long long c[kDiagWords];
         std::memset(c, 0, sizeof(c));
@@ -2064,6 +2210,9 @@ void akmc_free(akmc_handle* h)
                          " (k>0 rounds %.0f) L2+E2 %.0f L3+partials %.0f E3 %.0f\n", d[11] / n, d[12] / n, d[13] / n,
                          d[14] / n, d[15] / n, d[19] / n, d[16] / n, d[17] / n, d[18] / n);
             if (d[29]) std::fprintf(stderr, "[akmc engine] memo-hit chain: %llu events of %llu checks (%.1f per CTA-launch)\n", d[29], d[30], d[29] / n);
+            if (d[90])
+                std::fprintf(stderr, "[akmc overlap] %llu phases: boundary list published %.1f us after the engine start "
+                             "(%llu before it); engine %.1f us\n", d[90], 1e-3 * d[88] / d[90], d[91], 1e-3 * d[89] / d[90]);
             if (d[56] + d[57] + d[58])
                 std::fprintf(stderr, "[akmc engine] dataflow refill cycles/CTA: candidates %.0f readiness %.0f activation %.0f\n",
                              d[56] / n, d[57] / n, d[58] / n);

@@ -168,130 +168,6 @@ static __global__ void unpack_deltas_kernel(const int4* __restrict__ recvbuf, in
     unpack_done(FL, nfree0);
 }
 
-// ---------------------------------------------------------------- per-phase exchange over NVLink peer memory
-// Each rank owns a mailbox [npeer][2 parities][cap + 1] int4 and npeer epoch flags; peer r's deltas for
-// exchange e land in region (index of this rank in r's peer list... seen from r: its peer index of us,
-// parity e & 1) written by r's pack kernel with plain stores through the CUDA IPC mapping, followed by the
-// count header and a system-scope release of flag = e.  The receiver's unpack waits (acquire) for every
-// peer's flag >= e.  Two parities suffice: a peer can write exchange e + 2 only after it has received our
-// flag e + 1, which we raise after our unpack of e.
-struct PeerBoxes {
-    int4* box[kMaxPeers];                  // our region (parity 0) in peer r's mailbox; parity 1 at + cap + 1
-    unsigned long long* flag[kMaxPeers];   // our flag slot in peer r's flag array
-    int* cnt;                              // [npeer] local allocation counters of this exchange
-    unsigned int* done;                    // blocks of the pack kernel that have finished (last block publishes)
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
-{
-    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer_ns()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-constexpr int kExchangeTimeout = 1 << 30;  // flag bit in the exchange overflow word
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
-                                       DistParams D, const uint8_t* __restrict__ species, PeerBoxes B,
-                                       unsigned long long epoch, int* overflow)
-{
-    const int n = (int)min((unsigned long long)logcap, *nlog_p);
-    const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && *nlog_p > (unsigned long long)logcap) atomicAdd(overflow, 1);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        int4 e = log[i];
-        if (e.w < kMigrateBase) e.w = species[site_of(F, 0, e.x, e.y, e.z)];   // the site's FINAL value
-        const int p[3] = {e.x, e.y, e.z};
-        int gc[3], gp[3];
-        for (int a = 0; a < 3; ++a) {
-            gc[a] = imod((p[a] >> 1) + D.O[a], D.G[a]);
-            gp[a] = 2 * gc[a] + (p[a] & 1);
-        }
-        for (int r = 0; r < D.npeer; ++r) {
-            const bool want = (e.w >= kMigrateBase) ? in_block(gc, D.peerO[r], F, D) : in_extended(gc, D.peerO[r], F, D);
-            if (!want) continue;
-            const int k = atomicAdd(&B.cnt[r], 1);
-            if (k < D.cap) B.box[r][par + 1 + k] = make_int4(gp[0], gp[1], gp[2], e.w);   // NVLink store
-            else atomicAdd(overflow, 1);
-        }
-    }
-    __threadfence_system();
-    __syncthreads();
-    __shared__ bool last;
-    if (threadIdx.x == 0) last = atomicAdd(B.done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence_system();
-    const int r = threadIdx.x;
-    if (r < D.npeer) {
-        const int c = min(atomicAdd(&B.cnt[r], 0), D.cap);
-        B.box[r][par] = make_int4(c, 0, 0, 0);
-        __threadfence_system();
-        st_release_sys(B.flag[r], epoch);
-        B.cnt[r] = 0;
-    }
-    if (r == 0) { *B.done = 0u; *nlog_p = 0ull; }
-}
-
-// wait for every peer's deltas of exchange `epoch`, then apply them (same semantics as unpack_deltas_kernel)
-static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const unsigned long long* mflag, unsigned long long epoch,
-                                         Frame F, DistParams D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
-                                         int vcap, FreeList FL, int* overflow)
-{
-    const int nfree0 = *(volatile int*)&FL.cnt[0];
-    if (threadIdx.x < D.npeer) {
-        // bounded wait: a peer that never publishes (a crashed or diverged rank) must not hang the GPU -- after
-        // 30 s the exchange is abandoned and reported (kExchangeTimeout in the overflow word -> AKMC_ERR_RUNTIME)
-        const unsigned long long t0 = globaltimer_ns();
-        while (ld_acquire_sys(&mflag[threadIdx.x]) < epoch) {
-            __nanosleep(64);
-            if (globaltimer_ns() - t0 > 30000000000ull) { atomicOr(overflow, kExchangeTimeout); break; }
-        }
-    }
-    __syncthreads();
-    const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
-    for (int r = 0; r < D.npeer; ++r) {
-        const int4* buf = mbox + (size_t)r * 2 * (D.cap + 1) + par;
-        const int cnt = min(buf[0].x, D.cap);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-            const int4 e = buf[1 + i];
-            const int gp[3] = {e.x, e.y, e.z};
-            int lp[3];
-            bool ok = true;
-            for (int a = 0; a < 3; ++a) {
-                if (F.wrap[a]) { lp[a] = gp[a]; continue; }
-                int d = imod(gp[a] - 2 * D.O[a], 2 * D.G[a]);
-                if (d >= 2 * (F.L[a] + kHalo)) d -= 2 * D.G[a];
-                lp[a] = d;
-                if (d < -2 * kHalo || d >= 2 * (F.L[a] + kHalo)) ok = false;
-            }
-            if (!ok) { atomicAdd(overflow, 1); continue; }
-            if (e.w >= kMigrateBase) {
-                const int slot = arrival_slot(FL, nfree0, nvac_local);
-                if (slot < vcap) {
-                    vac[slot] = make_int4(0, lp[0], lp[1], lp[2]);
-                    gid[slot] = e.w - kMigrateBase;
-                } else {
-                    atomicAdd(overflow, 1);
-                }
-            } else {
-                write_site(species, F, 0, lp[0], lp[1], lp[2], (uint8_t)e.w);
-            }
-        }
-    }
-    unpack_done(FL, nfree0);
-}
-
 // ---------------------------------------------------------------- shift-staged per-phase exchange (AKMC_EXCHANGE=shift)
 // The paper's shift communication applied to the sparse per-phase deltas: the phase's entries (global
 // half-cell coordinates, final value or migration code) go through the decomposed axes in order; at stage a a

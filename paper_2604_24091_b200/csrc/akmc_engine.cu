@@ -87,6 +87,9 @@ struct Ctl {
     unsigned frees[kMaskWords];     // free slots left for single-slot domains, and their prefix counts
     int fpre[kMaskWords + 1];
     int npend, nnew, fetch, drained, ntot, s0, nhot;
+    int int_drained, bready, bdrained, ntot2;   // multi-rank overlap: interior list exhausted; boundary list
+                                                 // published, exhausted, size
+    unsigned long long bwait0;        // globaltimer when this CTA started waiting for the boundary list
     unsigned freew[kMaskWords], runw[kMaskWords];
     int nrows, nmiss, nrun, ebase;
     int wsum[kWarps];
@@ -529,8 +532,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     uint8_t* g_hi = kTC ? p.stage + ((size_t)cluster_id() * kClusterN + rank) * (2u * kStageSplitRows) : nullptr;
     uint8_t* g_lo = kTC ? g_hi + kStageSplitRows : nullptr;
 
+    if (tid == 0 && blockIdx.x == 0 && p.overlap && p.diag) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.ctr->t_e0 = t;
+    }
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
+        c.int_drained = 0; c.bready = 0; c.bdrained = 0; c.ntot2 = 0; c.bwait0 = 0;
         c.ntot = phase_mode ? (p.serial ? p.nseg_host : (int)p.ctr->nseg) : 0;
         c.nhot = (phase_mode && !p.serial && p.seg_cap > 0) ? (int)p.ctr->nhot : -1;
         c.events = 0; c.evals = 0; c.mrows = 0; c.clamps = 0;
@@ -666,13 +675,54 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     c.fetch = (!c.df_done_all && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) ? 2 : 0;
                     c.df_ring_head = 0;
                     c.df_nready = 0;
-                } else if (!c.drained && c.npend == 0 && nfree > 0 && (nfree >= kSlots / 4 || nrun0 == 0)) {
-                    const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)claim);
-                    if (s0 >= c.ntot) {
+                } else if (!c.drained) {
+                    // multi-rank overlap: the boundary domains' list is published (stream-parallel to this launch)
+                    // once the previous phase's halo deltas have been applied; it is polled every iteration and
+                    // taken before what is left of the interior list (boundary domains start late, so they go first)
+                    if (p.overlap && !c.bready) {
+                        long long f;
+                        asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(f) : "l"(&p.ctr->bready) : "memory");
+                        if (f == p.ph[0].phase + 1) {                   // (published as phase + 1: never 0)
+                            c.bready = 1;
+                            c.ntot2 = (int)*(volatile unsigned long long*)&p.ctr->nseg2;
+                        }
+                    }
+                    if (c.npend == 0 && nfree > 0) {
+                        if (p.overlap && c.bready && !c.bdrained) {
+                            const int share2 = max(1, (c.ntot2 + (int)gridDim.x - 1) / (int)gridDim.x);
+                            const int claim2 = min(nfree, share2);
+                            const int s2 = (int)atomicAdd(&p.ctr->chunk2, (unsigned long long)claim2);
+                            if (s2 >= c.ntot2) {
+                                c.bdrained = 1;
+                            } else {
+                                c.fetch = 3; c.s0 = s2; c.nnew = min(claim2, c.ntot2 - s2);
+                                ++d_refill;
+                            }
+                        }
+                        if (c.fetch == 0 && !c.int_drained && (nfree >= kSlots / 4 || nrun0 == 0)) {
+                            const int s0 = (int)atomicAdd(&p.ctr->chunk, (unsigned long long)claim);
+                            if (s0 >= c.ntot) {
+                                c.int_drained = 1;
+                            } else {
+                                c.fetch = 1; c.s0 = s0; c.nnew = min(claim, c.ntot - s0);
+                                ++d_refill;
+                            }
+                        }
+                    }
+                    if (c.int_drained && (!p.overlap || c.bdrained)) {
                         c.drained = 1;
-                    } else {
-                        c.fetch = 1; c.s0 = s0; c.nnew = min(claim, c.ntot - s0);
-                        ++d_refill;
+                    } else if (c.int_drained && p.overlap && !c.bready && c.fetch == 0) {
+                        // nothing left here but the unpublished boundary list: keep iterating (the cluster peers
+                        // are never held up), bounded
+                        unsigned long long now;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                        if (!c.bwait0) c.bwait0 = now;
+                        if (now - c.bwait0 > 30000000000ull) {          // never published: report, do not hang
+                            atomicAdd(p.overflow, 1ull);
+                            c.drained = 1;
+                        } else if (nrun0 == 0) {
+                            __nanosleep(256);
+                        }
                     }
                 }
             }
@@ -725,9 +775,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                     if (c.fetch) ++d_refill;
                 }
             }
-            if (c.fetch == 1 && !kDF && tid < c.nnew) {
+            if ((c.fetch == 1 || c.fetch == 3) && !kDF && tid < c.nnew) {
                 const int si = c.s0 + tid;
-                const Segment sg = p.segs[(c.nhot < 0 || si < c.nhot) ? si : p.seg_cap - 1 - (si - c.nhot)];
+                const Segment sg = c.fetch == 3 ? p.segs2[si]
+                                                : p.segs[(c.nhot < 0 || si < c.nhot) ? si : p.seg_cap - 1 - (si - c.nhot)];
                 const int q = c.npend + tid;
                 c.cand_dom[q] = (unsigned)sg.dom; c.cand_off[q] = sg.off; c.cand_cnt[q] = sg.cnt;
                 c.cand_q[q] = 0; c.cand_tp[q] = 0;                        // (one phase per launch: p.ph[0])
@@ -855,7 +906,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             }
             __syncthreads();
             if (tid == 0) lap(d_x[0]);
-            own_alive = (c.nrun > 0 || (kDF && (!c.df_done_all || c.npend > 0))) ? 1 : 0;
+            own_alive = (c.nrun > 0 || (kDF && (!c.df_done_all || c.npend > 0)) || (p.overlap && !c.drained)) ? 1 : 0;
             // ================= rows = active members of running domains, in slot/member order =================
             int total = 0;
             {
@@ -1513,6 +1564,19 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         trace_end();
     }
     if (tid == 0 && p.diag && phase_mode) atomicAdd(p.diag + 96 + 512 + min(tr_it, 63), 1ull);
+    if (tid == 0 && p.diag && p.overlap) {
+        // overlap timing: boundary list publication and engine end, relative to the engine's start (last CTA out)
+        __threadfence();
+        if (atomicAdd(&p.ctr->nexit, 1ull) == gridDim.x - 1) {
+            long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            const long long e0 = *(volatile long long*)&p.ctr->t_e0, tp = *(volatile long long*)&p.ctr->t_pub;
+            atomicAdd(p.diag + 88, (unsigned long long)max(0ll, tp - e0));
+            atomicAdd(p.diag + 89, (unsigned long long)max(0ll, now - e0));
+            atomicAdd(p.diag + 90, 1ull);
+            atomicAdd(p.diag + 91, tp < e0 ? 1ull : 0ull);
+        }
+    }
     if (tid == 0 && p.diag) {
         d_cc = d_x[0] + d_x[1] + d_x[2];
         d_x[3] = d_y[0] + d_y[1] + d_y[2];

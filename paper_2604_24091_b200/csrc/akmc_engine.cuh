@@ -87,6 +87,8 @@ struct EngineParams {
     int* term;              // serial: per-voxel terminal flags
     double* clock;          // serial: per-voxel clocks
     int seg_cap;            // phase: > 0 -> hot segments at segs[0, nhot), cold ones at segs[seg_cap-1-i]
+    int overlap;            // multi-rank: 1 -> segs holds the interior domains; the boundary ones follow in segs2
+    const Segment* segs2;   //   once ctr->bready == ph->phase + 1 (published by a stream-parallel kernel)
     int horizon;            // serial: 1 -> a voxel also stops at its first draw with clock + dt > t_end
     double t_end;           //   (akmc_run_until; the draw is discarded, its counter not consumed)
     // dataflow sweep (f1, P:405-418 readiness signals; single rank): one launch runs the 8 phases of a sweep; a

@@ -19,6 +19,13 @@ struct DevCounters {                 // device-side counters (unsigned long long
     unsigned long long chunk;        // phase engine: next segment to hand out (reset per phase)
     unsigned long long mrows;        // barrier-network rows actually evaluated (memo misses)
     unsigned long long nhot, ncold;  // phase engine: segments at the front (hot) / back (cold) of the list
+    // multi-rank overlap (akmc_api.cu step_sublattice): the boundary domains' segments, built after the previous
+    // phase's halo deltas arrived, their cursor, and the phase number they were published for (release / acquire)
+    unsigned long long nseg2, chunk2;
+    long long bready;
+    unsigned long long nbdom;       // multi-rank overlap: boundary domains holding active vacancies (listed)
+    long long t_e0, t_pub;          // (AKMC_PHASE_TIMING) globaltimer at the engine's start / at the publication
+    unsigned long long nexit;       //   and the engine CTAs that have exited
 };
 
 // memo layout as seen from the segment builder (MemoEntry lives in akmc_engine.cuh; asserted there)
@@ -264,6 +271,10 @@ struct SubParams {
     // multi-rank: local slots freed by departures (reused by arrivals, akmc_dist.cuh); fcnt[0] = free count
     int* freelist;
     int* fcnt;
+    // multi-rank: local block cells and decomposed axes (a domain within 3 cells of a decomposed face is a
+    // "boundary" domain: it reads the halo or receives arrivals; the others are "interior")
+    int Lb[3];
+    int dec[3];
 };
 
 // a vacancy left this rank's block: its local slot is marked departed and pushed on the free list
@@ -303,21 +314,57 @@ __device__ __forceinline__ void dom_sector(const int4& v, const SubParams& S, lo
     sec = ox | (oy << 1) | (oz << 2);
 }
 
-// nvac = slot capacity; nvac_dev (multi-rank) = live slot count (slots may be departed: vac.x < 0)
-static __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, const int* __restrict__ nvac_dev, SubParams S,
-                                const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr)
+// part of the domain a vacancy is in: 1 = interior (its phase reads and writes stay >= 3 - 2.5 cells inside the
+// block along every decomposed axis, so it neither reads the halo nor receives arrivals), 2 = boundary
+__device__ __forceinline__ int dom_part(const int4& v, const SubParams& S)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) { ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; ctr->chunk = 0; ctr->nhot = 0; ctr->ncold = 0; }
+    const int pc[3] = {v.y >> 1, v.z >> 1, v.w >> 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!S.dec[a]) continue;
+        const int gcell = imodk(pc[a] + S.O[a], S.Gc[a]);
+        const int lo = imodk((gcell / S.D[a]) * S.D[a] - S.O[a], S.Gc[a]);   // the domain's first local cell
+        if (lo < 3 || lo + S.D[a] + 3 > S.Lb[a]) return 2;
+    }
+    return 1;
+}
+
+__device__ __forceinline__ void reset_phase_counters(DevCounters* ctr)
+{
+    ctr->nseg = 0; ctr->total = 0; ctr->nrun = 0; ctr->nrows = 0; ctr->chunk = 0; ctr->nhot = 0; ctr->ncold = 0;
+    ctr->nseg2 = 0; ctr->chunk2 = 0; ctr->bready = 0; ctr->nexit = 0; ctr->nbdom = 0;
+}
+// the boundary segments of phase ph are complete: release them to the running engine
+static __global__ void publish_boundary_kernel(DevCounters* ctr, const PhaseInfo* __restrict__ ph)
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ctr->t_pub = t;
+    __threadfence();
+    asm volatile("st.release.gpu.global.s64 [%0], %1;" :: "l"(&ctr->bready), "l"(ph->phase + 1) : "memory");
+}
+
+// nvac = slot capacity; nvac_dev (multi-rank) = live slot count (slots may be departed: vac.x < 0);
+// part 0: every domain (and the counters are reset here), 1: interior domains only, 2: boundary domains only
+static __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, const int* __restrict__ nvac_dev, SubParams S,
+                                const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr,
+                                int part = 0, long long* bdom = nullptr)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0 && part == 0) reset_phase_counters(ctr);
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
-    if (i >= n) return;
-    const int4 v = vac[i];
-    if (v.x < 0) return;
-    long long d; int sec;
-    dom_sector(v, S, d, sec);
-    if (sec != ph->sector) return;
-    atomicMin(&dmin[d], S.gid ? S.gid[i] : i);       // owner = smallest global slot id
-    next[i] = atomicExch(&head[d], i);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 v = vac[i];
+        if (v.x < 0) continue;
+        long long d; int sec;
+        dom_sector(v, S, d, sec);
+        if (sec != ph->sector) continue;
+        if (part != 0 && dom_part(v, S) != part) continue;
+        atomicMin(&dmin[d], S.gid ? S.gid[i] : i);       // owner = smallest global slot id
+        const int prev = atomicExch(&head[d], i);
+        next[i] = prev;
+        // (overlap) the first member of a boundary domain lists the domain for segments_boundary_kernel
+        if (bdom && prev < 0 && dom_part(v, S) == 2) bdom[atomicAdd(&ctr->nbdom, 1ull)] = d;
+    }
 }
 
 // Block-aggregated allocation: one atomic per block, offsets in thread (= slot) order inside the
@@ -348,16 +395,13 @@ __device__ __forceinline__ int block_alloc(int v, unsigned long long* counter)
     return r;
 }
 
-static __global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac,
-                                                       const int* __restrict__ nvac_dev, SubParams S,
-                                                       const PhaseInfo* __restrict__ ph, int* dmin, int* head,
-                                                       const int* __restrict__ next, Segment* segs, int* members,
-                                                       uint8_t* mactive, DevCounters* ctr, int4* mpos,
-                                                       const unsigned char* memo = nullptr, int seg_cap = 0,
-                                                       double hot_events = 0.0)
+__device__ __forceinline__ void segments_one(int i, int n, const int4* __restrict__ vac, const SubParams& S,
+                                             const PhaseInfo* __restrict__ ph, int* dmin, int* head,
+                                             const int* __restrict__ next, Segment* segs, int* members,
+                                             uint8_t* mactive, DevCounters* ctr, int4* mpos,
+                                             const unsigned char* memo, int seg_cap, double hot_events, int part,
+                                             Segment* segs2)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     long long d = 0;
     int sec = -1;
     bool owner = false;
@@ -366,14 +410,18 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
         const int4 v = vac[i];
         if (v.x >= 0) {
             dom_sector(v, S, d, sec);
-            owner = (sec == ph->sector && dmin[d] == (S.gid ? S.gid[i] : i));   // smallest global slot owns
+            owner = (sec == ph->sector && (part == 0 || dom_part(v, S) == part) &&
+                     dmin[d] == (S.gid ? S.gid[i] : i));                        // smallest global slot owns
             if (owner)
                 for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
         }
     }
     const int off = block_alloc(cnt, &ctr->total);
     int seg;
-    if (memo) {
+    if (part == 2) {
+        // boundary segments (multi-rank overlap): their own list, handed out after the interior ones
+        seg = block_alloc(owner ? 1 : 0, &ctr->nseg2);
+    } else if (memo) {
         // phase engine: order the segment list by expected events (processing order is free, R6).  A domain
         // whose last memoised rates predict >= hot_events events in the window (R_d * window) goes to the
         // front, the rest fill the list from the back; CTAs claim the front first, so long event chains
@@ -410,9 +458,67 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
         for (int a = 0; a < cnt; ++a) mpos[off + a] = vac[members[off + a]];   // positions for the phase engine
     Segment sg;
     sg.dom = d; sg.off = off; sg.cnt = cnt; sg.t = 0.0; sg.it = 0u; sg.running = 1;
-    segs[seg] = sg;
+    (part == 2 ? segs2 : segs)[seg] = sg;
     head[d] = -1;
     dmin[d] = INT_MAX;
+}
+
+
+static __global__ void __launch_bounds__(256) segments_kernel(const int4* __restrict__ vac, int nvac,
+                                                       const int* __restrict__ nvac_dev, SubParams S,
+                                                       const PhaseInfo* __restrict__ ph, int* dmin, int* head,
+                                                       const int* __restrict__ next, Segment* segs, int* members,
+                                                       uint8_t* mactive, DevCounters* ctr, int4* mpos,
+                                                       const unsigned char* memo = nullptr, int seg_cap = 0,
+                                                       double hot_events = 0.0, int part = 0, Segment* segs2 = nullptr)
+{
+    const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
+    // block-uniform trip count: block_alloc needs every thread of the block
+    for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x)
+        segments_one(i0 + (int)threadIdx.x, n, vac, S, ph, dmin, head, next, segs, members, mactive, ctr, mpos, memo,
+                     seg_cap, hot_events, part, segs2);
+}
+
+// segments of the boundary domains of the phase (their lists were built by activate_kernel and by the arrivals of
+// unpack_p2p_kernel, which also listed the domains in bdom): one thread per listed domain, block-uniform trip
+// count for block_alloc
+static __global__ void __launch_bounds__(256) segments_boundary_kernel(const long long* __restrict__ bdom, SubParams S,
+                                                                      const int4* __restrict__ vac, int* dmin, int* head,
+                                                                      const int* __restrict__ next, Segment* segs2,
+                                                                      int* members, uint8_t* mactive, DevCounters* ctr,
+                                                                      int4* mpos)
+{
+    const long long nb = (long long)*(volatile unsigned long long*)&ctr->nbdom;
+    for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < nb; k0 += (long long)gridDim.x * blockDim.x) {
+        const long long k = k0 + threadIdx.x;
+        long long d = 0;
+        int cnt = 0;
+        if (k < nb) {
+            d = bdom[k];
+            for (int j = head[d]; j >= 0; j = next[j]) ++cnt;
+        }
+        const int off = block_alloc(cnt, &ctr->total);
+        const int seg = block_alloc(cnt > 0 ? 1 : 0, &ctr->nseg2);
+        if (cnt == 0) continue;
+        int c = 0;
+        for (int j = head[d]; j >= 0; j = next[j]) members[off + (c++)] = j;
+        for (int a = 1; a < cnt; ++a) {                 // insertion sort by global slot id
+            const int key = members[off + a];
+            const int kg = S.gid[key];
+            int b = a - 1;
+            while (b >= 0 && S.gid[members[off + b]] > kg) {
+                members[off + b + 1] = members[off + b];
+                --b;
+            }
+            members[off + b + 1] = key;
+        }
+        for (int a = 0; a < cnt; ++a) { mactive[off + a] = 1; mpos[off + a] = vac[members[off + a]]; }
+        Segment sg;
+        sg.dom = d; sg.off = off; sg.cnt = cnt; sg.t = 0.0; sg.it = 0u; sg.running = 1;
+        segs2[seg] = sg;
+        head[d] = -1;
+        dmin[d] = INT_MAX;
+    }
 }
 
 // rows of this inner iteration = active members of running segments; also resets nrun

@@ -53,6 +53,25 @@ def test_four_rank_invariance(tmp_path, grid, extra):
     assert res["events"] > 20
 
 
+@pytest.mark.parametrize("nproc,grid,extra", [(2, (2, 1, 1), ["--oracle"]),
+                                              (2, (2, 1, 1), ["--model", "mlp", "--precision", "fp32"]),
+                                              (4, (2, 2, 1), ["--oracle", "--nvac", "60"])])
+def test_overlapped_exchange_invariance(tmp_path, nproc, grid, extra):
+    """AKMC_OVERLAP=1: the receive side of each phase's exchange and the boundary domains' lists run on a second
+    stream while the next phase's engine runs the interior domains -- same lattices as 1 rank and the oracle."""
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    out = tmp_path / "multi_ov.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}", "--master-addr",
+           "127.0.0.1", "--master-port", str(29720 + 7 * nproc + 3 * len(extra)), os.path.join(ROOT, "tools", "multi_check.py"),
+           "--grid", *map(str, grid), "--out", str(out), *extra]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env={**os.environ, "AKMC_OVERLAP": "1"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"], res
+    assert res["events"] > 20
+
+
 def test_two_rank_nccl_transport(tmp_path):
     """SURVEY 4.2 L4 (transport equivalence): the per-phase deltas over NCCL send/recv (AKMC_EXCHANGE=nccl)
     give the same lattices as 1 rank and the oracle, like the default peer-mailbox path above."""

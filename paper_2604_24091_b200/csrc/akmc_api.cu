@@ -1506,14 +1506,22 @@ static int exchange_deltas(akmc_handle* h)
     if (h->p2p) {
         // deltas straight into the peers' mailboxes over NVLink, flag per peer; wait + apply (akmc_dist.cuh)
         h->epoch += 1;
-        pack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
-                                                          h->PB, h->epoch, h->d_dist_overflow);
-        if (h->xchg_mark) CK(h, cudaEventRecord(h->xchg_mark[1], h->stream));
-        unpack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
-                                                            h->d_vac, h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
-                                                            h->d_dist_overflow);
+        if (h->xchg_mark) {                            // (AKMC_PHASE_TIMING: separate launches, to time pack / unpack)
+            pack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
+                                                              h->PB, h->epoch, h->d_dist_overflow);
+            CK(h, cudaEventRecord(h->xchg_mark[1], h->stream));
+            unpack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
+                                                                h->d_vac, h->d_gid, h->d_nvac, h->vcap,
+                                                                FreeList{h->d_free, h->d_fcnt}, h->d_dist_overflow);
+            h->total.kernel_launches += 2;
+        } else {
+            exchange_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->PB,
+                                                                  h->epoch, h->d_mbox, h->d_species, h->d_vac, h->d_gid,
+                                                                  h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
+                                                                  h->d_dist_overflow);
+            h->total.kernel_launches += 1;
+        }
         CK(h, cudaGetLastError());
-        h->total.kernel_launches += 2;
         h->exchanges += 1;
         return AKMC_OK;
     }

@@ -51,9 +51,9 @@ __device__ __forceinline__ void put_entry(int4* dst, int g0, int g1, int g2, int
     st_relaxed_sys_u64(d + 1, (unsigned long long)(uint32_t)w | ((unsigned long long)tag << 32));
 }
 
-static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
-                                       DistParams D, const uint8_t* __restrict__ species, PeerBoxes B,
-                                       unsigned long long epoch, int* overflow)
+__device__ __forceinline__ void pack_p2p(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, const Frame& F,
+                                         const DistParams& D, const uint8_t* __restrict__ species, const PeerBoxes& B,
+                                         unsigned long long epoch, int* overflow)
 {
     const int n = (int)min((unsigned long long)logcap, *nlog_p);
     const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
@@ -102,16 +102,23 @@ static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned lo
         last = atomicAdd(B.done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last) return;
-    if (threadIdx.x == 0) __threadfence();
-    __syncthreads();
-    const int r = threadIdx.x;
-    if (r < D.npeer) {
-        const int c = min(atomicAdd(&B.cnt[r], 0), D.cap);
-        st_relaxed_sys_u64(&B.box[r][par], (unsigned long long)(uint32_t)c | ((unsigned long long)tag << 32));
-        B.cnt[r] = 0;
+    if (last) {
+        if (threadIdx.x == 0) __threadfence();
+        __syncthreads();
+        const int r = threadIdx.x;
+        if (r < D.npeer) {
+            const int c = min(atomicAdd(&B.cnt[r], 0), D.cap);
+            st_relaxed_sys_u64(&B.box[r][par], (unsigned long long)(uint32_t)c | ((unsigned long long)tag << 32));
+            B.cnt[r] = 0;
+        }
+        if (r == 0) { *B.done = 0u; *nlog_p = 0ull; }
     }
-    if (r == 0) { *B.done = 0u; *nlog_p = 0ull; }
+}
+static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
+                                       DistParams D, const uint8_t* __restrict__ species, PeerBoxes B,
+                                       unsigned long long epoch, int* overflow)
+{
+    pack_p2p(log, nlog_p, logcap, F, D, species, B, epoch, overflow);
 }
 
 // wait for every peer's deltas of exchange `epoch` (tags), then apply them (same semantics as unpack_deltas_kernel)
@@ -125,11 +132,10 @@ struct ArrivalActivation {
     long long* bdom;       // boundary domains holding active vacancies (appended: first member of a domain)
     DevCounters* ctr;
 };
-static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const unsigned long long* mflag, unsigned long long epoch,
-                                         Frame F, DistParams D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
-                                         int vcap, FreeList FL, int* overflow, ArrivalActivation act = ArrivalActivation{})
+__device__ __forceinline__ void unpack_p2p(const int4* __restrict__ mbox, unsigned long long epoch, const Frame& F,
+                                           const DistParams& D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
+                                           int vcap, const FreeList& FL, int* overflow, const ArrivalActivation& act)
 {
-    (void)mflag;
     const int nfree0 = *(volatile int*)&FL.cnt[0];
     const uint32_t tag = (uint32_t)epoch;
     const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
@@ -197,6 +203,24 @@ static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const un
         }
     }
     unpack_done(FL, nfree0);
+}
+static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const unsigned long long* mflag, unsigned long long epoch,
+                                         Frame F, DistParams D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
+                                         int vcap, FreeList FL, int* overflow, ArrivalActivation act = ArrivalActivation{})
+{
+    (void)mflag;
+    unpack_p2p(mbox, epoch, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, act);
+}
+// send and receive of one exchange in one launch (the unoverlapped per-phase path): every block packs its share,
+// the last one publishes the counts, then every block waits for the peers' deltas and applies its share
+static __global__ void exchange_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
+                                           DistParams D, PeerBoxes B, unsigned long long epoch, const int4* __restrict__ mbox,
+                                           uint8_t* species, int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL,
+                                           int* overflow)
+{
+    pack_p2p(log, nlog_p, logcap, F, D, species, B, epoch, overflow);
+    __syncthreads();
+    unpack_p2p(mbox, epoch, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, ArrivalActivation{});
 }
 
 } // namespace akmc

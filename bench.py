@@ -8,6 +8,7 @@ RPV composition, windowed synchronous sublattice (domains 8^3, lambda = 1/4), ba
 A step = one sublattice sweep (8 phases) over the GPU's block.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5|c4|c3|c2|c1]
+  python bench.py --workload c4 --world      (the world-model time mode, on a serial workload)
 
 N > 1 is launched by torchrun (one rank per GPU).  Rank 0 prints ONE JSON line.
 """
@@ -138,13 +139,31 @@ def sim_config(name: str, precision: int, model: int, lam: float, E0, rank: int 
                        nccl_id=nccl_id if decomposed else b""), pr
 
 
-def cpu_baseline(name: str, steps: int, lam: float, seconds_target: float = 15.0):
+def cpu_baseline(name: str, steps: int, lam: float, seconds_target: float = 15.0, world: bool = False):
     """The oracle as it stands (single thread, FP64 MLP) on a bounded sample of the workload."""
     import oracle
     oracle.build()
     eps, E0 = synth.illustrative_pair_params()
     mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=1)
     pr, cells, nvox = workload(name)
+    if world:
+        # world-model mode: one voxel of the serial recipe, orc_run_world events
+        pol, tnet, H, tau = world_nets(E0)
+        sp = synth.make_lattice(cells, 1, pr.fractions, pr.n_vac_per_voxel, seed=pr.seed)
+        cfg = oracle.Config(cells=cells, model=1, seed=pr.seed)
+        st = oracle.State.from_species(cfg, sp)
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            oracle.run_world(cfg, st, 1, eps, E0, pol, tnet, H, tau)
+            done += 1
+            el = time.perf_counter() - t0
+            if el >= seconds_target or done >= max(steps, 1) * 1000:
+                break
+        hop = int(st.counters[1])
+        return {"value": hop / el, "unit": UNIT, "cores": 1, "kind": "oracle", "steps": done,
+                "sample": f"one {cells[0]}^3 voxel of {name.upper()} ({pr.n_vac_per_voxel} V), world-model events "
+                          f"(orc_run_world, FP64); {done} step(s), {hop} hop evals in {el:.1f} s", **cpu_info()}, st, el
     if pr.domain[0]:
         # sample: a 256^3-cell block of the same recipe (same c_v, domains, lambda), whole sweeps
         sc = (256, 256, 256)
@@ -171,6 +190,18 @@ def cpu_baseline(name: str, steps: int, lam: float, seconds_target: float = 15.0
     hop = int(st.counters[1])
     return {"value": hop / el, "unit": UNIT, "cores": 1, "kind": "oracle", "steps": done,
             "sample": f"{sample}; {done} step(s), {hop} hop evals in {el:.1f} s", **cpu_info()}, st, el
+
+
+WORLD_H = 32
+FP64_PEAK_TFLOPS = 45.0     # B200 FP64 (blackwell_cuda_programming.md: "B200's 45"); the world mode's FP64 ceiling
+
+
+def world_nets(E0, T=563.0):
+    """World-model mode inputs (reading W2): policy logits z = -E/kT of the physics network (Eq. 2's law is then
+    the BKL law), a seeded Poisson-time net of width WORLD_H, tau_act = 1."""
+    eps, _ = synth.illustrative_pair_params()
+    phys = synth.physics_mlp(eps, E0, residual=0.02, seed=1)
+    return synth.policy_mlp(phys, 8.617333262e-5 * T), synth.poisson_net(7, H=WORLD_H), WORLD_H, 1.0
 
 
 def cpu_info() -> dict:
@@ -239,7 +270,8 @@ def run_reference(args):
     if rank != 0:
         return
     t_all = time.perf_counter()
-    cb, st, el = cpu_baseline(args.workload, args.steps, args.lam, seconds_target=max(10.0, 4.0 * args.steps))
+    cb, st, el = cpu_baseline(args.workload, args.steps, args.lam, seconds_target=max(10.0, 4.0 * args.steps),
+                              world=args.world)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / max(cb["steps"], 1),
             "higher_is_better": True,
@@ -272,6 +304,13 @@ def run_ours(args):
     model = akmc.MODEL_MLP if args.model == "mlp" else akmc.MODEL_PAIR
     eps, E0 = synth.illustrative_pair_params()
     mlp = synth.physics_mlp(eps, E0, residual=0.02, seed=1)
+    wnets = None
+    if args.world:
+        if workload(args.workload)[0].domain[0]:
+            raise SystemExit("--world: serial workloads only (c1, c2, c4)")
+        prec, model = akmc.PREC_FP64, akmc.MODEL_MLP       # the world mode is FP64 (bit-exact with orc_run_world)
+        wnets = world_nets(E0)
+        mlp = wnets[0]
     from paper_2604_24091_b200 import dist as D
     nid = D.broadcast_nccl_id(rank, device=dev) if world > 1 else b""
     cfg, pr = sim_config(args.workload, prec, model, args.lam, E0, rank, world, nid)
@@ -284,6 +323,8 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     # ---------------- device-resident timing ("value"): production path (per-sweep CUDA graph)
     sim = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    if wnets:
+        sim.set_world_model(wnets[1], wnets[2], wnets[3])
     vT = None
     if args.voxel_T:
         # C4 variant: per-voxel T uniform in 558-577 K, distinct per rank
@@ -361,6 +402,8 @@ def run_ours(args):
         dist.barrier()
     t0 = time.perf_counter()
     sim2 = akmc.Simulation(cfg, sp_host, eps, E0, mlp)
+    if wnets:
+        sim2.set_world_model(wnets[1], wnets[2], wnets[3])
     if vT is not None:
         sim2.set_voxel_temperatures(vT)
     t_init = time.perf_counter() - t0
@@ -431,7 +474,20 @@ def run_ours(args):
                            "dram_achieved": dram_gbs, "dram_frac": (dram_gbs / hbm_peak) if dram_gbs else None,
                            "what": "gather/encode/select bytes (64 B window + 16 B record per vac) / engine time; "
                                    "dram_achieved = ncu DRAM bytes per launch / warm average launch time"}
-        if executed:
+        if wnets and mlp_ms > 0:
+            w_ach = mlp_rows * FLOPS_PER_VAC / mlp_s / 1e12
+            roof = {"bound": "latency", "ceiling": "fp64 (CUDA cores)",
+                    "kernel": "world_serial_kernel (akmc_world.cu: one CTA per voxel; dirty rows through the FP64 "
+                              "network, policy softmax tree, Philox draw, Eq. 7 clock)",
+                    "achieved": w_ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": w_ach / FP64_PEAK_TFLOPS,
+                    "traffic": None, "algorithmic_flops_per_vac": FLOPS_PER_VAC, "rows": int(mlp_rows),
+                    "launches": int(mlp_launch), "kernel_ms": mlp_ms,
+                    "share_of_step": (mlp_ms / ms) if ms > 0 else None,
+                    "peak_note": "B200 FP64 45 TFLOP/s (guide figure, not measured)",
+                    "latency_bound": "each voxel's event chain is serial (one event at a time, S:195-203); a row's "
+                                     "FP64 layers run as 256-thread dot products inside the voxel's CTA",
+                    "work": "network rows actually evaluated (windows that changed) x 151,552 FLOPs / kernel time"}
+        if executed and not wnets:
             roof["executed"] = {"rows": int(mlp_rows), "achieved": executed, "frac": executed / tc_peak,
                                 "what": "network rows actually run (memo misses) x algorithmic FLOPs / engine time; the "
                                         f"memo served {1.0 - mlp_rows / max(logical_rows, 1):.0%} of the vacs"}
@@ -465,7 +521,9 @@ def run_ours(args):
                            "step": ("one sweep (8 sublattice phases)" if pr.domain[0] else
                                     f"{nstep} BKL events per voxel (one engine launch)"),
                            "temperature_K": ("per voxel, uniform 558-577" if vT is not None else cfg.temperature_K),
-                           "model": "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA",
+                           "model": ("world-model mode: policy logits -E/kT of the physics-embedded MLP (tau_act 1), "
+                                     f"Eq. 7 clock from a seeded Poisson-time net (H = {WORLD_H}), FP64" if wnets else
+                                     "MLP 448-256-256-8 physics-embedded + residual" if model else "pair KRA"),
                            "parallelism": ("1 GPU" if world == 1 else
                                            (f"spatial blocks {'x'.join(map(str, cfg.gpu_grid))}, halo deltas between "
                                             "phases written into the peers' mailboxes over NVLink (CUDA IPC)" if cfg.world > 1 else f"independent voxels x{world}")),
@@ -488,8 +546,9 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _, _ = cpu_baseline(args.workload, 1, args.lam)
-        cb["all_cores"] = cpu_baseline_all_cores(args.workload, args.lam)
+        cb, _, _ = cpu_baseline(args.workload, 1, args.lam, world=bool(wnets))
+        if not wnets:
+            cb["all_cores"] = cpu_baseline_all_cores(args.workload, args.lam)
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -512,6 +571,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--events", type=int, default=100, help="serial workloads: BKL events per voxel per step")
     ap.add_argument("--voxel-T", action="store_true", help="per-voxel temperature uniform in 558-577 K (C4 variant)")
+    ap.add_argument("--world", action="store_true",
+                    help="serial workloads: the world-model time mode (SURVEY 8(f) f2; FP64: policy logits -E/kT of the "
+                         "physics network, Eq. 7 clock from a seeded Poisson-time net)")
     ap.add_argument("--ramp-s", type=float, default=1.0, help="untimed clock ramp before the warm-up steps")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -1230,7 +1230,20 @@ static int step_serial(akmc_handle* h, int64_t n, bool horizon = false, double t
             w.mlp = h->d_mlp; w.tnet = h->d_tnet; w.H = h->world_H; w.tau_act = h->world_tau;
             w.nvox = h->nvox; w.vstart = h->d_vstart; w.n_events = chunk;
             w.nev = h->d_nev; w.term = h->d_term; w.clock = h->d_clock; w.seed = h->cfg.seed; w.ctr = h->d_ctr;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (h->profile) {                          // CUDA events around the launch (mlp_ms)
+                if (h->ev_used + 2 > h->ev.size())
+                    for (int i = 0; i < 64; ++i) {
+                        cudaEvent_t e;
+                        CK(h, cudaEventCreate(&e));
+                        h->ev.push_back(e);
+                    }
+                e0 = h->ev[h->ev_used++];
+                e1 = h->ev[h->ev_used++];
+                CK(h, cudaEventRecord(e0, h->stream));
+            }
             CK(h, launch_world(w, h->num_sms, h->stream));
+            if (h->profile) CK(h, cudaEventRecord(e1, h->stream));
             h->total.kernel_launches += 1;
             h->total.mlp_launches += 1;
             done += chunk;
@@ -1821,7 +1834,7 @@ static int step_common(akmc_handle* h, int64_t n, akmc_counters* ctr, bool horiz
     const auto t1 = std::chrono::steady_clock::now();
     h->total.events += (int64_t)(c1.events - c0.events);
     h->total.hop_evals += (int64_t)(c1.hop_evals - c0.hop_evals);
-    h->total.mlp_rows += ((h->engine && h->sub) || h->serial_engine) ? (int64_t)(c1.mrows - c0.mrows)
+    h->total.mlp_rows += ((h->engine && h->sub) || h->serial_engine || h->world) ? (int64_t)(c1.mrows - c0.mrows)
                                                                       : (int64_t)(c1.hop_evals - c0.hop_evals) / 8;
     h->total.clamps += (int64_t)(c1.clamps - c0.clamps);
     h->total.terminal_voxels += (int64_t)(c1.terminal - c0.terminal);

@@ -43,6 +43,7 @@ struct WorldSmem {
     double h1[kHid], h2[kHid], z[8];
     double hp[kHid];                      // Poisson-net hidden layer
     int cnt[448];
+    double xf[448];                       // pooled Poisson-net input count_f / m
     int4 pos[kWorldMaxVac];
     int slot[kWorldMaxVac];
     int dirty[kWorldMaxVac];
@@ -51,7 +52,7 @@ struct WorldSmem {
 };
 
 // evaluate the voxel's state: windows, (re)evaluate dirty rows, trees, uhat
-__device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox)
+__device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, unsigned long long& rows)
 {
     const int tid = threadIdx.x;
     // windows of all members (thread = (member, slot)); dirty = window differs from the cached evaluation
@@ -75,17 +76,23 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox)
     const double* b3 = W3 + kHid * 8;
     for (int a = 0; a < m; ++a) {
         if (!S.dirty[a]) continue;                      // block-uniform (shared flag after a barrier)
+        ++rows;                                         // a network row actually evaluated (R4 mlp_rows)
+        // (loops unrolled so that many weight loads are in flight ahead of the sequential FP64 chain: the sums keep
+        // the oracle's order, bit for bit)
         const int j = tid;
         double acc = b1[j];
+#pragma unroll 16
         for (int s = 0; s < kWin; ++s) acc = __dadd_rn(acc, W1[(size_t)(kSpecies * s + S.win[a][s]) * kHid + j]);
         S.h1[j] = acc > 0.0 ? acc : 0.0;
         __syncthreads();
         acc = b2[j];
+#pragma unroll 32
         for (int i = 0; i < kHid; ++i) acc = __fma_rn(S.h1[i], W2[(size_t)i * kHid + j], acc);
         S.h2[j] = acc > 0.0 ? acc : 0.0;
         __syncthreads();
         if (j < 8) {
             acc = b3[j];
+#pragma unroll 32
             for (int i = 0; i < kHid; ++i) acc = __fma_rn(S.h2[i], W3[i * 8 + j], acc);
             S.z[j] = acc;                                // raw output = policy logit (no clamp)
         }
@@ -115,13 +122,14 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox)
         atomicAdd(&S.cnt[kSpecies * j + S.win[a][j]], 1);
     }
     __syncthreads();
+    // pooled input x_f = count_f / m, each quotient formed once (the same division the oracle does per use)
+    for (int f = tid; f < 448; f += kWT) S.xf[f] = __ddiv_rn((double)S.cnt[f], (double)m);
+    __syncthreads();
     if (tid < p.H) {
         const int j = tid;
         double acc = p.tnet[448 * (size_t)p.H + j];                    // bt1
-        for (int f = 0; f < 448; ++f) {
-            const double x = __ddiv_rn((double)S.cnt[f], (double)m);
-            acc = __fma_rn(x, p.tnet[(size_t)f * p.H + j], acc);
-        }
+#pragma unroll 16
+        for (int f = 0; f < 448; ++f) acc = __fma_rn(S.xf[f], p.tnet[(size_t)f * p.H + j], acc);
         S.hp[j] = acc > 0.0 ? acc : 0.0;
     }
     __syncthreads();
@@ -150,14 +158,14 @@ __global__ void __launch_bounds__(kWT) world_serial_kernel(const __grid_constant
     extern __shared__ __align__(16) uint8_t wsm[];
     WorldSmem& S = *reinterpret_cast<WorldSmem*>(wsm);
     const int tid = threadIdx.x;
-    unsigned long long events = 0, evals = 0, terminal = 0;
+    unsigned long long events = 0, evals = 0, terminal = 0, rows = 0;
     for (int v = blockIdx.x; v < p.nvox; v += gridDim.x) {
         const int s0 = p.vstart[v], m = p.vstart[v + 1] - s0;
         if (tid < m) { S.slot[tid] = s0 + tid; S.pos[tid] = p.vac[s0 + tid]; }
         for (int t = tid; t < m * kWin; t += kWT) S.cached[t / kWin][t % kWin] = 0xFF;   // nothing cached
         __syncthreads();
         if (p.term[v]) continue;                       // a terminal voxel stays frozen
-        world_eval(p, S, m, v);
+        world_eval(p, S, m, v, rows);
         for (int e = 0; e < p.n_events; ++e) {
             evals += 8ull * (unsigned long long)m;
             if (!(S.wtot > 0.0) || !(S.gtot > 0.0)) {   // no feasible event
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(kWT) world_serial_kernel(const __grid_constant
             __threadfence_block();
             __syncthreads();
             const double u_s = S.uhat, g_s = S.gtot;
-            world_eval(p, S, m, v);                    // s' (also the next event's s)
+            world_eval(p, S, m, v, rows);              // s' (also the next event's s)
             if (tid == 0) {
                 const double dt = dtau_hat_dev(u_s, g_s, S.uhat, S.gtot);
                 const double fl = __ddiv_rn(1e-3, g_s);
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__(kWT) world_serial_kernel(const __grid_constant
         if (events) atomicAdd(&p.ctr->events, events);
         if (evals) atomicAdd(&p.ctr->hop_evals, evals);
         if (terminal) atomicAdd(&p.ctr->terminal, terminal);
+        if (rows) atomicAdd(&p.ctr->mrows, rows);
     }
 }
 

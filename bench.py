@@ -519,6 +519,7 @@ def run_ours(args):
                            "vacancies_per_gpu": pr.n_vac_per_voxel * cfg.n_voxels,
                            "domain_cells": list(cfg.domain_cells), "lambda": args.lam, "window_s": cfg.window_s,
                            "step": ("one sweep (8 sublattice phases)" if pr.domain[0] else
+                                    f"{nstep} world-model events per voxel (one world-kernel launch)" if wnets else
                                     f"{nstep} BKL events per voxel (one engine launch)"),
                            "temperature_K": ("per voxel, uniform 558-577" if vT is not None else cfg.temperature_K),
                            "model": ("world-model mode: policy logits -E/kT of the physics-embedded MLP (tau_act 1), "

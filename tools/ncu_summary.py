@@ -50,7 +50,8 @@ def full(rep, out):
     def num(name):
         v, u = get.get(name, ("nan", ""))
         x = float(v.replace(",", ""))
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+                 "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6}
         return x * scale.get(u, 1), u
     rd, _ = num("dram__bytes_read.sum")
     wr, _ = num("dram__bytes_write.sum")

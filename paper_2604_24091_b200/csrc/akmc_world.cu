@@ -68,6 +68,29 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, u
         if (S.win[a][j] != S.cached[a][j]) S.dirty[a] = 1;
     }
     __syncthreads();
+    // Poisson-time network input on the pooled windows (counts of the 448 one-hot features, x_f = count_f / m, each
+    // quotient formed once -- the same division the oracle does per use): it needs only the windows, so its hidden
+    // chains can run beside the barrier network's last stage below
+    for (int f = tid; f < 448; f += kWT) S.cnt[f] = 0;
+    __syncthreads();
+    for (int t = tid; t < m * kWin; t += kWT) {
+        const int a = t / kWin, j = t % kWin;
+        atomicAdd(&S.cnt[kSpecies * j + S.win[a][j]], 1);
+    }
+    __syncthreads();
+    for (int f = tid; f < 448; f += kWT) S.xf[f] = __ddiv_rn((double)S.cnt[f], (double)m);
+    int last_dirty = -1;
+    for (int a = 0; a < m; ++a) if (S.dirty[a]) last_dirty = a;       // (block-uniform: shared flags)
+    __syncthreads();
+    // the Poisson net's hidden unit j: one sequential fma chain over f (the oracle's order); threads 32 .. 32 + H
+    // (beside the last dirty row's layer 3 / rates on threads 0-7), else after the rows on threads 0 .. H
+    auto poisson_hidden = [&](int j) {
+        double acc = p.tnet[448 * (size_t)p.H + j];                    // bt1
+#pragma unroll 16
+        for (int f = 0; f < 448; ++f) acc = __fma_rn(S.xf[f], p.tnet[(size_t)f * p.H + j], acc);
+        S.hp[j] = acc > 0.0 ? acc : 0.0;
+    };
+    const bool pois_beside = last_dirty >= 0 && p.H <= kWT - 32;
     const double* W1 = p.mlp;
     const double* b1 = W1 + 448 * kHid;
     const double* W2 = b1 + kHid;
@@ -94,14 +117,10 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, u
             acc = b3[j];
 #pragma unroll 32
             for (int i = 0; i < kHid; ++i) acc = __fma_rn(S.h2[i], W3[i * 8 + j], acc);
-            S.z[j] = acc;                                // raw output = policy logit (no clamp)
-        }
-        __syncthreads();
-        if (j < 8) {
-            // Eq. 1 mask and temperature; physical pair-KRA rate of the same hop
+            // Eq. 1 mask and temperature on the raw output (the policy logit, no clamp); physical pair-KRA rate
             double w = 0.0, g = 0.0;
             if (S.win[a][j] != (uint8_t)kVac) {
-                double zh = __ddiv_rn(S.z[j], p.tau_act);
+                double zh = __ddiv_rn(acc, p.tau_act);
                 if (zh > 700.0) zh = 700.0;
                 w = det_exp(zh);
                 double E = 0.0;
@@ -110,34 +129,23 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, u
             }
             S.W[a][j] = w;
             S.G[a][j] = g;
+        } else if (pois_beside && a == last_dirty && tid >= 32 && tid < 32 + p.H) {
+            poisson_hidden(tid - 32);
         }
         if (j < kWin) S.cached[a][j] = S.win[a][j];
         __syncthreads();
     }
-    // Poisson-time network on the pooled windows: counts of the 448 one-hot features
-    for (int f = tid; f < 448; f += kWT) S.cnt[f] = 0;
-    __syncthreads();
-    for (int t = tid; t < m * kWin; t += kWT) {
-        const int a = t / kWin, j = t % kWin;
-        atomicAdd(&S.cnt[kSpecies * j + S.win[a][j]], 1);
+    if (!pois_beside) {
+        if (tid < p.H) poisson_hidden(tid);
+        __syncthreads();
     }
-    __syncthreads();
-    // pooled input x_f = count_f / m, each quotient formed once (the same division the oracle does per use)
-    for (int f = tid; f < 448; f += kWT) S.xf[f] = __ddiv_rn((double)S.cnt[f], (double)m);
-    __syncthreads();
-    if (tid < p.H) {
-        const int j = tid;
-        double acc = p.tnet[448 * (size_t)p.H + j];                    // bt1
-#pragma unroll 16
-        for (int f = 0; f < 448; ++f) acc = __fma_rn(S.xf[f], p.tnet[(size_t)f * p.H + j], acc);
-        S.hp[j] = acc > 0.0 ? acc : 0.0;
-    }
-    __syncthreads();
+    // serial tail, two threads of different warps at once: uhat (thread 0); member sums and trees (thread 32)
     if (tid == 0) {
         const double* wt2 = p.tnet + 448 * (size_t)p.H + p.H;
         double y = wt2[p.H];                                           // bt2
         for (int j = 0; j < p.H; ++j) y = __fma_rn(S.hp[j], wt2[j], y);
         S.uhat = m > 0 ? softplus_dev(y) : 0.0;
+    } else if (tid == 32) {
         // per-member sums in hop order, then the canonical trees (A17); Rw keeps the policy tree
         for (int a = 0; a < m; ++a) {
             double sw = 0.0, sg = 0.0;

@@ -86,7 +86,7 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, u
     // (beside the last dirty row's layer 3 / rates on threads 0-7), else after the rows on threads 0 .. H
     auto poisson_hidden = [&](int j) {
         double acc = p.tnet[448 * (size_t)p.H + j];                    // bt1
-#pragma unroll 16
+#pragma unroll 32
         for (int f = 0; f < 448; ++f) acc = __fma_rn(S.xf[f], p.tnet[(size_t)f * p.H + j], acc);
         S.hp[j] = acc > 0.0 ? acc : 0.0;
     };
@@ -104,7 +104,7 @@ __device__ void world_eval(const WorldParams& p, WorldSmem& S, int m, int vox, u
         // the oracle's order, bit for bit)
         const int j = tid;
         double acc = b1[j];
-#pragma unroll 16
+#pragma unroll 32
         for (int s = 0; s < kWin; ++s) acc = __dadd_rn(acc, W1[(size_t)(kSpecies * s + S.win[a][s]) * kHid + j]);
         S.h1[j] = acc > 0.0 ? acc : 0.0;
         __syncthreads();

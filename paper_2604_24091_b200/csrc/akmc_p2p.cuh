@@ -160,12 +160,14 @@ __device__ __forceinline__ void unpack_p2p(const int4* __restrict__ mbox, unsign
             const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&buf[1 + i]);
             unsigned long long a, b;
             const unsigned long long t0 = globaltimer_ns();
+            bool arrived = true;
             for (;;) {
                 a = ld_relaxed_sys_u64(src);
                 b = ld_relaxed_sys_u64(src + 1);
                 if ((uint32_t)(b >> 32) == tag && (uint32_t)(a >> 48) == (tag & 0xFFFFu)) break;
-                if (globaltimer_ns() - t0 > 30000000000ull) { atomicOr(overflow, kExchangeTimeout); break; }
+                if (globaltimer_ns() - t0 > 30000000000ull) { atomicOr(overflow, kExchangeTimeout); arrived = false; break; }
             }
+            if (!arrived) continue;                      // (reported; a stale word is never applied)
             const int gp[3] = {(int)(a & 0xFFFFu), (int)((a >> 16) & 0xFFFFu), (int)((a >> 32) & 0xFFFFu)};
             const int w = (int)(uint32_t)b;
             int lp[3];

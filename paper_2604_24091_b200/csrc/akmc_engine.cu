@@ -45,6 +45,12 @@
 #ifndef AKMC_CHAIN_NRUN         //  per sweep with 64; gated to the tail (<= 4 / 16 running domains) 1.97 / 2.04)
 #define AKMC_CHAIN_NRUN 1024    // ... only while the CTA holds at most this many running domains
 #endif
+#ifndef AKMC_ENGINE_L1_ROWS
+#define AKMC_ENGINE_L1_ROWS 2   // layer-1 rows per warp call in the engine, W1' rows per row in flight (A/B: 4 x 1,
+#endif                          // no spills, 2.05 vs 1.97 ms per C5 sweep)
+#ifndef AKMC_ENGINE_L1_BATCH
+#define AKMC_ENGINE_L1_BATCH 2
+#endif
 #ifndef AKMC_SERIAL_CLOCK
 #define AKMC_SERIAL_CLOCK 1     // serial mode: voxel clock cached in the slot (no per-event global load)
 #endif
@@ -55,6 +61,7 @@
 namespace akmc {
 
 namespace {
+constexpr int kEL1Rows = AKMC_ENGINE_L1_ROWS, kEL1Batch = AKMC_ENGINE_L1_BATCH;
 using namespace ptx;
 
 constexpr int kThreads = 256;
@@ -1078,14 +1085,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
             // ---- FP32-equivalent evaluator: rounds in lockstep over the cluster
             if (phase_mode) {
                 // memo insert, part 1, for every miss of this iteration: way 1 <- way 0, way 0 key <- window
-                // (E3 fills way 0's rates); a warp moves kL1Rows entries at a time
+                // (E3 fills way 0's rates); a warp moves kEL1Rows entries at a time
                 const int nmiss = c.nmiss;
-                for (int q0 = warp; q0 < nmiss; q0 += kL1Rows * kWarps) {
-                    MemoEntry* me[kL1Rows];
-                    uint4 tm[kL1Rows];
-                    uint32_t kw[kL1Rows];
+                for (int q0 = warp; q0 < nmiss; q0 += kEL1Rows * kWarps) {
+                    MemoEntry* me[kEL1Rows];
+                    uint4 tm[kEL1Rows];
+                    uint32_t kw[kEL1Rows];
 #pragma unroll
-                    for (int q = 0; q < kL1Rows; ++q) {
+                    for (int q = 0; q < kEL1Rows; ++q) {
                         const int qq = q0 + q * kWarps;
                         tm[q] = make_uint4(0, 0, 0, 0);
                         kw[q] = 0;
@@ -1098,11 +1105,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         }
                     }
 #pragma unroll
-                    for (int q = 0; q < kL1Rows; ++q)
+                    for (int q = 0; q < kEL1Rows; ++q)
                         if (me[q] && lane < 9) reinterpret_cast<uint4*>(&me[q][1])[lane] = tm[q];
                     __syncwarp();
 #pragma unroll
-                    for (int q = 0; q < kL1Rows; ++q)
+                    for (int q = 0; q < kEL1Rows; ++q)
                         if (me[q] && lane < 16) reinterpret_cast<uint32_t*>(me[q][0].key)[lane] = kw[q];
                 }
             }
@@ -1113,15 +1120,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                 if (phase_mode) {
                     own_n = min(kRoundRows, max(0, c.nmiss - kRoundRows * k_round));
                     // layer 1 of this round's own rows (two per warp at a time); memo way 1 <- way 0, key <- window
-                    for (int i = warp; i < own_n; i += kL1Rows * kWarps) {
-                        const int nv = min(kL1Rows, (own_n - i + kWarps - 1) / kWarps);
-                        int rr[kL1Rows], mr[kL1Rows];
+                    for (int i = warp; i < own_n; i += kEL1Rows * kWarps) {
+                        const int nv = min(kEL1Rows, (own_n - i + kWarps - 1) / kWarps);
+                        int rr[kEL1Rows], mr[kEL1Rows];
 #pragma unroll
-                        for (int q = 0; q < kL1Rows; ++q) {
+                        for (int q = 0; q < kEL1Rows; ++q) {
                             rr[q] = c.miss[kRoundRows * k_round + (q < nv ? i + q * kWarps : i)];
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast, p.W.h1s,
+                        layer1_rows<kEL1Rows, kEL1Batch>(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                                                         fast, p.W.h1s,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) {
@@ -1155,15 +1163,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
                         l1_list_store(i, a0, a1, l1n, l1l);
                     }
                     __syncwarp();
-                    for (int i = warp; i < own_n; i += kL1Rows * kWarps) {
-                        const int nv = min(kL1Rows, (own_n - i + kWarps - 1) / kWarps);
-                        int rr[kL1Rows], mr[kL1Rows];
+                    for (int i = warp; i < own_n; i += kEL1Rows * kWarps) {
+                        const int nv = min(kEL1Rows, (own_n - i + kWarps - 1) / kWarps);
+                        int rr[kEL1Rows], mr[kEL1Rows];
 #pragma unroll
-                        for (int q = 0; q < kL1Rows; ++q) {
+                        for (int q = 0; q < kEL1Rows; ++q) {
                             rr[q] = q < nv ? i + q * kWarps : i;
                             mr[q] = kRoundRows * (int)rank + i + q * kWarps;
                         }
-                        layer1_rows(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf, fast, p.W.h1s,
+                        layer1_rows<kEL1Rows, kEL1Batch>(rr, nv, win, l1n, l1l, p.W.W1f, mr, A_hi, A_lo, g_hi, g_lo, ovf,
+                                                         fast, p.W.h1s,
                                     (AKMC_L1_PROBE && tid == 0 && p.diag) ? d_z : nullptr);
                     }
                     if (tid == 0) { hdr[rank].n = own_n; hdr[rank].more = 0; hdr[rank].alive = own_n > 0 ? 1 : 0; }

@@ -166,13 +166,17 @@ __device__ __forceinline__ void l1_store(const double (&acc)[8], int m, uint8_t*
 
 // layer 1 of up to kL1Rows rows (one warp), all loads of a batch in flight at once; b1s = a shared-memory copy
 // of b1' (row 0 of W1'), or nullptr to read it from W1f (same values, so the same bits)
+// (R rows per call, B W1' rows per row per batch: a per-kernel register trade-off; the per-row sum order -- b1' then
+// the listed rows in slot order -- is the same for every R and B, so are the bits)
 constexpr int kL1Rows = AKMC_L1_ROWS;
-__device__ __forceinline__ void layer1_rows(const int (&rr)[kL1Rows], int nv, const uint8_t* win, const uint8_t* l1n,
+template <int kR = kL1Rows, int kB = kL1Batch>
+__device__ __forceinline__ void layer1_rows(const int (&rr)[kR], int nv, const uint8_t* win, const uint8_t* l1n,
                                             const uint16_t* l1l, const float* __restrict__ W1f,
-                                            const int (&m)[kL1Rows], uint8_t* A_hi, uint8_t* A_lo,
+                                            const int (&m)[kR], uint8_t* A_hi, uint8_t* A_lo,
                                             uint8_t* g_hi, uint8_t* g_lo, unsigned long long& ovf, bool fast,
                                             float sc, long long* lp = nullptr, const float* b1s = nullptr)
 {
+    constexpr int kL1Rows = kR, kL1Batch = kB;
     const int lane = threadIdx.x & 31;
     long long t0 = lp ? clock64() : 0;
     auto plap = [&](int i) { if (lp) { const long long t = clock64(); lp[i] += t - t0; t0 = t; } };

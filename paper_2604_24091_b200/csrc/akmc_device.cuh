@@ -97,7 +97,11 @@ __device__ __forceinline__ double det_exp(double x)
     p = __fma_rn(p, r, c6);  p = __fma_rn(p, r, c5);  p = __fma_rn(p, r, c4);
     p = __fma_rn(p, r, c3);  p = __fma_rn(p, r, c2);  p = __fma_rn(p, r, c1);
     p = __fma_rn(p, r, c0);
-    return ldexp(p, (int)k);
+    // p * 2^k: for |k| <= 1000 (every caller's range) 2^k is a normal double and the product with p in [0.7, 1.5)
+    // is exact and normal, so one multiply by the constructed power gives ldexp's bits
+    const int ki = (int)k;
+    if (ki >= -1000 && ki <= 1000) return __dmul_rn(p, __longlong_as_double((long long)(ki + 1023) << 52));
+    return ldexp(p, ki);
 }
 
 __device__ __forceinline__ double det_log(double u)

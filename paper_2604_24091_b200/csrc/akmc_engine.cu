@@ -31,7 +31,7 @@
 #define AKMC_REFILL_FAST 1      // skip slot placement when nothing is pending (-2 %)
 #endif
 #ifndef AKMC_GATHER_ROWS
-#define AKMC_GATHER_ROWS 8      // gather rows per warp in flight
+#define AKMC_GATHER_ROWS 8      // gather rows per warp in flight (A/B at round-2 HEAD: 12 -> same, 16 -> +8 %)
 #endif
 #ifndef AKMC_PREFETCH
 #define AKMC_PREFETCH 0         // L2 prefetch of the next window/memo at hop/placement (+1.6 %, slower)

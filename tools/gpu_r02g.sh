@@ -1,7 +1,8 @@
-# 2-GPU box: bulk v2 correctness + timing (1 GPU), then the 2-rank C5 bench (p2p) under a watchdog
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build=$?
-timeout 600 python -m pytest tests/test_gpu_guards.py -q -k "bulk or crowded or large_activ or overflow or resume" -p no:cacheprovider --timeout 300 > gpurun_out/pytest_bulk2_r02g.log 2>&1; echo bulktests=$?
-AKMC_PHASE_TIMING=1 python tools/bulk_probe.py 5 > gpurun_out/bulk_probe2.log 2>&1; echo probe=$?
-AKMC_WATCHDOG=1 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29502 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/scale_c5_n2b.json 2> gpurun_out/scale_c5_n2b.err; echo scale2=$?
-tail -5 gpurun_out/pytest_bulk2_r02g.log; cat gpurun_out/bulk_probe2.log | grep -v "^\[akmc iter\|engine" | tail -8
-tail -c 400 gpurun_out/scale_c5_n2b.json; grep -v "^  " gpurun_out/scale_c5_n2b.err | tail -20
+# engine gather rows in flight per warp: 8 (default) vs 12 vs 16 (A/B, same box)
+for rep in 1 2; do
+for v in "" _g12 _g16; do
+  if [ -n "$v" ]; then export AKMC_LIB=paper_2604_24091_b200/lib/libakmc$v.so; else unset AKMC_LIB; fi
+  timeout 600 python bench.py --no-cpu-baseline --steps 20 --warmup 5 > gpurun_out/bg$v$rep.json 2>/dev/null
+  python -c "import json; d=json.loads(open('gpurun_out/bg$v$rep.json').read().strip().splitlines()[-1]); print('g$v', $rep, d['value'], d['ms_per_step'])"
+done
+done

@@ -21,6 +21,31 @@
 
 using namespace akmc;
 
+
+// Device memory of a handle comes from the device's default stream-ordered pool with an unlimited release
+// threshold: what akmc_free returns stays reserved in the process, so the next handle (a restart, bench.py's e2e
+// handle) reuses it instead of paying the driver's fresh mapping of gigabytes again.  (The IPC-shared mailboxes of
+// the multi-GPU exchange keep cudaMalloc: pool memory is not exportable through cudaIpcGetMemHandle.)
+template <typename T>
+static cudaError_t pool_malloc(T** p, size_t n)
+{
+    *p = nullptr;
+    if (n == 0) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&pool, dev);
+    if (e == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    void* q = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync(&q, n, (cudaStream_t)0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)0);   // usable from any stream from here on
+    if (e == cudaSuccess) *p = static_cast<T*>(q);
+    return e;
+}
+
 namespace {
 
 thread_local std::string g_init_error;
@@ -470,21 +495,21 @@ int prepare_engine_weights(akmc_handle* h, const double* mlp)
         for (int k = 0; k < kHid; ++k)
             for (int n = 0; n < kHid; ++n)
                 put_split(w2f.data() + (size_t)(k / 16) * w2s, kHid, n, k % 16, std::ldexp(W2[(size_t)k * kHid + n], s2));
-        CK(h, cudaMalloc(&h->d_W2full, w2f.size()));
+        CK(h, pool_malloc(&h->d_W2full, w2f.size()));
         CK(h, cudaMemcpy(h->d_W2full, w2f.data(), w2f.size(), cudaMemcpyHostToDevice));
-        CK(h, cudaMalloc(&h->d_W1f, w1f.size() * sizeof(float)));
-        CK(h, cudaMalloc(&h->d_W2e, w2e.size()));
-        CK(h, cudaMalloc(&h->d_W3d, (size_t)kHid * 8 * sizeof(double)));
+        CK(h, pool_malloc(&h->d_W1f, w1f.size() * sizeof(float)));
+        CK(h, pool_malloc(&h->d_W2e, w2e.size()));
+        CK(h, pool_malloc(&h->d_W3d, (size_t)kHid * 8 * sizeof(double)));
         CK(h, cudaMemcpy(h->d_W1f, w1f.data(), w1f.size() * sizeof(float), cudaMemcpyHostToDevice));
         CK(h, cudaMemcpy(h->d_W2e, w2e.data(), w2e.size(), cudaMemcpyHostToDevice));
         CK(h, cudaMemcpy(h->d_W3d, W3, (size_t)kHid * 8 * sizeof(double), cudaMemcpyHostToDevice));
     }
-    CK(h, cudaMalloc(&h->d_b2, kHid * 4));
-    CK(h, cudaMalloc(&h->d_b3, 8 * 8));
+    CK(h, pool_malloc(&h->d_b2, kHid * 4));
+    CK(h, pool_malloc(&h->d_b3, 8 * 8));
     CK(h, cudaMemcpy(h->d_b2, b2f.data(), kHid * 4, cudaMemcpyHostToDevice));
     CK(h, cudaMemcpy(h->d_b3, b3, 8 * 8, cudaMemcpyHostToDevice));
     if (std::getenv("AKMC_PHASE_TIMING")) {
-        CK(h, cudaMalloc(&h->d_phase_cycles, kDiagWords * sizeof(unsigned long long)));
+        CK(h, pool_malloc(&h->d_phase_cycles, kDiagWords * sizeof(unsigned long long)));
         CK(h, cudaMemset(h->d_phase_cycles, 0, kDiagWords * sizeof(unsigned long long)));
     }
     return AKMC_OK;
@@ -658,8 +683,8 @@ int halo_fill(akmc_handle* h)
         const int minus = rank_of(c, h->rc[0] - e[0], h->rc[1] - e[1], h->rc[2] - e[2]);
         const int plus = rank_of(c, h->rc[0] + e[0], h->rc[1] + e[1], h->rc[2] + e[2]);
         uint8_t *sb = nullptr, *rb = nullptr;
-        CK(h, cudaMalloc(&sb, bytes));
-        CK(h, cudaMalloc(&rb, bytes));
+        CK(h, pool_malloc(&sb, bytes));
+        CK(h, pool_malloc(&rb, bytes));
         const unsigned grid = (unsigned)h->num_sms * 4u;
         // lower face -> minus neighbour's upper halo; upper face -> plus neighbour's lower halo
         pack_slab_kernel<<<grid, 256, 0, h->stream>>>(h->d_species, h->F, face_lo, sb);
@@ -710,8 +735,8 @@ int setup_p2p(akmc_handle* h)
     const size_t per = (size_t)(h->DP.cap + 1);
     CK(h, cudaMalloc(&h->d_mbox, std::max<size_t>(1, (size_t)np * 2 * per) * sizeof(int4)));
     CK(h, cudaMalloc(&h->d_mflag, kMaxPeers * sizeof(unsigned long long)));
-    CK(h, cudaMalloc(&h->d_pcnt, kMaxPeers * sizeof(int)));
-    CK(h, cudaMalloc(&h->d_pdone, sizeof(unsigned int)));
+    CK(h, pool_malloc(&h->d_pcnt, kMaxPeers * sizeof(int)));
+    CK(h, pool_malloc(&h->d_pdone, sizeof(unsigned int)));
     CK(h, cudaMemset(h->d_mbox, 0, std::max<size_t>(1, (size_t)np * 2 * per) * sizeof(int4)));
     CK(h, cudaMemset(h->d_mflag, 0, kMaxPeers * sizeof(unsigned long long)));
     CK(h, cudaMemset(h->d_pcnt, 0, kMaxPeers * sizeof(int)));
@@ -721,8 +746,8 @@ int setup_p2p(akmc_handle* h)
     CK(h, cudaIpcGetMemHandle(&mine[1], h->d_mflag));
     const size_t hb = sizeof(mine);
     uint8_t *d_h = nullptr, *d_all = nullptr;
-    CK(h, cudaMalloc(&d_h, hb));
-    CK(h, cudaMalloc(&d_all, hb * c.world));
+    CK(h, pool_malloc(&d_h, hb));
+    CK(h, pool_malloc(&d_all, hb * c.world));
     CK(h, cudaMemcpy(d_h, mine, hb, cudaMemcpyHostToDevice));
     NCK(h, ncclAllGather(d_h, d_all, hb, ncclChar, h->comm, h->stream));
     std::vector<cudaIpcMemHandle_t> all((size_t)2 * c.world);
@@ -771,15 +796,15 @@ int init_multi(akmc_handle* h)
     h->DP.cap = 8192;
     h->S.logcap = 1 << 17;
     const size_t per = (size_t)(h->DP.cap + 1);
-    CK(h, cudaMalloc(&h->d_log, (size_t)h->S.logcap * sizeof(int4)));
-    CK(h, cudaMalloc(&h->d_nlog, sizeof(unsigned long long)));
-    CK(h, cudaMalloc(&h->d_send, std::max<size_t>(2, np) * per * sizeof(int4)));     // (shift: 2 buffers per axis)
-    CK(h, cudaMalloc(&h->d_recv, std::max<size_t>(2, np) * per * sizeof(int4)));
-    CK(h, cudaMalloc(&h->d_dist_overflow, sizeof(int)));
-    CK(h, cudaMalloc(&h->d_gid, (size_t)h->vcap * sizeof(int)));
-    CK(h, cudaMalloc(&h->d_nvac, sizeof(int)));
-    CK(h, cudaMalloc(&h->d_free, (size_t)h->vcap * sizeof(int)));
-    CK(h, cudaMalloc(&h->d_fcnt, 4 * sizeof(int)));
+    CK(h, pool_malloc(&h->d_log, (size_t)h->S.logcap * sizeof(int4)));
+    CK(h, pool_malloc(&h->d_nlog, sizeof(unsigned long long)));
+    CK(h, pool_malloc(&h->d_send, std::max<size_t>(2, np) * per * sizeof(int4)));     // (shift: 2 buffers per axis)
+    CK(h, pool_malloc(&h->d_recv, std::max<size_t>(2, np) * per * sizeof(int4)));
+    CK(h, pool_malloc(&h->d_dist_overflow, sizeof(int)));
+    CK(h, pool_malloc(&h->d_gid, (size_t)h->vcap * sizeof(int)));
+    CK(h, pool_malloc(&h->d_nvac, sizeof(int)));
+    CK(h, pool_malloc(&h->d_free, (size_t)h->vcap * sizeof(int)));
+    CK(h, pool_malloc(&h->d_fcnt, 4 * sizeof(int)));
     CK(h, cudaMemset(h->d_fcnt, 0, 4 * sizeof(int)));
     h->S.freelist = h->d_free;
     h->S.fcnt = h->d_fcnt;
@@ -801,8 +826,8 @@ int init_multi(akmc_handle* h)
         mine[(size_t)i] = 2 * (gx + (long long)h->S.Gc[0] * (gy + (long long)h->S.Gc[1] * gz)) + (p.y & 1);
     }
     long long *d_cnt = nullptr, *d_all = nullptr, *d_mine = nullptr, *d_gath = nullptr;
-    CK(h, cudaMalloc(&d_cnt, sizeof(long long)));
-    CK(h, cudaMalloc(&d_all, c.world * sizeof(long long)));
+    CK(h, pool_malloc(&d_cnt, sizeof(long long)));
+    CK(h, pool_malloc(&d_all, c.world * sizeof(long long)));
     const long long cnt = h->nvac;
     CK(h, cudaMemcpy(d_cnt, &cnt, sizeof(long long), cudaMemcpyHostToDevice));
     NCK(h, ncclAllGather(d_cnt, d_all, 1, ncclInt64, h->comm, h->stream));
@@ -813,8 +838,8 @@ int init_multi(akmc_handle* h)
     for (long long x : counts) mx = std::max(mx, x);
     std::vector<long long> pad((size_t)mx, LLONG_MAX);
     std::copy(mine.begin(), mine.end(), pad.begin());
-    CK(h, cudaMalloc(&d_mine, (size_t)mx * sizeof(long long)));
-    CK(h, cudaMalloc(&d_gath, (size_t)mx * c.world * sizeof(long long)));
+    CK(h, pool_malloc(&d_mine, (size_t)mx * sizeof(long long)));
+    CK(h, pool_malloc(&d_gath, (size_t)mx * c.world * sizeof(long long)));
     CK(h, cudaMemcpy(d_mine, pad.data(), (size_t)mx * sizeof(long long), cudaMemcpyHostToDevice));
     NCK(h, ncclAllGather(d_mine, d_gath, (size_t)mx, ncclInt64, h->comm, h->stream));
     std::vector<long long> all((size_t)mx * c.world);
@@ -831,8 +856,8 @@ int init_multi(akmc_handle* h)
     if (ex && std::strcmp(ex, "shift") == 0) {
         h->shift = true;
         h->slistcap = h->S.logcap + 6 * (h->DP.cap + 1);
-        CK(h, cudaMalloc(&h->d_slist, (size_t)h->slistcap * sizeof(int4)));
-        CK(h, cudaMalloc(&h->d_nslist, sizeof(int)));
+        CK(h, pool_malloc(&h->d_slist, (size_t)h->slistcap * sizeof(int4)));
+        CK(h, pool_malloc(&h->d_nslist, sizeof(int)));
     } else if (!(ex && std::strcmp(ex, "nccl") == 0) &&
                2 * std::max(h->DP.G[0], std::max(h->DP.G[1], h->DP.G[2])) < 65536) {
         // (the tagged mailbox entries carry 16-bit global half-cell coordinates; larger global lattices use NCCL)
@@ -943,11 +968,11 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     CKI(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
     lap("context + stream");
-    CKI(cudaMalloc(&h->d_species, (size_t)h->sites));        // canonical upload buffer (temporary)
+    CKI(pool_malloc(&h->d_species, (size_t)h->sites));        // canonical upload buffer (temporary)
     lap("malloc canonical buffer");
     CKI(cudaMemcpy(h->d_species, species, (size_t)h->sites, cudaMemcpyHostToDevice));
     lap("H2D lattice");
-    CKI(cudaMalloc(&h->d_ctr, sizeof(DevCounters)));
+    CKI(pool_malloc(&h->d_ctr, sizeof(DevCounters)));
     CKI(cudaMemset(h->d_ctr, 0, sizeof(DevCounters)));
     CKI(cudaMallocHost(&h->h_ctr, sizeof(DevCounters)));
 
@@ -958,9 +983,9 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         int* d_bc = nullptr;
         unsigned int* d_max = nullptr;
         long long* d_tot = nullptr;
-        CKI(cudaMalloc(&d_bc, (size_t)nblk * sizeof(int)));
+        CKI(pool_malloc(&d_bc, (size_t)nblk * sizeof(int)));
         h->d_iscratch = d_bc;                                    // freed with the handle on error
-        CKI(cudaMalloc(&d_max, sizeof(unsigned int) + sizeof(long long) * 2));
+        CKI(pool_malloc(&d_max, sizeof(unsigned int) + sizeof(long long) * 2));
         h->d_overflow = reinterpret_cast<unsigned long long*>(d_max);
         d_tot = reinterpret_cast<long long*>(reinterpret_cast<char*>(d_max) + 8);
         CKI(cudaMemset(d_max, 0, sizeof(unsigned int) + sizeof(long long) * 2));
@@ -987,12 +1012,12 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
             if (want > INT32_MAX / 16) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many vacancies per rank for the slot capacity"); }
             h->vcap = (int)std::max<int64_t>(want, 1);
         }
-        CKI(cudaMalloc(&h->d_vac, (size_t)h->vcap * sizeof(int4)));
+        CKI(pool_malloc(&h->d_vac, (size_t)h->vcap * sizeof(int4)));
         // slots beyond nvac (vcap >= 1 even with no vacancy; multi-rank spare capacity) start departed (x < 0):
         // the activation reads vcap slots and must never see an uninitialised record as a vacancy
         CKI(cudaMemsetAsync(h->d_vac, 0xFF, (size_t)h->vcap * sizeof(int4), h->stream));
         scan_write_kernel<<<nblk, kScanThreads, 0, h->stream>>>(sp4, nwords, d_bc, h->F, h->d_vac);
-        CKI(cudaMalloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
+        CKI(pool_malloc(&h->d_vstart, (h->nvox + 1) * sizeof(int)));
         vstart_kernel<<<blocks_for(h->nvox + 1, 128), 128, 0, h->stream>>>(h->d_vac, (int)h->nvac, h->nvox, h->d_vstart);
         CKI(cudaGetLastError());
         CKI(cudaStreamSynchronize(h->stream));
@@ -1001,7 +1026,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         lap("vacancy scan");
         if (!h->sub) {
             unsigned long long* d_comp = nullptr;
-            CKI(cudaMalloc(&d_comp, (size_t)h->nvox * 8 * sizeof(unsigned long long)));
+            CKI(pool_malloc(&d_comp, (size_t)h->nvox * 8 * sizeof(unsigned long long)));
             CKI(cudaMemsetAsync(d_comp, 0, (size_t)h->nvox * 8 * sizeof(unsigned long long), h->stream));
             const unsigned bx = (unsigned)std::min<long long>(64, std::max<long long>(1, h->csites / 16 / 256));
             voxel_comp_kernel<<<dim3(bx, (unsigned)h->nvox), 256, 0, h->stream>>>(h->d_species, h->csites, d_comp);
@@ -1013,7 +1038,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         }
         // storage layout with halo ghosts (periodic images)
         uint8_t* st = nullptr;
-        CKI(cudaMalloc(&st, (size_t)h->ssites));
+        CKI(pool_malloc(&st, (size_t)h->ssites));
         lap("malloc storage");
         const long long nlines = 16ll * h->F.NB[0] * h->F.NB[1] * h->F.NB[2] * h->nvox;
         scatter_storage_kernel<<<blocks_for(nlines, 256), 256, 0, h->stream>>>(h->d_species, st, h->F, h->nvox);
@@ -1026,18 +1051,18 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     lap("scatter to bricks");
     const size_t nv = (size_t)h->vcap;
-    CKI(cudaMalloc(&h->d_rates, nv * 8 * sizeof(double)));
-    CKI(cudaMalloc(&h->d_E, nv * 8 * sizeof(double)));
-    CKI(cudaMalloc(&h->d_R, nv * sizeof(double)));
-    CKI(cudaMalloc(&h->d_scratch, (4 * nv + 64) * sizeof(double)));
-    CKI(cudaMalloc(&h->d_iscratch, (nv + 16) * sizeof(int)));
-    CKI(cudaMalloc(&h->d_clock, h->nvox * sizeof(double)));
+    CKI(pool_malloc(&h->d_rates, nv * 8 * sizeof(double)));
+    CKI(pool_malloc(&h->d_E, nv * 8 * sizeof(double)));
+    CKI(pool_malloc(&h->d_R, nv * sizeof(double)));
+    CKI(pool_malloc(&h->d_scratch, (4 * nv + 64) * sizeof(double)));
+    CKI(pool_malloc(&h->d_iscratch, (nv + 16) * sizeof(int)));
+    CKI(pool_malloc(&h->d_clock, h->nvox * sizeof(double)));
     CKI(cudaMemset(h->d_clock, 0, h->nvox * sizeof(double)));
-    CKI(cudaMalloc(&h->d_nev, h->nvox * sizeof(long long)));
+    CKI(pool_malloc(&h->d_nev, h->nvox * sizeof(long long)));
     CKI(cudaMemset(h->d_nev, 0, h->nvox * sizeof(long long)));
-    CKI(cudaMalloc(&h->d_term, h->nvox * sizeof(int)));
+    CKI(pool_malloc(&h->d_term, h->nvox * sizeof(int)));
     CKI(cudaMemset(h->d_term, 0, h->nvox * sizeof(int)));
-    CKI(cudaMalloc(&h->d_overflow, sizeof(unsigned long long)));
+    CKI(pool_malloc(&h->d_overflow, sizeof(unsigned long long)));
     CKI(cudaMemset(h->d_overflow, 0, sizeof(unsigned long long)));
     if (h->sub) {
         for (int a = 0; a < 3; ++a) {
@@ -1049,18 +1074,18 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->S.seed = cfg->seed;
         h->ndom_total = h->S.ndom_vox * h->nvox;
         if (h->ndom_total >= 0xFFFFFFFFll) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_INVALID, "too many domains for 32-bit domain ids (A16)"); }
-        CKI(cudaMalloc(&h->d_dmin, h->ndom_total * sizeof(int)));
-        CKI(cudaMalloc(&h->d_head, h->ndom_total * sizeof(int)));
+        CKI(pool_malloc(&h->d_dmin, h->ndom_total * sizeof(int)));
+        CKI(pool_malloc(&h->d_head, h->ndom_total * sizeof(int)));
         fill_int_kernel<<<blocks_for(h->ndom_total, 256), 256, 0, h->stream>>>(h->d_dmin, h->ndom_total, INT_MAX);
         fill_int_kernel<<<blocks_for(h->ndom_total, 256), 256, 0, h->stream>>>(h->d_head, h->ndom_total, -1);
         CKI(cudaGetLastError());
-        CKI(cudaMalloc(&h->d_next, nv * sizeof(int)));
-        CKI(cudaMalloc(&h->d_members, nv * sizeof(int)));
-        CKI(cudaMalloc(&h->d_mpos, nv * sizeof(int4)));
-        CKI(cudaMalloc(&h->d_rows, nv * sizeof(int)));
-        CKI(cudaMalloc(&h->d_segs, nv * sizeof(Segment)));
-        CKI(cudaMalloc(&h->d_mactive, nv));
-        CKI(cudaMalloc(&h->d_phase, 8 * sizeof(PhaseInfo)));
+        CKI(pool_malloc(&h->d_next, nv * sizeof(int)));
+        CKI(pool_malloc(&h->d_members, nv * sizeof(int)));
+        CKI(pool_malloc(&h->d_mpos, nv * sizeof(int4)));
+        CKI(pool_malloc(&h->d_rows, nv * sizeof(int)));
+        CKI(pool_malloc(&h->d_segs, nv * sizeof(Segment)));
+        CKI(pool_malloc(&h->d_mactive, nv));
+        CKI(pool_malloc(&h->d_phase, 8 * sizeof(PhaseInfo)));
         CKI(cudaMallocHost(&h->h_phase, 8 * sizeof(PhaseInfo)));
     }
     lap("per-vacancy / domain buffers");
@@ -1070,7 +1095,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     if (cfg->barrier_model == AKMC_MODEL_MLP) {
         const size_t n = 448 * kHid + kHid + kHid * kHid + kHid + kHid * 8 + 8;
-        CKI(cudaMalloc(&h->d_mlp, n * sizeof(double)));
+        CKI(pool_malloc(&h->d_mlp, n * sizeof(double)));
         CKI(cudaMemcpy(h->d_mlp, mlp, n * sizeof(double), cudaMemcpyHostToDevice));
         rc = prepare_engine_weights(h, mlp);
         if (rc != AKMC_OK) { std::string m = h->err; free_all(h); delete h; return fail(nullptr, rc, m); }
@@ -1095,8 +1120,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
             CKI(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
             CKI(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
             CKI(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-            CKI(cudaMalloc(&h->d_segs2, (size_t)h->vcap * sizeof(Segment)));
-            CKI(cudaMalloc(&h->d_bdom, (size_t)h->vcap * sizeof(long long)));
+            CKI(pool_malloc(&h->d_segs2, (size_t)h->vcap * sizeof(Segment)));
+            CKI(pool_malloc(&h->d_bdom, (size_t)h->vcap * sizeof(long long)));
             h->overlap_ok = true;
         }
     }
@@ -1108,7 +1133,7 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->n_clusters = engine_max_clusters();
         if (h->n_clusters <= 0) { free_all(h); delete h; return fail(nullptr, AKMC_ERR_CUDA, "no co-resident 8-CTA cluster for the evaluator"); }
     }
-    CKI(cudaMalloc(&h->d_cursor, sizeof(unsigned int)));
+    CKI(pool_malloc(&h->d_cursor, sizeof(unsigned int)));
     if (std::getenv("AKMC_WATCHDOG")) {
         CKI(cudaHostAlloc(&h->h_watch, 4096 * 8 * sizeof(int), cudaHostAllocMapped));
         std::memset(h->h_watch, 0, 4096 * 8 * sizeof(int));
@@ -1116,16 +1141,16 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
     }
     {
         const int ncl = std::max(h->n_clusters, 1) + 1;
-        CKI(cudaMalloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
-        CKI(cudaMalloc(&h->d_wstore, (size_t)std::max(h->num_sms, ncl * kClusterN) * kRowCap * kWin));
+        CKI(pool_malloc(&h->d_stage, (size_t)ncl * kClusterN * 2 * 65536));
+        CKI(pool_malloc(&h->d_wstore, (size_t)std::max(h->num_sms, ncl * kClusterN) * kRowCap * kWin));
     }
-    CKI(cudaMalloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
+    CKI(pool_malloc(&h->d_memo, (size_t)h->vcap * 2 * sizeof(MemoEntry)));
     CKI(cudaMemset(h->d_memo, 0xFF, (size_t)h->vcap * 2 * sizeof(MemoEntry)));   // key 0xFF..: empty
     {
         // per-voxel kT (uniform until akmc_set_voxel_temperatures); the pointer is fixed for the handle's
         // life, so kernel parameters captured in graphs stay valid when the values change
         const std::vector<double> kT((size_t)h->nvox, h->P.kT), ik((size_t)h->nvox, h->P.inv_kT);
-        CKI(cudaMalloc(&h->d_kT, 2 * kT.size() * sizeof(double)));
+        CKI(pool_malloc(&h->d_kT, 2 * kT.size() * sizeof(double)));
         CKI(cudaMemcpy(h->d_kT, kT.data(), kT.size() * sizeof(double), cudaMemcpyHostToDevice));
         CKI(cudaMemcpy(h->d_kT + h->nvox, ik.data(), ik.size() * sizeof(double), cudaMemcpyHostToDevice));
         h->P.kT_vox = h->d_kT;
@@ -1144,8 +1169,8 @@ int akmc_init(const akmc_config* cfg, const uint8_t* species, const double* eps,
         h->serial_engine = h->engine && maxm <= kRowCap;     // a voxel must fit one CTA's member capacity
         std::vector<int> mem((size_t)std::max<int64_t>(h->nvac, 1));
         for (int64_t i = 0; i < h->nvac; ++i) mem[(size_t)i] = (int)i;
-        CKI(cudaMalloc(&h->d_segs, sg.size() * sizeof(Segment)));
-        CKI(cudaMalloc(&h->d_members, mem.size() * sizeof(int)));
+        CKI(pool_malloc(&h->d_segs, sg.size() * sizeof(Segment)));
+        CKI(pool_malloc(&h->d_members, mem.size() * sizeof(int)));
         CKI(cudaMemcpy(h->d_members, mem.data(), mem.size() * sizeof(int), cudaMemcpyHostToDevice));
         h->vT.assign((size_t)h->nvox, cfg->temperature_K);
         h->vstart_host = vs;
@@ -1178,7 +1203,7 @@ int akmc_debug_math(int32_t fn, const double* x, int64_t n, double* y)
     if ((fn != 0 && fn != 1) || n < 0 || (n > 0 && (!x || !y))) return AKMC_ERR_INVALID;
     if (n == 0) return AKMC_OK;
     double* d = nullptr;
-    if (cudaMalloc(&d, (size_t)n * 2 * sizeof(double)) != cudaSuccess) return AKMC_ERR_CUDA;
+    if (pool_malloc(&d, (size_t)n * 2 * sizeof(double)) != cudaSuccess) return AKMC_ERR_CUDA;
     cudaError_t e = cudaMemcpy(d, x, (size_t)n * sizeof(double), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
         debug_math_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(fn, d, (long long)n, d + n);
@@ -1933,7 +1958,7 @@ int akmc_state(akmc_handle* h, uint8_t* species_out, int64_t* vac_sites_out, int
     if (vac_sites_out && (!n_vac_inout || *n_vac_inout < (int64_t)vr.size()))
         return fail(h, AKMC_ERR_INVALID, "vacancy buffer too short");
     if (species_out) {
-        if (!h->d_canon) CK(h, cudaMalloc(&h->d_canon, (size_t)h->sites));   // kept for later readbacks
+        if (!h->d_canon) CK(h, pool_malloc(&h->d_canon, (size_t)h->sites));   // kept for later readbacks
         uint8_t* canon = h->d_canon;
         const long long nchunks = (long long)((h->F.L[0] + 3) / 4) * h->F.L[1] * h->F.L[2] * h->nvox;
         gather_canonical_kernel<<<blocks_for(nchunks, 256), 256, 0, h->stream>>>(h->d_species, canon, h->F, h->nvox);
@@ -1984,7 +2009,7 @@ int akmc_set_world_model(akmc_handle* h, const double* tnet, int32_t hidden, dou
             return fail(h, AKMC_ERR_INVALID, "world-model mode: more than 64 vacancies in a voxel");
     CK(h, cudaStreamSynchronize(h->stream));
     if (h->d_tnet) { cudaFree(h->d_tnet); h->d_tnet = nullptr; }
-    CK(h, cudaMalloc(&h->d_tnet, n * sizeof(double)));
+    CK(h, pool_malloc(&h->d_tnet, n * sizeof(double)));
     CK(h, cudaMemcpy(h->d_tnet, tnet, n * sizeof(double), cudaMemcpyHostToDevice));
     h->world_H = hidden;
     h->world_tau = tau_act;
@@ -2018,20 +2043,20 @@ int akmc_set_dataflow(akmc_handle* h, int32_t on)
         h->df_ntiles = (int)nt;
         h->df_grid = grid;
         const size_t ring = (size_t)grid * h->df_ring_cap;
-        CK(h, cudaMalloc(&h->d_done_phase, nt * sizeof(long long)));
-        CK(h, cudaMalloc(&h->d_tile_off, (nt + 1) * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_tile_cnt, nt * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_tile_cur, nt * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_tile_mem, (size_t)h->vcap * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_arr_cnt, nt * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_arr_slot, nt * kArrCap * sizeof(int)));
+        CK(h, pool_malloc(&h->d_done_phase, nt * sizeof(long long)));
+        CK(h, pool_malloc(&h->d_tile_off, (nt + 1) * sizeof(int)));
+        CK(h, pool_malloc(&h->d_tile_cnt, nt * sizeof(int)));
+        CK(h, pool_malloc(&h->d_tile_cur, nt * sizeof(int)));
+        CK(h, pool_malloc(&h->d_tile_mem, (size_t)h->vcap * sizeof(int)));
+        CK(h, pool_malloc(&h->d_arr_cnt, nt * sizeof(int)));
+        CK(h, pool_malloc(&h->d_arr_slot, nt * kArrCap * sizeof(int)));
         CK(h, cudaMemset(h->d_arr_slot, 0xFF, nt * kArrCap * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_ring_slot, ring * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_ring_pos, ring * sizeof(int4)));
-        CK(h, cudaMalloc(&h->d_ring_key, ring * sizeof(unsigned long long)));
-        CK(h, cudaMalloc(&h->d_df_scratch, (4 * ring + 64) * sizeof(double)));
-        CK(h, cudaMalloc(&h->d_df_iscratch, (ring + 16) * sizeof(int)));
-        CK(h, cudaMalloc(&h->d_df_err, sizeof(int)));
+        CK(h, pool_malloc(&h->d_ring_slot, ring * sizeof(int)));
+        CK(h, pool_malloc(&h->d_ring_pos, ring * sizeof(int4)));
+        CK(h, pool_malloc(&h->d_ring_key, ring * sizeof(unsigned long long)));
+        CK(h, pool_malloc(&h->d_df_scratch, (4 * ring + 64) * sizeof(double)));
+        CK(h, pool_malloc(&h->d_df_iscratch, (ring + 16) * sizeof(int)));
+        CK(h, pool_malloc(&h->d_df_err, sizeof(int)));
         CK(h, cudaMemset(h->d_df_err, 0, sizeof(int)));
     }
     h->df = true;
@@ -2126,7 +2151,7 @@ int akmc_debug_extended(akmc_handle* h, uint8_t* out)
     for (int a = 0; a < 3; ++a) { R.lo[a] = -kHalo; R.hi[a] = h->F.L[a] + kHalo; }
     const size_t bytes = 2ull * (h->F.L[0] + 2 * kHalo) * (h->F.L[1] + 2 * kHalo) * (h->F.L[2] + 2 * kHalo);
     uint8_t* d = nullptr;
-    CK(h, cudaMalloc(&d, bytes));
+    CK(h, pool_malloc(&d, bytes));
     pack_slab_kernel<<<h->num_sms * 4, 256, 0, h->stream>>>(h->d_species, h->F, R, d);
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e == cudaSuccess) e = cudaMemcpy(out, d, bytes, cudaMemcpyDeviceToHost);
@@ -2184,8 +2209,8 @@ int akmc_eval_windows(akmc_handle* h, const uint8_t* windows, int64_t n, int32_t
     if (n == 0) return AKMC_OK;
     uint8_t* d_w = nullptr;
     double* d_e = nullptr;
-    CK(h, cudaMalloc(&d_w, (size_t)n * kWin));
-    CK(h, cudaMalloc(&d_e, (size_t)n * 8 * sizeof(double)));
+    CK(h, pool_malloc(&d_w, (size_t)n * kWin));
+    CK(h, pool_malloc(&d_e, (size_t)n * 8 * sizeof(double)));
     CK(h, cudaMemcpy(d_w, windows, (size_t)n * kWin, cudaMemcpyHostToDevice));
     int rc = eval_rows(h, nullptr, nullptr, (int)n, (int)n, d_w, precision, nullptr, nullptr, d_e);
     if (rc == AKMC_OK) {

@@ -9,6 +9,7 @@ A step = one sublattice sweep (8 phases) over the GPU's block.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5|c4|c3|c2|c1]
   python bench.py --workload c4 --world      (the world-model time mode, on a serial workload)
+  python bench.py --workload c1 --replicas 4096   (C1's batched-replica variant for throughput)
 
 N > 1 is launched by torchrun (one rank per GPU).  Rank 0 prints ONE JSON line.
 """
@@ -54,12 +55,17 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+REPLICAS = None                         # --replicas: serial workloads as a batch of independent replica voxels
+
+
 def workload(name: str):
     pr = synth.preset(name.upper())
     cells = pr.cells
     nvox = pr.n_voxels
     if name == "c4":
         nvox = 512                      # per GPU (4096 over 8 GPUs)
+    if REPLICAS and not pr.domain[0]:
+        nvox = REPLICAS                 # (C1 "plus a batched-replica variant for throughput")
     return pr, cells, nvox
 
 
@@ -572,11 +578,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--events", type=int, default=100, help="serial workloads: BKL events per voxel per step")
     ap.add_argument("--voxel-T", action="store_true", help="per-voxel temperature uniform in 558-577 K (C4 variant)")
+    ap.add_argument("--replicas", type=int, default=0,
+                    help="serial workloads: this many independent replica voxels per GPU (e.g. C1 x 4096)")
     ap.add_argument("--world", action="store_true",
                     help="serial workloads: the world-model time mode (SURVEY 8(f) f2; FP64: policy logits -E/kT of the "
                          "physics network, Eq. 7 clock from a seeded Poisson-time net)")
     ap.add_argument("--ramp-s", type=float, default=1.0, help="untimed clock ramp before the warm-up steps")
     args = ap.parse_args()
+    global REPLICAS
+    REPLICAS = args.replicas or None
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -194,14 +194,21 @@ __device__ __forceinline__ int tree_descend(const double* buf, int n, int P, int
 // first k with r < cumsum_k (sequential), guard: last k with Gamma > 0
 __device__ __forceinline__ int pick_hop(const double* G8, double r)
 {
+    // the 8 rates are read up front (one burst of independent loads; with the early exit inside the scan each
+    // load would wait for the previous comparison), then scanned in hop order exactly as before
+    double g[kHops];
+#pragma unroll
+    for (int k = 0; k < kHops; ++k) g[k] = G8[k];
     double cs = 0.0;
+#pragma unroll
     for (int k = 0; k < kHops; ++k) {
-        cs = __dadd_rn(cs, G8[k]);
+        cs = __dadd_rn(cs, g[k]);
         if (r < cs) return k;
     }
     int last = -1;
+#pragma unroll
     for (int k = 0; k < kHops; ++k)
-        if (G8[k] > 0.0) last = k;
+        if (g[k] > 0.0) last = k;
     return last;
 }
 

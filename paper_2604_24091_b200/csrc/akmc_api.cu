@@ -172,7 +172,7 @@ struct akmc_handle {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool overlap_ok = false;          // p2p transport, phase engine: the overlapped sweep is available
     bool xpending = false;            // a packed exchange whose unpack has not been enqueued yet
-    unsigned long long xepoch = 0;
+
     uint8_t* d_mactive = nullptr;
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;     // pinned
@@ -270,11 +270,11 @@ struct akmc_handle {
     int4* d_mbox = nullptr;                    // [npeer][2][cap + 1]
     unsigned long long* d_mflag = nullptr;     // [kMaxPeers]
     int* d_pcnt = nullptr;
+    unsigned long long* d_pepoch = nullptr;   // peer-mailbox exchanges completed (device-side epoch)
     unsigned int* d_pdone = nullptr;
     PeerBoxes PB{};
     void* ipc_box[kMaxPeers] = {};
     void* ipc_flag[kMaxPeers] = {};
-    unsigned long long epoch = 0;
 };
 
 namespace {
@@ -355,7 +355,7 @@ void free_all(akmc_handle* h)
     for (void* p : dfptrs)
         if (p) cudaFree(p);
     void* dptrs[] = {h->d_slist, h->d_nslist, h->d_free, h->d_fcnt, h->d_gid, h->d_nvac, h->d_log, h->d_nlog, h->d_send, h->d_recv, h->d_dist_overflow,
-                     h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone};
+                     h->d_mbox, h->d_mflag, h->d_pcnt, h->d_pdone, h->d_pepoch};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     for (int q = 0; q < 8; ++q)
@@ -737,6 +737,8 @@ int setup_p2p(akmc_handle* h)
     CK(h, cudaMalloc(&h->d_mflag, kMaxPeers * sizeof(unsigned long long)));
     CK(h, pool_malloc(&h->d_pcnt, kMaxPeers * sizeof(int)));
     CK(h, pool_malloc(&h->d_pdone, sizeof(unsigned int)));
+    CK(h, pool_malloc(&h->d_pepoch, sizeof(unsigned long long)));
+    CK(h, cudaMemset(h->d_pepoch, 0, sizeof(unsigned long long)));
     CK(h, cudaMemset(h->d_mbox, 0, std::max<size_t>(1, (size_t)np * 2 * per) * sizeof(int4)));
     CK(h, cudaMemset(h->d_mflag, 0, kMaxPeers * sizeof(unsigned long long)));
     CK(h, cudaMemset(h->d_pcnt, 0, kMaxPeers * sizeof(int)));
@@ -771,6 +773,7 @@ int setup_p2p(akmc_handle* h)
     }
     h->PB.cnt = h->d_pcnt;
     h->PB.done = h->d_pdone;
+    h->PB.ep = h->d_pepoch;
     h->p2p = true;
     return AKMC_OK;
 }
@@ -1418,6 +1421,7 @@ static int enqueue_iteration(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s
 // CUDA graph of phases [q0, q1): activate + segments, then a conditional WHILE node whose body is one
 // inner iteration (rows, eval, select, condition) -- the a8 loop runs on the device with no host
 // synchronisation; the phase table (sector permutation) is a device array updated per sweep.
+static void enqueue_exchange_p2p(akmc_handle* h, cudaStream_t s);
 static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGraphExec_t* out, int* launches_out)
 {
     cudaStream_t cs = nullptr, bs = nullptr;
@@ -1446,6 +1450,10 @@ static int build_graph(akmc_handle* h, int q0, int q1, bool with_window, cudaGra
         if (h->engine) {
             rc = enqueue_phase_engine(h, ph, cs);
             launches += 3;
+            if (h->multi && h->p2p && !h->shift && !h->df && with_window) {   // (a multi-rank handle's sweep graph)
+                enqueue_exchange_p2p(h, cs);
+                launches += 1;
+            }
             continue;
         }
         enqueue_phase_start(h, ph, cs);
@@ -1535,6 +1543,14 @@ static int exchange_shift(akmc_handle* h)
     return AKMC_OK;
 }
 
+// the per-phase peer-mailbox exchange as one launch (graph-capturable: its epoch lives on the device)
+static void enqueue_exchange_p2p(akmc_handle* h, cudaStream_t s)
+{
+    exchange_p2p_kernel<<<kP2PBlocks, 256, 0, s>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->PB, h->d_mbox,
+                                                   h->d_species, h->d_vac, h->d_gid, h->d_nvac, h->vcap,
+                                                   FreeList{h->d_free, h->d_fcnt}, h->d_dist_overflow);
+}
+
 static int exchange_deltas(akmc_handle* h)
 {
     if (h->shift) return exchange_shift(h);
@@ -1543,20 +1559,16 @@ static int exchange_deltas(akmc_handle* h)
     h->messages += np;
     if (h->p2p) {
         // deltas straight into the peers' mailboxes over NVLink, flag per peer; wait + apply (akmc_dist.cuh)
-        h->epoch += 1;
         if (h->xchg_mark) {                            // (AKMC_PHASE_TIMING: separate launches, to time pack / unpack)
             pack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species,
-                                                              h->PB, h->epoch, h->d_dist_overflow);
+                                                              h->PB, h->d_dist_overflow);
             CK(h, cudaEventRecord(h->xchg_mark[1], h->stream));
-            unpack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_mbox, h->d_mflag, h->epoch, h->F, h->DP, h->d_species,
+            unpack_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_mbox, h->d_pepoch, h->F, h->DP, h->d_species,
                                                                 h->d_vac, h->d_gid, h->d_nvac, h->vcap,
                                                                 FreeList{h->d_free, h->d_fcnt}, h->d_dist_overflow);
             h->total.kernel_launches += 2;
         } else {
-            exchange_p2p_kernel<<<kP2PBlocks, 256, 0, h->stream>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->PB,
-                                                                  h->epoch, h->d_mbox, h->d_species, h->d_vac, h->d_gid,
-                                                                  h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
-                                                                  h->d_dist_overflow);
+            enqueue_exchange_p2p(h, h->stream);
             h->total.kernel_launches += 1;
         }
         CK(h, cudaGetLastError());
@@ -1715,7 +1727,7 @@ static void enqueue_unpack_p2p(akmc_handle* h, cudaStream_t s, const PhaseInfo* 
         act.ph = ph_next; act.S = h->S; act.dmin = h->d_dmin; act.head = h->d_head; act.next = h->d_next;
         act.bdom = h->d_bdom; act.ctr = h->d_ctr;
     }
-    unpack_p2p_kernel<<<kP2PBlocks, 256, 0, s>>>(h->d_mbox, h->d_mflag, h->xepoch, h->F, h->DP, h->d_species, h->d_vac,
+    unpack_p2p_kernel<<<kP2PBlocks, 256, 0, s>>>(h->d_mbox, h->d_pepoch, h->F, h->DP, h->d_species, h->d_vac,
                                                  h->d_gid, h->d_nvac, h->vcap, FreeList{h->d_free, h->d_fcnt},
                                                  h->d_dist_overflow, act);
     h->xpending = false;
@@ -1761,10 +1773,8 @@ static int step_sublattice_overlap(akmc_handle* h, int64_t n)
             CK(h, launch_engine(p, h->tc, std::max(1, std::min(h->n_clusters, spare / 4)), spare, A));
             CK(h, cudaStreamWaitEvent(A, h->ev_join, 0));
             // send side of this phase's exchange
-            h->epoch += 1;
-            h->xepoch = h->epoch;
             pack_p2p_kernel<<<kP2PBlocks, 256, 0, A>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->d_species, h->PB,
-                                                       h->epoch, h->d_dist_overflow);
+                                                       h->d_dist_overflow);
             CK(h, cudaGetLastError());
             h->xpending = true;
             h->messages += np;
@@ -1788,11 +1798,14 @@ static int step_sublattice(akmc_handle* h, int64_t n)
     if (h->profile) return step_sublattice_host(h, n);
     if (h->multi && h->overlap_ok && !h->df) return step_sublattice_overlap(h, n);
     int launches_phase = 0;
-    if (!h->multi && !h->sweep_exec) {
+    // one graph per sweep: a single rank, or ranks exchanging through the peer mailboxes (the exchange kernel's
+    // epoch lives on the device, so it replays inside the graph); NCCL / shift exchanges run between phase graphs
+    const bool one_graph = !h->multi || (h->p2p && !h->shift && h->engine && !h->df);
+    if (one_graph && !h->sweep_exec) {
         const int rc = build_graph(h, 0, 8, true, &h->sweep_exec, &h->graph_launches_per_sweep);
         if (rc != AKMC_OK) return rc;
     }
-    if (h->multi && !h->phase_exec[0]) {
+    if (!one_graph && !h->phase_exec[0]) {
         for (int q = 0; q < 8; ++q) {
             const int rc = build_graph(h, q, q + 1, false, &h->phase_exec[q], &launches_phase);
             if (rc != AKMC_OK) return rc;
@@ -1804,9 +1817,10 @@ static int step_sublattice(akmc_handle* h, int64_t n)
         phase_table(h, h->sweep, t.p);
         set_phase_kernel<<<1, 32, 0, h->stream>>>(h->d_phase, t);
         CK(h, cudaGetLastError());
-        if (!h->multi) {
+        if (one_graph) {
             CK(h, cudaGraphLaunch(h->sweep_exec, h->stream));
             watchdog_wait(h, "sweep");
+            if (h->multi) { h->messages += 8 * h->DP.npeer; h->exchanges += 8; }
         } else {
             for (int q = 0; q < 8; ++q) {
                 CK(h, cudaGraphLaunch(h->phase_exec[q], h->stream));

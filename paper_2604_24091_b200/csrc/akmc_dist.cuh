@@ -81,7 +81,9 @@ __device__ __forceinline__ int arrival_slot(const FreeList& FL, int nfree0, int*
     return k < nfree0 ? FL.slots[nfree0 - 1 - k] : atomicAdd(nvac_local, 1);
 }
 
-__device__ __forceinline__ void unpack_done(const FreeList& FL, int nfree0)
+// (ep: the peer-mailbox exchange's device epoch counter -- the last block records that exchange `epoch` is done)
+__device__ __forceinline__ void unpack_done(const FreeList& FL, int nfree0, unsigned long long* ep = nullptr,
+                                            unsigned long long epoch = 0)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -90,6 +92,7 @@ __device__ __forceinline__ void unpack_done(const FreeList& FL, int nfree0)
             const int pops = atomicExch(&FL.cnt[1], 0);
             FL.cnt[0] = max(0, nfree0 - pops);
             FL.cnt[2] = 0;
+            if (ep) *ep = epoch;
             __threadfence();
         }
     }

@@ -22,7 +22,8 @@ struct PeerBoxes {
     unsigned long long* flag[kMaxPeers];   // (unused by the tagged protocol; kept for the mapping's layout)
     int* cnt;                              // [npeer] local allocation counters of this exchange
     unsigned int* done;                    // blocks of the pack kernel that have finished (last block publishes)
-};
+    unsigned long long* ep;                // exchanges completed on this rank (device-side, so that the exchange
+};                                         // can live inside a replayed CUDA graph): exchange e = *ep + 1
 
 __device__ __forceinline__ void st_relaxed_sys_u64(void* p, unsigned long long v)
 {
@@ -54,7 +55,7 @@ __device__ __forceinline__ void put_entry(int4* dst, int g0, int g1, int g2, int
 __device__ __forceinline__ void pack_p2p(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, const Frame& F,
                                          const DistParams& D, const uint8_t* __restrict__ species, const PeerBoxes& B,
                                          unsigned long long epoch, int* overflow)
-{
+{   // (epoch = *B.ep + 1, read by the caller before any block can complete the exchange)
     const int n = (int)min((unsigned long long)logcap, *nlog_p);
     const size_t par = (size_t)(epoch & 1ull) * (size_t)(D.cap + 1);
     const uint32_t tag = (uint32_t)epoch;
@@ -115,10 +116,9 @@ __device__ __forceinline__ void pack_p2p(const int4* __restrict__ log, unsigned 
     }
 }
 static __global__ void pack_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
-                                       DistParams D, const uint8_t* __restrict__ species, PeerBoxes B,
-                                       unsigned long long epoch, int* overflow)
+                                       DistParams D, const uint8_t* __restrict__ species, PeerBoxes B, int* overflow)
 {
-    pack_p2p(log, nlog_p, logcap, F, D, species, B, epoch, overflow);
+    pack_p2p(log, nlog_p, logcap, F, D, species, B, *(volatile unsigned long long*)B.ep + 1, overflow);
 }
 
 // wait for every peer's deltas of exchange `epoch` (tags), then apply them (same semantics as unpack_deltas_kernel)
@@ -134,7 +134,8 @@ struct ArrivalActivation {
 };
 __device__ __forceinline__ void unpack_p2p(const int4* __restrict__ mbox, unsigned long long epoch, const Frame& F,
                                            const DistParams& D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
-                                           int vcap, const FreeList& FL, int* overflow, const ArrivalActivation& act)
+                                           int vcap, const FreeList& FL, int* overflow, const ArrivalActivation& act,
+                                           unsigned long long* ep)
 {
     const int nfree0 = *(volatile int*)&FL.cnt[0];
     const uint32_t tag = (uint32_t)epoch;
@@ -204,25 +205,25 @@ __device__ __forceinline__ void unpack_p2p(const int4* __restrict__ mbox, unsign
             }
         }
     }
-    unpack_done(FL, nfree0);
+    unpack_done(FL, nfree0, ep, epoch);
 }
-static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, const unsigned long long* mflag, unsigned long long epoch,
-                                         Frame F, DistParams D, uint8_t* species, int4* vac, int* gid, int* nvac_local,
-                                         int vcap, FreeList FL, int* overflow, ArrivalActivation act = ArrivalActivation{})
+static __global__ void unpack_p2p_kernel(const int4* __restrict__ mbox, unsigned long long* ep, Frame F, DistParams D,
+                                         uint8_t* species, int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL,
+                                         int* overflow, ArrivalActivation act = ArrivalActivation{})
 {
-    (void)mflag;
-    unpack_p2p(mbox, epoch, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, act);
+    unpack_p2p(mbox, *(volatile unsigned long long*)ep + 1, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, act, ep);
 }
 // send and receive of one exchange in one launch (the unoverlapped per-phase path): every block packs its share,
 // the last one publishes the counts, then every block waits for the peers' deltas and applies its share
 static __global__ void exchange_p2p_kernel(const int4* __restrict__ log, unsigned long long* nlog_p, int logcap, Frame F,
-                                           DistParams D, PeerBoxes B, unsigned long long epoch, const int4* __restrict__ mbox,
+                                           DistParams D, PeerBoxes B, const int4* __restrict__ mbox,
                                            uint8_t* species, int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL,
                                            int* overflow)
 {
+    const unsigned long long epoch = *(volatile unsigned long long*)B.ep + 1;   // (raised by the last block at the end)
     pack_p2p(log, nlog_p, logcap, F, D, species, B, epoch, overflow);
     __syncthreads();
-    unpack_p2p(mbox, epoch, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, ArrivalActivation{});
+    unpack_p2p(mbox, epoch, F, D, species, vac, gid, nvac_local, vcap, FL, overflow, ArrivalActivation{}, B.ep);
 }
 
 } // namespace akmc

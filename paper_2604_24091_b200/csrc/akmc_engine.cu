@@ -51,6 +51,9 @@
 #ifndef AKMC_ENGINE_L1_BATCH
 #define AKMC_ENGINE_L1_BATCH 2
 #endif
+#ifndef AKMC_PDL
+#define AKMC_PDL 1              // programmatic dependent launch of the engine (A/B knob)
+#endif
 #ifndef AKMC_SERIAL_CLOCK
 #define AKMC_SERIAL_CLOCK 1     // serial mode: voxel clock cached in the slot (no per-event global load)
 #endif
@@ -547,8 +550,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     if (tid == 0) {
         c.npend = 0; c.drained = 0; c.nrun = 0;
         c.int_drained = 0; c.bready = 0; c.bdrained = 0; c.ntot2 = 0; c.bwait0 = 0;
-        c.ntot = phase_mode ? (p.serial ? p.nseg_host : (int)p.ctr->nseg) : 0;
-        c.nhot = (phase_mode && !p.serial && p.seg_cap > 0) ? (int)p.ctr->nhot : -1;
         c.events = 0; c.evals = 0; c.mrows = 0; c.clamps = 0;
         if (kTC) {
             mbar_init(bar_req, kClusterN);
@@ -591,6 +592,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     } else {
         __syncthreads();
     }
+    // programmatic dependent launch (AKMC_PDL): everything above -- barriers, TMEM, the weight slices -- overlaps the
+    // tail of the kernel this launch depends on; nothing that kernel (or an earlier one) writes is read before here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) {
+        c.ntot = phase_mode ? (p.serial ? p.nseg_host : (int)p.ctr->nseg) : 0;
+        c.nhot = (phase_mode && !p.serial && p.seg_cap > 0) ? (int)p.ctr->nhot : -1;
+    }
+    __syncthreads();
     const int nrows_eval = (!phase_mode) ? (p.nrows_dev ? *p.nrows_dev : p.nrows_host) : 0;
     // diagnostics (thread 0): iterations, rounds, evaluation rounds, cycles in control / rounds / selection
     unsigned long long d_it = 0, d_rounds = 0, d_erounds = 0, d_refill = 0;
@@ -1737,17 +1746,19 @@ cudaError_t launch_engine(const EngineParams& p, bool tc, int nclusters, int num
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kClusterN;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the previous kernel
+    attr[1].val.programmaticStreamSerializationAllowed = AKMC_PDL;
     cfg.gridDim = dim3(kClusterN * nclusters, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = kSmemTotal;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (p.df) return p.fast ? cudaLaunchKernelEx(&cfg, engine_kernel<true, true, true>, p)
                             : cudaLaunchKernelEx(&cfg, engine_kernel<true, false, true>, p);
     return p.fast ? cudaLaunchKernelEx(&cfg, engine_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, engine_kernel<true>, p);

@@ -479,6 +479,9 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
                                                        const unsigned char* memo = nullptr, int seg_cap = 0,
                                                        double hot_events = 0.0, int part = 0, Segment* segs2 = nullptr)
 {
+    // the phase engine launched after this kernel may start its prologue now (it waits for this grid's
+    // completion with griddepcontrol.wait before it reads anything written here)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     // block-uniform trip count: block_alloc needs every thread of the block
     for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x)

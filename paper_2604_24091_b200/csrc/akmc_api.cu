@@ -46,6 +46,27 @@ static cudaError_t pool_malloc(T** p, size_t n)
     return e;
 }
 
+#ifndef AKMC_PDL_LISTS
+#define AKMC_PDL_LISTS 1        // activate / segments kernels with programmatic dependent launch (A/B knob)
+#endif
+// a launch with programmatic stream serialisation (the kernel waits with griddepcontrol.wait before it reads what
+// the previous kernel writes; its blocks may be resident earlier and start without the launch gap)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args&&... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = AKMC_PDL_LISTS;
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(block, 1, 1);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+
 namespace {
 
 thread_local std::string g_init_error;
@@ -1347,18 +1368,18 @@ __global__ void set_phase_kernel(PhaseInfo* dst, PhaseTable8 t)
     if (threadIdx.x < 8) dst[threadIdx.x] = t.p[threadIdx.x];
 }
 
-// one inner iteration (a1 rows, a2-a5 eval, a6-a7 select) on stream s; cond != 0 adds the a8 condition kernel
+// the phase's domain lists and segments from the registry as it stands (a1)
 static void enqueue_phase_start(akmc_handle* h, const PhaseInfo* ph, cudaStream_t s)
 {
     const int nv = h->vcap;
     const int* nd = h->multi ? h->d_nvac : nullptr;
-    activate_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                        h->d_ctr);
-    segments_kernel<<<blocks_for(nv, 256), 256, 0, s>>>(h->d_vac, nv, nd, h->S, ph, h->d_dmin, h->d_head, h->d_next,
-                                                        h->d_segs, h->d_members, h->d_mactive, h->d_ctr, h->d_mpos,
-                                                        h->engine && h->hot_events > 0.0
-                                                            ? reinterpret_cast<const unsigned char*>(h->d_memo) : nullptr,
-                                                        nv, h->hot_events);
+    const unsigned char* memo = h->engine && h->hot_events > 0.0 ? reinterpret_cast<const unsigned char*>(h->d_memo)
+                                                                  : nullptr;
+    launch_pdl(activate_kernel, blocks_for(nv, 256), 256, s, (const int4*)h->d_vac, nv, nd, h->S, ph, h->d_dmin,
+               h->d_head, h->d_next, h->d_ctr, 0, (long long*)nullptr);
+    launch_pdl(segments_kernel, blocks_for(nv, 256), 256, s, (const int4*)h->d_vac, nv, nd, h->S, ph, h->d_dmin,
+               h->d_head, (const int*)h->d_next, h->d_segs, h->d_members, h->d_mactive, h->d_ctr, h->d_mpos, memo, nv,
+               h->hot_events, 0, (Segment*)nullptr);
 }
 
 // dataflow sweep (f1): tile base lists, then ONE engine launch that runs all 8 phases of the sweep, every tile
@@ -1546,9 +1567,9 @@ static int exchange_shift(akmc_handle* h)
 // the per-phase peer-mailbox exchange as one launch (graph-capturable: its epoch lives on the device)
 static void enqueue_exchange_p2p(akmc_handle* h, cudaStream_t s)
 {
-    exchange_p2p_kernel<<<kP2PBlocks, 256, 0, s>>>(h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP, h->PB, h->d_mbox,
-                                                   h->d_species, h->d_vac, h->d_gid, h->d_nvac, h->vcap,
-                                                   FreeList{h->d_free, h->d_fcnt}, h->d_dist_overflow);
+    launch_pdl(exchange_p2p_kernel, kP2PBlocks, 256, s, (const int4*)h->d_log, h->d_nlog, h->S.logcap, h->F, h->DP,
+               h->PB, (const int4*)h->d_mbox, h->d_species, h->d_vac, h->d_gid, h->d_nvac, h->vcap,
+               FreeList{h->d_free, h->d_fcnt}, h->d_dist_overflow);
 }
 
 static int exchange_deltas(akmc_handle* h)

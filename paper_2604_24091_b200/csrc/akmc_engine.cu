@@ -1581,6 +1581,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (tid == 0) lap(d_cs);
         trace_end();
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (the next phase's activation may launch)
     if (tid == 0 && p.diag && phase_mode) atomicAdd(p.diag + 96 + 512 + min(tr_it, 63), 1ull);
     if (tid == 0 && p.diag && p.overlap) {
         // overlap timing: boundary list publication and engine end, relative to the engine's start (last CTA out)

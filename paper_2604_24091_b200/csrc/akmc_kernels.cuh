@@ -357,6 +357,10 @@ static __global__ void activate_kernel(const int4* __restrict__ vac, int nvac, c
                                 const PhaseInfo* __restrict__ ph, int* dmin, int* head, int* next, DevCounters* ctr,
                                 int part = 0, long long* bdom = nullptr)
 {
+    // (programmatic dependent launch: this grid may be resident before the previous kernel has finished; it reads
+    // nothing before the wait, and lets the segments kernel after it launch at once)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (blockIdx.x == 0 && threadIdx.x == 0 && part == 0) reset_phase_counters(ctr);
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -481,6 +485,7 @@ static __global__ void __launch_bounds__(256) segments_kernel(const int4* __rest
 {
     // the phase engine launched after this kernel may start its prologue now (it waits for this grid's
     // completion with griddepcontrol.wait before it reads anything written here)
+    asm volatile("griddepcontrol.wait;" ::: "memory");                 // (the activate kernel's lists)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int n = nvac_dev ? min(*nvac_dev, nvac) : nvac;
     // block-uniform trip count: block_alloc needs every thread of the block

@@ -220,6 +220,8 @@ static __global__ void exchange_p2p_kernel(const int4* __restrict__ log, unsigne
                                            uint8_t* species, int4* vac, int* gid, int* nvac_local, int vcap, FreeList FL,
                                            int* overflow)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");                // (PDL: the phase's engine has completed)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next activation may become resident
     const unsigned long long epoch = *(volatile unsigned long long*)B.ep + 1;   // (raised by the last block at the end)
     pack_p2p(log, nlog_p, logcap, F, D, species, B, epoch, overflow);
     __syncthreads();
